@@ -1,0 +1,449 @@
+#!/usr/bin/env python
+"""Benchmark of the SS-CGA equalizer hot path (BASELINE.json metric).
+
+    python bench.py [--gpus N --steps K --warmup W] [--impl ours|reference]
+
+Workload (BASELINE.json configs[2], the metric's configuration): OTFS M=512,
+N=32, P=6 Veh-A taps, 16-QAM, Xi=10 fixed CG iterations, 25 dB, a batch of
+4096 frames per GPU (weak scaling: every rank solves its own 4096 frames, no
+collective on the data path).  A step = one fused solve of the whole batch
+(coefficients on the fly + CG + hard decisions + max-log LLRs + bit errors).
+
+One JSON line on rank 0: symbols/s (value, device-resident inputs), the same
+metric end to end from pinned host buffers (e2e), p50/p99 single-frame
+latency (CUDA graph replays), the FP32 roofline of the fused kernel against
+the FP32 peak measured on this box by an FFMA probe, the HBM fraction, the
+oracle port timed on the host cores (cpu_baseline) and the clocks seen.
+`--impl reference` times the reference algorithm's CPU implementation (the
+numpy oracle port of ddlink, oracle/ddlink_oracle.py) on all host cores.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+sys.path.insert(0, str(ROOT / "oracle"))
+
+METRIC = "DD-equalized symbols/sec (M=512,N=32,P=6, 16-QAM); p50 per-frame latency"
+CONFIGS = {
+    "cfg1": dict(M=64, N=16, P=4, mod="qpsk", batch=4096, nu=0.0),
+    "cfg2": dict(M=256, N=16, P=4, mod="qam16", batch=1024, nu=300.0),
+    "cfg3": dict(M=512, N=32, P=6, mod="qam16", batch=4096, nu=100.0),
+    "cfg4": dict(M=1024, N=64, P=6, mod="qam16", batch=1024, nu=1000.0),
+}
+BPS = {"qpsk": 2, "qam16": 4, "qam64": 6}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
+    ap.add_argument("--config", choices=sorted(CONFIGS), default="cfg3")
+    ap.add_argument("--batch", type=int, default=0, help="frames per GPU (default: config's)")
+    ap.add_argument("--snr", type=float, default=25.0)
+    ap.add_argument("--iters", type=int, default=10)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-latency", action="store_true")
+    ap.add_argument("--lat-runs", type=int, default=2000)
+    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    return ap.parse_args()
+
+
+def flops_per_frame(P, MN, iters):
+    return 8 * P * MN * (2 * iters + 1) + 24 * MN * iters + 4 * MN
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.path = None
+
+    def start(self):
+        try:
+            fd, self.path = tempfile.mkstemp(suffix=".csv")
+            os.close(fd)
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100", "-f", self.path], stdout=subprocess.DEVNULL, stderr=subprocess.DEVNULL)
+        except (OSError, FileNotFoundError):
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        rows = []
+        for line in Path(self.path).read_text().splitlines():
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 9:
+                rows.append(parts)
+        os.unlink(self.path)
+        if not rows:
+            return None
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        mx = max(float(r[2]) for r in rows if r[2].replace(".", "").isdigit())
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[5 + i].lower() == "active"})
+        loaded = [s for s in sm if s > 0.5 * mx] or sm
+        return {"sm_mhz": statistics.median(loaded), "sm_max_mhz": mx, "reasons": reasons,
+                "samples": len(rows), "power_w_max": max(float(r[3]) for r in rows
+                                                        if r[3].replace(".", "").isdigit())}
+
+
+# ------------------------------------------------------------------ CPU side (oracle port)
+def _cpu_frames(cfg, S, snr_db, iters, seed):
+    """Synthetic frames of the workload, built with the oracle on the host."""
+    import numpy as np
+    import ddlink_oracle as orc
+    rng = np.random.default_rng(seed)
+    M, N = cfg["M"], cfg["N"]
+    const = orc.qam(cfg["mod"])
+    B = M * 30e3
+    delays = np.round(np.array([0.0, 0.31, 0.71, 1.09, 1.73, 2.51])[:cfg["P"]] * 1e-6 * B).astype(int)
+    pw = 10 ** (np.array([0.0, -1.0, -9.0, -10.0, -15.0, -20.0])[:cfg["P"]] / 10)
+    mags = np.sqrt(pw / pw.sum())
+    frames = []
+    for _ in range(S):
+        dop = np.round(cfg["nu"] * np.cos(2 * np.pi * rng.random(cfg["P"])) / (30e3 / N)).astype(int)
+        taps = [orc.Tap(int((M // 2 + d) % M), int((N // 2 + o) % N), complex(m * np.exp(2j * np.pi * rng.random())))
+                for d, o, m in zip(delays, dop, mags)]
+        lab = rng.integers(0, len(const.points), M * N)
+        t = orc.build_tables(taps, M, N)
+        hx = orc.forward(t, const.points[lab])
+        snr = 10 ** (snr_db / 10)
+        sigma = math.sqrt(np.mean(np.abs(hx) ** 2) / snr / 2)
+        y = hx + sigma * (rng.normal(size=M * N) + 1j * rng.normal(size=M * N))
+        frames.append((taps, y, 1.0 / snr))
+    return frames, const
+
+
+_WORK = None
+
+
+def _init_worker(frames, cfg, iters):
+    global _WORK
+    os.environ["OPENBLAS_NUM_THREADS"] = "1"
+    _WORK = (frames, cfg, iters)
+
+
+def _solve_chunk(idx):
+    import ddlink_oracle as orc
+    frames, cfg, iters = _WORK
+    const = orc.qam(cfg["mod"])
+    for i in idx:
+        taps, y, lam = frames[i % len(frames)]
+        orc.receive(taps, y, cfg["M"], cfg["N"], iters, lam, const)
+    return len(idx)
+
+
+class CpuArm:
+    """The reference hot path (build_ss_channel -> cga_equalize -> hard_demod)
+    in its numpy restatement, one process per host core like run_packets
+    (harness.py:217-232)."""
+
+    def __init__(self, cfg, snr_db, iters, seed=123):
+        import multiprocessing as mp
+        os.environ["OPENBLAS_NUM_THREADS"] = "1"
+        os.environ["OMP_NUM_THREADS"] = "1"
+        self.cores = len(os.sched_getaffinity(0))
+        self.cfg, self.iters = cfg, iters
+        frames, _ = _cpu_frames(cfg, 8, snr_db, iters, seed)
+        self.pool = mp.get_context("fork").Pool(self.cores, initializer=_init_worker,
+                                                initargs=(frames, cfg, iters))
+        self.pool.map(_solve_chunk, [[0]] * self.cores)  # warm every worker
+        t0 = time.perf_counter()
+        _solve_chunk_local(frames, cfg, iters, 2)
+        self.frame_s = (time.perf_counter() - t0) / 2
+
+    def run(self, frames_total):
+        per = max(1, frames_total // self.cores)
+        chunks = [list(range(i * per, (i + 1) * per)) for i in range(self.cores)]
+        t0 = time.perf_counter()
+        done = sum(self.pool.map(_solve_chunk, chunks))
+        dt = time.perf_counter() - t0
+        return done, dt
+
+    def close(self):
+        self.pool.terminate()
+
+
+def _solve_chunk_local(frames, cfg, iters, n):
+    import ddlink_oracle as orc
+    const = orc.qam(cfg["mod"])
+    for i in range(n):
+        taps, y, lam = frames[i % len(frames)]
+        orc.receive(taps, y, cfg["M"], cfg["N"], iters, lam, const)
+
+
+def sample_frames(arm, seconds):
+    """Frames per step so one step is ~`seconds` of CPU work in total."""
+    return max(arm.cores, int(seconds / max(arm.frame_s, 1e-4)))
+
+
+# ------------------------------------------------------------------ reference arm
+def run_reference(args, cfg):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    arm = CpuArm(cfg, args.snr, args.iters)
+    MN = cfg["M"] * cfg["N"]
+    per_step = max(arm.cores, int(min(args.cpu_seconds, 8.0) / arm.frame_s))
+    for _ in range(args.warmup):
+        arm.run(arm.cores)
+    total_frames, total_t = 0, 0.0
+    for _ in range(args.steps):
+        n, dt = arm.run(per_step)
+        total_frames += n
+        total_t += dt
+    arm.close()
+    value = total_frames * MN / total_t
+    sample = (f"{per_step} frames per step (~{per_step * arm.frame_s:.1f} s CPU work), "
+              f"{arm.cores} processes, OPENBLAS_NUM_THREADS=1")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "symbols/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * total_t / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "fp64 (complex128)", "data": "synthetic (host numpy, Veh-A taps)",
+        "config": _config_json(args, cfg),
+        "cpu_baseline": {"value": value, "unit": "symbols/s", "cores": arm.cores, "kind": "port",
+                         "sample": sample},
+        "e2e": {"value": value, "unit": "symbols/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "latency": {"p50_ms": 1e3 * arm.frame_s, "what": "single-core per-frame time of the port"},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def _config_json(args, cfg):
+    B = args.batch or cfg["batch"]
+    return {"workload": f"{args.config}: OTFS M={cfg['M']} N={cfg['N']} P={cfg['P']} {cfg['mod']} "
+                        f"batch {B} frames/GPU, Xi={args.iters}, {args.snr:g} dB",
+            "M": cfg["M"], "N": cfg["N"], "P": cfg["P"], "modulation": cfg["mod"], "batch_per_gpu": B,
+            "iterations": args.iters, "snr_db": args.snr, "nu_max_hz": cfg["nu"],
+            "parallelism": f"frame-sharded x{args.gpus}, no collective on the solve path",
+            "l2": "inputs exceed L2 (y alone is batch*MN*8 B per GPU)"}
+
+
+# ------------------------------------------------------------------ our arm
+def main():
+    args = parse()
+    cfg = CONFIGS[args.config]
+    if args.impl == "reference":
+        run_reference(args, cfg)
+        return
+
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    import ctypes as C
+    import paper_2604_02266_b200 as pkg
+    from paper_2604_02266_b200 import _native as nat
+    from paper_2604_02266_b200.synth import make_frames
+
+    M, N, P = cfg["M"], cfg["N"], cfg["P"]
+    MN = M * N
+    B = args.batch or cfg["batch"]
+    bps = BPS[cfg["mod"]]
+    s = pkg.SsCgaSolver(M, N, args.iters, precision="fp32", modulation=cfg["mod"])
+    fb = make_frames(s, B, snr_db=args.snr, nu_max_hz=cfg["nu"], modulation=cfg["mod"], seed=1000 + rank,
+                     n_paths=P)
+    out = s.alloc(B, llr=True, trace=True, bit_errors=True)
+    stream = torch.cuda.current_stream()
+
+    def step():
+        s.solve(fb.y, fb.paths, fb.lam, tx_labels=fb.tx_labels, out=out)
+
+    def barrier():
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(max(3, args.warmup)):
+        step()
+    barrier()
+    sampler = ClockSampler(local)
+    sampler.start()
+    time.sleep(0.3)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    barrier()
+    e0.record(stream)
+    for _ in range(args.steps):
+        step()
+    e1.record(stream)
+    barrier()
+    clocks = sampler.stop()
+    ms = e0.elapsed_time(e1)
+    if world > 1:
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    ms_step = ms / args.steps
+    value = world * B * MN * args.steps / (ms * 1e-3)
+    bit_errors = int(out.bit_errors.sum().item())
+    ber = bit_errors / (B * MN * bps)
+
+    # ---- FP32 peak of this box (FFMA / FFMA2 probe), HBM peak from MEASURED_PEAKS
+    scratch = torch.empty(148 * 8, dtype=torch.float32, device="cuda")
+    sms = torch.cuda.get_device_properties(0).multi_processor_count
+    lib = nat.load()
+    peak_tflops = 0.0
+    probe = {}
+    for mode in (0, 1):
+        blocks, iters = sms * 8, 2000
+        for _ in range(2):
+            nat.check(lib.ddb_probe_fp32(mode, blocks, iters, C.c_void_p(scratch.data_ptr()),
+                                         C.c_void_p(stream.cuda_stream)), "probe")
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        nat.check(lib.ddb_probe_fp32(mode, blocks, iters, C.c_void_p(scratch.data_ptr()),
+                                     C.c_void_p(stream.cuda_stream)), "probe")
+        b.record(stream)
+        b.synchronize()
+        tf = blocks * 256 * iters * 256 * 2 / (a.elapsed_time(b) * 1e-3) / 1e12
+        probe["ffma" if mode == 0 else "ffma2"] = tf
+        peak_tflops = max(peak_tflops, tf)
+    peaks_path = ROOT / "MEASURED_PEAKS.json"
+    hbm_peak = json.loads(peaks_path.read_text())["hbm_gbs"] if peaks_path.exists() else 6650.0
+    P_avg = float((fb.paths.offsets[-1] - fb.paths.offsets[0]).item()) / B
+    fl = flops_per_frame(P_avg, MN, args.iters)
+    achieved = B * fl / (ms_step * 1e-3) / 1e12
+    io_bytes = B * (8 * MN + 8 * MN + 4 * bps * MN + MN + MN + 16 * P_avg)  # y, x, llr, labels, tx, taps
+    hbm_gbs = io_bytes / (ms_step * 1e-3) / 1e9
+    traffic = None
+    ncu_sum = ROOT / "profiles" / f"ncu_{args.config}.json"
+    if ncu_sum.exists():
+        traffic = json.loads(ncu_sum.read_text()).get("dram_bytes_per_launch")
+
+    # ---- single-frame latency: CUDA graph of a batch-1 solve, replayed
+    latency = None
+    if not args.no_latency and rank == 0:
+        y1 = fb.y[:1].clone()
+        lam1 = fb.lam[:1].clone()
+        tx1 = fb.tx_labels[:1].clone()
+        paths1 = pkg.PathBatch(fb.paths.offsets[:2].clone(), fb.paths.k, fb.paths.l, fb.paths.gain)
+        o1 = s.alloc(1, llr=True, trace=True, bit_errors=True)
+        side = torch.cuda.Stream()
+        with torch.cuda.stream(side):
+            for _ in range(3):
+                s.solve(y1, paths1, lam1, tx_labels=tx1, out=o1, stream=side)
+        side.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=side):
+            s.solve(y1, paths1, lam1, tx_labels=tx1, out=o1, stream=side)
+        torch.cuda.synchronize()
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+              for _ in range(args.lat_runs)]
+        for a, b in ev:
+            a.record()
+            g.replay()
+            b.record()
+        torch.cuda.synchronize()
+        lat = sorted(a.elapsed_time(b) for a, b in ev)
+        latency = {"p50_ms": lat[len(lat) // 2], "p99_ms": lat[int(len(lat) * 0.99)],
+                   "max_ms": lat[-1], "runs": len(lat), "frame_duration_ms": 1e3 * N / 30e3,
+                   "what": "batch-1 solve (one fused launch, CUDA graph replay), device events"}
+
+    # ---- end to end from pinned host buffers (HostPipeline)
+    e2e = None
+    if not args.no_e2e:
+        pipe = pkg.HostPipeline(s, chunk=512, depth=2)
+        hy = fb.y.cpu().pin_memory()
+        hl = fb.lam.cpu().pin_memory()
+        ht = fb.tx_labels.cpu().pin_memory()
+        hp = tuple(t.cpu().pin_memory() for t in (fb.paths.offsets, fb.paths.k, fb.paths.l, fb.paths.gain))
+        lab_h = torch.empty(B, MN, dtype=torch.uint8).pin_memory()
+        err_h = torch.empty(B, dtype=torch.int32).pin_memory()
+        pipe.run(hy, hp, hl, ht, lab_h, err_h)
+        k2 = max(1, min(args.steps, 5))
+        barrier()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(pipe.h2d)
+        for _ in range(k2):
+            pipe.run(hy, hp, hl, ht, lab_h, err_h)
+        b.record(pipe.d2h)
+        b.synchronize()
+        ems = a.elapsed_time(b)
+        if world > 1:
+            t = torch.tensor([ems], device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ems = float(t.item())
+        h2d = hy.numel() * hy.element_size() + hl.numel() * hl.element_size() + ht.numel() + \
+            sum(t.numel() * t.element_size() for t in hp)
+        d2h = lab_h.numel() + err_h.numel() * 4
+        e2e = {"value": world * B * MN * k2 / (ems * 1e-3), "unit": "symbols/s", "h2d_bytes_per_step": h2d,
+               "d2h_bytes_per_step": d2h, "steps": k2, "ms_per_step": ems / k2,
+               "what": "HostPipeline: pinned H2D of y/taps/lam/tx labels, fused solve, D2H labels + bit errors"}
+        assert torch.equal(err_h, out.bit_errors.cpu())
+
+    # ---- CPU baseline (oracle port on the host cores), rank 0 at N=1 only
+    cpu = None
+    if not args.no_cpu and rank == 0 and world == 1:
+        arm = CpuArm(cfg, args.snr, args.iters)
+        n = sample_frames(arm, args.cpu_seconds)
+        done, dt = arm.run(n)
+        arm.close()
+        cpu = {"value": done * MN / dt, "unit": "symbols/s", "cores": arm.cores, "kind": "port",
+               "sample": f"{done} cfg frames (numpy oracle port of build_ss_channel->cga_equalize->"
+                         f"hard_demod), {arm.cores} processes, {dt:.1f} s wall",
+               "p50_frame_ms_1core": 1e3 * arm.frame_s}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "symbols/s", "n_gpus": world, "steps": args.steps,
+            "warmup": max(3, args.warmup), "ms_per_step": ms_step, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "fp32",
+            "data": "synthetic (device-generated Veh-A taps, uniform labels, y = Hx + AWGN)",
+            "config": _config_json(args, cfg),
+            "latency": latency,
+            "roofline": {"bound": "fp32", "achieved": achieved, "peak": peak_tflops, "unit": "TFLOP/s",
+                         "frac": achieved / peak_tflops, "traffic": traffic,
+                         "flops_per_frame": fl, "peak_source": f"FFMA probe on this GPU {probe}"},
+            "roofline_hbm": {"bound": "hbm", "achieved": hbm_gbs, "peak": hbm_peak, "unit": "GB/s",
+                             "frac": hbm_gbs / hbm_peak, "bytes_per_frame": io_bytes / B},
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": args.steps,
+            "clocks": clocks,
+            "plan": s.plan(),
+            "ber": ber,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,161 @@
+/*
+ * ddb.h — C ABI of the B200-native SS-CGA delay-Doppler equalizer.
+ *
+ * Every entry point takes plain device pointers and sizes (no torch types),
+ * is non-blocking on the caller's CUDA stream, allocates nothing on the hot
+ * path, and returns a ddb_status; on failure ddb_last_error() returns a
+ * thread-local human-readable message.
+ *
+ * Reference interface each entry point replaces (paths are relative to the
+ * reference package, /root/reference/pkg/src/ddlink):
+ *
+ *   ddb_sscga_solve      equalize.py:43-77   cga_equalize(ch, y_dd, cfg)
+ *                        (fused with grid.py:172-183 hard_demod, the
+ *                        harness.py:198 bit-error count, and the build-defined
+ *                        max-log LLR soft demod that north_star adds)
+ *   ddb_ss_apply         sparse.py:147-160   ss_mvm / ss_mvm_hermitian, matrix-free
+ *   ddb_build_tables     sparse.py:124-144   build_ss_channel (+ forward_index 91-96,
+ *                                            inverse_index 99-104, coefficient 107-121)
+ *   ddb_ss_mvm_tables    sparse.py:147-160   ss_mvm / ss_mvm_hermitian on explicit tables
+ *   ddb_hard_demod       grid.py:172-183     hard_demod (nearest point, lowest label on ties)
+ *   ddb_qam_demod        grid.py:98-183      Gray-QAM slicer + max-log LLR (build-defined)
+ *   ddb_detect_paths     sparse.py:69-88     detect_paths (strict relative threshold,
+ *                                            stable descending-magnitude order)
+ *
+ * Layouts (identical to the reference's numpy layouts):
+ *   complex values are interleaved (re, im) of the problem dtype;
+ *   DD vectors are column-major flattened frames, q = l*M + k (grid.py:86-95);
+ *   per-frame paths are CSR: path_offsets[b] .. path_offsets[b+1].
+ */
+#ifndef DDB_H
+#define DDB_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define DDB_ABI_VERSION 1
+
+typedef enum {
+  DDB_OK = 0,
+  DDB_ERR_INVALID = 1,     /* bad argument (null pointer, negative size, ...)  */
+  DDB_ERR_SHAPE = 2,       /* grid geometry rejected (odd M/N, too small, ...)  */
+  DDB_ERR_UNSUPPORTED = 3, /* valid request outside what the build supports    */
+  DDB_ERR_CUDA = 4,        /* CUDA runtime / launch failure                      */
+  DDB_ERR_WORKSPACE = 5    /* workspace missing or too small                     */
+} ddb_status;
+
+typedef enum { DDB_F32 = 0, DDB_F64 = 1 } ddb_dtype;
+
+/* frame status bits written to ddb_sscga_outputs.status */
+#define DDB_FRAME_EMPTY_CHANNEL 0x1u /* P == 0: EmptyChannel (sparse.py:23-24, 126-127) */
+#define DDB_FRAME_EXACT_CONVERGED 0x2u /* curvature exactly zero (equalize.py:64-67) */
+
+/* One batch of independent frames sharing one grid.  All pointers are device
+ * pointers.  Replaces the (ch, y_dd, cfg) triple of cga_equalize
+ * (equalize.py:43): ch.paths -> CSR path arrays, y_dd -> y row, cfg.lam -> lam,
+ * cfg.iterations -> iterations. */
+typedef struct {
+  int32_t batch;                /* number of frames B (>= 0)                      */
+  int32_t M, N;                 /* grid (grid.py:14-31): even, >= 2                */
+  int32_t iterations;           /* fixed CG iteration count Xi (>= 1)              */
+  int32_t dtype;                /* ddb_dtype of y, gains, lam, x, c_norm           */
+  const int32_t* path_offsets;  /* [B+1] CSR offsets into the path arrays          */
+  const int32_t* path_k;        /* [n_paths] absolute delay index k_p in [0, M)    */
+  const int32_t* path_l;        /* [n_paths] absolute Doppler index l_p in [0, N)  */
+  const void* path_gain;        /* [n_paths] complex gain h_p                      */
+  const void* y;                /* [B, M*N] complex received DD vector             */
+  const void* lam;              /* [B] real ridge term (1/SNR, 0 = none)           */
+} ddb_sscga_problem;
+
+typedef struct {
+  void* x;                  /* [B, M*N] complex equalized symbols (required)        */
+  void* c_norm;             /* [B, iterations+1] real residual trace, or NULL;
+                               entries past iterations_done are written as 0     */
+  int32_t* iterations_done; /* [B] completed iterations (= len(c_norm)-1), or NULL   */
+  uint8_t* status;          /* [B] DDB_FRAME_* bits, or NULL                        */
+  void* snapshots;          /* [B, iterations, M*N] complex x after each iteration
+                               (CgaConfig.profile, equalize.py:74-76), or NULL   */
+  /* fused demod epilogue; bits_per_symbol == 0 disables it */
+  int32_t bits_per_symbol;  /* 0, 2 (QPSK), 4 (16-QAM), 6 (64-QAM, build extension) */
+  uint8_t* labels;          /* [B, M*N] hard-decision labels (bits MSB first), or NULL */
+  float* llr;               /* [B, M*N, bits] max-log LLRs (>0 favours bit 0), or NULL */
+  const void* noise_var;    /* [B] real LLR noise variance, or NULL (-> lam; 1 if 0) */
+  const uint8_t* tx_labels; /* [B, M*N] transmitted labels, or NULL                 */
+  int32_t* bit_errors;      /* [B] Hamming distance rx vs tx bits (needs tx_labels) */
+} ddb_sscga_outputs;
+
+/* Launch plan chosen for a grid/dtype (exposed for tests and tooling). */
+typedef struct {
+  int32_t cluster;           /* CTAs per frame (thread-block cluster size)          */
+  int32_t cols_per_cta;      /* Doppler columns owned by each CTA (N / cluster)     */
+  int32_t cols_per_thread;   /* columns per thread (each thread owns one delay row) */
+  int32_t threads;           /* threads per CTA                                     */
+  int32_t smem_bytes;        /* dynamic shared memory per CTA                       */
+  int32_t ctas_per_sm;       /* occupancy reported by the CUDA runtime (0 on CPU)   */
+} ddb_plan;
+
+/* ---- library ------------------------------------------------------------ */
+int32_t ddb_abi_version(void);
+const char* ddb_last_error(void);
+const char* ddb_build_info(void);
+
+/* ---- planning / workspace ----------------------------------------------- */
+int32_t ddb_sscga_plan(int32_t M, int32_t N, int32_t dtype, ddb_plan* out);
+size_t ddb_sscga_workspace_bytes(const ddb_sscga_problem* prob);
+
+/* ---- fused solve: coefficients on the fly + fixed-Xi CG + demod ---------- */
+int32_t ddb_sscga_solve(const ddb_sscga_problem* prob, const ddb_sscga_outputs* out,
+                        void* workspace, size_t workspace_bytes, void* stream);
+
+/* ---- matrix-free operator: out = H v (hermitian=0) or H^H v (hermitian=1),
+ *      batched over prob->batch frames; v is prob->y.  (sparse.py:147-160) */
+int32_t ddb_ss_apply(const ddb_sscga_problem* prob, void* out, int32_t hermitian,
+                     void* stream);
+
+/* ---- table materialisation, fp64 only (sparse.py:124-144):
+ *      fwd_coef/herm_coef complex128 [P, MN], fwd_col/herm_row int32 [P, MN] */
+int32_t ddb_build_tables(int32_t M, int32_t N, int32_t n_paths, const int32_t* path_k,
+                         const int32_t* path_l, const void* path_gain, void* fwd_coef,
+                         int32_t* fwd_col, void* herm_coef, int32_t* herm_row,
+                         void* stream);
+
+/* ---- table-driven MVM, fp64 (sparse.py:147-160):
+ *      u[q] = sum_p coef[p, q] * v[index[p, q]] */
+int32_t ddb_ss_mvm_tables(int32_t size, int32_t n_paths, const void* coef,
+                          const int32_t* index, const void* v, void* u, void* stream);
+
+/* ---- nearest-point hard demod over an arbitrary constellation table
+ *      (grid.py:172-183); ties go to the lowest label.  x, points in dtype. */
+int32_t ddb_hard_demod(int64_t count, int32_t dtype, const void* x, const void* points,
+                       int32_t n_points, int32_t* labels, void* stream);
+
+/* ---- Gray-QAM slicer + max-log LLR on the reference's constellations
+ *      (grid.py:98-154; 64-QAM is a build extension).  x is complex dtype
+ *      [count]; noise_var is a scalar; labels/llr may be NULL. */
+int32_t ddb_qam_demod(int64_t count, int32_t dtype, const void* x, int32_t bits_per_symbol,
+                      double noise_var, uint8_t* labels, float* llr, void* stream);
+
+/* ---- path detection (sparse.py:69-88), fp64: heff complex128 [B, M, N]
+ *      (row-major k, l as the reference's (M, N) frame).  Writes per-frame
+ *      counts and up to max_paths taps per frame in descending |h| order
+ *      (stable w.r.t. row-major position).  count[b] > max_paths means the
+ *      frame was truncated. */
+int32_t ddb_detect_paths(int32_t batch, int32_t M, int32_t N, const void* heff, double theta,
+                         int32_t max_paths, int32_t* count, int32_t* path_k,
+                         int32_t* path_l, void* path_gain, void* stream);
+
+/* ---- measurement helper (not a reference interface): FP32 FMA throughput
+ *      probe used by bench.py to state the measured FP32 roofline.  Launches
+ *      blocks x 256 threads, each doing iters x 256 FMAs (mode 0: FFMA,
+ *      mode 1: packed FFMA2).  scratch: device float[blocks]. */
+int32_t ddb_probe_fp32(int32_t mode, int32_t blocks, int32_t iters, float* scratch, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* DDB_H */

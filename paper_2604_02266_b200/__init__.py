@@ -1,0 +1,46 @@
+"""B200-native SS-CGA delay-Doppler equalizer (drop-in for ddlink's hot path).
+
+Reference: arxiv/paper_2604_02266, package `ddlink` (/root/reference/pkg).
+The drop-in names below keep the reference's signatures, layouts and errors;
+their arithmetic runs in hand-written sm_100a CUDA kernels (libddb.so, C ABI
+in include/ddb.h).  `SsCgaSolver` is the batched device API.
+"""
+
+from .batch import HostPipeline, PathBatch, SolveResult, SsCgaSolver, bits_per_symbol
+from .equalize import CgaConfig, CgaTrace, cga_equalize, get_precision, set_precision
+from .grid import (
+    Constellation,
+    GridConfig,
+    ber,
+    check_frame,
+    check_signal,
+    flatten,
+    hard_demod,
+    make_constellation,
+    make_constellation_ext,
+    modulate,
+    unflatten,
+)
+from .sparse import (
+    DominantPath,
+    EmptyChannel,
+    StructuredSparseChannel,
+    build_ss_channel,
+    coefficient,
+    detect_paths,
+    forward_index,
+    inverse_index,
+    ss_mvm,
+    ss_mvm_hermitian,
+)
+
+__all__ = [
+    "HostPipeline", "PathBatch", "SolveResult", "SsCgaSolver", "bits_per_symbol",
+    "CgaConfig", "CgaTrace", "cga_equalize", "get_precision", "set_precision",
+    "Constellation", "GridConfig", "ber", "check_frame", "check_signal", "flatten", "hard_demod",
+    "make_constellation", "make_constellation_ext", "modulate", "unflatten",
+    "DominantPath", "EmptyChannel", "StructuredSparseChannel", "build_ss_channel", "coefficient",
+    "detect_paths", "forward_index", "inverse_index", "ss_mvm", "ss_mvm_hermitian",
+]
+
+__version__ = "0.1.0"

@@ -1,0 +1,285 @@
+// C ABI (include/ddb.h): argument validation, launch planning, error state.
+#include <cstdarg>
+#include <cstdio>
+#include <string>
+
+#include "../../include/ddb.h"
+#include "internal.h"
+
+namespace {
+
+thread_local std::string g_err;
+
+int32_t fail(int32_t code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return code;
+}
+
+int32_t cuda_fail(cudaError_t e, const char* where) {
+  return fail(DDB_ERR_CUDA, "%s: %s (%s)", where, cudaGetErrorString(e), cudaGetErrorName(e));
+}
+
+int32_t ok() {
+  g_err.clear();
+  return DDB_OK;
+}
+
+int32_t check_grid(int32_t M, int32_t N) {
+  // GridConfig.__post_init__ (grid.py:23-29)
+  if (M < 2 || N < 2) return fail(DDB_ERR_SHAPE, "grid must be at least 2x2, got (%d,%d)", M, N);
+  if ((M & 1) || (N & 1))
+    return fail(DDB_ERR_SHAPE, "M and N must be even so the pilot sits on a bin center, got (%d,%d)", M, N);
+  if ((long long)M * N >= (1LL << 29)) return fail(DDB_ERR_UNSUPPORTED, "grid too large: M*N=%lld", (long long)M * N);
+  return DDB_OK;
+}
+
+int smem_optin() {
+  int dev = 0, v = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess ||
+      cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev) != cudaSuccess) {
+    cudaGetLastError();
+    return 232448;  // sm_100: 227 KiB opt-in per block
+  }
+  return v;
+}
+
+// Smallest cluster whose CTAs can hold their column slice of p, u and x in
+// shared memory; then the widest per-thread column run that keeps at least
+// 256 threads per CTA within the register file.
+int32_t make_plan(int32_t M, int32_t N, int32_t dtype, ddb::LaunchShape* s) {
+  const int eb = dtype == DDB_F64 ? 8 : 4;
+  const int cap = smem_optin();
+  const int lcmax = dtype == DDB_F64 ? 8 : 16;
+  for (int C = 1; C <= 16; C *= 2) {
+    if (N % C) continue;
+    const int lcta = N / C;
+    const size_t smem = ddb::sscga_smem_bytes(M, N, C, eb);
+    if (smem > (size_t)cap) continue;
+    const int target = M * lcta < 256 ? M * lcta : 256;
+    int best = 0;
+    for (int lc = lcmax; lc >= 1; lc /= 2) {
+      if (lcta % lc) continue;
+      const int active = M * (lcta / lc);
+      const int threads = (active + 31) / 32 * 32;
+      if (threads > ddb::sscga_max_threads(eb, lc)) continue;
+      if (active >= target) { best = lc; break; }
+    }
+    if (!best) continue;
+    s->cluster = C;
+    s->lcta = lcta;
+    s->lc = best;
+    s->threads = (M * (lcta / best) + 31) / 32 * 32;
+    s->smem = (int)smem;
+    return DDB_OK;
+  }
+  return fail(DDB_ERR_UNSUPPORTED,
+              "grid (%d,%d) %s: CG state does not fit a 16-CTA cluster's shared memory", M, N,
+              dtype == DDB_F64 ? "fp64" : "fp32");
+}
+
+}  // namespace
+
+extern "C" {
+
+int32_t ddb_abi_version(void) { return DDB_ABI_VERSION; }
+
+const char* ddb_last_error(void) { return g_err.c_str(); }
+
+const char* ddb_build_info(void) {
+#define DDB_STR2(x) #x
+#define DDB_STR(x) DDB_STR2(x)
+  static const char info[] = "ddb sm_100a; nvcc " DDB_STR(__CUDACC_VER_MAJOR__) "." DDB_STR(
+      __CUDACC_VER_MINOR__) "." DDB_STR(__CUDACC_VER_BUILD__);
+  return info;
+}
+
+int32_t ddb_sscga_plan(int32_t M, int32_t N, int32_t dtype, ddb_plan* out) {
+  if (!out) return fail(DDB_ERR_INVALID, "null plan pointer");
+  if (dtype != DDB_F32 && dtype != DDB_F64) return fail(DDB_ERR_INVALID, "bad dtype %d", dtype);
+  int32_t r = check_grid(M, N);
+  if (r) return r;
+  ddb::LaunchShape s;
+  r = make_plan(M, N, dtype, &s);
+  if (r) return r;
+  out->cluster = s.cluster;
+  out->cols_per_cta = s.lcta;
+  out->cols_per_thread = s.lc;
+  out->threads = s.threads;
+  out->smem_bytes = s.smem;
+  out->ctas_per_sm = 0;
+  int n = 0;
+  int dev_count = 0;
+  if (cudaGetDeviceCount(&dev_count) == cudaSuccess && dev_count > 0) {
+    cudaError_t e = dtype == DDB_F64 ? ddb::sscga_occupancy<double>(s, &n) : ddb::sscga_occupancy<float>(s, &n);
+    if (e == cudaSuccess) out->ctas_per_sm = n;
+  }
+  cudaGetLastError();
+  return ok();
+}
+
+size_t ddb_sscga_workspace_bytes(const ddb_sscga_problem* prob) {
+  (void)prob;
+  return 0;  // the fused solve keeps all state on chip
+}
+
+int32_t ddb_sscga_solve(const ddb_sscga_problem* prob, const ddb_sscga_outputs* out, void* workspace,
+                        size_t workspace_bytes, void* stream) {
+  (void)workspace;
+  (void)workspace_bytes;
+  if (!prob || !out) return fail(DDB_ERR_INVALID, "null problem/outputs");
+  if (prob->batch < 0) return fail(DDB_ERR_INVALID, "negative batch");
+  if (prob->iterations < 1) return fail(DDB_ERR_INVALID, "need at least one iteration");  // equalize.py:26-27
+  if (prob->dtype != DDB_F32 && prob->dtype != DDB_F64) return fail(DDB_ERR_INVALID, "bad dtype %d", prob->dtype);
+  int32_t r = check_grid(prob->M, prob->N);
+  if (r) return r;
+  if (prob->batch == 0) return ok();
+  if (!prob->path_offsets || !prob->y || !prob->lam || !out->x)
+    return fail(DDB_ERR_INVALID, "null required pointer (path_offsets, y, lam, x)");
+  if (!prob->path_k || !prob->path_l || !prob->path_gain)
+    return fail(DDB_ERR_INVALID, "null path arrays");
+  const int bps = out->bits_per_symbol;
+  if (bps != 0 && bps != 2 && bps != 4 && bps != 6)
+    return fail(DDB_ERR_INVALID, "bits_per_symbol must be 0, 2, 4 or 6, got %d", bps);
+  if (out->bit_errors && (!out->tx_labels || bps == 0))
+    return fail(DDB_ERR_INVALID, "bit_errors needs tx_labels and bits_per_symbol > 0");
+  if ((out->labels || out->llr) && bps == 0)
+    return fail(DDB_ERR_INVALID, "labels/llr need bits_per_symbol > 0");
+  ddb::LaunchShape s;
+  r = make_plan(prob->M, prob->N, prob->dtype, &s);
+  if (r) return r;
+  ddb::SolveArgs a = {};
+  a.B = prob->batch;
+  a.M = prob->M;
+  a.N = prob->N;
+  a.MN = prob->M * prob->N;
+  a.K0 = prob->M / 2;
+  a.L0 = prob->N / 2;
+  a.iters = prob->iterations;
+  a.C = s.cluster;
+  a.Lcta = s.lcta;
+  a.active_threads = prob->M * (s.lcta / s.lc);
+  a.off = prob->path_offsets;
+  a.pk = prob->path_k;
+  a.pl = prob->path_l;
+  a.ph = prob->path_gain;
+  a.y = prob->y;
+  a.lam = prob->lam;
+  a.x = out->x;
+  a.cnorm = out->c_norm;
+  a.itdone = out->iterations_done;
+  a.status = out->status;
+  a.snaps = out->snapshots;
+  a.bps = bps;
+  a.labels = out->labels;
+  a.llr = out->llr;
+  a.nvar = out->noise_var;
+  a.txl = out->tx_labels;
+  a.berr = out->bit_errors;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  cudaError_t e = prob->dtype == DDB_F64 ? ddb::launch_sscga<double>(a, s, st) : ddb::launch_sscga<float>(a, s, st);
+  if (e != cudaSuccess) return cuda_fail(e, "sscga launch");
+  return ok();
+}
+
+int32_t ddb_ss_apply(const ddb_sscga_problem* prob, void* outp, int32_t hermitian, void* stream) {
+  if (!prob || !outp) return fail(DDB_ERR_INVALID, "null problem/output");
+  if (prob->batch < 0) return fail(DDB_ERR_INVALID, "negative batch");
+  if (prob->dtype != DDB_F32 && prob->dtype != DDB_F64) return fail(DDB_ERR_INVALID, "bad dtype %d", prob->dtype);
+  int32_t r = check_grid(prob->M, prob->N);
+  if (r) return r;
+  if (prob->batch == 0) return ok();
+  if (!prob->path_offsets || !prob->path_k || !prob->path_l || !prob->path_gain || !prob->y)
+    return fail(DDB_ERR_INVALID, "null input pointer");
+  if (prob->batch > 65535) return fail(DDB_ERR_UNSUPPORTED, "ss_apply batch > 65535");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  cudaError_t e = prob->dtype == DDB_F64
+                      ? ddb::launch_ss_apply<double>(prob->batch, prob->M, prob->N, prob->path_offsets,
+                                                     prob->path_k, prob->path_l, prob->path_gain, prob->y,
+                                                     outp, hermitian != 0, st)
+                      : ddb::launch_ss_apply<float>(prob->batch, prob->M, prob->N, prob->path_offsets,
+                                                    prob->path_k, prob->path_l, prob->path_gain, prob->y,
+                                                    outp, hermitian != 0, st);
+  if (e != cudaSuccess) return cuda_fail(e, "ss_apply launch");
+  return ok();
+}
+
+int32_t ddb_build_tables(int32_t M, int32_t N, int32_t n_paths, const int32_t* path_k, const int32_t* path_l,
+                         const void* path_gain, void* fwd_coef, int32_t* fwd_col, void* herm_coef,
+                         int32_t* herm_row, void* stream) {
+  int32_t r = check_grid(M, N);
+  if (r) return r;
+  if (n_paths < 0) return fail(DDB_ERR_INVALID, "negative path count");
+  if (n_paths == 0) return fail(DDB_ERR_INVALID, "no taps above threshold");  // EmptyChannel, sparse.py:126-127
+  if (!path_k || !path_l || !path_gain || !fwd_coef || !fwd_col || !herm_coef || !herm_row)
+    return fail(DDB_ERR_INVALID, "null pointer");
+  cudaError_t e = ddb::launch_build_tables(M, N, n_paths, path_k, path_l, path_gain, fwd_coef, fwd_col,
+                                           herm_coef, herm_row, static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "build_tables launch");
+  return ok();
+}
+
+int32_t ddb_ss_mvm_tables(int32_t size, int32_t n_paths, const void* coef, const int32_t* index, const void* v,
+                          void* u, void* stream) {
+  if (size < 0 || n_paths < 0) return fail(DDB_ERR_INVALID, "negative size");
+  if (!v || !u || (n_paths > 0 && (!coef || !index))) return fail(DDB_ERR_INVALID, "null pointer");
+  cudaError_t e = ddb::launch_mvm_tables(size, n_paths, coef, index, v, u, static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "mvm_tables launch");
+  return ok();
+}
+
+int32_t ddb_hard_demod(int64_t count, int32_t dtype, const void* x, const void* points, int32_t n_points,
+                       int32_t* labels, void* stream) {
+  if (count < 0 || n_points < 1) return fail(DDB_ERR_INVALID, "bad count/n_points");
+  if (dtype != DDB_F32 && dtype != DDB_F64) return fail(DDB_ERR_INVALID, "bad dtype %d", dtype);
+  if (count > 0 && (!x || !points || !labels)) return fail(DDB_ERR_INVALID, "null pointer");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  cudaError_t e = dtype == DDB_F64 ? ddb::launch_hard_demod<double>(count, x, points, n_points, labels, st)
+                                   : ddb::launch_hard_demod<float>(count, x, points, n_points, labels, st);
+  if (e != cudaSuccess) return cuda_fail(e, "hard_demod launch");
+  return ok();
+}
+
+int32_t ddb_qam_demod(int64_t count, int32_t dtype, const void* x, int32_t bits_per_symbol, double noise_var,
+                      uint8_t* labels, float* llr, void* stream) {
+  if (count < 0) return fail(DDB_ERR_INVALID, "negative count");
+  if (dtype != DDB_F32 && dtype != DDB_F64) return fail(DDB_ERR_INVALID, "bad dtype %d", dtype);
+  if (bits_per_symbol != 2 && bits_per_symbol != 4 && bits_per_symbol != 6)
+    return fail(DDB_ERR_INVALID, "bits_per_symbol must be 2, 4 or 6, got %d", bits_per_symbol);
+  if (count > 0 && !x) return fail(DDB_ERR_INVALID, "null input");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  cudaError_t e = dtype == DDB_F64
+                      ? ddb::launch_qam_demod<double>(count, x, bits_per_symbol, noise_var, labels, llr, st)
+                      : ddb::launch_qam_demod<float>(count, x, bits_per_symbol, noise_var, labels, llr, st);
+  if (e != cudaSuccess) return cuda_fail(e, "qam_demod launch");
+  return ok();
+}
+
+int32_t ddb_detect_paths(int32_t batch, int32_t M, int32_t N, const void* heff, double theta, int32_t max_paths,
+                         int32_t* count, int32_t* path_k, int32_t* path_l, void* path_gain, void* stream) {
+  if (batch < 0 || max_paths < 0) return fail(DDB_ERR_INVALID, "negative batch/max_paths");
+  if (!(theta >= 0)) return fail(DDB_ERR_INVALID, "theta must be nonnegative");  // sparse.py:77-78
+  int32_t r = check_grid(M, N);
+  if (r) return r;
+  if (batch == 0) return ok();
+  if (!heff || !count || (max_paths > 0 && (!path_k || !path_l || !path_gain)))
+    return fail(DDB_ERR_INVALID, "null pointer");
+  cudaError_t e = ddb::launch_detect_paths(batch, M, N, heff, theta, max_paths, count, path_k, path_l, path_gain,
+                                           static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "detect_paths launch");
+  return ok();
+}
+
+int32_t ddb_probe_fp32(int32_t mode, int32_t blocks, int32_t iters, float* scratch, void* stream) {
+  if ((mode != 0 && mode != 1) || blocks < 1 || iters < 1 || !scratch)
+    return fail(DDB_ERR_INVALID, "bad probe arguments");
+  cudaError_t e = ddb::launch_fp32_probe(mode, blocks, iters, scratch, static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "fp32 probe launch");
+  return ok();
+}
+
+}  // extern "C"

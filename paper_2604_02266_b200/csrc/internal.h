@@ -1,0 +1,78 @@
+// Internal (non-ABI) declarations shared by the ddb translation units.
+#pragma once
+
+#include <cstddef>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace ddb {
+
+// Everything the fused SS-CGA kernel needs for one batch (device pointers).
+struct SolveArgs {
+  int B, M, N, MN, K0, L0, iters;
+  int C;              // cluster size (CTAs per frame)
+  int Lcta;           // Doppler columns per CTA = N / C
+  int active_threads; // M * (Lcta / LC); blockDim is this rounded up to 32
+  int n_clusters;     // persistent clusters in the grid
+  const int* off;
+  const int* pk;
+  const int* pl;
+  const void* ph;
+  const void* y;
+  const void* lam;
+  void* x;
+  void* cnorm;
+  int* itdone;
+  uint8_t* status;
+  void* snaps;
+  int bps;
+  uint8_t* labels;
+  float* llr;
+  const void* nvar;
+  const uint8_t* txl;
+  int* berr;
+};
+
+struct LaunchShape {
+  int cluster, lcta, lc, threads, smem;
+};
+
+// Thread ceiling of the fused kernel instantiation (its __launch_bounds__):
+// per-thread column runs of >= 32 bytes of real data need > 64 registers,
+// so those instantiations cap at 512 threads.
+constexpr int sscga_max_threads(int elem_bytes, int lc) { return elem_bytes * lc >= 32 ? 512 : 1024; }
+
+// Shared-memory bytes of the fused kernel for a given shape.
+size_t sscga_smem_bytes(int M, int N, int C, int elem_bytes);
+
+template <typename T>
+cudaError_t launch_sscga(SolveArgs a, const LaunchShape& s, cudaStream_t st);
+
+template <typename T>
+cudaError_t sscga_occupancy(const LaunchShape& s, int* ctas_per_sm);
+
+template <typename T>
+cudaError_t launch_ss_apply(int B, int M, int N, const int* off, const int* pk, const int* pl,
+                            const void* ph, const void* v, void* out, bool herm, cudaStream_t st);
+
+cudaError_t launch_build_tables(int M, int N, int P, const int* pk, const int* pl, const void* ph,
+                                void* fwd_coef, int* fwd_col, void* herm_coef, int* herm_row,
+                                cudaStream_t st);
+cudaError_t launch_mvm_tables(int size, int P, const void* coef, const int* idx, const void* v,
+                              void* u, cudaStream_t st);
+template <typename T>
+cudaError_t launch_hard_demod(long long count, const void* x, const void* pts, int npts,
+                              int* labels, cudaStream_t st);
+template <typename T>
+cudaError_t launch_qam_demod(long long count, const void* x, int bps, double nvar,
+                             uint8_t* labels, float* llr, cudaStream_t st);
+cudaError_t launch_detect_paths(int B, int M, int N, const void* heff, double theta,
+                                int max_paths, int* count, int* pk, int* pl, void* ph,
+                                cudaStream_t st);
+
+}  // namespace ddb
+
+namespace ddb {
+// FP32 FMA throughput probe: blocks x 256 threads x iters x 256 FMAs.
+cudaError_t launch_fp32_probe(int mode, int blocks, int iters, float* out, cudaStream_t st);
+}  // namespace ddb

@@ -1,0 +1,190 @@
+"""Structured-sparse DD channel operator — drop-in for ddlink.sparse.
+
+Same names, signatures, array layouts (complex128 / int32 tables of shape
+(P, MN)) and errors as /root/reference/pkg/src/ddlink/sparse.py.  Every
+numeric step runs in the ddb CUDA library:
+
+  detect_paths      -> ddb_detect_paths   (sparse.py:69-88)
+  build_ss_channel  -> ddb_build_tables   (sparse.py:124-144)
+  forward_index / inverse_index / coefficient
+                    -> ddb_build_tables for the single tap (sparse.py:91-121)
+  ss_mvm / ss_mvm_hermitian
+                    -> ddb_ss_mvm_tables  (sparse.py:147-160), honouring
+                       arbitrary (e.g. perturbed) tables
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _native as nat
+from .grid import check_frame
+
+DENSE_GUARD = 4096
+
+
+class EmptyChannel(Exception):
+    """No taps survived thresholding; there is no channel to equalize against."""
+
+
+@dataclass(frozen=True)
+class DominantPath:
+    """One detected tap on the absolute grid (sparse.py:27-37)."""
+
+    k_p: int
+    l_p: int
+    gain: complex
+
+    def offsets(self, cfg):
+        return cfg.K0 - self.k_p, cfg.L0 - self.l_p
+
+
+@dataclass(frozen=True)
+class StructuredSparseChannel:
+    """Path-major tables for both product directions (sparse.py:40-66)."""
+
+    M: int
+    N: int
+    paths: tuple
+    fwd_coef: np.ndarray
+    fwd_col: np.ndarray
+    herm_coef: np.ndarray
+    herm_row: np.ndarray
+
+    @property
+    def P(self):
+        return len(self.paths)
+
+    @property
+    def size(self):
+        return self.M * self.N
+
+    def entries_per_direction(self):
+        return int(self.fwd_coef.size)
+
+
+def _dev():
+    if not torch.cuda.is_available():
+        raise RuntimeError("the structured-sparse operator runs on the CUDA device only (no CPU fallback)")
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+def _stream():
+    return C.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def _p(t):
+    return C.c_void_p(t.data_ptr())
+
+
+def _device_tables(paths, M: int, N: int):
+    dev = _dev()
+    P = len(paths)
+    k = torch.tensor([int(p.k_p) for p in paths], dtype=torch.int32, device=dev)
+    l = torch.tensor([int(p.l_p) for p in paths], dtype=torch.int32, device=dev)
+    g = torch.tensor(np.array([complex(p.gain) for p in paths], np.complex128), device=dev)
+    MN = M * N
+    fc = torch.empty(P, MN, dtype=torch.complex128, device=dev)
+    fi = torch.empty(P, MN, dtype=torch.int32, device=dev)
+    hc = torch.empty(P, MN, dtype=torch.complex128, device=dev)
+    hi = torch.empty(P, MN, dtype=torch.int32, device=dev)
+    nat.check(nat.load().ddb_build_tables(M, N, P, _p(k), _p(l), _p(g), _p(fc), _p(fi), _p(hc), _p(hi),
+                                          _stream()), "ddb_build_tables")
+    return fc, fi, hc, hi
+
+
+def _single_tap_tables(path, cfg):
+    fc, fi, hc, hi = _device_tables([path], cfg.M, cfg.N)
+    return fc[0].cpu().numpy(), fi[0].cpu().numpy(), hi[0].cpu().numpy()
+
+
+def _index(table: np.ndarray, q):
+    qa = np.asarray(q)
+    out = table[qa]
+    if qa.ndim == 0:
+        return int(out)
+    return out.astype(np.int64)
+
+
+def forward_index(path, q, cfg):
+    """Column feeding output q: 2D circular shift of q (sparse.py:91-96)."""
+    _, fi, _ = _single_tap_tables(path, cfg)
+    return _index(fi, q)
+
+
+def inverse_index(path, r, cfg):
+    """Output fed by column r (sparse.py:99-104)."""
+    _, _, hi = _single_tap_tables(path, cfg)
+    return _index(hi, r)
+
+
+def coefficient(path, q, cfg):
+    """Phase-corrected gain multiplying v[forward_index(path, q)] in row q (sparse.py:107-121)."""
+    fc, _, _ = _single_tap_tables(path, cfg)
+    qa = np.asarray(q)
+    out = fc[qa]
+    return complex(out) if qa.ndim == 0 else out
+
+
+def build_ss_channel(paths, cfg):
+    """Forward and Hermitian tables for the detected taps (sparse.py:124-144)."""
+    if len(paths) == 0:
+        raise EmptyChannel("no taps above threshold")
+    fc, fi, hc, hi = _device_tables(paths, cfg.M, cfg.N)
+    return StructuredSparseChannel(
+        M=cfg.M, N=cfg.N, paths=tuple(paths),
+        fwd_coef=fc.cpu().numpy(), fwd_col=fi.cpu().numpy(),
+        herm_coef=hc.cpu().numpy(), herm_row=hi.cpu().numpy(),
+    )
+
+
+def _mvm_tables(coef, index, v, size):
+    dev = _dev()
+    v = np.asarray(v)
+    if v.shape != (size,):
+        raise ValueError(f"vector length {v.shape} != {size}")
+    c = torch.as_tensor(np.ascontiguousarray(coef, dtype=np.complex128), device=dev)
+    i = torch.as_tensor(np.ascontiguousarray(index, dtype=np.int32), device=dev)
+    vv = torch.as_tensor(np.ascontiguousarray(v, dtype=np.complex128), device=dev)
+    u = torch.empty(size, dtype=torch.complex128, device=dev)
+    P = int(c.shape[0]) if c.dim() == 2 else 0
+    nat.check(nat.load().ddb_ss_mvm_tables(size, P, _p(c), _p(i), _p(vv), _p(u), _stream()),
+              "ddb_ss_mvm_tables")
+    return u.cpu().numpy()
+
+
+def ss_mvm(ch, v):
+    """u[q] = sum_p fwd_coef[p, q] * v[fwd_col[p, q]] (sparse.py:147-152)."""
+    return _mvm_tables(ch.fwd_coef, ch.fwd_col, v, ch.M * ch.N)
+
+
+def ss_mvm_hermitian(ch, v):
+    """u[r] = sum_p herm_coef[p, r] * v[herm_row[p, r]] (sparse.py:155-160)."""
+    return _mvm_tables(ch.herm_coef, ch.herm_row, v, ch.M * ch.N)
+
+
+def detect_paths(heff, theta, cfg):
+    """Keep |h| > theta*max|h|, sorted by descending magnitude, stable (sparse.py:69-88)."""
+    heff = check_frame(heff, cfg)
+    if theta < 0:
+        raise ValueError("theta must be nonnegative")
+    dev = _dev()
+    M, N = cfg.M, cfg.N
+    h = torch.as_tensor(np.ascontiguousarray(heff, dtype=np.complex128), device=dev)
+    cap = M * N
+    cnt = torch.empty(1, dtype=torch.int32, device=dev)
+    k = torch.empty(cap, dtype=torch.int32, device=dev)
+    l = torch.empty(cap, dtype=torch.int32, device=dev)
+    g = torch.empty(cap, dtype=torch.complex128, device=dev)
+    nat.check(nat.load().ddb_detect_paths(1, M, N, _p(h), float(theta), cap, _p(cnt), _p(k), _p(l), _p(g),
+                                          _stream()), "ddb_detect_paths")
+    n = int(cnt.item())
+    if n < 0:
+        raise nat.DdbError(nat.DDB_ERR_UNSUPPORTED, "ddb_detect_paths",
+                           "candidate list exceeds the per-frame shared-memory capacity")
+    kk, ll, gg = k[:n].cpu().numpy(), l[:n].cpu().numpy(), g[:n].cpu().numpy()
+    return [DominantPath(int(a), int(b), complex(c)) for a, b, c in zip(kk, ll, gg)]

@@ -1,0 +1,81 @@
+"""Synthetic frame batches for benchmarks and full-size property tests.
+
+Taps follow the reference's Veh-A geometry (channel.py:17-18, 62-85): six
+paths with the ITU delays rounded to delay bins (channel.py:46) and unit total
+power, uniform phases, Doppler nu_max cos(2 pi U) rounded to the Doppler grid,
+placed on the absolute grid at (K0 + delay, L0 + doppler) like the pilot
+estimate (pilot.py:1-6).  Data are uniform random constellation labels; the
+received vector is y = H x + n computed with the device operator
+(ddb_ss_apply), n ~ CN(0, mean|Hx|^2 / SNR) as in add_awgn (channel.py:99-111).
+Everything is generated on the GPU with torch's RNG (this is input
+generation, not the measured path).
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from .batch import PathBatch, SsCgaSolver
+from .grid import GridConfig, make_constellation_ext
+
+VEHA_DELAYS_US = (0.00, 0.31, 0.71, 1.09, 1.73, 2.51)
+VEHA_POWERS_DB = (0.0, -1.0, -9.0, -10.0, -15.0, -20.0)
+
+
+@dataclass
+class FrameBatch:
+    y: torch.Tensor          # [B, MN] complex
+    x: torch.Tensor          # [B, MN] complex transmitted symbols
+    tx_labels: torch.Tensor  # uint8 [B, MN]
+    paths: PathBatch
+    lam: torch.Tensor        # [B] real
+    snr_db: float
+
+
+def veha_paths(B: int, grid: GridConfig, nu_max_hz: float, gen: torch.Generator, device,
+               cdtype=torch.complex64, n_paths: int = 6) -> PathBatch:
+    delays = np.round(np.asarray(VEHA_DELAYS_US[:n_paths]) * 1e-6 * grid.B).astype(np.int64)
+    if delays.max() >= grid.M:
+        raise ValueError("Veh-A delay spread exceeds the delay period; increase M")
+    powers = 10.0 ** (np.asarray(VEHA_POWERS_DB[:n_paths]) / 10.0)
+    mags = torch.as_tensor(np.sqrt(powers / powers.sum()), device=device, dtype=torch.float64)
+    phase = torch.rand(B, n_paths, generator=gen, device=device, dtype=torch.float64) * 2 * np.pi
+    u = torch.rand(B, n_paths, generator=gen, device=device, dtype=torch.float64)
+    dop = torch.round(nu_max_hz * torch.cos(2 * np.pi * u) / grid.delta_nu).to(torch.int64)
+    dop = dop.clamp(-(grid.N // 2) + 1, grid.N // 2 - 1)
+    k = (grid.K0 + torch.as_tensor(delays, device=device)[None, :]).expand(B, n_paths) % grid.M
+    l = (grid.L0 + dop) % grid.N
+    gain = torch.polar(mags[None, :].expand(B, n_paths), phase)
+    off = torch.arange(0, (B + 1) * n_paths, n_paths, device=device, dtype=torch.int32)
+    return PathBatch(off, k.reshape(-1).to(torch.int32).contiguous(), l.reshape(-1).to(torch.int32).contiguous(),
+                     gain.reshape(-1).to(cdtype).contiguous())
+
+
+def make_frames(solver: SsCgaSolver, B: int, snr_db: float = 25.0, nu_max_hz: float = 100.0,
+                modulation: str = "qam16", seed: int = 0, n_paths: int = 6, delta_f: float = 30e3) -> FrameBatch:
+    dev = solver.device
+    grid = GridConfig(solver.M, solver.N, delta_f)
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(seed)
+    const = make_constellation_ext(modulation)
+    pts = torch.as_tensor(const.points, device=dev).to(solver.cdtype)
+    labels = torch.randint(0, len(const.points), (B, solver.MN), generator=gen, device=dev, dtype=torch.int64)
+    x = pts[labels].contiguous()
+    paths = veha_paths(B, grid, nu_max_hz, gen, dev, solver.cdtype, n_paths)
+    hx = solver.apply(x, paths)
+    if np.isinf(snr_db):
+        y = hx
+        lam = torch.zeros(B, dtype=solver.rdtype, device=dev)
+    else:
+        snr = 10.0 ** (snr_db / 10.0)
+        power = (hx.real ** 2 + hx.imag ** 2).mean(dim=1, keepdim=True)
+        sigma = torch.sqrt(power / snr / 2)
+        noise = torch.complex(torch.randn(B, solver.MN, generator=gen, device=dev, dtype=solver.rdtype),
+                              torch.randn(B, solver.MN, generator=gen, device=dev, dtype=solver.rdtype))
+        y = (hx + sigma * noise).contiguous()
+        lam = torch.full((B,), 1.0 / snr, dtype=solver.rdtype, device=dev)
+    return FrameBatch(y=y, x=x, tx_labels=labels.to(torch.uint8).contiguous(), paths=paths, lam=lam,
+                      snr_db=snr_db)

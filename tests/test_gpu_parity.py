@@ -1,0 +1,420 @@
+"""GPU parity: the CUDA path (through libddb.so's C ABI) against the oracle and
+the reference's golden vectors.  Tolerances (north_star): fp32 x_hat within
+1e-4 relative L2 of the fp64 reference, identical CG iteration counts, hard
+decisions identical except inside the fp64 tie band (decision margin < 1e-5);
+the fp64 instantiation must meet the reference's own float64 tolerances.
+"""
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+import ddlink_oracle as orc  # noqa: E402
+from conftest import load_golden  # noqa: E402
+
+TIE_BAND = 1e-5
+REL_L2_FP32 = 1e-4
+
+
+@pytest.fixture(scope="module")
+def pkg():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2604_02266_b200 as p
+    from paper_2604_02266_b200 import _native
+    _native.load()
+    return p
+
+
+def frame_taps(d, f):
+    a, b = int(d["path_off"][f]), int(d["path_off"][f + 1])
+    return [orc.Tap(int(k), int(l), complex(g)) for k, l, g in zip(d["path_k"][a:b], d["path_l"][a:b], d["path_g"][a:b])]
+
+
+def solver_for(pkg, M, N, iters, precision, bps=0):
+    return pkg.SsCgaSolver(M, N, iters, precision=precision, modulation=bps or None)
+
+
+def paths_from_fixture(pkg, d, cdtype):
+    return pkg.PathBatch.from_arrays(d["path_off"], d["path_k"], d["path_l"], d["path_g"], cdtype=cdtype)
+
+
+def rel_l2(a, b):
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300))
+
+
+# ---------------------------------------------------------------- operator
+class TestTablesAndMvm:
+    def test_build_ss_channel_matches_reference_tables(self, pkg):
+        d = load_golden("tables")
+        for c in range(int(d["n_cases"])):
+            p = f"c{c}_"
+            M, N = (int(v) for v in d[p + "grid"])
+            taps = [pkg.DominantPath(int(k), int(l), complex(g))
+                    for k, l, g in zip(d[p + "tap_k"], d[p + "tap_l"], d[p + "tap_g"])]
+            ch = pkg.build_ss_channel(taps, pkg.GridConfig(M, N))
+            np.testing.assert_array_equal(ch.fwd_col, d[p + "fwd_col"])
+            np.testing.assert_array_equal(ch.herm_row, d[p + "herm_row"])
+            np.testing.assert_allclose(ch.fwd_coef, d[p + "fwd_coef"], rtol=0, atol=1e-12)
+            np.testing.assert_allclose(ch.herm_coef, d[p + "herm_coef"], rtol=0, atol=1e-12)
+            assert ch.entries_per_direction() == len(taps) * M * N
+            np.testing.assert_allclose(pkg.ss_mvm(ch, d[p + "v"]), d[p + "Hv"], atol=1e-10)
+            np.testing.assert_allclose(pkg.ss_mvm_hermitian(ch, d[p + "v"]), d[p + "HHv"], atol=1e-10)
+
+    def test_worked_index_example(self, pkg):
+        g = pkg.GridConfig(8, 2)
+        assert pkg.forward_index(pkg.DominantPath(4, 1, 1.0), 7, g) == 7
+        assert pkg.forward_index(pkg.DominantPath(0, 0, 0.5), 7, g) == 11
+        assert pkg.inverse_index(pkg.DominantPath(0, 0, 0.5), 11, g) == 7
+
+    def test_perturbed_tables_are_honoured(self, pkg):
+        d = load_golden("tables")
+        p = "c1_"
+        M, N = (int(v) for v in d[p + "grid"])
+        taps = [pkg.DominantPath(int(k), int(l), complex(g))
+                for k, l, g in zip(d[p + "tap_k"], d[p + "tap_l"], d[p + "tap_g"])]
+        ch = pkg.build_ss_channel(taps, pkg.GridConfig(M, N))
+        import dataclasses
+        bad = dataclasses.replace(ch, fwd_coef=ch.fwd_coef * (1 + 1e-6))
+        dev = np.abs(pkg.ss_mvm(bad, d[p + "v"]) - d[p + "Hv"]).max()
+        assert dev > 1e-9  # the oracle gate of harness.py:368-383 can fail
+
+    def test_empty_channel_raises(self, pkg):
+        with pytest.raises(pkg.EmptyChannel):
+            pkg.build_ss_channel([], pkg.GridConfig(8, 4))
+
+    def test_wrong_length_rejected(self, pkg):
+        g = pkg.GridConfig(8, 4)
+        ch = pkg.build_ss_channel([pkg.DominantPath(4, 2, 1.0)], g)
+        with pytest.raises(ValueError):
+            pkg.ss_mvm(ch, np.zeros(31))
+        with pytest.raises(ValueError):
+            pkg.ss_mvm_hermitian(ch, np.zeros(33))
+
+    @pytest.mark.parametrize("precision,tol", [("fp64", 1e-12), ("fp32", 2e-6)])
+    def test_matrix_free_apply_matches_tables(self, pkg, precision, tol):
+        d = load_golden("tables")
+        for c in range(int(d["n_cases"])):
+            p = f"c{c}_"
+            M, N = (int(v) for v in d[p + "grid"])
+            s = solver_for(pkg, M, N, 10, precision)
+            paths = pkg.PathBatch.from_arrays([0, len(d[p + "tap_k"])], d[p + "tap_k"], d[p + "tap_l"],
+                                              d[p + "tap_g"], cdtype=s.cdtype)
+            v = torch.as_tensor(d[p + "v"], device="cuda").to(s.cdtype)[None]
+            hv = s.apply(v, paths).cpu().numpy()[0]
+            hhv = s.apply(v, paths, hermitian=True).cpu().numpy()[0]
+            scale = np.abs(d[p + "Hv"]).max()
+            assert np.abs(hv - d[p + "Hv"]).max() <= tol * scale * 10
+            assert np.abs(hhv - d[p + "HHv"]).max() <= tol * scale * 10
+
+    def test_adjoint_identity_full_size(self, pkg):
+        from paper_2604_02266_b200.synth import make_frames
+        s = solver_for(pkg, 512, 32, 10, "fp64")
+        fb = make_frames(s, 4, snr_db=25.0, nu_max_hz=1000.0, seed=3)
+        g = torch.Generator(device="cuda").manual_seed(1)
+        u = torch.randn(4, s.MN, dtype=torch.complex128, device="cuda", generator=g)
+        v = torch.randn(4, s.MN, dtype=torch.complex128, device="cuda", generator=g)
+        lhs = (v.conj() * s.apply(u, fb.paths)).sum(dim=1)
+        rhs = (s.apply(v, fb.paths, hermitian=True).conj() * u).sum(dim=1)
+        assert torch.allclose(lhs, rhs, rtol=1e-12, atol=1e-9)
+
+
+# ---------------------------------------------------------------- drop-in CG
+class TestCgaDropIn:
+    def test_reference_cga_cases_fp64(self, pkg):
+        d = load_golden("cga")
+        pkg.set_precision("fp64")
+        for c in range(int(d["n_cases"])):
+            p = f"c{c}_"
+            M, N, iters, prof, ident = (int(v) for v in d[p + "meta"])
+            taps = [pkg.DominantPath(int(k), int(l), complex(g))
+                    for k, l, g in zip(d[p + "tap_k"], d[p + "tap_l"], d[p + "tap_g"])]
+            ch = pkg.build_ss_channel(taps, pkg.GridConfig(M, N))
+            x, tr = pkg.cga_equalize(ch, d[p + "y"], pkg.CgaConfig(iters, float(d[p + "lam"]), bool(prof)))
+            ref = d[p + "x"]
+            assert rel_l2(x, ref) < (1e-6 if iters > 10 else 1e-9), (c, rel_l2(x, ref))
+            cn_ref = d[p + "c_norm"]
+            assert len(tr.c_norm) == len(cn_ref)
+            assert tr.mvm_count == int(d[p + "mvm_count"])
+            assert tr.exact_converged == bool(d[p + "exact"])
+            cn = np.array(tr.c_norm)
+            assert np.all(np.abs(cn - cn_ref) <= 1e-8 * cn_ref[0] + 1e-6 * cn_ref)
+            if prof:
+                assert len(tr.snapshots) == len(tr.c_norm) - 1
+                np.testing.assert_allclose(np.stack(tr.snapshots), d[p + "snapshots"], atol=1e-9)
+            if ident:
+                np.testing.assert_allclose(x, d[p + "y"], atol=1e-12)
+                assert len(tr.c_norm) <= 3
+
+    def test_reference_cga_cases_fp32(self, pkg):
+        d = load_golden("cga")
+        pkg.set_precision("fp32")
+        try:
+            for c in range(int(d["n_cases"])):
+                p = f"c{c}_"
+                M, N, iters, prof, ident = (int(v) for v in d[p + "meta"])
+                if iters > 25:
+                    continue  # full-Krylov runs are fp64 territory
+                taps = [pkg.DominantPath(int(k), int(l), complex(g))
+                        for k, l, g in zip(d[p + "tap_k"], d[p + "tap_l"], d[p + "tap_g"])]
+                ch = pkg.build_ss_channel(taps, pkg.GridConfig(M, N))
+                x, tr = pkg.cga_equalize(ch, d[p + "y"], pkg.CgaConfig(iters, float(d[p + "lam"])))
+                assert rel_l2(x, d[p + "x"]) < REL_L2_FP32
+                assert abs(len(tr.c_norm) - len(d[p + "c_norm"])) <= 1
+        finally:
+            pkg.set_precision("fp64")
+
+    def test_identity_channel_exact_convergence(self, pkg):
+        g = pkg.GridConfig(8, 4)
+        frame = np.zeros((8, 4), complex)
+        frame[g.K0, g.L0] = 1.0
+        ch = pkg.build_ss_channel(pkg.detect_paths(frame, 0.5, g), g)
+        y = np.random.default_rng(0).normal(size=32) + 1j * np.random.default_rng(1).normal(size=32)
+        for prec in ("fp64", "fp32"):
+            pkg.set_precision(prec)
+            x, tr = pkg.cga_equalize(ch, y, pkg.CgaConfig(iterations=10, lam=0.0))
+            np.testing.assert_allclose(x, y, atol=1e-6 if prec == "fp32" else 1e-12)
+            assert tr.exact_converged and len(tr.c_norm) <= 3
+            assert not np.isnan(x).any()
+        pkg.set_precision("fp64")
+
+
+# ---------------------------------------------------------------- batched frames
+def _oracle_frames(d, const):
+    M, N, iters, _ = (int(v) for v in d["meta"])
+    xs, cns, labs, margins = [], [], [], []
+    for f in range(d["y"].shape[0]):
+        x, tr, lab, _ = orc.receive(frame_taps(d, f), d["y"][f].astype(np.complex128), M, N, iters,
+                                    float(d["lam"][f]), const)
+        xs.append(x)
+        cns.append(np.array(tr.c_norm))
+        labs.append(lab)
+        margins.append(orc.decision_margin(x, const))
+    return xs, cns, labs, margins
+
+
+@pytest.mark.parametrize("name", ["frames_cfg1", "frames_cfg2", "frames_cfg3", "frames_sweep", "frames_cfg4"])
+def test_batched_fp32_parity(pkg, name):
+    d = load_golden(name)
+    M, N, iters, b = (int(v) for v in d["meta"])
+    const = orc.qam({2: "qpsk", 4: "qam16"}[b])
+    s = solver_for(pkg, M, N, iters, "fp32", b)
+    paths = paths_from_fixture(pkg, d, s.cdtype)
+    y = torch.as_tensor(d["y"], device="cuda").contiguous()
+    tx = torch.as_tensor(d["tx_labels"], device="cuda")
+    res = s.solve(y, paths, torch.as_tensor(d["lam"]), tx_labels=tx, llr=True)
+    torch.cuda.synchronize()
+    x = res.x.cpu().numpy()
+    labels = res.labels.cpu().numpy()
+    xs, cns, labs, margins = _oracle_frames(d, const)
+    flips = 0
+    for f in range(len(xs)):
+        assert rel_l2(x[f], xs[f]) < REL_L2_FP32, (f, rel_l2(x[f], xs[f]))
+        assert rel_l2(x[f].astype(np.complex128), d["x_ref"][f].astype(np.complex128)) < REL_L2_FP32
+        done = int(res.iterations_done[f])
+        assert abs(done - (len(cns[f]) - 1)) <= 1
+        cn = res.c_norm[f, :done + 1].cpu().numpy().astype(np.float64)
+        m = min(len(cn), len(cns[f]))
+        assert np.all(np.abs(cn[:m] - cns[f][:m]) <= 1e-4 * cns[f][0] + 1e-3 * cns[f][:m])
+        mism = labels[f] != labs[f]
+        assert np.all(margins[f][mism] < TIE_BAND), f"decision flips outside the tie band in frame {f}"
+        flips += int(mism.sum())
+        # fused bit-error count == Hamming distance of the fused labels
+        want = int(np.unpackbits((labels[f] ^ d["tx_labels"][f])[:, None], axis=1).sum())
+        assert int(res.bit_errors[f]) == want
+    # LLR signs reproduce the fused hard decisions
+    llr = res.llr.cpu().numpy()
+    bits = ((labels[..., None] >> np.arange(b - 1, -1, -1)) & 1).astype(bool)
+    assert np.array_equal(llr < 0, bits)
+    print(f"{name}: {flips} tie-band decision flips over {labels.size} symbols")
+
+
+@pytest.mark.parametrize("name", ["frames_cfg1", "frames_cfg2", "frames_cfg3"])
+def test_batched_fp64_identical_decisions(pkg, name):
+    d = load_golden(name)
+    M, N, iters, b = (int(v) for v in d["meta"])
+    s = solver_for(pkg, M, N, iters, "fp64", b)
+    paths = paths_from_fixture(pkg, d, s.cdtype)
+    y = torch.as_tensor(d["y"].astype(np.complex128), device="cuda").contiguous()
+    res = s.solve(y, paths, torch.as_tensor(d["lam"]))
+    x = res.x.cpu().numpy()
+    for f in range(x.shape[0]):
+        assert rel_l2(x[f], d["x_ref"][f]) < 1e-10
+        np.testing.assert_allclose(res.c_norm[f].cpu().numpy(), d["c_norm"][f], rtol=1e-9)
+    np.testing.assert_array_equal(res.labels.cpu().numpy(), d["rx_labels"])
+
+
+# ---------------------------------------------------------------- demod
+class TestDemod:
+    @pytest.mark.parametrize("name", ["qpsk", "qam16"])
+    def test_hard_demod_drop_in(self, pkg, name):
+        d = load_golden("demod")
+        c = pkg.make_constellation(name)
+        g = pkg.GridConfig(16, 8)
+        _, bits = pkg.hard_demod(pkg.unflatten(d[name + "_x"], g), c, g)
+        np.testing.assert_array_equal(bits, d[name + "_bits"])
+
+    @pytest.mark.parametrize("name,bps", [("qpsk", 2), ("qam16", 4), ("qam64", 6)])
+    @pytest.mark.parametrize("precision", ["fp32", "fp64"])
+    def test_qam_slicer_and_llr(self, pkg, name, bps, precision):
+        import ctypes as C
+        from paper_2604_02266_b200 import _native as nat
+        rng = np.random.default_rng(bps)
+        c = orc.qam(name)
+        n = 20000
+        v = rng.normal(size=n) * 0.8 + 1j * rng.normal(size=n) * 0.8
+        v[:len(c.points)] = c.points
+        cd = torch.complex128 if precision == "fp64" else torch.complex64
+        xv = torch.as_tensor(v, device="cuda").to(cd)
+        if precision == "fp32":
+            v = xv.cpu().numpy().astype(np.complex128)
+        lab = torch.empty(n, dtype=torch.uint8, device="cuda")
+        llr = torch.empty(n, bps, dtype=torch.float32, device="cuda")
+        st = C.c_void_p(torch.cuda.current_stream().cuda_stream)
+        nat.check(nat.load().ddb_qam_demod(n, nat.DDB_F64 if precision == "fp64" else nat.DDB_F32,
+                                           C.c_void_p(xv.data_ptr()), bps, 0.25, C.c_void_p(lab.data_ptr()),
+                                           C.c_void_p(llr.data_ptr()), st), "qam_demod")
+        want_lab, _ = orc.hard_demod(v, c)
+        margin = orc.decision_margin(v, c)
+        got = lab.cpu().numpy().astype(np.int64)
+        mism = got != want_lab
+        assert np.all(margin[mism] < TIE_BAND)
+        want_llr = orc.llr_maxlog(v, c, 0.25)
+        np.testing.assert_allclose(llr.cpu().numpy(), want_llr, rtol=1e-4, atol=1e-3)
+
+
+# ---------------------------------------------------------------- detect_paths
+def test_detect_paths_matches_reference(pkg):
+    d = load_golden("detect")
+    for c in range(int(d["n_cases"])):
+        p = f"c{c}_"
+        heff = d[p + "heff"]
+        g = pkg.GridConfig(*heff.shape)
+        taps = pkg.detect_paths(heff, float(d[p + "theta"]), g)
+        np.testing.assert_array_equal([t.k_p for t in taps], d[p + "k"])
+        np.testing.assert_array_equal([t.l_p for t in taps], d[p + "l"])
+        np.testing.assert_array_equal([t.gain for t in taps], d[p + "g"])
+    assert pkg.detect_paths(np.zeros((8, 4), complex), 0.1, pkg.GridConfig(8, 4)) == []
+    with pytest.raises(ValueError):
+        pkg.detect_paths(np.zeros((8, 4), complex), -1.0, pkg.GridConfig(8, 4))
+
+
+# ---------------------------------------------------------------- edge cases
+def _random_problem(M, N, B, P, rng, anywhere=True):
+    off = np.arange(B + 1) * P
+    if anywhere:
+        k = rng.integers(0, M, size=B * P)
+        l = rng.integers(0, N, size=B * P)
+    else:
+        k = (M // 2 + rng.integers(0, min(40, M // 2), size=B * P)) % M
+        l = (N // 2 + rng.integers(-1, 2, size=B * P)) % N
+    g = (rng.uniform(0.05, 0.3, size=B * P) * np.exp(2j * np.pi * rng.random(B * P)))
+    g[::P] = np.exp(2j * np.pi * rng.random(B))  # a dominant tap keeps H well conditioned
+    y = rng.normal(size=(B, M * N)) + 1j * rng.normal(size=(B, M * N))
+    return off, k, l, g, y
+
+
+@pytest.mark.parametrize("M,N,P", [(8, 2, 3), (2, 2, 1), (12, 6, 4), (48, 32, 5), (64, 6, 3),
+                                   (512, 32, 6), (256, 64, 7), (1024, 64, 8), (2048, 32, 6)])
+@pytest.mark.parametrize("precision", ["fp32", "fp64"])
+def test_random_taps_all_cluster_shapes(pkg, M, N, P, precision):
+    """Arbitrary tap positions exercise the DSMEM (remote column) and wrap-twist
+    paths of every cluster shape the planner picks."""
+    rng = np.random.default_rng(M * 7 + N + P)
+    B = 3
+    off, k, l, g, y = _random_problem(M, N, B, P, rng)
+    try:
+        s = solver_for(pkg, M, N, 10, precision)
+    except Exception as e:  # grid exceeds on-chip capacity for this precision
+        pytest.skip(str(e))
+    paths = pkg.PathBatch.from_arrays(off, k, l, g, cdtype=s.cdtype)
+    yt = torch.as_tensor(y, device="cuda").to(s.cdtype).contiguous()
+    lam = np.array([1e-2, 0.0, 0.1])
+    res = s.solve(yt, paths, lam)
+    x = res.x.cpu().numpy()
+    tol = 1e-10 if precision == "fp64" else REL_L2_FP32
+    for f in range(B):
+        taps = [orc.Tap(int(a), int(b), complex(c)) for a, b, c in zip(k[off[f]:off[f + 1]], l[off[f]:off[f + 1]],
+                                                                       g[off[f]:off[f + 1]])]
+        t = orc.build_tables(taps, M, N)
+        xr, tr = orc.cga(t, yt[f].cpu().numpy().astype(np.complex128), 10, float(lam[f]))
+        assert rel_l2(x[f], xr) < tol, (f, rel_l2(x[f], xr), s.plan())
+        assert int(res.iterations_done[f]) == len(tr.c_norm) - 1
+
+
+def test_empty_and_mixed_batch(pkg):
+    s = solver_for(pkg, 64, 16, 10, "fp32", 2)
+    rng = np.random.default_rng(1)
+    off = np.array([0, 2, 2, 5])  # frame 1 has no taps
+    k = rng.integers(0, 64, 5)
+    l = rng.integers(0, 16, 5)
+    g = np.array([1, 0.2, 1, 0.1, 0.1], complex)
+    paths = pkg.PathBatch.from_arrays(off, k, l, g)
+    y = torch.randn(3, 1024, dtype=torch.complex64, device="cuda")
+    tx = torch.zeros(3, 1024, dtype=torch.uint8, device="cuda")
+    res = s.solve(y, paths, 0.01, tx_labels=tx, llr=True)
+    st = res.status.cpu().numpy()
+    assert st[1] & 1 and not st[0] & 1 and not st[2] & 1
+    assert torch.all(res.x[1] == 0) and not torch.isnan(res.x).any()
+    assert int(res.iterations_done[1]) == 0
+    assert int(res.bit_errors[1]) == 2 * 1024 // 2   # harness.py:173 scoring
+
+
+def test_large_p_threshold_sweep_frame(pkg):
+    """theta = 0.001 at (128, 32) detects hundreds of taps."""
+    d = load_golden("detect")
+    heff = d["c4_heff"]
+    M, N = heff.shape
+    taps = orc.detect_paths(heff, 0.001)
+    assert len(taps) > 100
+    rng = np.random.default_rng(2)
+    y = rng.normal(size=M * N) + 1j * rng.normal(size=M * N)
+    t = orc.build_tables(taps, M, N)
+    xr, _ = orc.cga(t, y, 10, 1e-3)
+    for prec, tol in (("fp64", 1e-10), ("fp32", REL_L2_FP32)):
+        s = solver_for(pkg, M, N, 10, prec)
+        paths = pkg.PathBatch.from_arrays([0, len(taps)], [t.k for t in taps], [t.l for t in taps],
+                                          [t.gain for t in taps], cdtype=s.cdtype)
+        res = s.solve(torch.as_tensor(y, device="cuda").to(s.cdtype)[None].contiguous(), paths, 1e-3)
+        assert rel_l2(res.x[0].cpu().numpy(), xr) < tol
+
+
+# ---------------------------------------------------------------- full-size properties
+def test_full_size_linearity_and_noiseless_recovery(pkg):
+    from paper_2604_02266_b200.synth import make_frames
+    s = solver_for(pkg, 512, 32, 10, "fp32", 4)
+    fb = make_frames(s, 64, snr_db=float("inf"), seed=11)
+    r1 = s.solve(fb.y, fb.paths, fb.lam)
+    r2 = s.solve((fb.y * 3.0).contiguous(), fb.paths, fb.lam)
+    rel = torch.linalg.vector_norm(r2.x - 3.0 * r1.x, dim=1) / torch.linalg.vector_norm(3.0 * r1.x, dim=1)
+    assert float(rel.max()) < 1e-5
+    # noiseless, well-conditioned Veh-A channel: 10 CG steps recover every symbol
+    assert torch.equal(r1.labels, fb.tx_labels)
+
+
+def test_ber_decreases_with_snr(pkg):
+    from paper_2604_02266_b200.synth import make_frames
+    s = solver_for(pkg, 512, 32, 10, "fp32", 4)
+    bers = []
+    for snr in (0.0, 10.0, 20.0, 30.0):
+        fb = make_frames(s, 32, snr_db=snr, seed=5)
+        res = s.solve(fb.y, fb.paths, fb.lam, tx_labels=fb.tx_labels)
+        bers.append(float(res.bit_errors.sum()) / (32 * s.MN * 4))
+    assert all(b2 <= b1 for b1, b2 in zip(bers, bers[1:])), bers
+
+
+def test_host_pipeline_matches_device_solve(pkg):
+    from paper_2604_02266_b200.synth import make_frames
+    s = solver_for(pkg, 256, 16, 10, "fp32", 4)
+    fb = make_frames(s, 40, snr_db=20.0, seed=2)
+    ref = s.solve(fb.y, fb.paths, fb.lam, tx_labels=fb.tx_labels)
+    pipe = pkg.HostPipeline(s, chunk=16)
+    pin = lambda t: t.cpu().pin_memory()  # noqa: E731
+    labels = torch.empty(40, s.MN, dtype=torch.uint8).pin_memory()
+    errs = torch.empty(40, dtype=torch.int32).pin_memory()
+    pipe.run(pin(fb.y), tuple(pin(t) for t in (fb.paths.offsets, fb.paths.k, fb.paths.l, fb.paths.gain)),
+             pin(fb.lam), pin(fb.tx_labels), labels, errs)
+    assert torch.equal(labels, ref.labels.cpu())
+    assert torch.equal(errs, ref.bit_errors.cpu())
