@@ -96,6 +96,7 @@ typedef struct {
   int32_t threads;           /* threads per CTA                                     */
   int32_t smem_bytes;        /* dynamic shared memory per CTA                       */
   int32_t ctas_per_sm;       /* occupancy reported by the CUDA runtime (0 on CPU)   */
+  int32_t halo_rows;         /* quasi-periodic extension rows kept around p and u   */
 } ddb_plan;
 
 /* ---- library ------------------------------------------------------------ */

@@ -58,6 +58,7 @@ class Plan(C.Structure):
     _fields_ = [
         ("cluster", C.c_int32), ("cols_per_cta", C.c_int32), ("cols_per_thread", C.c_int32),
         ("threads", C.c_int32), ("smem_bytes", C.c_int32), ("ctas_per_sm", C.c_int32),
+        ("halo_rows", C.c_int32),
     ]
 
 

@@ -96,8 +96,9 @@ __global__ void hard_demod_kernel(long long count, const Vec<T>* __restrict__ x,
   T bestd = T(0);
   for (int s = 0; s < npts; ++s) {
     const Vec<T> pt = pts[s];
-    const T dr = v.x - pt.x, di = v.y - pt.y;
-    const T d = dr * dr + di * di;
+    // np.abs(v - s) ** 2, rounded exactly as numpy does it
+    const T m = np_cabs(v.x - pt.x, v.y - pt.y);
+    const T d = m * m;
     if (s == 0 || d < bestd) { bestd = d; best = s; }
   }
   labels[i] = best;
@@ -203,7 +204,7 @@ __global__ void __launch_bounds__(kDetectThreads) detect_paths_kernel(
   const int n = M * N;
   const double2* h = heff + (size_t)f * n;
   double peak = 0.0;
-  for (int i = threadIdx.x; i < n; i += blockDim.x) peak = fmax(peak, hypot(h[i].x, h[i].y));
+  for (int i = threadIdx.x; i < n; i += blockDim.x) peak = fmax(peak, np_cabs(h[i].x, h[i].y));
   peak = block_max(peak, dscratch);
   if (peak == 0.0) {  // sparse.py:81-82
     if (threadIdx.x == 0) count[f] = 0;
@@ -214,13 +215,13 @@ __global__ void __launch_bounds__(kDetectThreads) detect_paths_kernel(
   const int i0 = threadIdx.x * chunk;
   const int i1 = min(n, i0 + chunk);
   int mine = 0;
-  for (int i = i0; i < i1; ++i) mine += hypot(h[i].x, h[i].y) > thr;
+  for (int i = i0; i < i1; ++i) mine += np_cabs(h[i].x, h[i].y) > thr;
   int total = 0;
   int pos = block_exscan(mine, iscratch, &total);
   if (threadIdx.x == 0) count[f] = total > cap ? -1 : total;
   if (total > cap) return;  // -1: candidate list exceeds shared memory; host reports it
   for (int i = i0; i < i1; ++i) {
-    const double m = hypot(h[i].x, h[i].y);
+    const double m = np_cabs(h[i].x, h[i].y);
     if (m > thr) { cmag[pos] = m; cidx[pos] = i; ++pos; }
   }
   __syncthreads();
@@ -274,7 +275,7 @@ __global__ void __launch_bounds__(256) fp32_probe_kernel(float* out, int iters, 
   if (MODE == 0) {
     for (int it = 0; it < iters; ++it) {
 #pragma unroll
-      for (int u = 0; u < 16; ++u)
+      for (int u = 0; u < 32; ++u)
 #pragma unroll
         for (int i = 0; i < 8; ++i) a[i] = fmaf(a[i], m, c);
     }

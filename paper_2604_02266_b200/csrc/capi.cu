@@ -55,27 +55,41 @@ int32_t make_plan(int32_t M, int32_t N, int32_t dtype, ddb::LaunchShape* s) {
   const int eb = dtype == DDB_F64 ? 8 : 4;
   const int cap = smem_optin();
   const int lcmax = dtype == DDB_F64 ? 8 : 16;
-  for (int C = 1; C <= 16; C *= 2) {
-    if (N % C) continue;
-    const int lcta = N / C;
-    const size_t smem = ddb::sscga_smem_bytes(M, N, C, eb);
-    if (smem > (size_t)cap) continue;
-    const int target = M * lcta < 256 ? M * lcta : 256;
-    int best = 0;
-    for (int lc = lcmax; lc >= 1; lc /= 2) {
-      if (lcta % lc) continue;
-      const int active = M * (lcta / lc);
-      const int threads = (active + 31) / 32 * 32;
-      if (threads > ddb::sscga_max_threads(eb, lc)) continue;
-      if (active >= target) { best = lc; break; }
+  const int pcap = 256;
+  int TL = 0, TH = 0;
+  ddb::twiddle_split(M * N, &TL, &TH);
+  const int hmin = M < 64 ? M : 64;  // Veh-A delay spread is <= 39 bins at M = 512
+  for (int pass = 0; pass < 2; ++pass) {
+    for (int C = 1; C <= 16; C *= 2) {
+      if (N % C) continue;
+      const int lcta = N / C;
+      const size_t base = ddb::sscga_layout(M, N, C, eb, 0, TL, TH, pcap).total;
+      if (base > (size_t)cap) continue;
+      long long h = (long long)(cap - base) / (2LL * lcta * 2 * eb);
+      while (h > 0 && ddb::sscga_layout(M, N, C, eb, (int)h, TL, TH, pcap).total > (size_t)cap) --h;
+      if (h > M) h = M;  // a delay shift spans at most M - 1 rows
+      if (pass == 0 && h < hmin) continue;
+      const int target = M * lcta < 256 ? M * lcta : 256;
+      int best = 0;
+      for (int lc = lcmax; lc >= 1; lc /= 2) {
+        if (lcta % lc) continue;
+        const int active = M * (lcta / lc);
+        const int threads = (active + 31) / 32 * 32;
+        if (threads > ddb::sscga_max_threads(eb, lc)) continue;
+        if (active >= target) { best = lc; break; }
+      }
+      if (!best) continue;
+      s->cluster = C;
+      s->lcta = lcta;
+      s->lc = best;
+      s->threads = (M * (lcta / best) + 31) / 32 * 32;
+      s->halo = (int)h;
+      s->tl = TL;
+      s->th = TH;
+      s->pcap = pcap;
+      s->smem = (int)ddb::sscga_layout(M, N, C, eb, (int)h, TL, TH, pcap).total;
+      return DDB_OK;
     }
-    if (!best) continue;
-    s->cluster = C;
-    s->lcta = lcta;
-    s->lc = best;
-    s->threads = (M * (lcta / best) + 31) / 32 * 32;
-    s->smem = (int)smem;
-    return DDB_OK;
   }
   return fail(DDB_ERR_UNSUPPORTED,
               "grid (%d,%d) %s: CG state does not fit a 16-CTA cluster's shared memory", M, N,
@@ -112,6 +126,7 @@ int32_t ddb_sscga_plan(int32_t M, int32_t N, int32_t dtype, ddb_plan* out) {
   out->threads = s.threads;
   out->smem_bytes = s.smem;
   out->ctas_per_sm = 0;
+  out->halo_rows = s.halo;
   int n = 0;
   int dev_count = 0;
   if (cudaGetDeviceCount(&dev_count) == cudaSuccess && dev_count > 0) {
@@ -163,6 +178,11 @@ int32_t ddb_sscga_solve(const ddb_sscga_problem* prob, const ddb_sscga_outputs* 
   a.C = s.cluster;
   a.Lcta = s.lcta;
   a.active_threads = prob->M * (s.lcta / s.lc);
+  a.S = prob->M + s.halo;
+  a.H = s.halo;
+  a.TL = s.tl;
+  a.TH = s.th;
+  a.pcap = s.pcap;
   a.off = prob->path_offsets;
   a.pk = prob->path_k;
   a.pl = prob->path_l;

@@ -14,6 +14,10 @@ struct SolveArgs {
   int Lcta;           // Doppler columns per CTA = N / C
   int active_threads; // M * (Lcta / LC); blockDim is this rounded up to 32
   int n_clusters;     // persistent clusters in the grid
+  int S;              // column stride (rows) of the extended p/u buffers = M + H
+  int H;              // quasi-periodic halo capacity (rows) of p/u
+  int TL, TH;         // two-level W_MN twiddle tables: e = hi * TL + lo
+  int pcap;           // per-frame tap table capacity in shared memory
   const int* off;
   const int* pk;
   const int* pl;
@@ -34,7 +38,7 @@ struct SolveArgs {
 };
 
 struct LaunchShape {
-  int cluster, lcta, lc, threads, smem;
+  int cluster, lcta, lc, threads, smem, halo, tl, th, pcap;
 };
 
 // Thread ceiling of the fused kernel instantiation (its __launch_bounds__):
@@ -42,8 +46,12 @@ struct LaunchShape {
 // so those instantiations cap at 512 threads.
 constexpr int sscga_max_threads(int elem_bytes, int lc) { return elem_bytes * lc >= 32 ? 512 : 1024; }
 
-// Shared-memory bytes of the fused kernel for a given shape.
-size_t sscga_smem_bytes(int M, int N, int C, int elem_bytes);
+// Shared-memory layout of the fused kernel (byte offsets, 16-byte aligned).
+struct SmemLayout {
+  size_t p, u, x, tlo, thi, tw, ptab, red, total;
+};
+SmemLayout sscga_layout(int M, int N, int C, int elem_bytes, int H, int TL, int TH, int pcap);
+void twiddle_split(int MN, int* TL, int* TH);
 
 template <typename T>
 cudaError_t launch_sscga(SolveArgs a, const LaunchShape& s, cudaStream_t st);
@@ -70,9 +78,7 @@ cudaError_t launch_detect_paths(int B, int M, int N, const void* heff, double th
                                 int max_paths, int* count, int* pk, int* pl, void* ph,
                                 cudaStream_t st);
 
-}  // namespace ddb
-
-namespace ddb {
 // FP32 FMA throughput probe: blocks x 256 threads x iters x 256 FMAs.
 cudaError_t launch_fp32_probe(int mode, int blocks, int iters, float* out, cudaStream_t st);
+
 }  // namespace ddb

@@ -2,41 +2,52 @@
 // conjugate gradient + demod epilogue, one thread-block cluster per frame.
 //
 // Reference algorithm: equalize.py:43-77 (cga_equalize) on the operator of
-// sparse.py:91-160.  Nothing of H_dd is stored: for tap p (k_p, l_p, h_p) with
-// offsets d_k = K0 - k_p, d_l = L0 - l_p (sparse.py:35-37) the forward product
-// is, for output (k, l),
-//     a = k + d_k,  n = floor(a / M),  k_s = a - n M
-//     u[k, l] += h_p W_MN^{-d_l k_s} W_N^{n l} v[k_s, (l + d_l) mod N]
-// and the Hermitian product is, with a = k - d_k, n = floor(a / M), k_s = a - n M,
-//     u[k, l] += conj(h_p) W_MN^{d_l (k - n M)} W_N^{n l} v[k_s, (l - d_l) mod N]
-// (W_X^e = exp(j 2 pi e / X); both are the closed forms of the tables built by
-// sparse.py:124-144, checked entry-by-entry in tests/test_oracle.py).  The
-// coefficient of a (tap, delay row) pair is the same for every Doppler column
-// except for the quasi-periodic wrap twist W_N^{n l}, which only rows whose
-// source wraps across the delay period see.
+// sparse.py:91-160.  Nothing of H_dd is stored.  For tap p = (k_p, l_p, h_p),
+// d_k = K0 - k_p, d_l = L0 - l_p (sparse.py:35-37), the tables of
+// sparse.py:124-144 reduce to (W_X^e = exp(j 2 pi e / X)):
 //
-// Layout: frame q = l M + k (grid.py:86-95).  The cluster's CTA r owns the
-// Doppler columns [r Lcta, (r+1) Lcta); inside it thread (k, g) owns delay row
-// k of the LC columns g LC .. g LC + LC - 1.  Shared memory holds this CTA's
-// slice of p (gathered by H), u = H p (gathered by H^H) and x; the residual c
-// and the MVM accumulators live in registers.  Gathers whose source column is
-// owned by another CTA of the cluster read it through DSMEM
-// (ld.shared::cluster), so no halo copies are needed.
+//   forward,   output (k, l):  u += h_p       W_MN^{-d_l a} ext_v[a, (l + d_l) mod N],  a = k + d_k
+//   hermitian, output (k, l):  u += conj(h_p) W_MN^{ d_l k} ext_v[a, (l - d_l) mod N],  a = k - d_k
 //
-// CG step, per iteration (equalize.py:59-76):
-//   u = H p;             ||u||^2 reduced cluster-wide          (barrier B)
-//   denom = ||u||^2 + lam ||p||^2  (= Re p^H (H^H H + lam I) p, equalize.py:60-64,
-//   evaluated from the forward product so it needs no extra barrier)
+// where ext_v is the Zak-domain quasi-periodic extension of v along delay,
+//   ext_v[a, l] = v[a mod M, l] * W_N^{floor(a / M) l},
+// i.e. the wrap phase of coefficient() (sparse.py:115-120) moved onto the data.
+// With it the coefficient of a (tap, delay row) pair is the same for every
+// Doppler column, so a thread that owns one delay row and a run of columns
+// does, per tap, one table-twiddle and a run of pure gather-FMAs.  The
+// extension rows (a halo of H rows around the M real rows of every column) are
+// written whenever p or u is written, by the threads owning the rows they copy.
+// Closed forms checked against the reference tables in tests/test_oracle.py.
+//
+// Layout: frame q = l M + k (grid.py:86-95).  CTA r of the cluster owns the
+// Doppler columns [r Lcta, (r+1) Lcta); thread (k, g) owns delay row k of the
+// LC columns g LC .. g LC + LC - 1.  Shared memory: this CTA's columns of
+// ext_p (gathered by H), ext_u (gathered by H^H), x, the twiddle tables and the
+// frame's tap table.  The residual c and the accumulators live in registers.
+// A gather whose source column belongs to another CTA reads it through DSMEM
+// (mapa + ld.shared::cluster).  A frame whose taps span more delay rows than
+// the halo holds falls back to wrapping rows in registers (same results).
+//
+// CG step, per iteration (equalize.py:59-76), three cluster barriers:
+//   u = H p;                 ||u||^2                           (barrier B)
+//   denom = ||u||^2 + lam ||p||^2 = Re p^H (H^H H + lam I) p (equalize.py:60-64)
 //   denom == 0 -> exact convergence (equalize.py:64-67)
-//   ap = H^H u + lam p;  x += alpha p;  c -= alpha ap;  ||c||^2  (barrier C)
-//   p = c + beta p;      ||p||^2                              (barrier A)
-// Reductions are deterministic: every warp of every CTA sums the same
-// per-warp partials in the same order, so all CTAs take identical branches.
+//   ap = H^H u + lam p;  x += alpha p;  c -= alpha ap;  ||c||^2 (barrier C)
+//   p = c + beta p;          ||p||^2                           (barrier A)
+// Reductions are deterministic: every warp of every CTA sums the same per-warp
+// partials in the same order, so all CTAs take identical branches.
+#include <climits>
+
 #include "common.cuh"
 #include "demod.cuh"
 #include "internal.h"
 
 namespace ddb {
+
+template <typename T> struct __align__(16) PathEnt {
+  int dk, dl;
+  Vec<T> h;
+};
 
 struct Ctx {
   int k;        // delay row owned by this thread
@@ -46,66 +57,109 @@ struct Ctx {
   bool active;  // padding threads (M * G not a multiple of 32) compute but never store
 };
 
-// acc[j] = (H v)[k, colbase + j]  (HERM = false)  or  (H^H v)[k, colbase + j]
+struct FrameCtx {
+  int P0, P;
+  bool in_smem;  // tap table staged in shared memory
+  bool halo;     // every tap's source row lies inside the extension halo
+  int lo_p, hi_p, lo_u, hi_u;
+};
+
+template <typename T> struct Sm {
+  Vec<T>* p;
+  Vec<T>* u;
+  Vec<T>* x;
+  Vec<T>* tlo;
+  Vec<T>* thi;
+  Vec<T>* tw;
+  PathEnt<T>* ptab;
+  T* red;
+  int tlb;  // log2(TL)
+};
+
+template <typename T>
+__device__ __forceinline__ Vec<T> twid(const Sm<T>& sm, int e) {
+  return cmul(sm.thi[e >> sm.tlb], sm.tlo[e & ((1 << sm.tlb) - 1)]);
+}
+
+template <typename T>
+__device__ __forceinline__ void get_path(const SolveArgs& a, const Sm<T>& sm, const FrameCtx& fc, int p,
+                                         int& dk, int& dl, Vec<T>& h) {
+  if (fc.in_smem) {
+    const PathEnt<T> e = sm.ptab[p];
+    dk = e.dk;
+    dl = e.dl;
+    h = e.h;
+  } else {
+    dk = a.K0 - __ldg(a.pk + fc.P0 + p);
+    dl = a.L0 - __ldg(a.pl + fc.P0 + p);
+    h = __ldg(reinterpret_cast<const Vec<T>*>(a.ph) + fc.P0 + p);
+  }
+}
+
+// acc[j] = (H v)[k, colbase + j]  (HERM = false)  or  (H^H v)[k, colbase + j];
+// buf is the extended buffer of v (column stride a.S, real row 0 at offset lo).
 template <typename T, int LC, bool HERM>
-__device__ __forceinline__ void ss_mvm_cluster(const SolveArgs& a, const Ctx& cx, int P0, int P,
-                                               const Vec<T>* __restrict__ buf,
-                                               const Vec<T>* __restrict__ tw, Vec<T> (&acc)[LC]) {
+__device__ __forceinline__ void ss_mvm(const SolveArgs& a, const Ctx& cx, const Sm<T>& sm, const FrameCtx& fc,
+                                       const Vec<T>* __restrict__ buf, int lo,
+                                       typename Acc<T>::type (&acc)[LC]) {
   using V = Vec<T>;
-  const int M = a.M, N = a.N, MN = a.MN, Lcta = a.Lcta;
-  const V* gains = reinterpret_cast<const V*>(a.ph);
+  using A = Acc<T>;
+  const int M = a.M, N = a.N, MN = a.MN, S = a.S, Lcta = a.Lcta;
 #pragma unroll
-  for (int j = 0; j < LC; ++j) acc[j] = czero<V>();
+  for (int j = 0; j < LC; ++j) acc[j] = A::zero();
   const uint32_t buf_s = smem_addr(buf);
-  const int first_col = cx.rank * Lcta;
-  for (int p = 0; p < P; ++p) {
-    const int kp = __ldg(a.pk + P0 + p);
-    const int lp = __ldg(a.pl + P0 + p);
-    V h = __ldg(gains + P0 + p);
-    const int dk = a.K0 - kp, dl = a.L0 - lp;
-    const int ar = HERM ? cx.k - dk : cx.k + dk;
-    const int n = ar < 0 ? -1 : (ar >= M ? 1 : 0);
-    const int ks = ar - n * M;
-    int e;
-    if (HERM) {
-      e = mod_pos(dl * (cx.k - n * M), MN);
-      h = cconj(h);
-    } else {
-      e = mod_pos(-dl * ks, MN);
+  const int first = cx.rank * Lcta;
+  for (int p = 0; p < fc.P; ++p) {
+    int dk, dl;
+    V h;
+    get_path(a, sm, fc, p, dk, dl, h);
+    const int ar = HERM ? cx.k - dk : cx.k + dk;  // unwrapped source row
+    const int e = mod_pos(HERM ? dl * cx.k : -dl * ar, MN);
+    if (HERM) h = cconj(h);
+    const V coef = cmul(h, twid(sm, e));
+    int row = ar, nw = 0;
+    if (!fc.halo) {
+      nw = ar < 0 ? -1 : (ar >= M ? 1 : 0);
+      row = ar - nw * M;
     }
-    const V coef = cmul(h, twiddle(T(0), e, MN));
     const int base = mod_pos(cx.colbase + (HERM ? -dl : dl), N);
-    const int loc0 = base - first_col;
-    const bool fast = (n == 0) && loc0 >= 0 && loc0 + LC <= Lcta;
-    if (__all_sync(0xffffffffu, fast)) {
-      // every column local and contiguous, no wrap twist: pure gather-FMA
-      const V* s = buf + loc0 * M + ks;
+    const int loc0 = base - first;
+    const bool contig = loc0 >= 0 && loc0 + LC <= Lcta;
+    const bool nowrap = __all_sync(0xffffffffu, nw == 0);
+    if (contig && nowrap) {
+      // all columns local and contiguous: LDS + 2 FFMA2 per element
+      const V* s = buf + loc0 * S + lo + row;
 #pragma unroll
-      for (int j = 0; j < LC; ++j) cfma(acc[j], coef, s[j * M]);
+      for (int j = 0; j < LC; ++j) A::mac(acc[j], coef, s[j * S]);
     } else {
 #pragma unroll
       for (int j = 0; j < LC; ++j) {
         int ls = base + j;
         if (ls >= N) ls -= N;
         const int owner = ls / Lcta;
-        const int lloc = ls - owner * Lcta;
+        const int idx = (ls - owner * Lcta) * S + lo + row;
         V v;
-        if (owner == cx.rank) {
-          v = buf[lloc * M + ks];
-        } else {
-          v = ld_cluster(static_cast<V*>(nullptr),
-                         map_rank(buf_s + (uint32_t)((lloc * M + ks) * (int)sizeof(V)), owner));
+        if (owner == cx.rank) v = buf[idx];
+        else v = ld_cluster(static_cast<V*>(nullptr), map_rank(buf_s + (uint32_t)(idx * (int)sizeof(V)), owner));
+        if (nw != 0) {  // quasi-periodic wrap applied in registers (no halo this frame)
+          V t = sm.tw[ls];
+          if (nw < 0) t = cconj(t);
+          v = cmul(v, t);
         }
-        V cj = coef;
-        if (n != 0) {
-          V t = tw[cx.colbase + j];
-          if (n < 0) t = cconj(t);
-          cj = cmul(coef, t);
-        }
-        cfma(acc[j], cj, v);
+        A::mac(acc[j], coef, v);
       }
     }
   }
+}
+
+// Store element (k, local column lc) of p or u and its quasi-periodic copies.
+template <typename T>
+__device__ __forceinline__ void put_ext(Vec<T>* buf, int S, int lo, int hi, int M, int k, int lc, int gcol,
+                                       Vec<T> w, const Vec<T>* tw) {
+  Vec<T>* col = buf + lc * S + lo;
+  col[k] = w;
+  if (k >= M - lo) col[k - M] = cmul(w, cconj(tw[gcol]));  // row k - M: W_N^{-l}
+  if (k < hi) col[k + M] = cmul(w, tw[gcol]);               // row k + M: W_N^{+l}
 }
 
 template <typename T>
@@ -132,17 +186,54 @@ __device__ __forceinline__ T cluster_sum(T part, T* slot, int C, int nwarps, int
   return warp_sum(s);
 }
 
+__host__ __device__ static inline size_t align16(size_t v) { return (v + 15) & ~size_t(15); }
+
+__host__ __device__ static inline SmemLayout layout_impl(int M, int N, int C, int eb, int H, int TL, int TH,
+                                                         int pcap) {
+  const size_t vb = 2 * (size_t)eb;
+  const size_t lcta = (size_t)N / C;
+  SmemLayout L;
+  size_t o = 0;
+  L.p = o; o = align16(o + lcta * (size_t)(M + H) * vb);
+  L.u = o; o = align16(o + lcta * (size_t)(M + H) * vb);
+  L.x = o; o = align16(o + lcta * (size_t)M * vb);
+  L.tlo = o; o = align16(o + (size_t)TL * vb);
+  L.thi = o; o = align16(o + (size_t)TH * vb);
+  L.tw = o; o = align16(o + (size_t)N * vb);
+  L.ptab = o; o = align16(o + (size_t)pcap * (eb == 8 ? 32 : 16));
+  L.red = o; o = align16(o + 3 * 2 * 32 * (size_t)eb);
+  L.total = o;
+  return L;
+}
+
+SmemLayout sscga_layout(int M, int N, int C, int eb, int H, int TL, int TH, int pcap) {
+  return layout_impl(M, N, C, eb, H, TL, TH, pcap);
+}
+
+void twiddle_split(int MN, int* TL, int* TH) {
+  int tl = 1;
+  while ((long long)tl * tl < MN) tl <<= 1;
+  *TL = tl;
+  *TH = (MN + tl - 1) / tl;
+}
+
 template <typename T, int LC>
 __global__ void __launch_bounds__(sscga_max_threads(sizeof(T), LC), 1) sscga_kernel(const SolveArgs a) {
   using V = Vec<T>;
+  using A = Acc<T>;
   extern __shared__ __align__(16) unsigned char smem[];
-  const int M = a.M;
-  const int nelem = a.Lcta * M;
-  V* pbuf = reinterpret_cast<V*>(smem);
-  V* ubuf = pbuf + nelem;
-  V* xbuf = ubuf + nelem;
-  T* red = reinterpret_cast<T*>(xbuf + nelem);  // [3 kinds][2 parities][32 warps]
-  V* tw = reinterpret_cast<V*>(red + 3 * 2 * 32);  // W_N^l, l in [0, N)
+  const int M = a.M, N = a.N, S = a.S;
+  const SmemLayout L = layout_impl(M, N, a.C, (int)sizeof(T), a.H, a.TL, a.TH, a.pcap);
+  Sm<T> sm;
+  sm.p = reinterpret_cast<V*>(smem + L.p);
+  sm.u = reinterpret_cast<V*>(smem + L.u);
+  sm.x = reinterpret_cast<V*>(smem + L.x);
+  sm.tlo = reinterpret_cast<V*>(smem + L.tlo);
+  sm.thi = reinterpret_cast<V*>(smem + L.thi);
+  sm.tw = reinterpret_cast<V*>(smem + L.tw);
+  sm.ptab = reinterpret_cast<PathEnt<T>*>(smem + L.ptab);
+  sm.red = reinterpret_cast<T*>(smem + L.red);
+  sm.tlb = __ffs(a.TL) - 1;
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
   Ctx cx;
@@ -153,7 +244,9 @@ __global__ void __launch_bounds__(sscga_max_threads(sizeof(T), LC), 1) sscga_ker
   cx.g = t / M;
   cx.colbase = cx.rank * a.Lcta + cx.g * LC;
 
-  for (int l = tid; l < a.N; l += blockDim.x) tw[l] = twiddle(T(0), l, a.N);
+  for (int i = tid; i < a.TL; i += blockDim.x) sm.tlo[i] = twiddle(T(0), i, a.MN);
+  for (int i = tid; i < a.TH; i += blockDim.x) sm.thi[i] = twiddle(T(0), (int)(((long long)i * a.TL) % a.MN), a.MN);
+  for (int l = tid; l < N; l += blockDim.x) sm.tw[l] = twiddle(T(0), l, N);
   __syncthreads();
 
   const V* y = reinterpret_cast<const V*>(a.y);
@@ -167,11 +260,12 @@ __global__ void __launch_bounds__(sscga_max_threads(sizeof(T), LC), 1) sscga_ker
   int par[3] = {0, 0, 0};  // 0: ||p||^2, 1: ||u||^2, 2: ||c||^2
 
   for (int f = blockIdx.x / a.C; f < a.B; f += a.n_clusters) {
-    const int P0 = __ldg(a.off + f);
-    const int P = __ldg(a.off + f + 1) - P0;
+    FrameCtx fc;
+    fc.P0 = __ldg(a.off + f);
+    fc.P = __ldg(a.off + f + 1) - fc.P0;
     const size_t fo = (size_t)f * a.MN;
 
-    if (P <= 0) {  // EmptyChannel (sparse.py:126-127): flag it, no NaNs
+    if (fc.P <= 0) {  // EmptyChannel (sparse.py:126-127): flag it, no NaNs
       if (cx.active) {
 #pragma unroll
         for (int j = 0; j < LC; ++j) {
@@ -190,31 +284,64 @@ __global__ void __launch_bounds__(sscga_max_threads(sizeof(T), LC), 1) sscga_ker
       }
       continue;
     }
-    const T lam = lamv[f];
 
-    // y -> ubuf (own columns); b = H^H y is gathered from it
+    // ---- frame setup: tap table, extension halo sizes
+    fc.in_smem = fc.P <= a.pcap;
+    if (fc.in_smem) {
+      const V* gains = reinterpret_cast<const V*>(a.ph);
+      for (int i = tid; i < fc.P; i += blockDim.x) {
+        PathEnt<T> e;
+        e.dk = a.K0 - __ldg(a.pk + fc.P0 + i);
+        e.dl = a.L0 - __ldg(a.pl + fc.P0 + i);
+        e.h = __ldg(gains + fc.P0 + i);
+        sm.ptab[i] = e;
+      }
+    }
+    const T lam = lamv[f];
+    __syncthreads();
+    {
+      int dmin = INT_MAX, dmax = INT_MIN;
+      for (int p = 0; p < fc.P; ++p) {
+        const int dk = fc.in_smem ? sm.ptab[p].dk : a.K0 - __ldg(a.pk + fc.P0 + p);
+        dmin = min(dmin, dk);
+        dmax = max(dmax, dk);
+      }
+      fc.lo_p = max(0, -dmin);
+      fc.hi_p = max(0, dmax);
+      fc.lo_u = max(0, dmax);
+      fc.hi_u = max(0, -dmin);
+      fc.halo = fc.lo_p + fc.hi_p <= a.H;
+      if (!fc.halo) fc.lo_p = fc.hi_p = fc.lo_u = fc.hi_u = 0;
+    }
+
+    // y -> ext_u (own columns); b = H^H y is gathered from it
     if (cx.active) {
 #pragma unroll
-      for (int j = 0; j < LC; ++j)
-        ubuf[(cx.g * LC + j) * M + cx.k] = y[fo + (size_t)(cx.colbase + j) * M + cx.k];
+      for (int j = 0; j < LC; ++j) {
+        const int lc = cx.g * LC + j;
+        put_ext<T>(sm.u, S, fc.lo_u, fc.hi_u, M, cx.k, lc, cx.colbase + j,
+                   y[fo + (size_t)(cx.colbase + j) * M + cx.k], sm.tw);
+      }
     }
     if (lead && a.berr) a.berr[f] = 0;
     cl_sync<T>(a.C);
 
-    V acc[LC], c[LC];
-    ss_mvm_cluster<T, LC, true>(a, cx, P0, P, ubuf, tw, acc);  // b = H^H y (equalize.py:52)
+    typename A::type acc[LC];
+    V c[LC];
+    ss_mvm<T, LC, true>(a, cx, sm, fc, sm.u, fc.lo_u, acc);  // b = H^H y (equalize.py:52)
     T part = T(0);
 #pragma unroll
     for (int j = 0; j < LC; ++j) {
-      c[j] = acc[j];
+      const V b = A::get(acc[j]);
+      c[j] = b;
       if (cx.active) {
-        const int o = (cx.g * LC + j) * M + cx.k;
-        pbuf[o] = acc[j];
-        xbuf[o] = czero<V>();
-        part += cabs2(acc[j]);
+        const int lc = cx.g * LC + j;
+        put_ext<T>(sm.p, S, fc.lo_p, fc.hi_p, M, cx.k, lc, cx.colbase + j, b, sm.tw);
+        sm.x[lc * M + cx.k] = czero<V>();
+        part += cabs2(b);
       }
     }
-    T cn = cluster_sum<T>(part, red + (0 * 2 + par[0]) * 32, a.C, nwarps, lane, warp);
+    T cn = cluster_sum<T>(part, sm.red + (0 * 2 + par[0]) * 32, a.C, nwarps, lane, warp);
     par[0] ^= 1;
     T pp = cn;
     if (lead && cnorm) cnorm[(size_t)f * stride] = cn;
@@ -222,16 +349,17 @@ __global__ void __launch_bounds__(sscga_max_threads(sizeof(T), LC), 1) sscga_ker
     int done = 0;
     bool exact = false;
     for (int it = 0; it < a.iters; ++it) {
-      ss_mvm_cluster<T, LC, false>(a, cx, P0, P, pbuf, tw, acc);  // u = H p
+      ss_mvm<T, LC, false>(a, cx, sm, fc, sm.p, fc.lo_p, acc);  // u = H p
       part = T(0);
 #pragma unroll
       for (int j = 0; j < LC; ++j) {
         if (cx.active) {
-          ubuf[(cx.g * LC + j) * M + cx.k] = acc[j];
-          part += cabs2(acc[j]);
+          const V uj = A::get(acc[j]);
+          put_ext<T>(sm.u, S, fc.lo_u, fc.hi_u, M, cx.k, cx.g * LC + j, cx.colbase + j, uj, sm.tw);
+          part += cabs2(uj);
         }
       }
-      const T uu = cluster_sum<T>(part, red + (1 * 2 + par[1]) * 32, a.C, nwarps, lane, warp);
+      const T uu = cluster_sum<T>(part, sm.red + (1 * 2 + par[1]) * 32, a.C, nwarps, lane, warp);
       par[1] ^= 1;
       const T denom = uu + lam * pp;
       if (denom == T(0)) {  // equalize.py:64-67
@@ -239,32 +367,32 @@ __global__ void __launch_bounds__(sscga_max_threads(sizeof(T), LC), 1) sscga_ker
         break;
       }
       const T alpha = cn / denom;
-      ss_mvm_cluster<T, LC, true>(a, cx, P0, P, ubuf, tw, acc);  // H^H u
+      ss_mvm<T, LC, true>(a, cx, sm, fc, sm.u, fc.lo_u, acc);  // H^H u
       part = T(0);
 #pragma unroll
       for (int j = 0; j < LC; ++j) {
         if (cx.active) {
-          const int o = (cx.g * LC + j) * M + cx.k;
-          const V pj = pbuf[o];
-          const V ap = cadd(acc[j], cscale(pj, lam));
-          const V xj = cadd(xbuf[o], cscale(pj, alpha));
-          xbuf[o] = xj;
+          const int lc = cx.g * LC + j;
+          const V pj = sm.p[lc * S + fc.lo_p + cx.k];
+          const V ap = cadd(A::get(acc[j]), cscale(pj, lam));
+          const V xj = cadd(sm.x[lc * M + cx.k], cscale(pj, alpha));
+          sm.x[lc * M + cx.k] = xj;
           c[j] = csub(c[j], cscale(ap, alpha));
           part += cabs2(c[j]);
           if (snaps)
             snaps[((size_t)f * a.iters + it) * a.MN + (size_t)(cx.colbase + j) * M + cx.k] = xj;
         }
       }
-      const T nn = cluster_sum<T>(part, red + (2 * 2 + par[2]) * 32, a.C, nwarps, lane, warp);
+      const T nn = cluster_sum<T>(part, sm.red + (2 * 2 + par[2]) * 32, a.C, nwarps, lane, warp);
       par[2] ^= 1;
       const T beta = nn / cn;
       part = T(0);
 #pragma unroll
       for (int j = 0; j < LC; ++j) {
         if (cx.active) {
-          const int o = (cx.g * LC + j) * M + cx.k;
-          const V pj = cadd(c[j], cscale(pbuf[o], beta));
-          pbuf[o] = pj;
+          const int lc = cx.g * LC + j;
+          const V pj = cadd(c[j], cscale(sm.p[lc * S + fc.lo_p + cx.k], beta));
+          put_ext<T>(sm.p, S, fc.lo_p, fc.hi_p, M, cx.k, lc, cx.colbase + j, pj, sm.tw);
           part += cabs2(pj);
         }
       }
@@ -272,7 +400,7 @@ __global__ void __launch_bounds__(sscga_max_threads(sizeof(T), LC), 1) sscga_ker
       done = it + 1;
       if (lead && cnorm) cnorm[(size_t)f * stride + done] = cn;
       if (done < a.iters) {
-        pp = cluster_sum<T>(part, red + (0 * 2 + par[0]) * 32, a.C, nwarps, lane, warp);
+        pp = cluster_sum<T>(part, sm.red + (0 * 2 + par[0]) * 32, a.C, nwarps, lane, warp);
         par[0] ^= 1;
       }
     }
@@ -293,7 +421,7 @@ __global__ void __launch_bounds__(sscga_max_threads(sizeof(T), LC), 1) sscga_ker
 #pragma unroll
       for (int j = 0; j < LC; ++j) {
         const size_t q = fo + (size_t)(cx.colbase + j) * M + cx.k;
-        const V xj = xbuf[(cx.g * LC + j) * M + cx.k];
+        const V xj = sm.x[(cx.g * LC + j) * M + cx.k];
         xo[q] = xj;
         if (a.bps) {
           const int lab = qam_demod_symbol<T>(xj.x, xj.y, a.bps, scale, a.llr ? a.llr + q * a.bps : nullptr);
@@ -307,12 +435,6 @@ __global__ void __launch_bounds__(sscga_max_threads(sizeof(T), LC), 1) sscga_ker
       if (lane == 0 && errs) atomicAdd(a.berr + f, errs);
     }
   }
-}
-
-size_t sscga_smem_bytes(int M, int N, int C, int elem_bytes) {
-  const size_t vb = 2 * (size_t)elem_bytes;
-  const size_t lcta = (size_t)N / C;
-  return 3 * lcta * M * vb + 3 * 2 * 32 * (size_t)elem_bytes + (size_t)N * vb;
 }
 
 template <typename T, int LC>
@@ -391,7 +513,8 @@ template cudaError_t sscga_occupancy<double>(const LaunchShape&, int*);
 
 // ---------------------------------------------------------------------------
 // Matrix-free batched operator over global memory (ss_mvm / ss_mvm_hermitian,
-// sparse.py:147-160, without tables).  One thread per output element.
+// sparse.py:147-160, without tables).  One thread per output element; used for
+// input synthesis and operator tests, not on the solve path.
 template <typename T, bool HERM>
 __global__ void ss_apply_kernel(int M, int N, const int* __restrict__ off, const int* __restrict__ pk,
                                 const int* __restrict__ pl, const Vec<T>* __restrict__ ph,
