@@ -55,7 +55,7 @@ int32_t make_plan(int32_t M, int32_t N, int32_t dtype, ddb::LaunchShape* s) {
   const int eb = dtype == DDB_F64 ? 8 : 4;
   const int cap = smem_optin();
   const int lcmax = dtype == DDB_F64 ? 8 : 16;
-  const int pcap = 256;
+  const int pcap = 64;  // larger tap sets read their entries from global memory
   int TL = 0, TH = 0;
   ddb::twiddle_split(M * N, &TL, &TH);
   const int hmin = M < 64 ? M : 64;  // Veh-A delay spread is <= 39 bins at M = 512
@@ -179,6 +179,7 @@ int32_t ddb_sscga_solve(const ddb_sscga_problem* prob, const ddb_sscga_outputs* 
   a.Lcta = s.lcta;
   a.active_threads = prob->M * (s.lcta / s.lc);
   a.S = prob->M + s.halo;
+  a.RS = ddb::row_stride(s.lcta, prob->dtype == DDB_F64 ? 8 : 4);
   a.H = s.halo;
   a.TL = s.tl;
   a.TH = s.th;

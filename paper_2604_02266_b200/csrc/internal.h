@@ -14,7 +14,8 @@ struct SolveArgs {
   int Lcta;           // Doppler columns per CTA = N / C
   int active_threads; // M * (Lcta / LC); blockDim is this rounded up to 32
   int n_clusters;     // persistent clusters in the grid
-  int S;              // column stride (rows) of the extended p/u buffers = M + H
+  int S;              // rows of the extended p/u buffers = M + H
+  int RS;             // row stride in complex elements (row_stride())
   int H;              // quasi-periodic halo capacity (rows) of p/u
   int TL, TH;         // two-level W_MN twiddle tables: e = hi * TL + lo
   int pcap;           // per-frame tap table capacity in shared memory
@@ -45,6 +46,14 @@ struct LaunchShape {
 // per-thread column runs of >= 32 bytes of real data need > 64 registers,
 // so those instantiations cap at 512 threads.
 constexpr int sscga_max_threads(int elem_bytes, int lc) { return elem_bytes * lc >= 32 ? 512 : 1024; }
+
+// Row stride (complex elements) of the on-chip row-major slices: the Lcta
+// columns padded so that a row is a multiple of 16 bytes and == 16 (mod 32),
+// which makes 8 consecutive rows hit 8 distinct 16-byte bank groups (LDS.128
+// conflict-free when consecutive lanes own consecutive rows).
+__host__ __device__ constexpr int row_stride(int lcta, int elem_bytes) {
+  return (((lcta * 2 * elem_bytes + 31) / 32) * 32 + 16) / (2 * elem_bytes);
+}
 
 // Shared-memory layout of the fused kernel (byte offsets, 16-byte aligned).
 struct SmemLayout {

@@ -44,9 +44,13 @@
 
 namespace ddb {
 
+// Per-frame tap entry: offsets and both direction's row-invariant gain factor,
+// hf = h W_MN^{-d_l d_k} (forward) and hh = conj(h) (hermitian), so a thread
+// only adds its own row's W_MN^{-+d_l k} (skipped when d_l == 0).
 template <typename T> struct __align__(16) PathEnt {
   int dk, dl;
-  Vec<T> h;
+  Vec<T> hf;
+  Vec<T> hh;
 };
 
 struct Ctx {
@@ -81,67 +85,114 @@ __device__ __forceinline__ Vec<T> twid(const Sm<T>& sm, int e) {
   return cmul(sm.thi[e >> sm.tlb], sm.tlo[e & ((1 << sm.tlb) - 1)]);
 }
 
-template <typename T>
-__device__ __forceinline__ void get_path(const SolveArgs& a, const Sm<T>& sm, const FrameCtx& fc, int p,
-                                         int& dk, int& dl, Vec<T>& h) {
-  if (fc.in_smem) {
-    const PathEnt<T> e = sm.ptab[p];
-    dk = e.dk;
-    dl = e.dl;
-    h = e.h;
-  } else {
-    dk = a.K0 - __ldg(a.pk + fc.P0 + p);
-    dl = a.L0 - __ldg(a.pl + fc.P0 + p);
-    h = __ldg(reinterpret_cast<const Vec<T>*>(a.ph) + fc.P0 + p);
-  }
+// (x mod m) for x in (-m, 2m)
+__device__ __forceinline__ int wrap1(int x, int m) {
+  x = x < 0 ? x + m : x;
+  return x >= m ? x - m : x;
 }
 
-// acc[j] = (H v)[k, colbase + j]  (HERM = false)  or  (H^H v)[k, colbase + j];
-// buf is the extended buffer of v (column stride a.S, real row 0 at offset lo).
+template <typename T>
+__device__ __forceinline__ PathEnt<T> make_path(const SolveArgs& a, const Sm<T>& sm, int kp, int lp, Vec<T> h) {
+  PathEnt<T> e;
+  e.dk = a.K0 - kp;
+  e.dl = a.L0 - lp;
+  // -d_l d_k: |d_l| <= N/2, |d_k| <= M/2 -> within (-MN, MN)
+  e.hf = e.dl ? cmul(h, twid(sm, wrap1(-e.dl * e.dk, a.MN))) : h;
+  e.hh = cconj(h);
+  return e;
+}
+
+template <typename T>
+__device__ __forceinline__ PathEnt<T> get_path(const SolveArgs& a, const Sm<T>& sm, const FrameCtx& fc, int p) {
+  if (fc.in_smem) return sm.ptab[p];
+  return make_path(a, sm, __ldg(a.pk + fc.P0 + p), __ldg(a.pl + fc.P0 + p),
+                   __ldg(reinterpret_cast<const Vec<T>*>(a.ph) + fc.P0 + p));
+}
+
+// Contiguous run of LC source columns starting at rp (16-byte aligned row,
+// offset `odd` elements): 128-bit loads, two complex values each; an odd start
+// loads one extra aligned chunk and uses the other halves (register naming only).
+template <int LC>
+__device__ __forceinline__ void gather_run(const float2* rp, bool odd, float2 c, unsigned long long (&acc)[LC]) {
+  if constexpr (LC == 1) {
+    cmac2(acc[0], c.x, c.y, rp[0]);
+  } else {
+    if (!odd) {
+      const float4* q = reinterpret_cast<const float4*>(rp);
+#pragma unroll
+      for (int m = 0; m < LC / 2; ++m) {
+        const float4 w = q[m];
+        cmac2(acc[2 * m], c.x, c.y, make_float2(w.x, w.y));
+        cmac2(acc[2 * m + 1], c.x, c.y, make_float2(w.z, w.w));
+      }
+    } else {
+      const float4* q = reinterpret_cast<const float4*>(rp - 1);
+      float4 w = q[0];
+      cmac2(acc[0], c.x, c.y, make_float2(w.z, w.w));
+#pragma unroll
+      for (int m = 1; m < LC / 2; ++m) {
+        w = q[m];
+        cmac2(acc[2 * m - 1], c.x, c.y, make_float2(w.x, w.y));
+        cmac2(acc[2 * m], c.x, c.y, make_float2(w.z, w.w));
+      }
+      w = q[LC / 2];
+      cmac2(acc[LC - 1], c.x, c.y, make_float2(w.x, w.y));
+    }
+  }
+}
+template <int LC>
+__device__ __forceinline__ void gather_run(const double2* rp, bool, double2 c, double2 (&acc)[LC]) {
+#pragma unroll
+  for (int j = 0; j < LC; ++j) Acc<double>::mac(acc[j], c, rp[j]);
+}
+
+// acc[j] = (H v)[k, colbase + j]  (HERM = false)  or  (H^H v)[k, colbase + j].
+// buf is the extended buffer of v: row r (= lo + a for extended row a) at
+// buf + r * RS, the CTA's Lcta columns contiguous inside a row.
 template <typename T, int LC, bool HERM>
 __device__ __forceinline__ void ss_mvm(const SolveArgs& a, const Ctx& cx, const Sm<T>& sm, const FrameCtx& fc,
                                        const Vec<T>* __restrict__ buf, int lo,
                                        typename Acc<T>::type (&acc)[LC]) {
   using V = Vec<T>;
   using A = Acc<T>;
-  const int M = a.M, N = a.N, MN = a.MN, S = a.S, Lcta = a.Lcta;
+  const int M = a.M, N = a.N, MN = a.MN, RS = a.RS, Lcta = a.Lcta;
 #pragma unroll
   for (int j = 0; j < LC; ++j) acc[j] = A::zero();
-  const uint32_t buf_s = smem_addr(buf);
-  const int first = cx.rank * Lcta;
+  const int gcol = cx.g * LC;  // first owned column inside the CTA
   for (int p = 0; p < fc.P; ++p) {
-    int dk, dl;
-    V h;
-    get_path(a, sm, fc, p, dk, dl, h);
+    const PathEnt<T> pe = get_path(a, sm, fc, p);
+    const int dk = pe.dk, dl = pe.dl;
     const int ar = HERM ? cx.k - dk : cx.k + dk;  // unwrapped source row
-    const int e = mod_pos(HERM ? dl * cx.k : -dl * ar, MN);
-    if (HERM) h = cconj(h);
-    const V coef = cmul(h, twid(sm, e));
+    V coef = HERM ? pe.hh : pe.hf;
+    if (dl != 0) coef = cmul(coef, twid(sm, wrap1(HERM ? dl * cx.k : -dl * cx.k, MN)));
     int row = ar, nw = 0;
     if (!fc.halo) {
       nw = ar < 0 ? -1 : (ar >= M ? 1 : 0);
       row = ar - nw * M;
     }
-    const int base = mod_pos(cx.colbase + (HERM ? -dl : dl), N);
-    const int loc0 = base - first;
+    const int sh = HERM ? -dl : dl;
+    const int loc0 = gcol + sh;  // source column inside this CTA, if contiguous
     const bool contig = loc0 >= 0 && loc0 + LC <= Lcta;
     const bool nowrap = __all_sync(0xffffffffu, nw == 0);
     if (contig && nowrap) {
-      // all columns local and contiguous: LDS + 2 FFMA2 per element
-      const V* s = buf + loc0 * S + lo + row;
-#pragma unroll
-      for (int j = 0; j < LC; ++j) A::mac(acc[j], coef, s[j * S]);
+      gather_run<LC>(buf + (lo + row) * RS + loc0, (loc0 & 1) != 0, coef, acc);
     } else {
+      // columns owned by other CTAs of the cluster (DSMEM) and/or wrapping mod N;
+      // the run crosses at most one owner boundary since LC <= Lcta
+      const int base = wrap1(cx.colbase + sh, N);
+      const int own0 = base / Lcta;
+      const int l0 = base - own0 * Lcta;
+      const int split = Lcta - l0;
+      const int own1 = own0 + 1 == a.C ? 0 : own0 + 1;
+      const uint32_t rowaddr = smem_addr(buf + (lo + row) * RS);
+      const uint32_t a0 = map_rank(rowaddr + (uint32_t)(l0 * (int)sizeof(V)), own0);
+      const uint32_t a1 = map_rank(rowaddr, own1);
 #pragma unroll
       for (int j = 0; j < LC; ++j) {
-        int ls = base + j;
-        if (ls >= N) ls -= N;
-        const int owner = ls / Lcta;
-        const int idx = (ls - owner * Lcta) * S + lo + row;
-        V v;
-        if (owner == cx.rank) v = buf[idx];
-        else v = ld_cluster(static_cast<V*>(nullptr), map_rank(buf_s + (uint32_t)(idx * (int)sizeof(V)), owner));
+        const uint32_t ad = j < split ? a0 + (uint32_t)(j * (int)sizeof(V)) : a1 + (uint32_t)((j - split) * (int)sizeof(V));
+        V v = ld_cluster(static_cast<V*>(nullptr), ad);
         if (nw != 0) {  // quasi-periodic wrap applied in registers (no halo this frame)
+          const int ls = base + j < N ? base + j : base + j - N;
           V t = sm.tw[ls];
           if (nw < 0) t = cconj(t);
           v = cmul(v, t);
@@ -152,14 +203,53 @@ __device__ __forceinline__ void ss_mvm(const SolveArgs& a, const Ctx& cx, const 
   }
 }
 
-// Store element (k, local column lc) of p or u and its quasi-periodic copies.
-template <typename T>
-__device__ __forceinline__ void put_ext(Vec<T>* buf, int S, int lo, int hi, int M, int k, int lc, int gcol,
-                                       Vec<T> w, const Vec<T>* tw) {
-  Vec<T>* col = buf + lc * S + lo;
-  col[k] = w;
-  if (k >= M - lo) col[k - M] = cmul(w, cconj(tw[gcol]));  // row k - M: W_N^{-l}
-  if (k < hi) col[k + M] = cmul(w, tw[gcol]);               // row k + M: W_N^{+l}
+// Run helpers for a thread's own LC contiguous elements of one row.
+template <typename T, int LC>
+__device__ __forceinline__ void load_run(const Vec<T>* rp, Vec<T> (&v)[LC]) {
+  if constexpr (sizeof(T) == 4 && LC >= 2) {
+    const float4* q = reinterpret_cast<const float4*>(rp);
+#pragma unroll
+    for (int m = 0; m < LC / 2; ++m) {
+      const float4 w = q[m];
+      v[2 * m] = make_float2(w.x, w.y);
+      v[2 * m + 1] = make_float2(w.z, w.w);
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < LC; ++j) v[j] = rp[j];
+  }
+}
+template <typename T, int LC>
+__device__ __forceinline__ void store_run(Vec<T>* rp, const Vec<T> (&v)[LC]) {
+  if constexpr (sizeof(T) == 4 && LC >= 2) {
+    float4* q = reinterpret_cast<float4*>(rp);
+#pragma unroll
+    for (int m = 0; m < LC / 2; ++m) q[m] = make_float4(v[2 * m].x, v[2 * m].y, v[2 * m + 1].x, v[2 * m + 1].y);
+  } else {
+#pragma unroll
+    for (int j = 0; j < LC; ++j) rp[j] = v[j];
+  }
+}
+
+// Store the thread's run of p or u (row k) and its quasi-periodic copies
+// ext[k - M] = v W_N^{-l} (if k >= M - lo) and ext[k + M] = v W_N^{+l} (if k < hi).
+template <typename T, int LC>
+__device__ __forceinline__ void put_ext(Vec<T>* buf, int RS, int lo, int hi, int M, const Ctx& cx,
+                                       const Vec<T> (&v)[LC], const Vec<T>* tw) {
+  const int gcol = cx.g * LC;
+  store_run<T, LC>(buf + (lo + cx.k) * RS + gcol, v);
+  if (cx.k >= M - lo) {
+    Vec<T> w[LC];
+#pragma unroll
+    for (int j = 0; j < LC; ++j) w[j] = cmul(v[j], cconj(tw[cx.colbase + j]));
+    store_run<T, LC>(buf + (lo + cx.k - M) * RS + gcol, w);
+  }
+  if (cx.k < hi) {
+    Vec<T> w[LC];
+#pragma unroll
+    for (int j = 0; j < LC; ++j) w[j] = cmul(v[j], tw[cx.colbase + j]);
+    store_run<T, LC>(buf + (lo + cx.k + M) * RS + gcol, w);
+  }
 }
 
 template <typename T>
@@ -191,16 +281,16 @@ __host__ __device__ static inline size_t align16(size_t v) { return (v + 15) & ~
 __host__ __device__ static inline SmemLayout layout_impl(int M, int N, int C, int eb, int H, int TL, int TH,
                                                          int pcap) {
   const size_t vb = 2 * (size_t)eb;
-  const size_t lcta = (size_t)N / C;
+  const size_t rs = (size_t)row_stride(N / C, eb);
   SmemLayout L;
   size_t o = 0;
-  L.p = o; o = align16(o + lcta * (size_t)(M + H) * vb);
-  L.u = o; o = align16(o + lcta * (size_t)(M + H) * vb);
-  L.x = o; o = align16(o + lcta * (size_t)M * vb);
+  L.p = o; o = align16(o + rs * (size_t)(M + H) * vb);
+  L.u = o; o = align16(o + rs * (size_t)(M + H) * vb);
+  L.x = o; o = align16(o + rs * (size_t)M * vb);
   L.tlo = o; o = align16(o + (size_t)TL * vb);
   L.thi = o; o = align16(o + (size_t)TH * vb);
   L.tw = o; o = align16(o + (size_t)N * vb);
-  L.ptab = o; o = align16(o + (size_t)pcap * (eb == 8 ? 32 : 16));
+  L.ptab = o; o = align16(o + (size_t)pcap * (eb == 8 ? 48 : 32));
   L.red = o; o = align16(o + 3 * 2 * 32 * (size_t)eb);
   L.total = o;
   return L;
@@ -222,7 +312,7 @@ __global__ void __launch_bounds__(sscga_max_threads(sizeof(T), LC), 1) sscga_ker
   using V = Vec<T>;
   using A = Acc<T>;
   extern __shared__ __align__(16) unsigned char smem[];
-  const int M = a.M, N = a.N, S = a.S;
+  const int M = a.M, N = a.N;
   const SmemLayout L = layout_impl(M, N, a.C, (int)sizeof(T), a.H, a.TL, a.TH, a.pcap);
   Sm<T> sm;
   sm.p = reinterpret_cast<V*>(smem + L.p);
@@ -289,13 +379,8 @@ __global__ void __launch_bounds__(sscga_max_threads(sizeof(T), LC), 1) sscga_ker
     fc.in_smem = fc.P <= a.pcap;
     if (fc.in_smem) {
       const V* gains = reinterpret_cast<const V*>(a.ph);
-      for (int i = tid; i < fc.P; i += blockDim.x) {
-        PathEnt<T> e;
-        e.dk = a.K0 - __ldg(a.pk + fc.P0 + i);
-        e.dl = a.L0 - __ldg(a.pl + fc.P0 + i);
-        e.h = __ldg(gains + fc.P0 + i);
-        sm.ptab[i] = e;
-      }
+      for (int i = tid; i < fc.P; i += blockDim.x)
+        sm.ptab[i] = make_path(a, sm, __ldg(a.pk + fc.P0 + i), __ldg(a.pl + fc.P0 + i), __ldg(gains + fc.P0 + i));
     }
     const T lam = lamv[f];
     __syncthreads();
@@ -314,14 +399,16 @@ __global__ void __launch_bounds__(sscga_max_threads(sizeof(T), LC), 1) sscga_ker
       if (!fc.halo) fc.lo_p = fc.hi_p = fc.lo_u = fc.hi_u = 0;
     }
 
+    const int RS = a.RS;
+    const int gcol = cx.g * LC;
+    V* xrow = sm.x + cx.k * RS + gcol;  // this thread's run of x
+
     // y -> ext_u (own columns); b = H^H y is gathered from it
+    V w[LC];
     if (cx.active) {
 #pragma unroll
-      for (int j = 0; j < LC; ++j) {
-        const int lc = cx.g * LC + j;
-        put_ext<T>(sm.u, S, fc.lo_u, fc.hi_u, M, cx.k, lc, cx.colbase + j,
-                   y[fo + (size_t)(cx.colbase + j) * M + cx.k], sm.tw);
-      }
+      for (int j = 0; j < LC; ++j) w[j] = y[fo + (size_t)(cx.colbase + j) * M + cx.k];
+      put_ext<T, LC>(sm.u, RS, fc.lo_u, fc.hi_u, M, cx, w, sm.tw);
     }
     if (lead && a.berr) a.berr[f] = 0;
     cl_sync<T>(a.C);
@@ -332,14 +419,15 @@ __global__ void __launch_bounds__(sscga_max_threads(sizeof(T), LC), 1) sscga_ker
     T part = T(0);
 #pragma unroll
     for (int j = 0; j < LC; ++j) {
-      const V b = A::get(acc[j]);
-      c[j] = b;
-      if (cx.active) {
-        const int lc = cx.g * LC + j;
-        put_ext<T>(sm.p, S, fc.lo_p, fc.hi_p, M, cx.k, lc, cx.colbase + j, b, sm.tw);
-        sm.x[lc * M + cx.k] = czero<V>();
-        part += cabs2(b);
-      }
+      c[j] = A::get(acc[j]);
+      part += cabs2(c[j]);
+      w[j] = czero<V>();
+    }
+    if (cx.active) {
+      put_ext<T, LC>(sm.p, RS, fc.lo_p, fc.hi_p, M, cx, c, sm.tw);
+      store_run<T, LC>(xrow, w);
+    } else {
+      part = T(0);
     }
     T cn = cluster_sum<T>(part, sm.red + (0 * 2 + par[0]) * 32, a.C, nwarps, lane, warp);
     par[0] ^= 1;
@@ -353,12 +441,11 @@ __global__ void __launch_bounds__(sscga_max_threads(sizeof(T), LC), 1) sscga_ker
       part = T(0);
 #pragma unroll
       for (int j = 0; j < LC; ++j) {
-        if (cx.active) {
-          const V uj = A::get(acc[j]);
-          put_ext<T>(sm.u, S, fc.lo_u, fc.hi_u, M, cx.k, cx.g * LC + j, cx.colbase + j, uj, sm.tw);
-          part += cabs2(uj);
-        }
+        w[j] = A::get(acc[j]);
+        part += cabs2(w[j]);
       }
+      if (cx.active) put_ext<T, LC>(sm.u, RS, fc.lo_u, fc.hi_u, M, cx, w, sm.tw);
+      else part = T(0);
       const T uu = cluster_sum<T>(part, sm.red + (1 * 2 + par[1]) * 32, a.C, nwarps, lane, warp);
       par[1] ^= 1;
       const T denom = uu + lam * pp;
@@ -369,19 +456,25 @@ __global__ void __launch_bounds__(sscga_max_threads(sizeof(T), LC), 1) sscga_ker
       const T alpha = cn / denom;
       ss_mvm<T, LC, true>(a, cx, sm, fc, sm.u, fc.lo_u, acc);  // H^H u
       part = T(0);
+      V pv[LC], xv[LC];
+      load_run<T, LC>(sm.p + (fc.lo_p + cx.k) * RS + gcol, pv);
+      load_run<T, LC>(xrow, xv);
 #pragma unroll
       for (int j = 0; j < LC; ++j) {
-        if (cx.active) {
-          const int lc = cx.g * LC + j;
-          const V pj = sm.p[lc * S + fc.lo_p + cx.k];
-          const V ap = cadd(A::get(acc[j]), cscale(pj, lam));
-          const V xj = cadd(sm.x[lc * M + cx.k], cscale(pj, alpha));
-          sm.x[lc * M + cx.k] = xj;
-          c[j] = csub(c[j], cscale(ap, alpha));
-          part += cabs2(c[j]);
-          if (snaps)
-            snaps[((size_t)f * a.iters + it) * a.MN + (size_t)(cx.colbase + j) * M + cx.k] = xj;
+        const V ap = cadd(A::get(acc[j]), cscale(pv[j], lam));
+        xv[j] = cadd(xv[j], cscale(pv[j], alpha));
+        c[j] = csub(c[j], cscale(ap, alpha));
+        part += cabs2(c[j]);
+      }
+      if (cx.active) {
+        store_run<T, LC>(xrow, xv);
+        if (snaps) {
+#pragma unroll
+          for (int j = 0; j < LC; ++j)
+            snaps[((size_t)f * a.iters + it) * a.MN + (size_t)(cx.colbase + j) * M + cx.k] = xv[j];
         }
+      } else {
+        part = T(0);
       }
       const T nn = cluster_sum<T>(part, sm.red + (2 * 2 + par[2]) * 32, a.C, nwarps, lane, warp);
       par[2] ^= 1;
@@ -389,13 +482,11 @@ __global__ void __launch_bounds__(sscga_max_threads(sizeof(T), LC), 1) sscga_ker
       part = T(0);
 #pragma unroll
       for (int j = 0; j < LC; ++j) {
-        if (cx.active) {
-          const int lc = cx.g * LC + j;
-          const V pj = cadd(c[j], cscale(sm.p[lc * S + fc.lo_p + cx.k], beta));
-          put_ext<T>(sm.p, S, fc.lo_p, fc.hi_p, M, cx.k, lc, cx.colbase + j, pj, sm.tw);
-          part += cabs2(pj);
-        }
+        pv[j] = cadd(c[j], cscale(pv[j], beta));
+        part += cabs2(pv[j]);
       }
+      if (cx.active) put_ext<T, LC>(sm.p, RS, fc.lo_p, fc.hi_p, M, cx, pv, sm.tw);
+      else part = T(0);
       cn = nn;
       done = it + 1;
       if (lead && cnorm) cnorm[(size_t)f * stride + done] = cn;
@@ -418,10 +509,10 @@ __global__ void __launch_bounds__(sscga_max_threads(sizeof(T), LC), 1) sscga_ker
     }
     int errs = 0;
     if (cx.active) {
-#pragma unroll
+#pragma unroll 1
       for (int j = 0; j < LC; ++j) {
         const size_t q = fo + (size_t)(cx.colbase + j) * M + cx.k;
-        const V xj = sm.x[(cx.g * LC + j) * M + cx.k];
+        const V xj = xrow[j];
         xo[q] = xj;
         if (a.bps) {
           const int lab = qam_demod_symbol<T>(xj.x, xj.y, a.bps, scale, a.llr ? a.llr + q * a.bps : nullptr);

@@ -1,0 +1,59 @@
+"""Opt-in rebinding of a loaded `ddlink` package onto the B200 kernels.
+
+    import ddlink, paper_2604_02266_b200.patch as p
+    p.install(ddlink)               # hot-path names now run on the GPU
+
+or, for the reference's own test-suite, load it as a pytest plugin *before*
+the test modules import their names:
+
+    pytest -p paper_2604_02266_b200.pytest_plugin /path/to/ddlink/tests
+
+Rebinds the names the reference binds at import time:
+ddlink.sparse.{detect_paths, build_ss_channel, ss_mvm, ss_mvm_hermitian,
+forward_index, inverse_index, coefficient}, ddlink.equalize.cga_equalize,
+ddlink.harness.cga_equalize (bound by name, harness.py:23), ddlink.grid.hard_demod
+and the package-level re-exports (__init__.py:14-63).  EmptyChannel stays the
+reference's class so run_packet's handler (harness.py:170) still catches it.
+"""
+
+from __future__ import annotations
+
+import importlib
+
+from . import equalize as _eq
+from . import grid as _gr
+from . import sparse as _sp
+
+_SPARSE = ("detect_paths", "build_ss_channel", "ss_mvm", "ss_mvm_hermitian",
+           "forward_index", "inverse_index", "coefficient")
+
+
+def install(ddlink_module=None, precision: str = "fp64") -> dict:
+    """Patch ddlink in place; returns the original bindings for `uninstall`."""
+    d = ddlink_module if ddlink_module is not None else importlib.import_module("ddlink")
+    sparse = importlib.import_module(d.__name__ + ".sparse")
+    equalize = importlib.import_module(d.__name__ + ".equalize")
+    grid = importlib.import_module(d.__name__ + ".grid")
+    harness = importlib.import_module(d.__name__ + ".harness")
+    _eq.set_precision(precision)
+    _sp.EmptyChannel = sparse.EmptyChannel  # keep the reference's exception type
+    saved = {}
+
+    def bind(mod, name, fn):
+        saved[(mod.__name__, name)] = getattr(mod, name)
+        setattr(mod, name, fn)
+
+    for name in _SPARSE:
+        bind(sparse, name, getattr(_sp, name))
+        bind(d, name, getattr(_sp, name))
+    bind(equalize, "cga_equalize", _eq.cga_equalize)
+    bind(harness, "cga_equalize", _eq.cga_equalize)
+    bind(d, "cga_equalize", _eq.cga_equalize)
+    bind(grid, "hard_demod", _gr.hard_demod)
+    bind(d, "hard_demod", _gr.hard_demod)
+    return saved
+
+
+def uninstall(saved: dict) -> None:
+    for (modname, name), fn in saved.items():
+        setattr(importlib.import_module(modname), name, fn)

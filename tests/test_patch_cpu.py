@@ -1,0 +1,37 @@
+"""The opt-in ddlink patcher rebinds the hot-path names (CPU only; skipped
+where the reference package is not importable, e.g. on the GPU box)."""
+
+import sys
+
+import pytest
+
+REF = "/root/reference/pkg/src"
+
+
+@pytest.fixture
+def ddlink():
+    if REF not in sys.path:
+        sys.path.insert(0, REF)
+    return pytest.importorskip("ddlink")
+
+
+def test_install_and_uninstall(ddlink):
+    import paper_2604_02266_b200 as b200
+    from paper_2604_02266_b200 import patch
+
+    orig_cga = ddlink.harness.cga_equalize
+    saved = patch.install(ddlink)
+    try:
+        assert ddlink.harness.cga_equalize is b200.cga_equalize
+        assert ddlink.equalize.cga_equalize is b200.cga_equalize
+        assert ddlink.sparse.build_ss_channel is b200.build_ss_channel
+        assert ddlink.grid.hard_demod is b200.hard_demod
+        assert ddlink.detect_paths is b200.detect_paths
+        # the reference's EmptyChannel is what the drop-in raises (harness.py:170)
+        with pytest.raises(ddlink.EmptyChannel):
+            b200.build_ss_channel([], ddlink.GridConfig(8, 4))
+    finally:
+        patch.uninstall(saved)
+        import paper_2604_02266_b200.sparse as sp
+        sp.EmptyChannel = b200.EmptyChannel
+    assert ddlink.harness.cga_equalize is orig_cga
