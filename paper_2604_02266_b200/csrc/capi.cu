@@ -87,7 +87,12 @@ int32_t make_plan(int32_t M, int32_t N, int32_t dtype, ddb::LaunchShape* s) {
       s->tl = TL;
       s->th = TH;
       s->pcap = pcap;
+      s->tcols = ddb::sscga_tmem_cols(s->threads, best, eb);
       s->smem = (int)ddb::sscga_layout(M, N, C, eb, (int)h, TL, TH, pcap).total;
+      // keep (CTAs per SM) x (TMEM columns per CTA) <= 512 so tcgen05.alloc never
+      // waits on a co-resident CTA: pad tiny CTAs' shared memory accordingly
+      const int floor_smem = 456 * s->tcols;
+      if (s->smem < floor_smem) s->smem = floor_smem;
       return DDB_OK;
     }
   }
@@ -184,6 +189,7 @@ int32_t ddb_sscga_solve(const ddb_sscga_problem* prob, const ddb_sscga_outputs* 
   a.TL = s.tl;
   a.TH = s.th;
   a.pcap = s.pcap;
+  a.tcols = s.tcols;
   a.off = prob->path_offsets;
   a.pk = prob->path_k;
   a.pl = prob->path_l;

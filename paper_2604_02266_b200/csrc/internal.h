@@ -19,6 +19,7 @@ struct SolveArgs {
   int H;              // quasi-periodic halo capacity (rows) of p/u
   int TL, TH;         // two-level W_MN twiddle tables: e = hi * TL + lo
   int pcap;           // per-frame tap table capacity in shared memory
+  int tcols;          // TMEM columns allocated per CTA (x lives in TMEM)
   const int* off;
   const int* pk;
   const int* pl;
@@ -39,8 +40,17 @@ struct SolveArgs {
 };
 
 struct LaunchShape {
-  int cluster, lcta, lc, threads, smem, halo, tl, th, pcap;
+  int cluster, lcta, lc, threads, smem, halo, tl, th, pcap, tcols;
 };
+
+// TMEM columns for x: (warps per lane quarter) x (32-bit words per thread run),
+// rounded to the allocator's power-of-two granularity (>= 32).
+constexpr int sscga_tmem_cols(int threads, int lc, int elem_bytes) {
+  int need = ((threads / 32 + 3) / 4) * lc * 2 * elem_bytes / 4;
+  int c = 32;
+  while (c < need) c *= 2;
+  return c;
+}
 
 // Thread ceiling of the fused kernel instantiation (its __launch_bounds__):
 // per-thread column runs of >= 32 bytes of real data need > 64 registers,

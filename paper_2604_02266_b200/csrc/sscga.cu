@@ -71,7 +71,7 @@ struct FrameCtx {
 template <typename T> struct Sm {
   Vec<T>* p;
   Vec<T>* u;
-  Vec<T>* x;
+  uint32_t* tslot;
   Vec<T>* tlo;
   Vec<T>* thi;
   Vec<T>* tw;
@@ -203,6 +203,48 @@ __device__ __forceinline__ void ss_mvm(const SolveArgs& a, const Ctx& cx, const 
   }
 }
 
+// x chunks in TMEM: NE complex elements = NE * sizeof(V) / 4 lane-local columns.
+template <typename T, int NE>
+__device__ __forceinline__ void x_load(uint32_t ta, Vec<T> (&v)[NE]) {
+  constexpr int W = NE * (int)sizeof(Vec<T>) / 4;
+  uint32_t r[W];
+  tmem_ld<W>(ta, r);
+  tmem_wait_ld();
+#pragma unroll
+  for (int j = 0; j < NE; ++j) {
+    if constexpr (sizeof(T) == 4) {
+      v[j] = make_float2(__uint_as_float(r[2 * j]), __uint_as_float(r[2 * j + 1]));
+    } else {
+      v[j] = make_double2(__hiloint2double((int)r[4 * j + 1], (int)r[4 * j]),
+                          __hiloint2double((int)r[4 * j + 3], (int)r[4 * j + 2]));
+    }
+  }
+}
+template <typename T, int NE>
+__device__ __forceinline__ void x_store(uint32_t ta, const Vec<T> (&v)[NE]) {
+  constexpr int W = NE * (int)sizeof(Vec<T>) / 4;
+  uint32_t r[W];
+#pragma unroll
+  for (int j = 0; j < NE; ++j) {
+    if constexpr (sizeof(T) == 4) {
+      r[2 * j] = __float_as_uint(v[j].x);
+      r[2 * j + 1] = __float_as_uint(v[j].y);
+    } else {
+      r[4 * j] = (uint32_t)__double2loint(v[j].x);
+      r[4 * j + 1] = (uint32_t)__double2hiint(v[j].x);
+      r[4 * j + 2] = (uint32_t)__double2loint(v[j].y);
+      r[4 * j + 3] = (uint32_t)__double2hiint(v[j].y);
+    }
+  }
+  tmem_st<W>(ta, r);
+  tmem_wait_st();
+}
+// elements per TMEM chunk: 16 columns (8 fp32 / 4 fp64 complex), or the whole run
+template <typename T, int LC> constexpr int x_chunk() {
+  constexpr int e = 16 / ((int)sizeof(Vec<T>) / 4);
+  return LC < e ? LC : e;
+}
+
 // Run helpers for a thread's own LC contiguous elements of one row.
 template <typename T, int LC>
 __device__ __forceinline__ void load_run(const Vec<T>* rp, Vec<T> (&v)[LC]) {
@@ -286,7 +328,7 @@ __host__ __device__ static inline SmemLayout layout_impl(int M, int N, int C, in
   size_t o = 0;
   L.p = o; o = align16(o + rs * (size_t)(M + H) * vb);
   L.u = o; o = align16(o + rs * (size_t)(M + H) * vb);
-  L.x = o; o = align16(o + rs * (size_t)M * vb);
+  L.x = o; o = align16(o + 16);  // TMEM base-address slot (x itself lives in TMEM)
   L.tlo = o; o = align16(o + (size_t)TL * vb);
   L.thi = o; o = align16(o + (size_t)TH * vb);
   L.tw = o; o = align16(o + (size_t)N * vb);
@@ -317,7 +359,7 @@ __global__ void __launch_bounds__(sscga_max_threads(sizeof(T), LC), 1) sscga_ker
   Sm<T> sm;
   sm.p = reinterpret_cast<V*>(smem + L.p);
   sm.u = reinterpret_cast<V*>(smem + L.u);
-  sm.x = reinterpret_cast<V*>(smem + L.x);
+  sm.tslot = reinterpret_cast<uint32_t*>(smem + L.x);
   sm.tlo = reinterpret_cast<V*>(smem + L.tlo);
   sm.thi = reinterpret_cast<V*>(smem + L.thi);
   sm.tw = reinterpret_cast<V*>(smem + L.tw);
@@ -337,7 +379,14 @@ __global__ void __launch_bounds__(sscga_max_threads(sizeof(T), LC), 1) sscga_ker
   for (int i = tid; i < a.TL; i += blockDim.x) sm.tlo[i] = twiddle(T(0), i, a.MN);
   for (int i = tid; i < a.TH; i += blockDim.x) sm.thi[i] = twiddle(T(0), (int)(((long long)i * a.TL) % a.MN), a.MN);
   for (int l = tid; l < N; l += blockDim.x) sm.tw[l] = twiddle(T(0), l, N);
+  // x lives in TMEM: warp w uses lanes 32 (w % 4) .. + 31, columns (w / 4) * XW ..
+  constexpr int XW = LC * (int)sizeof(V) / 4;  // 32-bit columns per thread run
+  if (warp == 0) tmem_alloc(sm.tslot, (uint32_t)a.tcols);
+  tmem_fence_before();
   __syncthreads();
+  tmem_fence_after();
+  const uint32_t tbase = *sm.tslot;
+  const uint32_t xta = tbase + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)((warp >> 2) * XW);
 
   const V* y = reinterpret_cast<const V*>(a.y);
   V* xo = reinterpret_cast<V*>(a.x);
@@ -401,7 +450,8 @@ __global__ void __launch_bounds__(sscga_max_threads(sizeof(T), LC), 1) sscga_ker
 
     const int RS = a.RS;
     const int gcol = cx.g * LC;
-    V* xrow = sm.x + cx.k * RS + gcol;  // this thread's run of x
+    constexpr int XC = x_chunk<T, LC>();       // x elements per TMEM access
+    constexpr int XCW = XC * (int)sizeof(V) / 4;
 
     // y -> ext_u (own columns); b = H^H y is gathered from it
     V w[LC];
@@ -423,11 +473,14 @@ __global__ void __launch_bounds__(sscga_max_threads(sizeof(T), LC), 1) sscga_ker
       part += cabs2(c[j]);
       w[j] = czero<V>();
     }
-    if (cx.active) {
-      put_ext<T, LC>(sm.p, RS, fc.lo_p, fc.hi_p, M, cx, c, sm.tw);
-      store_run<T, LC>(xrow, w);
-    } else {
-      part = T(0);
+    if (cx.active) put_ext<T, LC>(sm.p, RS, fc.lo_p, fc.hi_p, M, cx, c, sm.tw);
+    else part = T(0);
+    {
+      V z[XC];
+#pragma unroll
+      for (int j = 0; j < XC; ++j) z[j] = czero<V>();
+#pragma unroll
+      for (int c0 = 0; c0 < LC; c0 += XC) x_store<T, XC>(xta + (uint32_t)((c0 / XC) * XCW), z);  // x = 0
     }
     T cn = cluster_sum<T>(part, sm.red + (0 * 2 + par[0]) * 32, a.C, nwarps, lane, warp);
     par[0] ^= 1;
@@ -456,26 +509,28 @@ __global__ void __launch_bounds__(sscga_max_threads(sizeof(T), LC), 1) sscga_ker
       const T alpha = cn / denom;
       ss_mvm<T, LC, true>(a, cx, sm, fc, sm.u, fc.lo_u, acc);  // H^H u
       part = T(0);
-      V pv[LC], xv[LC];
+      V pv[LC];
       load_run<T, LC>(sm.p + (fc.lo_p + cx.k) * RS + gcol, pv);
-      load_run<T, LC>(xrow, xv);
 #pragma unroll
-      for (int j = 0; j < LC; ++j) {
-        const V ap = cadd(A::get(acc[j]), cscale(pv[j], lam));
-        xv[j] = cadd(xv[j], cscale(pv[j], alpha));
-        c[j] = csub(c[j], cscale(ap, alpha));
-        part += cabs2(c[j]);
-      }
-      if (cx.active) {
-        store_run<T, LC>(xrow, xv);
-        if (snaps) {
+      for (int c0 = 0; c0 < LC; c0 += XC) {
+        V xv[XC];
+        const uint32_t ta = xta + (uint32_t)((c0 / XC) * XCW);
+        x_load<T, XC>(ta, xv);
 #pragma unroll
-          for (int j = 0; j < LC; ++j)
-            snaps[((size_t)f * a.iters + it) * a.MN + (size_t)(cx.colbase + j) * M + cx.k] = xv[j];
+        for (int j = 0; j < XC; ++j) {
+          const V ap = cadd(A::get(acc[c0 + j]), cscale(pv[c0 + j], lam));
+          xv[j] = cadd(xv[j], cscale(pv[c0 + j], alpha));
+          c[c0 + j] = csub(c[c0 + j], cscale(ap, alpha));
+          part += cabs2(c[c0 + j]);
         }
-      } else {
-        part = T(0);
+        x_store<T, XC>(ta, xv);
+        if (snaps && cx.active) {
+#pragma unroll
+          for (int j = 0; j < XC; ++j)
+            snaps[((size_t)f * a.iters + it) * a.MN + (size_t)(cx.colbase + c0 + j) * M + cx.k] = xv[j];
+        }
       }
+      if (!cx.active) part = T(0);
       const T nn = cluster_sum<T>(part, sm.red + (2 * 2 + par[2]) * 32, a.C, nwarps, lane, warp);
       par[2] ^= 1;
       const T beta = nn / cn;
@@ -508,16 +563,21 @@ __global__ void __launch_bounds__(sscga_max_threads(sizeof(T), LC), 1) sscga_ker
       scale = nv > T(0) ? T(1) / nv : T(1);
     }
     int errs = 0;
-    if (cx.active) {
 #pragma unroll 1
-      for (int j = 0; j < LC; ++j) {
-        const size_t q = fo + (size_t)(cx.colbase + j) * M + cx.k;
-        const V xj = xrow[j];
-        xo[q] = xj;
-        if (a.bps) {
-          const int lab = qam_demod_symbol<T>(xj.x, xj.y, a.bps, scale, a.llr ? a.llr + q * a.bps : nullptr);
-          if (a.labels) a.labels[q] = (uint8_t)lab;
-          if (a.txl) errs += __popc((unsigned)(lab ^ a.txl[q]));
+    for (int c0 = 0; c0 < LC; c0 += XC) {
+      V xv[XC];
+      x_load<T, XC>(xta + (uint32_t)((c0 / XC) * XCW), xv);
+      if (cx.active) {
+#pragma unroll 1
+        for (int j = 0; j < XC; ++j) {
+          const size_t q = fo + (size_t)(cx.colbase + c0 + j) * M + cx.k;
+          const V xj = xv[j];
+          xo[q] = xj;
+          if (a.bps) {
+            const int lab = qam_demod_symbol<T>(xj.x, xj.y, a.bps, scale, a.llr ? a.llr + q * a.bps : nullptr);
+            if (a.labels) a.labels[q] = (uint8_t)lab;
+            if (a.txl) errs += __popc((unsigned)(lab ^ a.txl[q]));
+          }
         }
       }
     }
@@ -526,6 +586,10 @@ __global__ void __launch_bounds__(sscga_max_threads(sizeof(T), LC), 1) sscga_ker
       if (lane == 0 && errs) atomicAdd(a.berr + f, errs);
     }
   }
+  // no CTA may leave while a peer can still read its shared memory (DSMEM)
+  tmem_fence_before();
+  cl_sync<T>(a.C);
+  if (warp == 0) tmem_dealloc(tbase, (uint32_t)a.tcols);
 }
 
 template <typename T, int LC>

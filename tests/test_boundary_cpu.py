@@ -32,7 +32,7 @@ def test_library_is_sm100a(lib):
 
 @pytest.mark.parametrize("M,N,dt,cluster", [
     (64, 16, nat.DDB_F32, 1), (256, 16, nat.DDB_F32, 1), (512, 32, nat.DDB_F32, 2),
-    (512, 32, nat.DDB_F64, 4), (128, 32, nat.DDB_F64, 2), (8, 2, nat.DDB_F64, 1),
+    (512, 32, nat.DDB_F64, 4), (128, 32, nat.DDB_F64, 1), (8, 2, nat.DDB_F64, 1),
 ])
 def test_plan_without_gpu(lib, M, N, dt, cluster):
     p = nat.plan(M, N, dt)
