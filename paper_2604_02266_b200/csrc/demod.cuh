@@ -3,77 +3,86 @@
 // odd ones Q; per axis the Gray PAM levels follow TS 38.211 in the recursive
 // form of grid.py:98-109,
 //     level(c0..c_{ba-1}) = (1 - 2 c0) * mag,  mag = 2^{ba-m} - (1 - 2 c_m) mag'
-// with unit mean symbol energy (norm sqrt(2 (4^ba - 1) / 3): sqrt2, sqrt10,
-// sqrt42).  ba = 1, 2 reproduce qpsk / qam16 exactly; ba = 3 (64-QAM) is the
-// build extension the north star asks for (the reference rejects qam64,
-// tests/test_grid.py:85-87), so its parity is pinned only through the
-// LLR-sign == hard-decision identity.
+// divided by the rms norm sqrt(2 (4^ba - 1) / 3) (sqrt2, sqrt10, sqrt42), as
+// make_constellation does (grid.py:151).  ba = 1, 2 reproduce qpsk / qam16
+// exactly; ba = 3 (64-QAM) is the build extension the north star asks for
+// (the reference rejects qam64, tests/test_grid.py:85-87), so its parity is
+// pinned only through the LLR-sign == hard-decision identity.
 //
-// Nearest-point decisions for a separable Gray grid reduce to a per-axis
-// argmin; taking the lowest axis index on ties reproduces the lowest-label
-// tie rule of hard_demod (grid.py:172-183).
+// Nearest-point decisions on a separable Gray grid reduce to a per-axis
+// argmin; taking the lowest axis index on ties reproduces hard_demod's
+// lowest-label tie rule (grid.py:172-183).  Everything is specialised on the
+// bits per axis at compile time, so the levels are immediates.
 #pragma once
 
 #include "common.cuh"
 
 namespace ddb {
 
-__device__ __forceinline__ int qam_axis_level(int i, int ba) {
+template <int BA> __host__ __device__ constexpr int qam_level(int i) {
   int mag = 1;
-  for (int m = ba - 1; m >= 1; --m) {
-    const int cm = (i >> (ba - 1 - m)) & 1;
-    mag = (1 << (ba - m)) - (1 - 2 * cm) * mag;
+  for (int m = BA - 1; m >= 1; --m) {
+    const int cm = (i >> (BA - 1 - m)) & 1;
+    mag = (1 << (BA - m)) - (1 - 2 * cm) * mag;
   }
-  const int c0 = (i >> (ba - 1)) & 1;
-  return (1 - 2 * c0) * mag;
+  return (1 - 2 * ((i >> (BA - 1)) & 1)) * mag;
+}
+template <int BA> __host__ __device__ constexpr double qam_norm() {
+  return BA == 1 ? 1.4142135623730951 : (BA == 2 ? 3.1622776601683795 : 6.48074069840786);
 }
 
-// One axis: v is the normalised component.  Writes the axis index (bits MSB
-// first) and, if llr != nullptr, ba LLRs with stride 2 (interleaved I/Q).
-template <typename T>
-__device__ __forceinline__ int qam_axis(T v, int ba, T inv_norm, T scale, float* llr) {
-  T dmin1[3], dmin0[3];
+// One axis: returns the axis index (bits MSB first); writes BA LLRs to llr[2m]
+// (interleaved with the other axis) when llr != nullptr.
+template <typename T, int BA>
+__device__ __forceinline__ int qam_axis(T v, T scale, float* llr) {
+  constexpr int L = 1 << BA;
+  T d[L];
 #pragma unroll
-  for (int m = 0; m < 3; ++m) { dmin1[m] = T(3.0e38); dmin0[m] = dmin1[m]; }
-  int best = 0;
-  T bestd = T(0);
-  const int nlev = 1 << ba;
-  for (int i = 0; i < nlev; ++i) {
-    const T a = T(qam_axis_level(i, ba)) * inv_norm;
-    const T d = (v - a) * (v - a);
-    if (i == 0 || d < bestd) { bestd = d; best = i; }
-#pragma unroll
-    for (int m = 0; m < 3; ++m) {
-      if (m < ba) {
-        if ((i >> (ba - 1 - m)) & 1) dmin1[m] = d < dmin1[m] ? d : dmin1[m];
-        else dmin0[m] = d < dmin0[m] ? d : dmin0[m];
-      }
-    }
+  for (int i = 0; i < L; ++i) {
+    const T a = T((double)qam_level<BA>(i) / qam_norm<BA>());
+    d[i] = (v - a) * (v - a);
   }
+  int best = 0;
+  T bestd = d[0];
+#pragma unroll
+  for (int i = 1; i < L; ++i)
+    if (d[i] < bestd) { bestd = d[i]; best = i; }
   if (llr) {
 #pragma unroll
-    for (int m = 0; m < 3; ++m)
-      if (m < ba) llr[2 * m] = (float)((dmin1[m] - dmin0[m]) * scale);
+    for (int m = 0; m < BA; ++m) {
+      T d1 = T(3.0e38), d0 = T(3.0e38);
+#pragma unroll
+      for (int i = 0; i < L; ++i) {
+        if ((i >> (BA - 1 - m)) & 1) d1 = d[i] < d1 ? d[i] : d1;
+        else d0 = d[i] < d0 ? d[i] : d0;
+      }
+      llr[2 * m] = (float)((d1 - d0) * scale);
+    }
   }
   return best;
 }
 
-// Returns the constellation label of x; writes bps LLRs to llr if non-null.
-template <typename T>
-__device__ __forceinline__ int qam_demod_symbol(T re, T im, int bps, T scale, float* llr) {
-  const int ba = bps >> 1;
-  const T norm2 = T(2) * T((1 << (2 * ba)) - 1) / T(3);
-  const T inv_norm = T(1) / sqrt(norm2);
-  const int ii = qam_axis<T>(re, ba, inv_norm, scale, llr);
-  const int qi = qam_axis<T>(im, ba, inv_norm, scale, llr ? llr + 1 : nullptr);
+template <typename T, int BA>
+__device__ __forceinline__ int qam_symbol(T re, T im, T scale, float* llr) {
+  const int ii = qam_axis<T, BA>(re, scale, llr);
+  const int qi = qam_axis<T, BA>(im, scale, llr ? llr + 1 : nullptr);
   int label = 0;
-  for (int m = 0; m < ba; ++m) {
-    const int cm = (ii >> (ba - 1 - m)) & 1;
-    const int dm = (qi >> (ba - 1 - m)) & 1;
-    label |= cm << (bps - 1 - 2 * m);
-    label |= dm << (bps - 2 - 2 * m);
+#pragma unroll
+  for (int m = 0; m < BA; ++m) {
+    label |= ((ii >> (BA - 1 - m)) & 1) << (2 * BA - 1 - 2 * m);
+    label |= ((qi >> (BA - 1 - m)) & 1) << (2 * BA - 2 - 2 * m);
   }
   return label;
+}
+
+// Runtime-dispatched form (standalone kernels); bps in {2, 4, 6}.
+template <typename T>
+__device__ __forceinline__ int qam_demod_symbol(T re, T im, int bps, T scale, float* llr) {
+  switch (bps) {
+    case 2: return qam_symbol<T, 1>(re, im, scale, llr);
+    case 4: return qam_symbol<T, 2>(re, im, scale, llr);
+    default: return qam_symbol<T, 3>(re, im, scale, llr);
+  }
 }
 
 }  // namespace ddb

@@ -43,10 +43,10 @@ struct LaunchShape {
   int cluster, lcta, lc, threads, smem, halo, tl, th, pcap, tcols;
 };
 
-// TMEM columns for x: (warps per lane quarter) x (32-bit words per thread run),
-// rounded to the allocator's power-of-two granularity (>= 32).
+// TMEM columns for x and c: (warps per lane quarter) x 2 runs x (32-bit words
+// per run), rounded to the allocator's power-of-two granularity (>= 32).
 constexpr int sscga_tmem_cols(int threads, int lc, int elem_bytes) {
-  int need = ((threads / 32 + 3) / 4) * lc * 2 * elem_bytes / 4;
+  int need = ((threads / 32 + 3) / 4) * 2 * lc * 2 * elem_bytes / 4;
   int c = 32;
   while (c < need) c *= 2;
   return c;

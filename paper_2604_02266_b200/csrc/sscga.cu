@@ -349,6 +349,40 @@ void twiddle_split(int MN, int* TL, int* TH) {
   *TH = (MN + tl - 1) / tl;
 }
 
+// Epilogue for XC equalized symbols at global indices q0 + j M: x_hat, hard
+// labels, max-log LLRs (vector stores) and the bit-error count vs TX labels.
+template <typename T, int BA, int XC>
+__device__ __forceinline__ int epilogue(const SolveArgs& a, const Vec<T> (&xv)[XC], size_t q0, int M, T scale) {
+  Vec<T>* xo = reinterpret_cast<Vec<T>*>(a.x);
+  int errs = 0;
+  uint8_t tx[XC];
+  if (BA > 0 && a.txl) {
+#pragma unroll
+    for (int j = 0; j < XC; ++j) tx[j] = a.txl[q0 + (size_t)j * M];
+  }
+#pragma unroll
+  for (int j = 0; j < XC; ++j) {
+    const size_t q = q0 + (size_t)j * M;
+    xo[q] = xv[j];
+    if constexpr (BA > 0) {
+      float l[2 * BA];
+      const int lab = qam_symbol<T, BA>(xv[j].x, xv[j].y, scale, l);
+      if (a.llr) {
+        float* dst = a.llr + q * (2 * BA);
+        if constexpr (BA == 2) {
+          *reinterpret_cast<float4*>(dst) = make_float4(l[0], l[1], l[2], l[3]);
+        } else {
+#pragma unroll
+          for (int m = 0; m < BA; ++m) reinterpret_cast<float2*>(dst)[m] = make_float2(l[2 * m], l[2 * m + 1]);
+        }
+      }
+      if (a.labels) a.labels[q] = (uint8_t)lab;
+      if (a.txl) errs += __popc((unsigned)(lab ^ tx[j]));
+    }
+  }
+  return errs;
+}
+
 template <typename T, int LC>
 __global__ void __launch_bounds__(sscga_max_threads(sizeof(T), LC), 1) sscga_kernel(const SolveArgs a) {
   using V = Vec<T>;
@@ -379,14 +413,16 @@ __global__ void __launch_bounds__(sscga_max_threads(sizeof(T), LC), 1) sscga_ker
   for (int i = tid; i < a.TL; i += blockDim.x) sm.tlo[i] = twiddle(T(0), i, a.MN);
   for (int i = tid; i < a.TH; i += blockDim.x) sm.thi[i] = twiddle(T(0), (int)(((long long)i * a.TL) % a.MN), a.MN);
   for (int l = tid; l < N; l += blockDim.x) sm.tw[l] = twiddle(T(0), l, N);
-  // x lives in TMEM: warp w uses lanes 32 (w % 4) .. + 31, columns (w / 4) * XW ..
+  // x and the residual c live in TMEM: warp w uses lanes 32 (w % 4) .. + 31 and
+  // columns (w / 4) * 2 XW ..: first its x run, then its c run
   constexpr int XW = LC * (int)sizeof(V) / 4;  // 32-bit columns per thread run
   if (warp == 0) tmem_alloc(sm.tslot, (uint32_t)a.tcols);
   tmem_fence_before();
   __syncthreads();
   tmem_fence_after();
   const uint32_t tbase = *sm.tslot;
-  const uint32_t xta = tbase + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)((warp >> 2) * XW);
+  const uint32_t xta = tbase + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)((warp >> 2) * 2 * XW);
+  const uint32_t cta = xta + (uint32_t)XW;
 
   const V* y = reinterpret_cast<const V*>(a.y);
   V* xo = reinterpret_cast<V*>(a.x);
@@ -464,23 +500,27 @@ __global__ void __launch_bounds__(sscga_max_threads(sizeof(T), LC), 1) sscga_ker
     cl_sync<T>(a.C);
 
     typename A::type acc[LC];
-    V c[LC];
     ss_mvm<T, LC, true>(a, cx, sm, fc, sm.u, fc.lo_u, acc);  // b = H^H y (equalize.py:52)
     T part = T(0);
 #pragma unroll
     for (int j = 0; j < LC; ++j) {
-      c[j] = A::get(acc[j]);
-      part += cabs2(c[j]);
-      w[j] = czero<V>();
+      w[j] = A::get(acc[j]);
+      part += cabs2(w[j]);
     }
-    if (cx.active) put_ext<T, LC>(sm.p, RS, fc.lo_p, fc.hi_p, M, cx, c, sm.tw);
+    if (cx.active) put_ext<T, LC>(sm.p, RS, fc.lo_p, fc.hi_p, M, cx, w, sm.tw);
     else part = T(0);
     {
-      V z[XC];
+      V z[XC], cb[XC];
 #pragma unroll
-      for (int j = 0; j < XC; ++j) z[j] = czero<V>();
+      for (int c0 = 0; c0 < LC; c0 += XC) {
 #pragma unroll
-      for (int c0 = 0; c0 < LC; c0 += XC) x_store<T, XC>(xta + (uint32_t)((c0 / XC) * XCW), z);  // x = 0
+        for (int j = 0; j < XC; ++j) {
+          z[j] = czero<V>();
+          cb[j] = w[c0 + j];
+        }
+        x_store<T, XC>(xta + (uint32_t)((c0 / XC) * XCW), z);   // x = 0
+        x_store<T, XC>(cta + (uint32_t)((c0 / XC) * XCW), cb);  // c = b
+      }
     }
     T cn = cluster_sum<T>(part, sm.red + (0 * 2 + par[0]) * 32, a.C, nwarps, lane, warp);
     par[0] ^= 1;
@@ -513,17 +553,19 @@ __global__ void __launch_bounds__(sscga_max_threads(sizeof(T), LC), 1) sscga_ker
       load_run<T, LC>(sm.p + (fc.lo_p + cx.k) * RS + gcol, pv);
 #pragma unroll
       for (int c0 = 0; c0 < LC; c0 += XC) {
-        V xv[XC];
-        const uint32_t ta = xta + (uint32_t)((c0 / XC) * XCW);
-        x_load<T, XC>(ta, xv);
+        V xv[XC], cv[XC];
+        const uint32_t off = (uint32_t)((c0 / XC) * XCW);
+        x_load<T, XC>(xta + off, xv);
+        x_load<T, XC>(cta + off, cv);
 #pragma unroll
         for (int j = 0; j < XC; ++j) {
           const V ap = cadd(A::get(acc[c0 + j]), cscale(pv[c0 + j], lam));
           xv[j] = cadd(xv[j], cscale(pv[c0 + j], alpha));
-          c[c0 + j] = csub(c[c0 + j], cscale(ap, alpha));
-          part += cabs2(c[c0 + j]);
+          cv[j] = csub(cv[j], cscale(ap, alpha));
+          part += cabs2(cv[j]);
         }
-        x_store<T, XC>(ta, xv);
+        x_store<T, XC>(xta + off, xv);
+        x_store<T, XC>(cta + off, cv);
         if (snaps && cx.active) {
 #pragma unroll
           for (int j = 0; j < XC; ++j)
@@ -536,9 +578,14 @@ __global__ void __launch_bounds__(sscga_max_threads(sizeof(T), LC), 1) sscga_ker
       const T beta = nn / cn;
       part = T(0);
 #pragma unroll
-      for (int j = 0; j < LC; ++j) {
-        pv[j] = cadd(c[j], cscale(pv[j], beta));
-        part += cabs2(pv[j]);
+      for (int c0 = 0; c0 < LC; c0 += XC) {
+        V cv[XC];
+        x_load<T, XC>(cta + (uint32_t)((c0 / XC) * XCW), cv);
+#pragma unroll
+        for (int j = 0; j < XC; ++j) {
+          pv[c0 + j] = cadd(cv[j], cscale(pv[c0 + j], beta));
+          part += cabs2(pv[c0 + j]);
+        }
       }
       if (cx.active) put_ext<T, LC>(sm.p, RS, fc.lo_p, fc.hi_p, M, cx, pv, sm.tw);
       else part = T(0);
@@ -568,16 +615,12 @@ __global__ void __launch_bounds__(sscga_max_threads(sizeof(T), LC), 1) sscga_ker
       V xv[XC];
       x_load<T, XC>(xta + (uint32_t)((c0 / XC) * XCW), xv);
       if (cx.active) {
-#pragma unroll 1
-        for (int j = 0; j < XC; ++j) {
-          const size_t q = fo + (size_t)(cx.colbase + c0 + j) * M + cx.k;
-          const V xj = xv[j];
-          xo[q] = xj;
-          if (a.bps) {
-            const int lab = qam_demod_symbol<T>(xj.x, xj.y, a.bps, scale, a.llr ? a.llr + q * a.bps : nullptr);
-            if (a.labels) a.labels[q] = (uint8_t)lab;
-            if (a.txl) errs += __popc((unsigned)(lab ^ a.txl[q]));
-          }
+        const size_t q0 = fo + (size_t)(cx.colbase + c0) * M + cx.k;
+        switch (a.bps) {
+          case 0: epilogue<T, 0, XC>(a, xv, q0, M, scale); break;
+          case 2: errs += epilogue<T, 1, XC>(a, xv, q0, M, scale); break;
+          case 4: errs += epilogue<T, 2, XC>(a, xv, q0, M, scale); break;
+          default: errs += epilogue<T, 3, XC>(a, xv, q0, M, scale); break;
         }
       }
     }
