@@ -344,8 +344,9 @@ def main():
     hbm_gbs = io_bytes / (ms_step * 1e-3) / 1e9
     traffic = None
     ncu_sum = ROOT / "profiles" / f"ncu_{args.config}.json"
-    if ncu_sum.exists():
-        traffic = json.loads(ncu_sum.read_text()).get("dram_bytes_per_launch")
+    if ncu_sum.exists():  # per-frame DRAM bytes of the committed ncu --set full capture, scaled to this launch
+        per_frame = json.loads(ncu_sum.read_text()).get("dram_bytes_per_frame")
+        traffic = per_frame * B if per_frame else None
 
     # ---- single-frame latency: CUDA graph of a batch-1 solve, replayed
     latency = None

@@ -16,24 +16,27 @@
 // Doppler column, so a thread that owns one delay row and a run of columns
 // does, per tap, one table-twiddle and a run of pure gather-FMAs.  The
 // extension rows (a halo of H rows around the M real rows of every column) are
-// written whenever p or u is written, by the threads owning the rows they copy.
+// written whenever c or u is written, by the threads owning the rows they copy.
 // Closed forms checked against the reference tables in tests/test_oracle.py.
 //
 // Layout: frame q = l M + k (grid.py:86-95).  CTA r of the cluster owns the
 // Doppler columns [r Lcta, (r+1) Lcta); thread (k, g) owns delay row k of the
-// LC columns g LC .. g LC + LC - 1.  Shared memory: this CTA's columns of
-// ext_p (gathered by H), ext_u (gathered by H^H), x, the twiddle tables and the
-// frame's tap table.  The residual c and the accumulators live in registers.
-// A gather whose source column belongs to another CTA reads it through DSMEM
-// (mapa + ld.shared::cluster).  A frame whose taps span more delay rows than
-// the halo holds falls back to wrapping rows in registers (same results).
+// LC columns g LC .. g LC + LC - 1.  Shared memory holds this CTA's rows of
+// ext_c (gathered by H) and ext_u (gathered by H^H), row-major with the
+// thread's LC columns contiguous (128-bit conflict-free loads), plus the
+// twiddle tables and the frame's tap table.  x and p are only ever touched
+// elementwise and live in TMEM (tcgen05.ld/st); the MVM accumulators live in
+// registers.  A gather whose source column belongs to another CTA reads it
+// through DSMEM (mapa + ld.shared::cluster).  A frame whose taps span more
+// delay rows than the halo holds falls back to wrapping rows in registers.
 //
-// CG step, per iteration (equalize.py:59-76), three cluster barriers:
-//   u = H p;                 ||u||^2                           (barrier B)
+// CG step, per iteration (equalize.py:59-76), in the u-recurrence form that
+// needs two cluster barriers (u = H p is carried, never re-gathered from p):
+//   u = H c + beta u;  p = c + beta p;  ||u||^2, ||p||^2      (barrier B)
 //   denom = ||u||^2 + lam ||p||^2 = Re p^H (H^H H + lam I) p (equalize.py:60-64)
 //   denom == 0 -> exact convergence (equalize.py:64-67)
 //   ap = H^H u + lam p;  x += alpha p;  c -= alpha ap;  ||c||^2 (barrier C)
-//   p = c + beta p;          ||p||^2                           (barrier A)
+//   beta = ||c'||^2 / ||c||^2                                  (equalize.py:71-73)
 // Reductions are deterministic: every warp of every CTA sums the same per-warp
 // partials in the same order, so all CTAs take identical branches.
 #include <climits>
@@ -65,12 +68,12 @@ struct FrameCtx {
   int P0, P;
   bool in_smem;  // tap table staged in shared memory
   bool halo;     // every tap's source row lies inside the extension halo
-  int lo_p, hi_p, lo_u, hi_u;
+  int lo_c, hi_c, lo_u, hi_u;  // halo rows below / above the M real rows of c and u
 };
 
 template <typename T> struct Sm {
-  Vec<T>* p;
-  Vec<T>* u;
+  Vec<T>* c;  // extended residual c (gathered by H)
+  Vec<T>* u;  // extended u = H p (gathered by H^H); holds y for b = H^H y
   uint32_t* tslot;
   Vec<T>* tlo;
   Vec<T>* thi;
@@ -300,22 +303,52 @@ __device__ __forceinline__ void cl_sync(int C) {
   else __syncthreads();
 }
 
-// Deterministic cluster-wide sum.  slot: this CTA's [32] partial array for the
-// reduction kind / parity in use.  Contains the barrier.
+// Deterministic cluster-wide sum of a pair of partials.  slot: this CTA's [32]
+// pair array for the reduction kind / parity in use.  Contains the barrier.
+// Lane i of every warp sums the per-warp pairs i, i+32, ... of the whole
+// cluster (rank-major), then the warp butterflies: every warp of every CTA
+// gets bit-identical totals.  (r0, w0): lane's first (rank, warp) slot.
 template <typename T>
-__device__ __forceinline__ T cluster_sum(T part, T* slot, int C, int nwarps, int lane, int warp) {
-  T v = warp_sum(part);
-  if (lane == 0) slot[warp] = v;
+__device__ __forceinline__ Vec<T> cluster_sum(Vec<T> part, Vec<T>* slot, int C, int nwarps, int lane, int warp,
+                                              int r0, int w0) {
+  using V = Vec<T>;
+  part.x = warp_sum(part.x);
+  part.y = warp_sum(part.y);
+  if (lane == 0) slot[warp] = part;
   cl_sync<T>(C);
-  const int total = C * nwarps;
   const uint32_t base = smem_addr(slot);
-  T s = T(0);
-  for (int i = lane; i < total; i += 32) {
-    const int r = i / nwarps, w = i - r * nwarps;
-    s += (C > 1) ? ld_cluster_scalar(static_cast<T*>(nullptr), map_rank(base + w * (int)sizeof(T), r))
-                 : slot[w];
+  V s = czero<V>();
+  for (int r = r0, w = w0; r < C;) {
+    const V v = C > 1 ? ld_cluster(static_cast<V*>(nullptr), map_rank(base + w * (int)sizeof(V), r)) : slot[w];
+    s = cadd(s, v);
+    w += 32;
+    while (w >= nwarps) { w -= nwarps; ++r; }
   }
-  return warp_sum(s);
+  s.x = warp_sum(s.x);
+  s.y = warp_sum(s.y);
+  return s;
+}
+
+// ---- packed elementwise CG arithmetic (FFMA2 for fp32)
+// y + a x (a real, broadcast)
+__device__ __forceinline__ float2 axpy(float2 y, float a, float2 x) {
+  unsigned long long r = pack2(y.x, y.y);
+  asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(r) : "l"(pack2(a, a)), "l"(pack2(x.x, x.y)));
+  return unpack2(r);
+}
+__device__ __forceinline__ double2 axpy(double2 y, double a, double2 x) {
+  return make_double2(fma(a, x.x, y.x), fma(a, x.y, y.y));
+}
+// n += (v.x^2, v.y^2); the norm is n.x + n.y
+__device__ __forceinline__ void nacc(float2& n, float2 v) {
+  unsigned long long r = pack2(n.x, n.y);
+  const unsigned long long p = pack2(v.x, v.y);
+  asm("fma.rn.f32x2 %0, %1, %1, %0;" : "+l"(r) : "l"(p));
+  n = unpack2(r);
+}
+__device__ __forceinline__ void nacc(double2& n, double2 v) {
+  n.x = fma(v.x, v.x, n.x);
+  n.y = fma(v.y, v.y, n.y);
 }
 
 __host__ __device__ static inline size_t align16(size_t v) { return (v + 15) & ~size_t(15); }
@@ -333,7 +366,7 @@ __host__ __device__ static inline SmemLayout layout_impl(int M, int N, int C, in
   L.thi = o; o = align16(o + (size_t)TH * vb);
   L.tw = o; o = align16(o + (size_t)N * vb);
   L.ptab = o; o = align16(o + (size_t)pcap * (eb == 8 ? 48 : 32));
-  L.red = o; o = align16(o + 3 * 2 * 32 * (size_t)eb);
+  L.red = o; o = align16(o + 2 * 2 * 32 * vb);
   L.total = o;
   return L;
 }
@@ -391,7 +424,7 @@ __global__ void __launch_bounds__(sscga_max_threads(sizeof(T), LC), 1) sscga_ker
   const int M = a.M, N = a.N;
   const SmemLayout L = layout_impl(M, N, a.C, (int)sizeof(T), a.H, a.TL, a.TH, a.pcap);
   Sm<T> sm;
-  sm.p = reinterpret_cast<V*>(smem + L.p);
+  sm.c = reinterpret_cast<V*>(smem + L.p);
   sm.u = reinterpret_cast<V*>(smem + L.u);
   sm.tslot = reinterpret_cast<uint32_t*>(smem + L.x);
   sm.tlo = reinterpret_cast<V*>(smem + L.tlo);
@@ -413,8 +446,8 @@ __global__ void __launch_bounds__(sscga_max_threads(sizeof(T), LC), 1) sscga_ker
   for (int i = tid; i < a.TL; i += blockDim.x) sm.tlo[i] = twiddle(T(0), i, a.MN);
   for (int i = tid; i < a.TH; i += blockDim.x) sm.thi[i] = twiddle(T(0), (int)(((long long)i * a.TL) % a.MN), a.MN);
   for (int l = tid; l < N; l += blockDim.x) sm.tw[l] = twiddle(T(0), l, N);
-  // x and the residual c live in TMEM: warp w uses lanes 32 (w % 4) .. + 31 and
-  // columns (w / 4) * 2 XW ..: first its x run, then its c run
+  // x and the search direction p live in TMEM (only touched elementwise): warp
+  // w uses lanes 32 (w % 4) .. + 31 and columns (w / 4) * 2 XW ..: x run, p run
   constexpr int XW = LC * (int)sizeof(V) / 4;  // 32-bit columns per thread run
   if (warp == 0) tmem_alloc(sm.tslot, (uint32_t)a.tcols);
   tmem_fence_before();
@@ -422,7 +455,12 @@ __global__ void __launch_bounds__(sscga_max_threads(sizeof(T), LC), 1) sscga_ker
   tmem_fence_after();
   const uint32_t tbase = *sm.tslot;
   const uint32_t xta = tbase + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)((warp >> 2) * 2 * XW);
-  const uint32_t cta = xta + (uint32_t)XW;
+  const uint32_t pta = xta + (uint32_t)XW;
+  // reduction lane mapping: lane i starts at cluster slot i = (rank, warp)
+  const int rtot = a.C * nwarps;
+  const int r0 = lane < rtot ? lane / nwarps : a.C;
+  const int w0 = lane < rtot ? lane - (lane / nwarps) * nwarps : 0;
+  V* red = reinterpret_cast<V*>(sm.red);  // [2 kinds][2 parities][32 warps] pairs
 
   const V* y = reinterpret_cast<const V*>(a.y);
   V* xo = reinterpret_cast<V*>(a.x);
@@ -432,7 +470,7 @@ __global__ void __launch_bounds__(sscga_max_threads(sizeof(T), LC), 1) sscga_ker
   const T* nvar = reinterpret_cast<const T*>(a.nvar);
   const bool lead = (cx.rank == 0 && tid == 0);
   const int stride = a.iters + 1;
-  int par[3] = {0, 0, 0};  // 0: ||p||^2, 1: ||u||^2, 2: ||c||^2
+  int par[2] = {0, 0};  // 0: (||u||^2, ||p||^2), 1: (||c||^2, -)
 
   for (int f = blockIdx.x / a.C; f < a.B; f += a.n_clusters) {
     FrameCtx fc;
@@ -476,12 +514,12 @@ __global__ void __launch_bounds__(sscga_max_threads(sizeof(T), LC), 1) sscga_ker
         dmin = min(dmin, dk);
         dmax = max(dmax, dk);
       }
-      fc.lo_p = max(0, -dmin);
-      fc.hi_p = max(0, dmax);
+      fc.lo_c = max(0, -dmin);
+      fc.hi_c = max(0, dmax);
       fc.lo_u = max(0, dmax);
       fc.hi_u = max(0, -dmin);
-      fc.halo = fc.lo_p + fc.hi_p <= a.H;
-      if (!fc.halo) fc.lo_p = fc.hi_p = fc.lo_u = fc.hi_u = 0;
+      fc.halo = fc.lo_c + fc.hi_c <= a.H;
+      if (!fc.halo) fc.lo_c = fc.hi_c = fc.lo_u = fc.hi_u = 0;
     }
 
     const int RS = a.RS;
@@ -499,103 +537,112 @@ __global__ void __launch_bounds__(sscga_max_threads(sizeof(T), LC), 1) sscga_ker
     if (lead && a.berr) a.berr[f] = 0;
     cl_sync<T>(a.C);
 
+    // CG in the "u recurrence" form: with u = H p kept from the previous step,
+    //   u' = H c + beta u,  p' = c + beta p   (= H (c + beta p), c + beta p)
+    // so the gathered vectors are c (by H) and u (by H^H) and each iteration
+    // needs two cluster barriers.  Same algorithm as equalize.py:59-76.
     typename A::type acc[LC];
     ss_mvm<T, LC, true>(a, cx, sm, fc, sm.u, fc.lo_u, acc);  // b = H^H y (equalize.py:52)
-    T part = T(0);
+    V nrm = czero<V>();
 #pragma unroll
     for (int j = 0; j < LC; ++j) {
       w[j] = A::get(acc[j]);
-      part += cabs2(w[j]);
+      nacc(nrm, w[j]);
     }
-    if (cx.active) put_ext<T, LC>(sm.p, RS, fc.lo_p, fc.hi_p, M, cx, w, sm.tw);
-    else part = T(0);
+    if (cx.active) put_ext<T, LC>(sm.c,RS, fc.lo_c, fc.hi_c, M, cx, w, sm.tw);  // c = b
+    else nrm = czero<V>();
     {
-      V z[XC], cb[XC];
+      V z[XC];
 #pragma unroll
-      for (int c0 = 0; c0 < LC; c0 += XC) {
+      for (int j = 0; j < XC; ++j) z[j] = czero<V>();
 #pragma unroll
-        for (int j = 0; j < XC; ++j) {
-          z[j] = czero<V>();
-          cb[j] = w[c0 + j];
-        }
-        x_store<T, XC>(xta + (uint32_t)((c0 / XC) * XCW), z);   // x = 0
-        x_store<T, XC>(cta + (uint32_t)((c0 / XC) * XCW), cb);  // c = b
-      }
+      for (int c0 = 0; c0 < LC; c0 += XC) x_store<T, XC>(xta + (uint32_t)((c0 / XC) * XCW), z);  // x = 0
     }
-    T cn = cluster_sum<T>(part, sm.red + (0 * 2 + par[0]) * 32, a.C, nwarps, lane, warp);
-    par[0] ^= 1;
-    T pp = cn;
+    T cn = cluster_sum<T>(cmake<V>(nrm.x + nrm.y, T(0)), red + (1 * 2 + par[1]) * 32, a.C, nwarps, lane, warp,
+                          r0, w0).x;
+    par[1] ^= 1;
+    T beta = T(0);
     if (lead && cnorm) cnorm[(size_t)f * stride] = cn;
 
     int done = 0;
     bool exact = false;
     for (int it = 0; it < a.iters; ++it) {
-      ss_mvm<T, LC, false>(a, cx, sm, fc, sm.p, fc.lo_p, acc);  // u = H p
-      part = T(0);
+      // u = H c + beta u_old, p = c + beta p_old      (= H p, p of equalize.py:60, 72)
+      ss_mvm<T, LC, false>(a, cx, sm, fc, sm.c,fc.lo_c, acc);
+      V nu = czero<V>(), np = czero<V>();
+      {
+        V uo[LC];
+        load_run<T, LC>(sm.u + (fc.lo_u + cx.k) * RS + gcol, uo);
 #pragma unroll
-      for (int j = 0; j < LC; ++j) {
-        w[j] = A::get(acc[j]);
-        part += cabs2(w[j]);
+        for (int j = 0; j < LC; ++j) {
+          w[j] = it == 0 ? A::get(acc[j]) : axpy(A::get(acc[j]), beta, uo[j]);
+          nacc(nu, w[j]);
+        }
       }
       if (cx.active) put_ext<T, LC>(sm.u, RS, fc.lo_u, fc.hi_u, M, cx, w, sm.tw);
-      else part = T(0);
-      const T uu = cluster_sum<T>(part, sm.red + (1 * 2 + par[1]) * 32, a.C, nwarps, lane, warp);
-      par[1] ^= 1;
-      const T denom = uu + lam * pp;
+      {
+        V cr[LC];
+        load_run<T, LC>(sm.c +(fc.lo_c + cx.k) * RS + gcol, cr);
+#pragma unroll
+        for (int c0 = 0; c0 < LC; c0 += XC) {
+          V pv[XC];
+          const uint32_t off = (uint32_t)((c0 / XC) * XCW);
+          if (it == 0) {
+#pragma unroll
+            for (int j = 0; j < XC; ++j) pv[j] = cr[c0 + j];
+          } else {
+            x_load<T, XC>(pta + off, pv);
+#pragma unroll
+            for (int j = 0; j < XC; ++j) pv[j] = axpy(cr[c0 + j], beta, pv[j]);
+          }
+#pragma unroll
+          for (int j = 0; j < XC; ++j) nacc(np, pv[j]);
+          x_store<T, XC>(pta + off, pv);
+        }
+      }
+      if (!cx.active) nu = np = czero<V>();
+      const V up = cluster_sum<T>(cmake<V>(nu.x + nu.y, np.x + np.y), red + (0 * 2 + par[0]) * 32, a.C, nwarps,
+                                  lane, warp, r0, w0);
+      par[0] ^= 1;
+      const T denom = up.x + lam * up.y;  // ||H p||^2 + lam ||p||^2 = Re p^H (H^H H + lam I) p
       if (denom == T(0)) {  // equalize.py:64-67
         exact = true;
         break;
       }
       const T alpha = cn / denom;
-      ss_mvm<T, LC, true>(a, cx, sm, fc, sm.u, fc.lo_u, acc);  // H^H u
-      part = T(0);
-      V pv[LC];
-      load_run<T, LC>(sm.p + (fc.lo_p + cx.k) * RS + gcol, pv);
+      // ap = H^H u + lam p;  x += alpha p;  c -= alpha ap      (equalize.py:60-70)
+      ss_mvm<T, LC, true>(a, cx, sm, fc, sm.u, fc.lo_u, acc);
+      V nc = czero<V>();
+      load_run<T, LC>(sm.c +(fc.lo_c + cx.k) * RS + gcol, w);
 #pragma unroll
       for (int c0 = 0; c0 < LC; c0 += XC) {
-        V xv[XC], cv[XC];
+        V xv[XC], pv[XC];
         const uint32_t off = (uint32_t)((c0 / XC) * XCW);
         x_load<T, XC>(xta + off, xv);
-        x_load<T, XC>(cta + off, cv);
+        x_load<T, XC>(pta + off, pv);
 #pragma unroll
         for (int j = 0; j < XC; ++j) {
-          const V ap = cadd(A::get(acc[c0 + j]), cscale(pv[c0 + j], lam));
-          xv[j] = cadd(xv[j], cscale(pv[c0 + j], alpha));
-          cv[j] = csub(cv[j], cscale(ap, alpha));
-          part += cabs2(cv[j]);
+          const V ap = axpy(A::get(acc[c0 + j]), lam, pv[j]);
+          xv[j] = axpy(xv[j], alpha, pv[j]);
+          w[c0 + j] = axpy(w[c0 + j], -alpha, ap);
+          nacc(nc, w[c0 + j]);
         }
         x_store<T, XC>(xta + off, xv);
-        x_store<T, XC>(cta + off, cv);
         if (snaps && cx.active) {
 #pragma unroll
           for (int j = 0; j < XC; ++j)
             snaps[((size_t)f * a.iters + it) * a.MN + (size_t)(cx.colbase + c0 + j) * M + cx.k] = xv[j];
         }
       }
-      if (!cx.active) part = T(0);
-      const T nn = cluster_sum<T>(part, sm.red + (2 * 2 + par[2]) * 32, a.C, nwarps, lane, warp);
-      par[2] ^= 1;
-      const T beta = nn / cn;
-      part = T(0);
-#pragma unroll
-      for (int c0 = 0; c0 < LC; c0 += XC) {
-        V cv[XC];
-        x_load<T, XC>(cta + (uint32_t)((c0 / XC) * XCW), cv);
-#pragma unroll
-        for (int j = 0; j < XC; ++j) {
-          pv[c0 + j] = cadd(cv[j], cscale(pv[c0 + j], beta));
-          part += cabs2(pv[c0 + j]);
-        }
-      }
-      if (cx.active) put_ext<T, LC>(sm.p, RS, fc.lo_p, fc.hi_p, M, cx, pv, sm.tw);
-      else part = T(0);
+      if (cx.active) put_ext<T, LC>(sm.c,RS, fc.lo_c, fc.hi_c, M, cx, w, sm.tw);
+      else nc = czero<V>();
+      const T nn = cluster_sum<T>(cmake<V>(nc.x + nc.y, T(0)), red + (1 * 2 + par[1]) * 32, a.C, nwarps, lane,
+                                  warp, r0, w0).x;
+      par[1] ^= 1;
+      beta = nn / cn;
       cn = nn;
       done = it + 1;
       if (lead && cnorm) cnorm[(size_t)f * stride + done] = cn;
-      if (done < a.iters) {
-        pp = cluster_sum<T>(part, sm.red + (0 * 2 + par[0]) * 32, a.C, nwarps, lane, warp);
-        par[0] ^= 1;
-      }
     }
     if (lead) {
       if (cnorm) for (int i = done + 1; i < stride; ++i) cnorm[(size_t)f * stride + i] = T(0);

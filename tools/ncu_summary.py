@@ -47,16 +47,30 @@ KEEP = (
 )
 
 
+SCALE = {"ns": 1.0, "us": 1e3, "usecond": 1e3, "ms": 1e6, "msecond": 1e6, "s": 1e9, "second": 1e9,
+         "byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
+
+
 def raw(rep: str) -> list[dict]:
+    """Rows of the raw page with values normalised to ns (times) and bytes."""
     out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True, check=True)
     rows = list(csv.reader(io.StringIO(out.stdout)))
-    head = rows[0]
-    return [dict(zip(head, r)) for r in rows[2:]]
+    head, units = rows[0], rows[1]
+    res = []
+    for r in rows[2:]:
+        d = {}
+        for k, u, v in zip(head, units, r):
+            x = num(v)
+            if isinstance(x, float) and u in SCALE:
+                x *= SCALE[u]
+            d[k] = x
+        res.append(d)
+    return res
 
 
-def num(v: str):
+def num(v):
     try:
-        return float(v.replace(",", ""))
+        return float(str(v).replace(",", ""))
     except (ValueError, AttributeError):
         return v
 
@@ -90,8 +104,15 @@ def main():
         if args.frames and isinstance(t_ns, float):
             res["frames_per_launch"] = args.frames
             res["dram_bytes_per_frame"] = dram / args.frames
+            res["duration_ns_per_frame"] = t_ns / args.frames
             if args.flops_per_frame:
                 res["achieved_tflops_under_ncu"] = args.frames * args.flops_per_frame / (t_ns * 1e-9) / 1e12
+            shared = first.get("l1tex__data_pipe_lsu_wavefronts_mem_shared.sum")
+            if isinstance(shared, float):
+                res["smem_wavefronts_per_frame"] = shared / args.frames
+            inst = first.get("smsp__inst_executed.sum")
+            if isinstance(inst, float):
+                res["warp_instructions_per_frame"] = inst / args.frames
     Path(args.out).write_text(json.dumps(res, indent=1))
     print(json.dumps(res, indent=1)[:4000])
 
