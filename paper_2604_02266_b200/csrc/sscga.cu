@@ -49,9 +49,11 @@ namespace ddb {
 
 // Per-frame tap entry: offsets and both direction's row-invariant gain factor,
 // hf = h W_MN^{-d_l d_k} (forward) and hh = conj(h) (hermitian), so a thread
-// only adds its own row's W_MN^{-+d_l k} (skipped when d_l == 0).
+// only adds its own row's W_MN^{-+d_l k} (skipped when d_l == 0).  off is the
+// tap's shift in the row-major on-chip slices, d_k RS + d_l elements: the
+// forward gather of row k reads thread_base + off, the hermitian one - off.
 template <typename T> struct __align__(16) PathEnt {
-  int dk, dl;
+  int dk, dl, off, pad;
   Vec<T> hf;
   Vec<T> hh;
 };
@@ -99,6 +101,8 @@ __device__ __forceinline__ PathEnt<T> make_path(const SolveArgs& a, const Sm<T>&
   PathEnt<T> e;
   e.dk = a.K0 - kp;
   e.dl = a.L0 - lp;
+  e.off = e.dk * a.RS + e.dl;
+  e.pad = 0;
   // -d_l d_k: |d_l| <= N/2, |d_k| <= M/2 -> within (-MN, MN)
   e.hf = e.dl ? cmul(h, twid(sm, wrap1(-e.dl * e.dk, a.MN))) : h;
   e.hh = cconj(h);
@@ -162,9 +166,27 @@ __device__ __forceinline__ void ss_mvm(const SolveArgs& a, const Ctx& cx, const 
 #pragma unroll
   for (int j = 0; j < LC; ++j) acc[j] = A::zero();
   const int gcol = cx.g * LC;  // first owned column inside the CTA
+  // fast taps: source row inside the halo, source columns local and contiguous
+  if (fc.halo) {
+    const V* tb = buf + (lo + cx.k) * RS + gcol;
+    for (int p = 0; p < fc.P; ++p) {
+      const PathEnt<T> pe = get_path(a, sm, fc, p);
+      const int dl = pe.dl;
+      const int loc0 = gcol + (HERM ? -dl : dl);
+      if (loc0 < 0 || loc0 + LC > Lcta) continue;
+      V coef = HERM ? pe.hh : pe.hf;
+      if (dl != 0) coef = cmul(coef, twid(sm, wrap1(HERM ? dl * cx.k : -dl * cx.k, MN)));
+      gather_run<LC>(tb + (HERM ? -pe.off : pe.off), (loc0 & 1) != 0, coef, acc);
+    }
+  }
+  // remaining taps: columns owned by other CTAs (DSMEM) or wrapping mod N, or
+  // (no halo this frame) rows wrapping the delay period
   for (int p = 0; p < fc.P; ++p) {
     const PathEnt<T> pe = get_path(a, sm, fc, p);
     const int dk = pe.dk, dl = pe.dl;
+    const int sh = HERM ? -dl : dl;
+    const int loc0 = gcol + sh;
+    if (fc.halo && loc0 >= 0 && loc0 + LC <= Lcta) continue;
     const int ar = HERM ? cx.k - dk : cx.k + dk;  // unwrapped source row
     V coef = HERM ? pe.hh : pe.hf;
     if (dl != 0) coef = cmul(coef, twid(sm, wrap1(HERM ? dl * cx.k : -dl * cx.k, MN)));
@@ -173,13 +195,7 @@ __device__ __forceinline__ void ss_mvm(const SolveArgs& a, const Ctx& cx, const 
       nw = ar < 0 ? -1 : (ar >= M ? 1 : 0);
       row = ar - nw * M;
     }
-    const int sh = HERM ? -dl : dl;
-    const int loc0 = gcol + sh;  // source column inside this CTA, if contiguous
-    const bool contig = loc0 >= 0 && loc0 + LC <= Lcta;
-    const bool nowrap = __all_sync(0xffffffffu, nw == 0);
-    if (contig && nowrap) {
-      gather_run<LC>(buf + (lo + row) * RS + loc0, (loc0 & 1) != 0, coef, acc);
-    } else {
+    {
       // columns owned by other CTAs of the cluster (DSMEM) and/or wrapping mod N;
       // the run crosses at most one owner boundary since LC <= Lcta
       const int base = wrap1(cx.colbase + sh, N);
