@@ -91,7 +91,7 @@ int32_t make_plan(int32_t M, int32_t N, int32_t dtype, ddb::LaunchShape* s) {
       s->smem = (int)ddb::sscga_layout(M, N, C, eb, (int)h, TL, TH, pcap).total;
       // keep (CTAs per SM) x (TMEM columns per CTA) <= 512 so tcgen05.alloc never
       // waits on a co-resident CTA: pad tiny CTAs' shared memory accordingly
-      const int floor_smem = 456 * s->tcols;
+      const int floor_smem = 456 * s->tcols < cap ? 456 * s->tcols : cap;
       if (s->smem < floor_smem) s->smem = floor_smem;
       return DDB_OK;
     }

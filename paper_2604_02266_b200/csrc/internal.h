@@ -43,10 +43,11 @@ struct LaunchShape {
   int cluster, lcta, lc, threads, smem, halo, tl, th, pcap, tcols;
 };
 
-// TMEM columns for x and c: (warps per lane quarter) x 2 runs x (32-bit words
-// per run), rounded to the allocator's power-of-two granularity (>= 32).
+// TMEM columns for the thread-private runs of x, p and the own-element copies
+// of c and u: (warps per lane quarter) x 4 runs x (32-bit words per run),
+// rounded to the allocator's power-of-two granularity (>= 32).
 constexpr int sscga_tmem_cols(int threads, int lc, int elem_bytes) {
-  int need = ((threads / 32 + 3) / 4) * 2 * lc * 2 * elem_bytes / 4;
+  int need = ((threads / 32 + 3) / 4) * 4 * lc * 2 * elem_bytes / 4;
   int c = 32;
   while (c < need) c *= 2;
   return c;
@@ -55,7 +56,7 @@ constexpr int sscga_tmem_cols(int threads, int lc, int elem_bytes) {
 // Thread ceiling of the fused kernel instantiation (its __launch_bounds__):
 // per-thread column runs of >= 32 bytes of real data need > 64 registers,
 // so those instantiations cap at 512 threads.
-constexpr int sscga_max_threads(int elem_bytes, int lc) { return elem_bytes * lc > 32 ? 512 : 1024; }
+constexpr int sscga_max_threads(int elem_bytes, int lc) { return elem_bytes * lc >= 32 ? 512 : 1024; }
 
 // Row stride (complex elements) of the on-chip row-major slices: the Lcta
 // columns padded so that a row is a multiple of 16 bytes and == 16 (mod 32),

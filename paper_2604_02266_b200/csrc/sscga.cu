@@ -166,36 +166,26 @@ __device__ __forceinline__ void ss_mvm(const SolveArgs& a, const Ctx& cx, const 
 #pragma unroll
   for (int j = 0; j < LC; ++j) acc[j] = A::zero();
   const int gcol = cx.g * LC;  // first owned column inside the CTA
-  // fast taps: source row inside the halo, source columns local and contiguous
-  if (fc.halo) {
-    const V* tb = buf + (lo + cx.k) * RS + gcol;
-    for (int p = 0; p < fc.P; ++p) {
-      const PathEnt<T> pe = get_path(a, sm, fc, p);
-      const int dl = pe.dl;
-      const int loc0 = gcol + (HERM ? -dl : dl);
-      if (loc0 < 0 || loc0 + LC > Lcta) continue;
-      V coef = HERM ? pe.hh : pe.hf;
-      if (dl != 0) coef = cmul(coef, twid(sm, wrap1(HERM ? dl * cx.k : -dl * cx.k, MN)));
-      gather_run<LC>(tb + (HERM ? -pe.off : pe.off), (loc0 & 1) != 0, coef, acc);
-    }
-  }
-  // remaining taps: columns owned by other CTAs (DSMEM) or wrapping mod N, or
-  // (no halo this frame) rows wrapping the delay period
+  const V* tb = buf + (lo + cx.k) * RS + gcol;  // this thread's row in the slice
   for (int p = 0; p < fc.P; ++p) {
     const PathEnt<T> pe = get_path(a, sm, fc, p);
-    const int dk = pe.dk, dl = pe.dl;
+    const int dl = pe.dl;
     const int sh = HERM ? -dl : dl;
     const int loc0 = gcol + sh;
-    if (fc.halo && loc0 >= 0 && loc0 + LC <= Lcta) continue;
-    const int ar = HERM ? cx.k - dk : cx.k + dk;  // unwrapped source row
     V coef = HERM ? pe.hh : pe.hf;
     if (dl != 0) coef = cmul(coef, twid(sm, wrap1(HERM ? dl * cx.k : -dl * cx.k, MN)));
-    int row = ar, nw = 0;
-    if (!fc.halo) {
-      nw = ar < 0 ? -1 : (ar >= M ? 1 : 0);
-      row = ar - nw * M;
-    }
-    {
+    if (fc.halo && loc0 >= 0 && loc0 + LC <= Lcta) {
+      // source row inside the halo, source columns local and contiguous
+      gather_run<LC>(tb + (HERM ? -pe.off : pe.off), (loc0 & 1) != 0, coef, acc);
+    } else {
+      // columns owned by other CTAs (DSMEM) or wrapping mod N, or (no halo this
+      // frame) rows wrapping the delay period
+      const int ar = HERM ? cx.k - pe.dk : cx.k + pe.dk;  // unwrapped source row
+      int row = ar, nw = 0;
+      if (!fc.halo) {
+        nw = ar < 0 ? -1 : (ar >= M ? 1 : 0);
+        row = ar - nw * M;
+      }
       // columns owned by other CTAs of the cluster (DSMEM) and/or wrapping mod N;
       // the run crosses at most one owner boundary since LC <= Lcta
       const int base = wrap1(cx.colbase + sh, N);
@@ -262,6 +252,31 @@ __device__ __forceinline__ void x_store(uint32_t ta, const Vec<T> (&v)[NE]) {
 template <typename T, int LC> constexpr int x_chunk() {
   constexpr int e = 16 / ((int)sizeof(Vec<T>) / 4);
   return LC < e ? LC : e;
+}
+// whole LC-element run from / to TMEM in chunks
+template <typename T, int LC>
+__device__ __forceinline__ void run_tload(uint32_t ta, Vec<T> (&v)[LC]) {
+  constexpr int XC = x_chunk<T, LC>();
+  constexpr int XCW = XC * (int)sizeof(Vec<T>) / 4;
+#pragma unroll
+  for (int c0 = 0; c0 < LC; c0 += XC) {
+    Vec<T> t[XC];
+    x_load<T, XC>(ta + (uint32_t)((c0 / XC) * XCW), t);
+#pragma unroll
+    for (int j = 0; j < XC; ++j) v[c0 + j] = t[j];
+  }
+}
+template <typename T, int LC>
+__device__ __forceinline__ void run_tstore(uint32_t ta, const Vec<T> (&v)[LC]) {
+  constexpr int XC = x_chunk<T, LC>();
+  constexpr int XCW = XC * (int)sizeof(Vec<T>) / 4;
+#pragma unroll
+  for (int c0 = 0; c0 < LC; c0 += XC) {
+    Vec<T> t[XC];
+#pragma unroll
+    for (int j = 0; j < XC; ++j) t[j] = v[c0 + j];
+    x_store<T, XC>(ta + (uint32_t)((c0 / XC) * XCW), t);
+  }
 }
 
 // Run helpers for a thread's own LC contiguous elements of one row.
@@ -462,16 +477,20 @@ __global__ void __launch_bounds__(sscga_max_threads(sizeof(T), LC), 1) sscga_ker
   for (int i = tid; i < a.TL; i += blockDim.x) sm.tlo[i] = twiddle(T(0), i, a.MN);
   for (int i = tid; i < a.TH; i += blockDim.x) sm.thi[i] = twiddle(T(0), (int)(((long long)i * a.TL) % a.MN), a.MN);
   for (int l = tid; l < N; l += blockDim.x) sm.tw[l] = twiddle(T(0), l, N);
-  // x and the search direction p live in TMEM (only touched elementwise): warp
-  // w uses lanes 32 (w % 4) .. + 31 and columns (w / 4) * 2 XW ..: x run, p run
+  // x and the search direction p live in TMEM (only touched elementwise), next
+  // to lane-private copies of the thread's own c and u elements (so elementwise
+  // reads never touch shared memory): warp w uses lanes 32 (w % 4) .. + 31 and
+  // columns (w / 4) * 4 XW ..: x run, p run, c run, u run
   constexpr int XW = LC * (int)sizeof(V) / 4;  // 32-bit columns per thread run
   if (warp == 0) tmem_alloc(sm.tslot, (uint32_t)a.tcols);
   tmem_fence_before();
   __syncthreads();
   tmem_fence_after();
   const uint32_t tbase = *sm.tslot;
-  const uint32_t xta = tbase + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)((warp >> 2) * 2 * XW);
+  const uint32_t xta = tbase + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)((warp >> 2) * 4 * XW);
   const uint32_t pta = xta + (uint32_t)XW;
+  const uint32_t cta = xta + (uint32_t)(2 * XW);
+  const uint32_t uta = xta + (uint32_t)(3 * XW);
   // reduction lane mapping: lane i starts at cluster slot i = (rank, warp)
   const int rtot = a.C * nwarps;
   const int r0 = lane < rtot ? lane / nwarps : a.C;
@@ -565,8 +584,9 @@ __global__ void __launch_bounds__(sscga_max_threads(sizeof(T), LC), 1) sscga_ker
       w[j] = A::get(acc[j]);
       nacc(nrm, w[j]);
     }
-    if (cx.active) put_ext<T, LC>(sm.c,RS, fc.lo_c, fc.hi_c, M, cx, w, sm.tw);  // c = b
+    if (cx.active) put_ext<T, LC>(sm.c, RS, fc.lo_c, fc.hi_c, M, cx, w, sm.tw);  // c = b
     else nrm = czero<V>();
+    run_tstore<T, LC>(cta, w);
     {
       V z[XC];
 #pragma unroll
@@ -586,35 +606,36 @@ __global__ void __launch_bounds__(sscga_max_threads(sizeof(T), LC), 1) sscga_ker
       // u = H c + beta u_old, p = c + beta p_old      (= H p, p of equalize.py:60, 72)
       ss_mvm<T, LC, false>(a, cx, sm, fc, sm.c,fc.lo_c, acc);
       V nu = czero<V>(), np = czero<V>();
-      {
-        V uo[LC];
-        load_run<T, LC>(sm.u + (fc.lo_u + cx.k) * RS + gcol, uo);
 #pragma unroll
-        for (int j = 0; j < LC; ++j) {
-          w[j] = it == 0 ? A::get(acc[j]) : axpy(A::get(acc[j]), beta, uo[j]);
-          nacc(nu, w[j]);
+      for (int c0 = 0; c0 < LC; c0 += XC) {
+        const uint32_t off = (uint32_t)((c0 / XC) * XCW);
+        V uo[XC], t[XC];
+        if (it > 0) x_load<T, XC>(uta + off, uo);
+#pragma unroll
+        for (int j = 0; j < XC; ++j) {
+          w[c0 + j] = it == 0 ? A::get(acc[c0 + j]) : axpy(A::get(acc[c0 + j]), beta, uo[j]);
+          nacc(nu, w[c0 + j]);
+          t[j] = w[c0 + j];
         }
+        x_store<T, XC>(uta + off, t);
       }
       if (cx.active) put_ext<T, LC>(sm.u, RS, fc.lo_u, fc.hi_u, M, cx, w, sm.tw);
-      {
-        V cr[LC];
-        load_run<T, LC>(sm.c +(fc.lo_c + cx.k) * RS + gcol, cr);
 #pragma unroll
-        for (int c0 = 0; c0 < LC; c0 += XC) {
-          V pv[XC];
-          const uint32_t off = (uint32_t)((c0 / XC) * XCW);
-          if (it == 0) {
+      for (int c0 = 0; c0 < LC; c0 += XC) {
+        const uint32_t off = (uint32_t)((c0 / XC) * XCW);
+        V cr[XC], pv[XC];
+        x_load<T, XC>(cta + off, cr);
+        if (it == 0) {
 #pragma unroll
-            for (int j = 0; j < XC; ++j) pv[j] = cr[c0 + j];
-          } else {
-            x_load<T, XC>(pta + off, pv);
+          for (int j = 0; j < XC; ++j) pv[j] = cr[j];
+        } else {
+          x_load<T, XC>(pta + off, pv);
 #pragma unroll
-            for (int j = 0; j < XC; ++j) pv[j] = axpy(cr[c0 + j], beta, pv[j]);
-          }
-#pragma unroll
-          for (int j = 0; j < XC; ++j) nacc(np, pv[j]);
-          x_store<T, XC>(pta + off, pv);
+          for (int j = 0; j < XC; ++j) pv[j] = axpy(cr[j], beta, pv[j]);
         }
+#pragma unroll
+        for (int j = 0; j < XC; ++j) nacc(np, pv[j]);
+        x_store<T, XC>(pta + off, pv);
       }
       if (!cx.active) nu = np = czero<V>();
       const V up = cluster_sum<T>(cmake<V>(nu.x + nu.y, np.x + np.y), red + (0 * 2 + par[0]) * 32, a.C, nwarps,
@@ -629,28 +650,30 @@ __global__ void __launch_bounds__(sscga_max_threads(sizeof(T), LC), 1) sscga_ker
       // ap = H^H u + lam p;  x += alpha p;  c -= alpha ap      (equalize.py:60-70)
       ss_mvm<T, LC, true>(a, cx, sm, fc, sm.u, fc.lo_u, acc);
       V nc = czero<V>();
-      load_run<T, LC>(sm.c +(fc.lo_c + cx.k) * RS + gcol, w);
 #pragma unroll
       for (int c0 = 0; c0 < LC; c0 += XC) {
-        V xv[XC], pv[XC];
+        V xv[XC], pv[XC], cv[XC];
         const uint32_t off = (uint32_t)((c0 / XC) * XCW);
         x_load<T, XC>(xta + off, xv);
         x_load<T, XC>(pta + off, pv);
+        x_load<T, XC>(cta + off, cv);
 #pragma unroll
         for (int j = 0; j < XC; ++j) {
           const V ap = axpy(A::get(acc[c0 + j]), lam, pv[j]);
           xv[j] = axpy(xv[j], alpha, pv[j]);
-          w[c0 + j] = axpy(w[c0 + j], -alpha, ap);
-          nacc(nc, w[c0 + j]);
+          cv[j] = axpy(cv[j], -alpha, ap);
+          nacc(nc, cv[j]);
+          w[c0 + j] = cv[j];
         }
         x_store<T, XC>(xta + off, xv);
+        x_store<T, XC>(cta + off, cv);
         if (snaps && cx.active) {
 #pragma unroll
           for (int j = 0; j < XC; ++j)
             snaps[((size_t)f * a.iters + it) * a.MN + (size_t)(cx.colbase + c0 + j) * M + cx.k] = xv[j];
         }
       }
-      if (cx.active) put_ext<T, LC>(sm.c,RS, fc.lo_c, fc.hi_c, M, cx, w, sm.tw);
+      if (cx.active) put_ext<T, LC>(sm.c, RS, fc.lo_c, fc.hi_c, M, cx, w, sm.tw);
       else nc = czero<V>();
       const T nn = cluster_sum<T>(cmake<V>(nc.x + nc.y, T(0)), red + (1 * 2 + par[1]) * 32, a.C, nwarps, lane,
                                   warp, r0, w0).x;
