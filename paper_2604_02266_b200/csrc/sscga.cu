@@ -52,11 +52,24 @@ namespace ddb {
 // only adds its own row's W_MN^{-+d_l k} (skipped when d_l == 0).  off is the
 // tap's shift in the row-major on-chip slices, d_k RS + d_l elements: the
 // forward gather of row k reads thread_base + off, the hermitian one - off.
-template <typename T> struct __align__(16) PathEnt {
+template <typename T> struct PathEnt;
+template <> struct __align__(16) PathEnt<double> {
   int dk, dl, off, pad;
-  Vec<T> hf;
-  Vec<T> hh;
+  double2 hf, hh;
+  __device__ double2 coef(bool herm) const { return herm ? hh : hf; }
 };
+// fp32: gains stored as FFMA2-ready quads (g.x, g.x, -g.y, g.y), so a 128-bit
+// load yields the register pairs of both packed MACs directly.
+template <> struct __align__(16) PathEnt<float> {
+  int dk, dl, off, pad;
+  float4 hf, hh;
+  __device__ float2 coef(bool herm) const {
+    const float4 q = herm ? hh : hf;
+    return make_float2(q.x, q.w);
+  }
+};
+__device__ __forceinline__ float4 quad(float2 g) { return make_float4(g.x, g.x, -g.y, g.y); }
+__device__ __forceinline__ double2 quad(double2 g) { return g; }
 
 struct Ctx {
   int k;        // delay row owned by this thread
@@ -104,8 +117,8 @@ __device__ __forceinline__ PathEnt<T> make_path(const SolveArgs& a, const Sm<T>&
   e.off = e.dk * a.RS + e.dl;
   e.pad = 0;
   // -d_l d_k: |d_l| <= N/2, |d_k| <= M/2 -> within (-MN, MN)
-  e.hf = e.dl ? cmul(h, twid(sm, wrap1(-e.dl * e.dk, a.MN))) : h;
-  e.hh = cconj(h);
+  e.hf = quad(e.dl ? cmul(h, twid(sm, wrap1(-e.dl * e.dk, a.MN))) : h);
+  e.hh = quad(cconj(h));
   return e;
 }
 
@@ -119,31 +132,39 @@ __device__ __forceinline__ PathEnt<T> get_path(const SolveArgs& a, const Sm<T>& 
 // Contiguous run of LC source columns starting at rp (16-byte aligned row,
 // offset `odd` elements): 128-bit loads, two complex values each; an odd start
 // loads one extra aligned chunk and uses the other halves (register naming only).
+// acc += c v with c given as the FFMA2 operand pairs X = (c.x, c.x), Y = (-c.y, c.y)
+__device__ __forceinline__ void cmacxy(unsigned long long& acc, unsigned long long X, unsigned long long Y,
+                                       float a, float b) {
+  asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(acc) : "l"(X), "l"(pack2(a, b)));
+  asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(acc) : "l"(Y), "l"(pack2(b, a)));
+}
 template <int LC>
-__device__ __forceinline__ void gather_run(const float2* rp, bool odd, float2 c, unsigned long long (&acc)[LC]) {
+__device__ __forceinline__ void gather_run(const float2* rp, bool odd, unsigned long long X, unsigned long long Y,
+                                           unsigned long long (&acc)[LC]) {
   if constexpr (LC == 1) {
-    cmac2(acc[0], c.x, c.y, rp[0]);
+    const float2 v = rp[0];
+    cmacxy(acc[0], X, Y, v.x, v.y);
   } else {
     if (!odd) {
       const float4* q = reinterpret_cast<const float4*>(rp);
 #pragma unroll
       for (int m = 0; m < LC / 2; ++m) {
         const float4 w = q[m];
-        cmac2(acc[2 * m], c.x, c.y, make_float2(w.x, w.y));
-        cmac2(acc[2 * m + 1], c.x, c.y, make_float2(w.z, w.w));
+        cmacxy(acc[2 * m], X, Y, w.x, w.y);
+        cmacxy(acc[2 * m + 1], X, Y, w.z, w.w);
       }
     } else {
       const float4* q = reinterpret_cast<const float4*>(rp - 1);
       float4 w = q[0];
-      cmac2(acc[0], c.x, c.y, make_float2(w.z, w.w));
+      cmacxy(acc[0], X, Y, w.z, w.w);
 #pragma unroll
       for (int m = 1; m < LC / 2; ++m) {
         w = q[m];
-        cmac2(acc[2 * m - 1], c.x, c.y, make_float2(w.x, w.y));
-        cmac2(acc[2 * m], c.x, c.y, make_float2(w.z, w.w));
+        cmacxy(acc[2 * m - 1], X, Y, w.x, w.y);
+        cmacxy(acc[2 * m], X, Y, w.z, w.w);
       }
       w = q[LC / 2];
-      cmac2(acc[LC - 1], c.x, c.y, make_float2(w.x, w.y));
+      cmacxy(acc[LC - 1], X, Y, w.x, w.y);
     }
   }
 }
@@ -172,11 +193,25 @@ __device__ __forceinline__ void ss_mvm(const SolveArgs& a, const Ctx& cx, const 
     const int dl = pe.dl;
     const int sh = HERM ? -dl : dl;
     const int loc0 = gcol + sh;
-    V coef = HERM ? pe.hh : pe.hf;
+    V coef = pe.coef(HERM);
     if (dl != 0) coef = cmul(coef, twid(sm, wrap1(HERM ? dl * cx.k : -dl * cx.k, MN)));
     if (fc.halo && loc0 >= 0 && loc0 + LC <= Lcta) {
       // source row inside the halo, source columns local and contiguous
-      gather_run<LC>(tb + (HERM ? -pe.off : pe.off), (loc0 & 1) != 0, coef, acc);
+      const V* src = tb + (HERM ? -pe.off : pe.off);
+      if constexpr (sizeof(T) == 4) {
+        unsigned long long X, Y;
+        if (dl == 0) {  // warp-uniform gain: FFMA2 operand pairs straight from the table
+          const float4 q = HERM ? pe.hh : pe.hf;
+          X = pack2(q.x, q.y);
+          Y = pack2(q.z, q.w);
+        } else {
+          X = pack2(coef.x, coef.x);
+          Y = pack2(-coef.y, coef.y);
+        }
+        gather_run<LC>(src, (loc0 & 1) != 0, X, Y, acc);
+      } else {
+        gather_run<LC>(src, false, coef, acc);
+      }
     } else {
       // columns owned by other CTAs (DSMEM) or wrapping mod N, or (no halo this
       // frame) rows wrapping the delay period
@@ -396,7 +431,7 @@ __host__ __device__ static inline SmemLayout layout_impl(int M, int N, int C, in
   L.tlo = o; o = align16(o + (size_t)TL * vb);
   L.thi = o; o = align16(o + (size_t)TH * vb);
   L.tw = o; o = align16(o + (size_t)N * vb);
-  L.ptab = o; o = align16(o + (size_t)pcap * (eb == 8 ? 48 : 32));
+  L.ptab = o; o = align16(o + (size_t)pcap * 48);  // sizeof(PathEnt<T>) == 48
   L.red = o; o = align16(o + 2 * 2 * 32 * vb);
   L.total = o;
   return L;
