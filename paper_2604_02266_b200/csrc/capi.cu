@@ -1,6 +1,7 @@
 // C ABI (include/ddb.h): argument validation, launch planning, error state.
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <string>
 
 #include "../../include/ddb.h"
@@ -59,15 +60,22 @@ int32_t make_plan(int32_t M, int32_t N, int32_t dtype, ddb::LaunchShape* s) {
   int TL = 0, TH = 0;
   ddb::twiddle_split(M * N, &TL, &TH);
   const int hmin = M < 64 ? M : 64;  // Veh-A delay spread is <= 39 bins at M = 512
+  // tuning overrides (benchmarks only): DDB_PLAN_C = minimum cluster size,
+  // DDB_PLAN_LC = columns per thread (ignored when it does not fit)
+  const char* env_c = getenv("DDB_PLAN_C");
+  const char* env_lc = getenv("DDB_PLAN_LC");
+  const int cmin = env_c ? atoi(env_c) : 1;
+  const int force_lc = env_lc ? atoi(env_lc) : 0;
   for (int pass = 0; pass < 2; ++pass) {
     for (int C = 1; C <= 16; C *= 2) {
-      if (N % C) continue;
+      if (N % C || C < cmin) continue;
       const int lcta = N / C;
       const size_t base = ddb::sscga_layout(M, N, C, eb, 0, TL, TH, pcap).total;
       if (base > (size_t)cap) continue;
       long long h = (long long)(cap - base) / (2LL * lcta * 2 * eb);
       while (h > 0 && ddb::sscga_layout(M, N, C, eb, (int)h, TL, TH, pcap).total > (size_t)cap) --h;
       if (h > M) h = M;  // a delay shift spans at most M - 1 rows
+      if (const char* env_h = getenv("DDB_PLAN_H")) h = h < atoi(env_h) ? h : atoi(env_h);
       if (pass == 0 && h < hmin) continue;
       const int target = M * lcta < 256 ? M * lcta : 256;
       int best = 0;
@@ -76,7 +84,8 @@ int32_t make_plan(int32_t M, int32_t N, int32_t dtype, ddb::LaunchShape* s) {
         const int active = M * (lcta / lc);
         const int threads = (active + 31) / 32 * 32;
         if (threads > ddb::sscga_max_threads(eb, lc)) continue;
-        if (active >= target) { best = lc; break; }
+        if (force_lc && lc != force_lc) continue;
+        if (active >= target || force_lc) { best = lc; break; }
       }
       if (!best) continue;
       s->cluster = C;
@@ -91,7 +100,10 @@ int32_t make_plan(int32_t M, int32_t N, int32_t dtype, ddb::LaunchShape* s) {
       s->smem = (int)ddb::sscga_layout(M, N, C, eb, (int)h, TL, TH, pcap).total;
       // keep (CTAs per SM) x (TMEM columns per CTA) <= 512 so tcgen05.alloc never
       // waits on a co-resident CTA: pad tiny CTAs' shared memory accordingly
-      const int floor_smem = 456 * s->tcols < cap ? 456 * s->tcols : cap;
+      // 228 KiB per SM, 1 KiB reserved per CTA: at most 512 / tcols CTAs fit
+      const int max_ctas = 512 / s->tcols;
+      int floor_smem = 233472 / (max_ctas + 1) - 1024 + 16;
+      if (floor_smem > cap) floor_smem = cap;
       if (s->smem < floor_smem) s->smem = floor_smem;
       return DDB_OK;
     }
