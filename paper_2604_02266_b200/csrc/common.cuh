@@ -218,6 +218,12 @@ __device__ __forceinline__ double2 ld_cluster(double2*, uint32_t caddr) {
   asm volatile("ld.shared::cluster.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(caddr) : "memory");
   return v;
 }
+__device__ __forceinline__ void st_cluster(uint32_t caddr, float2 v) {
+  asm volatile("st.shared::cluster.v2.f32 [%0], {%1, %2};" :: "r"(caddr), "f"(v.x), "f"(v.y) : "memory");
+}
+__device__ __forceinline__ void st_cluster(uint32_t caddr, double2 v) {
+  asm volatile("st.shared::cluster.v2.f64 [%0], {%1, %2};" :: "r"(caddr), "d"(v.x), "d"(v.y) : "memory");
+}
 __device__ __forceinline__ float ld_cluster_scalar(float*, uint32_t caddr) {
   float v;
   asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(v) : "r"(caddr) : "memory");

@@ -374,21 +374,40 @@ __device__ __forceinline__ void cl_sync(int C) {
 // Lane i of every warp sums the per-warp pairs i, i+32, ... of the whole
 // cluster (rank-major), then the warp butterflies: every warp of every CTA
 // gets bit-identical totals.  (r0, w0): lane's first (rank, warp) slot.
+//
+// Small clusters (C * nwarps <= kPushSlots) push: lane r of every warp stores
+// the warp's pair into slot[rank * nwarps + warp] of CTA r before the barrier
+// (remote stores are released by barrier.cluster.arrive.release), so after it
+// every read is a local shared-memory load.  Larger clusters pull the peers'
+// per-warp pairs through DSMEM after the barrier.
+constexpr int kPushSlots = 64;
+
 template <typename T>
 __device__ __forceinline__ Vec<T> cluster_sum(Vec<T> part, Vec<T>* slot, int C, int nwarps, int lane, int warp,
-                                              int r0, int w0) {
+                                              int r0, int w0, int rank) {
   using V = Vec<T>;
   part.x = warp_sum(part.x);
   part.y = warp_sum(part.y);
-  if (lane == 0) slot[warp] = part;
-  cl_sync<T>(C);
-  const uint32_t base = smem_addr(slot);
+  const int total = C * nwarps;
   V s = czero<V>();
-  for (int r = r0, w = w0; r < C;) {
-    const V v = C > 1 ? ld_cluster(static_cast<V*>(nullptr), map_rank(base + w * (int)sizeof(V), r)) : slot[w];
-    s = cadd(s, v);
-    w += 32;
-    while (w >= nwarps) { w -= nwarps; ++r; }
+  if (total <= kPushSlots) {
+    const int idx = rank * nwarps + warp;
+    if (C == 1) {
+      if (lane == 0) slot[idx] = part;
+    } else if (lane < C) {
+      st_cluster(map_rank(smem_addr(slot + idx), lane), part);
+    }
+    cl_sync<T>(C);
+    for (int i = lane; i < total; i += 32) s = cadd(s, slot[i]);
+  } else {
+    if (lane == 0) slot[warp] = part;
+    cl_sync<T>(C);
+    const uint32_t base = smem_addr(slot);
+    for (int r = r0, w = w0; r < C;) {
+      s = cadd(s, ld_cluster(static_cast<V*>(nullptr), map_rank(base + w * (int)sizeof(V), r)));
+      w += 32;
+      while (w >= nwarps) { w -= nwarps; ++r; }
+    }
   }
   s.x = warp_sum(s.x);
   s.y = warp_sum(s.y);
@@ -432,7 +451,7 @@ __host__ __device__ static inline SmemLayout layout_impl(int M, int N, int C, in
   L.thi = o; o = align16(o + (size_t)TH * vb);
   L.tw = o; o = align16(o + (size_t)N * vb);
   L.ptab = o; o = align16(o + (size_t)pcap * 48);  // sizeof(PathEnt<T>) == 48
-  L.red = o; o = align16(o + 2 * 2 * 32 * vb);
+  L.red = o; o = align16(o + 2 * 2 * 64 * vb);  // [2 kinds][2 parities][kPushSlots] pairs
   L.total = o;
   return L;
 }
@@ -605,6 +624,16 @@ __global__ void __launch_bounds__(sscga_max_threads(sizeof(T), LC), 1) sscga_ker
       put_ext<T, LC>(sm.u, RS, fc.lo_u, fc.hi_u, M, cx, w, sm.tw);
     }
     if (lead && a.berr) a.berr[f] = 0;
+    // warm L2 with this cluster's next frame (y, TX labels) while this one solves
+    if (cx.active && f + a.n_clusters < a.B) {
+      const size_t fn = (size_t)(f + a.n_clusters) * a.MN;
+#pragma unroll
+      for (int j = 0; j < LC; ++j) {
+        const size_t q = fn + (size_t)(cx.colbase + j) * M + cx.k;
+        asm volatile("prefetch.global.L2 [%0];" :: "l"(y + q));
+        if (a.txl && (cx.k & 31) == 0) asm volatile("prefetch.global.L2 [%0];" :: "l"(a.txl + q));
+      }
+    }
     cl_sync<T>(a.C);
 
     // CG in the "u recurrence" form: with u = H p kept from the previous step,
@@ -629,8 +658,8 @@ __global__ void __launch_bounds__(sscga_max_threads(sizeof(T), LC), 1) sscga_ker
 #pragma unroll
       for (int c0 = 0; c0 < LC; c0 += XC) x_store<T, XC>(xta + (uint32_t)((c0 / XC) * XCW), z);  // x = 0
     }
-    T cn = cluster_sum<T>(cmake<V>(nrm.x + nrm.y, T(0)), red + (1 * 2 + par[1]) * 32, a.C, nwarps, lane, warp,
-                          r0, w0).x;
+    T cn = cluster_sum<T>(cmake<V>(nrm.x + nrm.y, T(0)), red + (1 * 2 + par[1]) * kPushSlots, a.C, nwarps, lane,
+                          warp, r0, w0, cx.rank).x;
     par[1] ^= 1;
     T beta = T(0);
     if (lead && cnorm) cnorm[(size_t)f * stride] = cn;
@@ -673,8 +702,8 @@ __global__ void __launch_bounds__(sscga_max_threads(sizeof(T), LC), 1) sscga_ker
         x_store<T, XC>(pta + off, pv);
       }
       if (!cx.active) nu = np = czero<V>();
-      const V up = cluster_sum<T>(cmake<V>(nu.x + nu.y, np.x + np.y), red + (0 * 2 + par[0]) * 32, a.C, nwarps,
-                                  lane, warp, r0, w0);
+      const V up = cluster_sum<T>(cmake<V>(nu.x + nu.y, np.x + np.y), red + (0 * 2 + par[0]) * kPushSlots, a.C,
+                                  nwarps, lane, warp, r0, w0, cx.rank);
       par[0] ^= 1;
       const T denom = up.x + lam * up.y;  // ||H p||^2 + lam ||p||^2 = Re p^H (H^H H + lam I) p
       if (denom == T(0)) {  // equalize.py:64-67
@@ -710,8 +739,8 @@ __global__ void __launch_bounds__(sscga_max_threads(sizeof(T), LC), 1) sscga_ker
       }
       if (cx.active) put_ext<T, LC>(sm.c, RS, fc.lo_c, fc.hi_c, M, cx, w, sm.tw);
       else nc = czero<V>();
-      const T nn = cluster_sum<T>(cmake<V>(nc.x + nc.y, T(0)), red + (1 * 2 + par[1]) * 32, a.C, nwarps, lane,
-                                  warp, r0, w0).x;
+      const T nn = cluster_sum<T>(cmake<V>(nc.x + nc.y, T(0)), red + (1 * 2 + par[1]) * kPushSlots, a.C, nwarps,
+                                  lane, warp, r0, w0, cx.rank).x;
       par[1] ^= 1;
       beta = nn / cn;
       cn = nn;
