@@ -56,7 +56,7 @@ constexpr int sscga_tmem_cols(int threads, int lc, int elem_bytes) {
 // Thread ceiling of the fused kernel instantiation (its __launch_bounds__):
 // per-thread column runs of >= 32 bytes of real data need > 64 registers,
 // so those instantiations cap at 512 threads.
-constexpr int sscga_max_threads(int elem_bytes, int lc) { return elem_bytes * lc > 32 ? 512 : 1024; }
+constexpr int sscga_max_threads(int elem_bytes, int lc) { return elem_bytes * lc >= 32 ? 512 : 1024; }
 
 // Row stride (complex elements) of the on-chip row-major slices: the Lcta
 // columns padded so that a row is a multiple of 16 bytes and == 16 (mod 32),

@@ -174,75 +174,123 @@ __device__ __forceinline__ void gather_run(const double2* rp, bool, double2 c, d
   for (int j = 0; j < LC; ++j) Acc<double>::mac(acc[j], c, rp[j]);
 }
 
+// The MVM runs in two passes around a split cluster barrier:
+//   local pass  (after the CTA barrier): acc = 0, then every tap whose source
+//                row lies in the halo and whose source columns are this CTA's
+//                own contiguous columns; returns the taps it skipped;
+//   remote pass (after the cluster barrier's wait): the skipped taps, whose
+//                columns belong to other CTAs (DSMEM) or wrap mod N, or whose
+//                rows wrap the delay period when the frame exceeds the halo.
 // acc[j] = (H v)[k, colbase + j]  (HERM = false)  or  (H^H v)[k, colbase + j].
 // buf is the extended buffer of v: row r (= lo + a for extended row a) at
 // buf + r * RS, the CTA's Lcta columns contiguous inside a row.
+struct Skipped {
+  uint32_t mask;  // skipped taps among the first 32
+  bool late;      // some tap >= 32 was skipped
+};
+
 template <typename T, int LC, bool HERM>
-__device__ __forceinline__ void ss_mvm(const SolveArgs& a, const Ctx& cx, const Sm<T>& sm, const FrameCtx& fc,
-                                       const Vec<T>* __restrict__ buf, int lo,
-                                       typename Acc<T>::type (&acc)[LC]) {
+__device__ __forceinline__ void tap_remote(const SolveArgs& a, const Ctx& cx, const Sm<T>& sm, const FrameCtx& fc,
+                                           const Vec<T>* __restrict__ buf, int lo, const PathEnt<T>& pe,
+                                           typename Acc<T>::type (&acc)[LC]) {
   using V = Vec<T>;
   using A = Acc<T>;
   const int M = a.M, N = a.N, MN = a.MN, RS = a.RS, Lcta = a.Lcta;
+  const int dl = pe.dl;
+  const int sh = HERM ? -dl : dl;
+  V coef = pe.coef(HERM);
+  if (dl != 0) coef = cmul(coef, twid(sm, wrap1(HERM ? dl * cx.k : -dl * cx.k, MN)));
+  const int ar = HERM ? cx.k - pe.dk : cx.k + pe.dk;  // unwrapped source row
+  int row = ar, nw = 0;
+  if (!fc.halo) {
+    nw = ar < 0 ? -1 : (ar >= M ? 1 : 0);
+    row = ar - nw * M;
+  }
+  // the run crosses at most one owner boundary since LC <= Lcta
+  const int base = wrap1(cx.colbase + sh, N);
+  const int own0 = base / Lcta;
+  const int l0 = base - own0 * Lcta;
+  const int split = Lcta - l0;
+  const int own1 = own0 + 1 == a.C ? 0 : own0 + 1;
+  const uint32_t rowaddr = smem_addr(buf + (lo + row) * RS);
+  const uint32_t a0 = map_rank(rowaddr + (uint32_t)(l0 * (int)sizeof(V)), own0);
+  const uint32_t a1 = map_rank(rowaddr, own1);
+#pragma unroll
+  for (int j = 0; j < LC; ++j) {
+    const uint32_t ad =
+        j < split ? a0 + (uint32_t)(j * (int)sizeof(V)) : a1 + (uint32_t)((j - split) * (int)sizeof(V));
+    V v = ld_cluster(static_cast<V*>(nullptr), ad);
+    if (nw != 0) {  // quasi-periodic wrap applied in registers (no halo this frame)
+      const int ls = base + j < N ? base + j : base + j - N;
+      V t = sm.tw[ls];
+      if (nw < 0) t = cconj(t);
+      v = cmul(v, t);
+    }
+    A::mac(acc[j], coef, v);
+  }
+}
+
+template <typename T, int LC, bool HERM>
+__device__ __forceinline__ bool tap_is_local(const FrameCtx& fc, const Ctx& cx, int dl, int Lcta) {
+  const int loc0 = cx.g * LC + (HERM ? -dl : dl);
+  return fc.halo && loc0 >= 0 && loc0 + LC <= Lcta;
+}
+
+template <typename T, int LC, bool HERM>
+__device__ __forceinline__ Skipped ss_mvm_local(const SolveArgs& a, const Ctx& cx, const Sm<T>& sm,
+                                                const FrameCtx& fc, const Vec<T>* __restrict__ buf, int lo,
+                                                typename Acc<T>::type (&acc)[LC]) {
+  using V = Vec<T>;
+  using A = Acc<T>;
+  const int MN = a.MN, RS = a.RS, Lcta = a.Lcta;
 #pragma unroll
   for (int j = 0; j < LC; ++j) acc[j] = A::zero();
-  const int gcol = cx.g * LC;  // first owned column inside the CTA
+  Skipped sk = {0u, false};
+  const int gcol = cx.g * LC;                    // first owned column inside the CTA
   const V* tb = buf + (lo + cx.k) * RS + gcol;  // this thread's row in the slice
   for (int p = 0; p < fc.P; ++p) {
     const PathEnt<T> pe = get_path(a, sm, fc, p);
     const int dl = pe.dl;
-    const int sh = HERM ? -dl : dl;
-    const int loc0 = gcol + sh;
-    V coef = pe.coef(HERM);
-    if (dl != 0) coef = cmul(coef, twid(sm, wrap1(HERM ? dl * cx.k : -dl * cx.k, MN)));
-    if (fc.halo && loc0 >= 0 && loc0 + LC <= Lcta) {
-      // source row inside the halo, source columns local and contiguous
-      const V* src = tb + (HERM ? -pe.off : pe.off);
-      if constexpr (sizeof(T) == 4) {
-        unsigned long long X, Y;
-        if (dl == 0) {  // warp-uniform gain: FFMA2 operand pairs straight from the table
-          const float4 q = HERM ? pe.hh : pe.hf;
-          X = pack2(q.x, q.y);
-          Y = pack2(q.z, q.w);
-        } else {
-          X = pack2(coef.x, coef.x);
-          Y = pack2(-coef.y, coef.y);
-        }
-        gather_run<LC>(src, (loc0 & 1) != 0, X, Y, acc);
+    if (!tap_is_local<T, LC, HERM>(fc, cx, dl, Lcta)) {
+      if (p < 32) sk.mask |= 1u << p;
+      else sk.late = true;
+      continue;
+    }
+    const int loc0 = gcol + (HERM ? -dl : dl);
+    const V* src = tb + (HERM ? -pe.off : pe.off);
+    if constexpr (sizeof(T) == 4) {
+      unsigned long long X, Y;
+      if (dl == 0) {  // warp-uniform gain: FFMA2 operand pairs straight from the table
+        const float4 q = HERM ? pe.hh : pe.hf;
+        X = pack2(q.x, q.y);
+        Y = pack2(q.z, q.w);
       } else {
-        gather_run<LC>(src, false, coef, acc);
+        const V coef = cmul(pe.coef(HERM), twid(sm, wrap1(HERM ? dl * cx.k : -dl * cx.k, MN)));
+        X = pack2(coef.x, coef.x);
+        Y = pack2(-coef.y, coef.y);
       }
+      gather_run<LC>(src, (loc0 & 1) != 0, X, Y, acc);
     } else {
-      // columns owned by other CTAs (DSMEM) or wrapping mod N, or (no halo this
-      // frame) rows wrapping the delay period
-      const int ar = HERM ? cx.k - pe.dk : cx.k + pe.dk;  // unwrapped source row
-      int row = ar, nw = 0;
-      if (!fc.halo) {
-        nw = ar < 0 ? -1 : (ar >= M ? 1 : 0);
-        row = ar - nw * M;
-      }
-      // columns owned by other CTAs of the cluster (DSMEM) and/or wrapping mod N;
-      // the run crosses at most one owner boundary since LC <= Lcta
-      const int base = wrap1(cx.colbase + sh, N);
-      const int own0 = base / Lcta;
-      const int l0 = base - own0 * Lcta;
-      const int split = Lcta - l0;
-      const int own1 = own0 + 1 == a.C ? 0 : own0 + 1;
-      const uint32_t rowaddr = smem_addr(buf + (lo + row) * RS);
-      const uint32_t a0 = map_rank(rowaddr + (uint32_t)(l0 * (int)sizeof(V)), own0);
-      const uint32_t a1 = map_rank(rowaddr, own1);
-#pragma unroll
-      for (int j = 0; j < LC; ++j) {
-        const uint32_t ad = j < split ? a0 + (uint32_t)(j * (int)sizeof(V)) : a1 + (uint32_t)((j - split) * (int)sizeof(V));
-        V v = ld_cluster(static_cast<V*>(nullptr), ad);
-        if (nw != 0) {  // quasi-periodic wrap applied in registers (no halo this frame)
-          const int ls = base + j < N ? base + j : base + j - N;
-          V t = sm.tw[ls];
-          if (nw < 0) t = cconj(t);
-          v = cmul(v, t);
-        }
-        A::mac(acc[j], coef, v);
-      }
+      V coef = pe.coef(HERM);
+      if (dl != 0) coef = cmul(coef, twid(sm, wrap1(HERM ? dl * cx.k : -dl * cx.k, MN)));
+      gather_run<LC>(src, false, coef, acc);
+    }
+  }
+  return sk;
+}
+
+template <typename T, int LC, bool HERM>
+__device__ __forceinline__ void ss_mvm_remote(const SolveArgs& a, const Ctx& cx, const Sm<T>& sm,
+                                              const FrameCtx& fc, const Vec<T>* __restrict__ buf, int lo,
+                                              Skipped sk, typename Acc<T>::type (&acc)[LC]) {
+  for (uint32_t m = sk.mask; m; m &= m - 1) {
+    const int p = __ffs(m) - 1;
+    tap_remote<T, LC, HERM>(a, cx, sm, fc, buf, lo, get_path(a, sm, fc, p), acc);
+  }
+  if (sk.late) {
+    for (int p = 32; p < fc.P; ++p) {
+      const PathEnt<T> pe = get_path(a, sm, fc, p);
+      if (!tap_is_local<T, LC, HERM>(fc, cx, pe.dl, a.Lcta)) tap_remote<T, LC, HERM>(a, cx, sm, fc, buf, lo, pe, acc);
     }
   }
 }
@@ -382,26 +430,32 @@ __device__ __forceinline__ void cl_sync(int C) {
 // per-warp pairs through DSMEM after the barrier.
 constexpr int kPushSlots = 64;
 
+// Publish this warp's pair (before the cluster barrier's arrive).
 template <typename T>
-__device__ __forceinline__ Vec<T> cluster_sum(Vec<T> part, Vec<T>* slot, int C, int nwarps, int lane, int warp,
-                                              int r0, int w0, int rank) {
-  using V = Vec<T>;
+__device__ __forceinline__ void red_push(Vec<T> part, Vec<T>* slot, int C, int nwarps, int lane, int warp, int rank) {
   part.x = warp_sum(part.x);
   part.y = warp_sum(part.y);
-  const int total = C * nwarps;
-  V s = czero<V>();
-  if (total <= kPushSlots) {
+  if (C * nwarps <= kPushSlots) {
     const int idx = rank * nwarps + warp;
     if (C == 1) {
       if (lane == 0) slot[idx] = part;
     } else if (lane < C) {
       st_cluster(map_rank(smem_addr(slot + idx), lane), part);
     }
-    cl_sync<T>(C);
+  } else if (lane == 0) {
+    slot[warp] = part;
+  }
+}
+
+// Cluster-wide total (after the cluster barrier's wait); identical in every warp.
+template <typename T>
+__device__ __forceinline__ Vec<T> red_read(const Vec<T>* slot, int C, int nwarps, int lane, int r0, int w0) {
+  using V = Vec<T>;
+  const int total = C * nwarps;
+  V s = czero<V>();
+  if (total <= kPushSlots) {
     for (int i = lane; i < total; i += 32) s = cadd(s, slot[i]);
   } else {
-    if (lane == 0) slot[warp] = part;
-    cl_sync<T>(C);
     const uint32_t base = smem_addr(slot);
     for (int r = r0, w = w0; r < C;) {
       s = cadd(s, ld_cluster(static_cast<V*>(nullptr), map_rank(base + w * (int)sizeof(V), r)));
@@ -412,6 +466,15 @@ __device__ __forceinline__ Vec<T> cluster_sum(Vec<T> part, Vec<T>* slot, int C, 
   s.x = warp_sum(s.x);
   s.y = warp_sum(s.y);
   return s;
+}
+
+// Split cluster barrier: arrive (release) -> CTA barrier -> ... -> wait (acquire).
+__device__ __forceinline__ void cl_arrive(int C) {
+  if (C > 1) asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+  __syncthreads();
+}
+__device__ __forceinline__ void cl_wait(int C) {
+  if (C > 1) asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
 
 // ---- packed elementwise CG arithmetic (FFMA2 for fp32)
@@ -473,11 +536,6 @@ template <typename T, int BA, int XC>
 __device__ __forceinline__ int epilogue(const SolveArgs& a, const Vec<T> (&xv)[XC], size_t q0, int M, T scale) {
   Vec<T>* xo = reinterpret_cast<Vec<T>*>(a.x);
   int errs = 0;
-  uint8_t tx[XC];
-  if (BA > 0 && a.txl) {
-#pragma unroll
-    for (int j = 0; j < XC; ++j) tx[j] = a.txl[q0 + (size_t)j * M];
-  }
 #pragma unroll
   for (int j = 0; j < XC; ++j) {
     const size_t q = q0 + (size_t)j * M;
@@ -495,7 +553,7 @@ __device__ __forceinline__ int epilogue(const SolveArgs& a, const Vec<T> (&xv)[X
         }
       }
       if (a.labels) a.labels[q] = (uint8_t)lab;
-      if (a.txl) errs += __popc((unsigned)(lab ^ tx[j]));
+      if (a.txl) errs += __popc((unsigned)(lab ^ a.txl[q]));
     }
   }
   return errs;
@@ -634,14 +692,17 @@ __global__ void __launch_bounds__(sscga_max_threads(sizeof(T), LC), 1) sscga_ker
         if (a.txl && (cx.k & 31) == 0) asm volatile("prefetch.global.L2 [%0];" :: "l"(a.txl + q));
       }
     }
-    cl_sync<T>(a.C);
-
     // CG in the "u recurrence" form: with u = H p kept from the previous step,
     //   u' = H c + beta u,  p' = c + beta p   (= H (c + beta p), c + beta p)
     // so the gathered vectors are c (by H) and u (by H^H) and each iteration
     // needs two cluster barriers.  Same algorithm as equalize.py:59-76.
+    // Every barrier is split: publish (data + reduction partials), arrive,
+    // CTA barrier, the local-tap half of the next MVM, wait, the remote taps.
     typename A::type acc[LC];
-    ss_mvm<T, LC, true>(a, cx, sm, fc, sm.u, fc.lo_u, acc);  // b = H^H y (equalize.py:52)
+    cl_arrive(a.C);  // y published
+    Skipped sk = ss_mvm_local<T, LC, true>(a, cx, sm, fc, sm.u, fc.lo_u, acc);  // b = H^H y (equalize.py:52)
+    cl_wait(a.C);
+    ss_mvm_remote<T, LC, true>(a, cx, sm, fc, sm.u, fc.lo_u, sk, acc);
     V nrm = czero<V>();
 #pragma unroll
     for (int j = 0; j < LC; ++j) {
@@ -658,9 +719,13 @@ __global__ void __launch_bounds__(sscga_max_threads(sizeof(T), LC), 1) sscga_ker
 #pragma unroll
       for (int c0 = 0; c0 < LC; c0 += XC) x_store<T, XC>(xta + (uint32_t)((c0 / XC) * XCW), z);  // x = 0
     }
-    T cn = cluster_sum<T>(cmake<V>(nrm.x + nrm.y, T(0)), red + (1 * 2 + par[1]) * kPushSlots, a.C, nwarps, lane,
-                          warp, r0, w0, cx.rank).x;
+    V* slot = red + (1 * 2 + par[1]) * kPushSlots;
     par[1] ^= 1;
+    red_push<T>(cmake<V>(nrm.x + nrm.y, T(0)), slot, a.C, nwarps, lane, warp, cx.rank);
+    cl_arrive(a.C);  // c = b published
+    sk = ss_mvm_local<T, LC, false>(a, cx, sm, fc, sm.c, fc.lo_c, acc);
+    cl_wait(a.C);
+    T cn = red_read<T>(slot, a.C, nwarps, lane, r0, w0).x;
     T beta = T(0);
     if (lead && cnorm) cnorm[(size_t)f * stride] = cn;
 
@@ -668,7 +733,7 @@ __global__ void __launch_bounds__(sscga_max_threads(sizeof(T), LC), 1) sscga_ker
     bool exact = false;
     for (int it = 0; it < a.iters; ++it) {
       // u = H c + beta u_old, p = c + beta p_old      (= H p, p of equalize.py:60, 72)
-      ss_mvm<T, LC, false>(a, cx, sm, fc, sm.c,fc.lo_c, acc);
+      ss_mvm_remote<T, LC, false>(a, cx, sm, fc, sm.c, fc.lo_c, sk, acc);
       V nu = czero<V>(), np = czero<V>();
 #pragma unroll
       for (int c0 = 0; c0 < LC; c0 += XC) {
@@ -702,17 +767,24 @@ __global__ void __launch_bounds__(sscga_max_threads(sizeof(T), LC), 1) sscga_ker
         x_store<T, XC>(pta + off, pv);
       }
       if (!cx.active) nu = np = czero<V>();
-      const V up = cluster_sum<T>(cmake<V>(nu.x + nu.y, np.x + np.y), red + (0 * 2 + par[0]) * kPushSlots, a.C,
-                                  nwarps, lane, warp, r0, w0, cx.rank);
+      slot = red + (0 * 2 + par[0]) * kPushSlots;
       par[0] ^= 1;
+      red_push<T>(cmake<V>(nu.x + nu.y, np.x + np.y), slot, a.C, nwarps, lane, warp, cx.rank);
+      cl_arrive(a.C);  // u published
+      // ap = H^H u + lam p;  x += alpha p;  c -= alpha ap      (equalize.py:60-70)
+      sk = ss_mvm_local<T, LC, true>(a, cx, sm, fc, sm.u, fc.lo_u, acc);
+      cl_wait(a.C);
+      ss_mvm_remote<T, LC, true>(a, cx, sm, fc, sm.u, fc.lo_u, sk, acc);
+      const V up = red_read<T>(slot, a.C, nwarps, lane, r0, w0);
       const T denom = up.x + lam * up.y;  // ||H p||^2 + lam ||p||^2 = Re p^H (H^H H + lam I) p
       if (denom == T(0)) {  // equalize.py:64-67
         exact = true;
+        // peers may still be reading this CTA's u: one more full barrier
+        cl_arrive(a.C);
+        cl_wait(a.C);
         break;
       }
       const T alpha = cn / denom;
-      // ap = H^H u + lam p;  x += alpha p;  c -= alpha ap      (equalize.py:60-70)
-      ss_mvm<T, LC, true>(a, cx, sm, fc, sm.u, fc.lo_u, acc);
       V nc = czero<V>();
 #pragma unroll
       for (int c0 = 0; c0 < LC; c0 += XC) {
@@ -739,9 +811,13 @@ __global__ void __launch_bounds__(sscga_max_threads(sizeof(T), LC), 1) sscga_ker
       }
       if (cx.active) put_ext<T, LC>(sm.c, RS, fc.lo_c, fc.hi_c, M, cx, w, sm.tw);
       else nc = czero<V>();
-      const T nn = cluster_sum<T>(cmake<V>(nc.x + nc.y, T(0)), red + (1 * 2 + par[1]) * kPushSlots, a.C, nwarps,
-                                  lane, warp, r0, w0, cx.rank).x;
+      slot = red + (1 * 2 + par[1]) * kPushSlots;
       par[1] ^= 1;
+      red_push<T>(cmake<V>(nc.x + nc.y, T(0)), slot, a.C, nwarps, lane, warp, cx.rank);
+      cl_arrive(a.C);  // c published
+      if (it + 1 < a.iters) sk = ss_mvm_local<T, LC, false>(a, cx, sm, fc, sm.c, fc.lo_c, acc);  // next H c
+      cl_wait(a.C);
+      const T nn = red_read<T>(slot, a.C, nwarps, lane, r0, w0).x;
       beta = nn / cn;
       cn = nn;
       done = it + 1;
