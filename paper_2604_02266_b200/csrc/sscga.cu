@@ -84,6 +84,10 @@ struct FrameCtx {
   bool in_smem;  // tap table staged in shared memory
   bool halo;     // every tap's source row lies inside the extension halo
   int lo_c, hi_c, lo_u, hi_u;  // halo rows below / above the M real rows of c and u
+  // P <= 32 with a halo: taps split into d_l == 0 ones (always local, gain
+  // warp-uniform, minimal loop) and the rest (general loop)
+  bool split;
+  uint32_t m0, m1;
 };
 
 template <typename T> struct Sm {
@@ -236,6 +240,43 @@ __device__ __forceinline__ bool tap_is_local(const FrameCtx& fc, const Ctx& cx, 
   return fc.halo && loc0 >= 0 && loc0 + LC <= Lcta;
 }
 
+// One tap of the local pass (general case): gather it if its columns are this
+// CTA's own and contiguous, else record it for the remote pass.
+template <typename T, int LC, bool HERM>
+__device__ __forceinline__ void local_tap(const SolveArgs& a, const Ctx& cx, const Sm<T>& sm, const FrameCtx& fc,
+                                          const Vec<T>* tb, int p, Skipped& sk,
+                                          typename Acc<T>::type (&acc)[LC]) {
+  using V = Vec<T>;
+  const int MN = a.MN, Lcta = a.Lcta;
+  const int gcol = cx.g * LC;
+  const PathEnt<T> pe = get_path(a, sm, fc, p);
+  const int dl = pe.dl;
+  if (!tap_is_local<T, LC, HERM>(fc, cx, dl, Lcta)) {
+    if (p < 32) sk.mask |= 1u << p;
+    else sk.late = true;
+    return;
+  }
+  const int loc0 = gcol + (HERM ? -dl : dl);
+  const V* src = tb + (HERM ? -pe.off : pe.off);
+  if constexpr (sizeof(T) == 4) {
+    unsigned long long X, Y;
+    if (dl == 0) {  // warp-uniform gain: FFMA2 operand pairs straight from the table
+      const float4 q = HERM ? pe.hh : pe.hf;
+      X = pack2(q.x, q.y);
+      Y = pack2(q.z, q.w);
+    } else {
+      const V coef = cmul(pe.coef(HERM), twid(sm, wrap1(HERM ? dl * cx.k : -dl * cx.k, MN)));
+      X = pack2(coef.x, coef.x);
+      Y = pack2(-coef.y, coef.y);
+    }
+    gather_run<LC>(src, (loc0 & 1) != 0, X, Y, acc);
+  } else {
+    V coef = pe.coef(HERM);
+    if (dl != 0) coef = cmul(coef, twid(sm, wrap1(HERM ? dl * cx.k : -dl * cx.k, MN)));
+    gather_run<LC>(src, false, coef, acc);
+  }
+}
+
 template <typename T, int LC, bool HERM>
 __device__ __forceinline__ Skipped ss_mvm_local(const SolveArgs& a, const Ctx& cx, const Sm<T>& sm,
                                                 const FrameCtx& fc, const Vec<T>* __restrict__ buf, int lo,
@@ -248,33 +289,23 @@ __device__ __forceinline__ Skipped ss_mvm_local(const SolveArgs& a, const Ctx& c
   Skipped sk = {0u, false};
   const int gcol = cx.g * LC;                    // first owned column inside the CTA
   const V* tb = buf + (lo + cx.k) * RS + gcol;  // this thread's row in the slice
-  for (int p = 0; p < fc.P; ++p) {
-    const PathEnt<T> pe = get_path(a, sm, fc, p);
-    const int dl = pe.dl;
-    if (!tap_is_local<T, LC, HERM>(fc, cx, dl, Lcta)) {
-      if (p < 32) sk.mask |= 1u << p;
-      else sk.late = true;
-      continue;
-    }
-    const int loc0 = gcol + (HERM ? -dl : dl);
-    const V* src = tb + (HERM ? -pe.off : pe.off);
-    if constexpr (sizeof(T) == 4) {
-      unsigned long long X, Y;
-      if (dl == 0) {  // warp-uniform gain: FFMA2 operand pairs straight from the table
+  if (fc.split) {
+    // d_l == 0 taps: source columns are this thread's own, gain is uniform
+    for (uint32_t m = fc.m0; m; m &= m - 1) {
+      const PathEnt<T>& pe = sm.ptab[__ffs(m) - 1];
+      const V* src = tb + (HERM ? -pe.off : pe.off);
+      if constexpr (sizeof(T) == 4) {
         const float4 q = HERM ? pe.hh : pe.hf;
-        X = pack2(q.x, q.y);
-        Y = pack2(q.z, q.w);
+        gather_run<LC>(src, false, pack2(q.x, q.y), pack2(q.z, q.w), acc);
       } else {
-        const V coef = cmul(pe.coef(HERM), twid(sm, wrap1(HERM ? dl * cx.k : -dl * cx.k, MN)));
-        X = pack2(coef.x, coef.x);
-        Y = pack2(-coef.y, coef.y);
+        gather_run<LC>(src, false, pe.coef(HERM), acc);
       }
-      gather_run<LC>(src, (loc0 & 1) != 0, X, Y, acc);
-    } else {
-      V coef = pe.coef(HERM);
-      if (dl != 0) coef = cmul(coef, twid(sm, wrap1(HERM ? dl * cx.k : -dl * cx.k, MN)));
-      gather_run<LC>(src, false, coef, acc);
     }
+  }
+  if (fc.split) {
+    for (uint32_t m = fc.m1; m; m &= m - 1) local_tap<T, LC, HERM>(a, cx, sm, fc, tb, __ffs(m) - 1, sk, acc);
+  } else {
+    for (int p = 0; p < fc.P; ++p) local_tap<T, LC, HERM>(a, cx, sm, fc, tb, p, sk, acc);
   }
   return sk;
 }
@@ -667,6 +698,14 @@ __global__ void __launch_bounds__(sscga_max_threads(sizeof(T), LC), 1) sscga_ker
       fc.hi_u = max(0, -dmin);
       fc.halo = fc.lo_c + fc.hi_c <= a.H;
       if (!fc.halo) fc.lo_c = fc.hi_c = fc.lo_u = fc.hi_u = 0;
+      fc.split = fc.halo && fc.in_smem && fc.P <= 32;
+      fc.m0 = fc.m1 = 0u;
+      if (fc.split) {
+        for (int p = 0; p < fc.P; ++p) {
+          if (sm.ptab[p].dl == 0) fc.m0 |= 1u << p;
+          else fc.m1 |= 1u << p;
+        }
+      }
     }
 
     const int RS = a.RS;
