@@ -71,6 +71,14 @@ template <> struct __align__(16) PathEnt<float> {
 __device__ __forceinline__ float4 quad(float2 g) { return make_float4(g.x, g.x, -g.y, g.y); }
 __device__ __forceinline__ double2 quad(double2 g) { return g; }
 
+// Dense per-frame list of the d_l == 0 taps (the hot loop): slice offset and
+// both direction's gains, 48 bytes, read with two broadcast 128-bit loads.
+template <typename T> struct __align__(16) Tap0 {
+  decltype(PathEnt<T>::hf) hf, hh;
+  int off, pad[3];
+};
+constexpr int kTap0Cap = 32;
+
 struct Ctx {
   int k;        // delay row owned by this thread
   int g;        // column group inside the CTA
@@ -88,6 +96,7 @@ struct FrameCtx {
   // warp-uniform, minimal loop) and the rest (general loop)
   bool split;
   uint32_t m0, m1;
+  int n0;  // number of d_l == 0 taps (dense list Sm::t0)
 };
 
 template <typename T> struct Sm {
@@ -98,6 +107,7 @@ template <typename T> struct Sm {
   Vec<T>* thi;
   Vec<T>* tw;
   PathEnt<T>* ptab;
+  Tap0<T>* t0;
   T* red;
   int tlb;  // log2(TL)
 };
@@ -291,14 +301,14 @@ __device__ __forceinline__ Skipped ss_mvm_local(const SolveArgs& a, const Ctx& c
   const V* tb = buf + (lo + cx.k) * RS + gcol;  // this thread's row in the slice
   if (fc.split) {
     // d_l == 0 taps: source columns are this thread's own, gain is uniform
-    for (uint32_t m = fc.m0; m; m &= m - 1) {
-      const PathEnt<T>& pe = sm.ptab[__ffs(m) - 1];
-      const V* src = tb + (HERM ? -pe.off : pe.off);
+    for (int i = 0; i < fc.n0; ++i) {
+      const Tap0<T>& e = sm.t0[i];
+      const V* src = tb + (HERM ? -e.off : e.off);
       if constexpr (sizeof(T) == 4) {
-        const float4 q = HERM ? pe.hh : pe.hf;
+        const float4 q = HERM ? e.hh : e.hf;
         gather_run<LC>(src, false, pack2(q.x, q.y), pack2(q.z, q.w), acc);
       } else {
-        gather_run<LC>(src, false, pe.coef(HERM), acc);
+        gather_run<LC>(src, false, HERM ? e.hh : e.hf, acc);
       }
     }
   }
@@ -544,7 +554,8 @@ __host__ __device__ static inline SmemLayout layout_impl(int M, int N, int C, in
   L.tlo = o; o = align16(o + (size_t)TL * vb);
   L.thi = o; o = align16(o + (size_t)TH * vb);
   L.tw = o; o = align16(o + (size_t)N * vb);
-  L.ptab = o; o = align16(o + (size_t)pcap * 48);  // sizeof(PathEnt<T>) == 48
+  // tap table (pcap PathEnt) followed by the dense d_l == 0 list (kTap0Cap Tap0), 48 B each
+  L.ptab = o; o = align16(o + (size_t)(pcap + kTap0Cap) * 48);
   L.red = o; o = align16(o + 2 * 2 * 64 * vb);  // [2 kinds][2 parities][kPushSlots] pairs
   L.total = o;
   return L;
@@ -605,6 +616,8 @@ __global__ void __launch_bounds__(sscga_max_threads(sizeof(T), LC), 1) sscga_ker
   sm.thi = reinterpret_cast<V*>(smem + L.thi);
   sm.tw = reinterpret_cast<V*>(smem + L.tw);
   sm.ptab = reinterpret_cast<PathEnt<T>*>(smem + L.ptab);
+  sm.t0 = reinterpret_cast<Tap0<T>*>(smem + L.ptab + (size_t)a.pcap * 48);
+  static_assert(sizeof(PathEnt<T>) == 48 && sizeof(Tap0<T>) == 48, "tap table stride");
   sm.red = reinterpret_cast<T*>(smem + L.red);
   sm.tlb = __ffs(a.TL) - 1;
 
@@ -698,14 +711,25 @@ __global__ void __launch_bounds__(sscga_max_threads(sizeof(T), LC), 1) sscga_ker
       fc.hi_u = max(0, -dmin);
       fc.halo = fc.lo_c + fc.hi_c <= a.H;
       if (!fc.halo) fc.lo_c = fc.hi_c = fc.lo_u = fc.hi_u = 0;
-      fc.split = fc.halo && fc.in_smem && fc.P <= 32;
+      fc.split = fc.halo && fc.in_smem && fc.P <= kTap0Cap;
       fc.m0 = fc.m1 = 0u;
+      fc.n0 = 0;
       if (fc.split) {
         for (int p = 0; p < fc.P; ++p) {
           if (sm.ptab[p].dl == 0) fc.m0 |= 1u << p;
           else fc.m1 |= 1u << p;
         }
+        fc.n0 = __popc(fc.m0);
+        if (tid < fc.P && ((fc.m0 >> tid) & 1u)) {
+          Tap0<T> e;
+          e.hf = sm.ptab[tid].hf;
+          e.hh = sm.ptab[tid].hh;
+          e.off = sm.ptab[tid].off;
+          e.pad[0] = e.pad[1] = e.pad[2] = 0;
+          sm.t0[__popc(fc.m0 & ((1u << tid) - 1u))] = e;
+        }
       }
+      __syncthreads();
     }
 
     const int RS = a.RS;
