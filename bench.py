@@ -55,6 +55,7 @@ def parse():
     ap.add_argument("--batch", type=int, default=0, help="frames per GPU (default: config's)")
     ap.add_argument("--snr", type=float, default=25.0)
     ap.add_argument("--iters", type=int, default=10)
+    ap.add_argument("--paths", type=int, default=0, help="override taps per frame (analysis only)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-latency", action="store_true")
@@ -272,7 +273,7 @@ def main():
     from paper_2604_02266_b200 import _native as nat
     from paper_2604_02266_b200.synth import make_frames
 
-    M, N, P = cfg["M"], cfg["N"], cfg["P"]
+    M, N, P = cfg["M"], cfg["N"], (args.paths or cfg["P"])
     MN = M * N
     B = args.batch or cfg["batch"]
     bps = BPS[cfg["mod"]]

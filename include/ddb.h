@@ -155,6 +155,14 @@ int32_t ddb_detect_paths(int32_t batch, int32_t M, int32_t N, const void* heff, 
  *      mode 1: packed FFMA2).  scratch: device float[blocks]. */
 int32_t ddb_probe_fp32(int32_t mode, int32_t blocks, int32_t iters, float* scratch, void* stream);
 
+/* ---- measurement helper (not a reference interface): ddb_sscga_solve with
+ *      clock64 phase accounting on thread 0 of every CTA.  phase_cycles:
+ *      device int64 [4736][12], zero-initialised by the caller; row = CTA,
+ *      columns = setup, arrive, mvm_local, wait, mvm_remote, read, step1,
+ *      step3, epilogue, tail. */
+int32_t ddb_sscga_profile_phases(const ddb_sscga_problem* prob, const ddb_sscga_outputs* out,
+                                 long long* phase_cycles, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -82,7 +82,9 @@ _SIGNATURES = {
     "ddb_detect_paths": (C.c_int32, [C.c_int32, C.c_int32, C.c_int32, C.c_void_p, C.c_double, C.c_int32,
                                      C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
     "ddb_probe_fp32": (C.c_int32, [C.c_int32, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p]),
+    "ddb_sscga_profile_phases": (C.c_int32, [C.POINTER(Problem), C.POINTER(Outputs), C.c_void_p, C.c_void_p]),
 }
+PHASES = ("setup", "arrive", "mvm_local", "wait", "mvm_remote", "read", "step1", "step3", "epilogue", "tail")
 
 _lock = threading.Lock()
 _lib = None

@@ -209,7 +209,10 @@ class SsCgaSolver:
     def solve(self, y: torch.Tensor, paths: PathBatch, lam, *, tx_labels: Optional[torch.Tensor] = None,
               noise_var: Optional[torch.Tensor] = None, out: Optional[SolveResult] = None,
               llr: bool = False, trace: bool = True, profile: bool = False,
-              stream: Optional[torch.cuda.Stream] = None) -> SolveResult:
+              stream: Optional[torch.cuda.Stream] = None,
+              phase_cycles: Optional[torch.Tensor] = None) -> SolveResult:
+        """phase_cycles (measurement only): zeroed int64 CUDA tensor [4736, 12] that
+        receives per-CTA clock64 phase totals (ddb_sscga_profile_phases)."""
         B = y.shape[0]
         lam = self.lam_tensor(lam, B)
         self._check_inputs(y, paths, lam)
@@ -229,8 +232,12 @@ class SsCgaSolver:
                                               or tx_labels is not None) else 0,
             _ptr(out.labels), _ptr(out.llr), _ptr(noise_var), _ptr(tx_labels),
             _ptr(out.bit_errors if tx_labels is not None else None))
-        nat.check(self.lib.ddb_sscga_solve(C.byref(prob), C.byref(outs), None, 0, _stream_handle(stream)),
-                  "ddb_sscga_solve")
+        if phase_cycles is not None:
+            nat.check(self.lib.ddb_sscga_profile_phases(C.byref(prob), C.byref(outs), _ptr(phase_cycles),
+                                                        _stream_handle(stream)), "ddb_sscga_profile_phases")
+        else:
+            nat.check(self.lib.ddb_sscga_solve(C.byref(prob), C.byref(outs), None, 0, _stream_handle(stream)),
+                      "ddb_sscga_solve")
         return out
 
     # -- matrix-free operator -------------------------------------------------

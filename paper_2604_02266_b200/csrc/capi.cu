@@ -159,10 +159,8 @@ size_t ddb_sscga_workspace_bytes(const ddb_sscga_problem* prob) {
   return 0;  // the fused solve keeps all state on chip
 }
 
-int32_t ddb_sscga_solve(const ddb_sscga_problem* prob, const ddb_sscga_outputs* out, void* workspace,
-                        size_t workspace_bytes, void* stream) {
-  (void)workspace;
-  (void)workspace_bytes;
+static int32_t solve_impl(const ddb_sscga_problem* prob, const ddb_sscga_outputs* out, long long* prof,
+                          void* stream) {
   if (!prob || !out) return fail(DDB_ERR_INVALID, "null problem/outputs");
   if (prob->batch < 0) return fail(DDB_ERR_INVALID, "negative batch");
   if (prob->iterations < 1) return fail(DDB_ERR_INVALID, "need at least one iteration");  // equalize.py:26-27
@@ -219,10 +217,24 @@ int32_t ddb_sscga_solve(const ddb_sscga_problem* prob, const ddb_sscga_outputs* 
   a.nvar = out->noise_var;
   a.txl = out->tx_labels;
   a.berr = out->bit_errors;
+  a.prof = prof;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   cudaError_t e = prob->dtype == DDB_F64 ? ddb::launch_sscga<double>(a, s, st) : ddb::launch_sscga<float>(a, s, st);
   if (e != cudaSuccess) return cuda_fail(e, "sscga launch");
   return ok();
+}
+
+int32_t ddb_sscga_solve(const ddb_sscga_problem* prob, const ddb_sscga_outputs* out, void* workspace,
+                        size_t workspace_bytes, void* stream) {
+  (void)workspace;
+  (void)workspace_bytes;
+  return solve_impl(prob, out, nullptr, stream);
+}
+
+int32_t ddb_sscga_profile_phases(const ddb_sscga_problem* prob, const ddb_sscga_outputs* out,
+                                 long long* phase_cycles, void* stream) {
+  if (!phase_cycles) return fail(DDB_ERR_INVALID, "null phase buffer");
+  return solve_impl(prob, out, phase_cycles, stream);
 }
 
 int32_t ddb_ss_apply(const ddb_sscga_problem* prob, void* outp, int32_t hermitian, void* stream) {

@@ -37,7 +37,10 @@ struct SolveArgs {
   const void* nvar;
   const uint8_t* txl;
   int* berr;
+  long long* prof;  // optional per-CTA phase cycle counters [gridDim.x][kProfPhases]
 };
+
+constexpr int kProfPhases = 12;
 
 struct LaunchShape {
   int cluster, lcta, lc, threads, smem, halo, tl, th, pcap, tcols;

@@ -556,7 +556,7 @@ __host__ __device__ static inline SmemLayout layout_impl(int M, int N, int C, in
   L.tw = o; o = align16(o + (size_t)N * vb);
   // tap table (pcap PathEnt) followed by the dense d_l == 0 list (kTap0Cap Tap0), 48 B each
   L.ptab = o; o = align16(o + (size_t)(pcap + kTap0Cap) * 48);
-  L.red = o; o = align16(o + 2 * 2 * 64 * vb);  // [2 kinds][2 parities][kPushSlots] pairs
+  L.red = o; o = align16(o + 2 * 2 * 64 * vb + kProfPhases * 8);  // [2][2][kPushSlots] pairs + prof
   L.total = o;
   return L;
 }
@@ -571,6 +571,23 @@ void twiddle_split(int MN, int* TL, int* TH) {
   *TL = tl;
   *TH = (MN + tl - 1) / tl;
 }
+
+// Phase timer (measurement builds of a launch only: SolveArgs::prof != null):
+// thread 0 of each CTA attributes clock64 intervals to the phase being run.
+enum Phase { kSetup, kArrive, kMvmLocal, kWait, kMvmRemote, kRead, kStep1, kStep3, kEpilogue, kTail };
+struct Prof {
+  long long* acc;  // shared [kProfPhases] on thread 0, nullptr elsewhere
+  long long t;
+  int cur;
+  __device__ __forceinline__ void mark(int next) {
+    if (acc) {
+      const long long now = clock64();
+      acc[cur] += now - t;
+      t = now;
+      cur = next;
+    }
+  }
+};
 
 // Epilogue for XC equalized symbols at global indices q0 + j M: x_hat, hard
 // labels, max-log LLRs (vector stores) and the bit-error count vs TX labels.
@@ -662,6 +679,15 @@ __global__ void __launch_bounds__(sscga_max_threads(sizeof(T), LC), 1) sscga_ker
   const bool lead = (cx.rank == 0 && tid == 0);
   const int stride = a.iters + 1;
   int par[2] = {0, 0};  // 0: (||u||^2, ||p||^2), 1: (||c||^2, -)
+  Prof pf;
+  pf.acc = nullptr;
+  pf.t = 0;
+  pf.cur = kTail;
+  if (a.prof && tid == 0) {
+    pf.acc = reinterpret_cast<long long*>(red + 2 * 2 * kPushSlots);
+    for (int i = 0; i < kProfPhases; ++i) pf.acc[i] = 0;
+    pf.t = clock64();
+  }
 
   for (int f = blockIdx.x / a.C; f < a.B; f += a.n_clusters) {
     FrameCtx fc;
@@ -690,6 +716,7 @@ __global__ void __launch_bounds__(sscga_max_threads(sizeof(T), LC), 1) sscga_ker
     }
 
     // ---- frame setup: tap table, extension halo sizes
+    pf.mark(kSetup);
     fc.in_smem = fc.P <= a.pcap;
     if (fc.in_smem) {
       const V* gains = reinterpret_cast<const V*>(a.ph);
@@ -762,10 +789,15 @@ __global__ void __launch_bounds__(sscga_max_threads(sizeof(T), LC), 1) sscga_ker
     // Every barrier is split: publish (data + reduction partials), arrive,
     // CTA barrier, the local-tap half of the next MVM, wait, the remote taps.
     typename A::type acc[LC];
+    pf.mark(kArrive);
     cl_arrive(a.C);  // y published
+    pf.mark(kMvmLocal);
     Skipped sk = ss_mvm_local<T, LC, true>(a, cx, sm, fc, sm.u, fc.lo_u, acc);  // b = H^H y (equalize.py:52)
+    pf.mark(kWait);
     cl_wait(a.C);
+    pf.mark(kMvmRemote);
     ss_mvm_remote<T, LC, true>(a, cx, sm, fc, sm.u, fc.lo_u, sk, acc);
+    pf.mark(kStep1);
     V nrm = czero<V>();
 #pragma unroll
     for (int j = 0; j < LC; ++j) {
@@ -785,9 +817,13 @@ __global__ void __launch_bounds__(sscga_max_threads(sizeof(T), LC), 1) sscga_ker
     V* slot = red + (1 * 2 + par[1]) * kPushSlots;
     par[1] ^= 1;
     red_push<T>(cmake<V>(nrm.x + nrm.y, T(0)), slot, a.C, nwarps, lane, warp, cx.rank);
+    pf.mark(kArrive);
     cl_arrive(a.C);  // c = b published
+    pf.mark(kMvmLocal);
     sk = ss_mvm_local<T, LC, false>(a, cx, sm, fc, sm.c, fc.lo_c, acc);
+    pf.mark(kWait);
     cl_wait(a.C);
+    pf.mark(kRead);
     T cn = red_read<T>(slot, a.C, nwarps, lane, r0, w0).x;
     T beta = T(0);
     if (lead && cnorm) cnorm[(size_t)f * stride] = cn;
@@ -796,7 +832,9 @@ __global__ void __launch_bounds__(sscga_max_threads(sizeof(T), LC), 1) sscga_ker
     bool exact = false;
     for (int it = 0; it < a.iters; ++it) {
       // u = H c + beta u_old, p = c + beta p_old      (= H p, p of equalize.py:60, 72)
+      pf.mark(kMvmRemote);
       ss_mvm_remote<T, LC, false>(a, cx, sm, fc, sm.c, fc.lo_c, sk, acc);
+      pf.mark(kStep1);
       V nu = czero<V>(), np = czero<V>();
 #pragma unroll
       for (int c0 = 0; c0 < LC; c0 += XC) {
@@ -833,12 +871,18 @@ __global__ void __launch_bounds__(sscga_max_threads(sizeof(T), LC), 1) sscga_ker
       slot = red + (0 * 2 + par[0]) * kPushSlots;
       par[0] ^= 1;
       red_push<T>(cmake<V>(nu.x + nu.y, np.x + np.y), slot, a.C, nwarps, lane, warp, cx.rank);
+      pf.mark(kArrive);
       cl_arrive(a.C);  // u published
       // ap = H^H u + lam p;  x += alpha p;  c -= alpha ap      (equalize.py:60-70)
+      pf.mark(kMvmLocal);
       sk = ss_mvm_local<T, LC, true>(a, cx, sm, fc, sm.u, fc.lo_u, acc);
+      pf.mark(kWait);
       cl_wait(a.C);
+      pf.mark(kMvmRemote);
       ss_mvm_remote<T, LC, true>(a, cx, sm, fc, sm.u, fc.lo_u, sk, acc);
+      pf.mark(kRead);
       const V up = red_read<T>(slot, a.C, nwarps, lane, r0, w0);
+      pf.mark(kStep3);
       const T denom = up.x + lam * up.y;  // ||H p||^2 + lam ||p||^2 = Re p^H (H^H H + lam I) p
       if (denom == T(0)) {  // equalize.py:64-67
         exact = true;
@@ -877,9 +921,13 @@ __global__ void __launch_bounds__(sscga_max_threads(sizeof(T), LC), 1) sscga_ker
       slot = red + (1 * 2 + par[1]) * kPushSlots;
       par[1] ^= 1;
       red_push<T>(cmake<V>(nc.x + nc.y, T(0)), slot, a.C, nwarps, lane, warp, cx.rank);
+      pf.mark(kArrive);
       cl_arrive(a.C);  // c published
+      pf.mark(kMvmLocal);
       if (it + 1 < a.iters) sk = ss_mvm_local<T, LC, false>(a, cx, sm, fc, sm.c, fc.lo_c, acc);  // next H c
+      pf.mark(kWait);
       cl_wait(a.C);
+      pf.mark(kRead);
       const T nn = red_read<T>(slot, a.C, nwarps, lane, r0, w0).x;
       beta = nn / cn;
       cn = nn;
@@ -893,6 +941,7 @@ __global__ void __launch_bounds__(sscga_max_threads(sizeof(T), LC), 1) sscga_ker
     }
 
     // epilogue: x_hat out, fused hard decisions / LLRs / bit errors
+    pf.mark(kEpilogue);
     T scale = T(1);
     if (a.bps) {
       const T nv = nvar ? nvar[f] : lam;
@@ -918,6 +967,9 @@ __global__ void __launch_bounds__(sscga_max_threads(sizeof(T), LC), 1) sscga_ker
       if (lane == 0 && errs) atomicAdd(a.berr + f, errs);
     }
   }
+  pf.mark(kTail);
+  if (pf.acc)
+    for (int i = 0; i < kProfPhases; ++i) a.prof[(size_t)blockIdx.x * kProfPhases + i] = pf.acc[i];
   // no CTA may leave while a peer can still read its shared memory (DSMEM)
   tmem_fence_before();
   cl_sync<T>(a.C);

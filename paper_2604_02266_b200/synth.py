@@ -37,15 +37,21 @@ class FrameBatch:
 
 def veha_paths(B: int, grid: GridConfig, nu_max_hz: float, gen: torch.Generator, device,
                cdtype=torch.complex64, n_paths: int = 6) -> PathBatch:
-    delays = np.round(np.asarray(VEHA_DELAYS_US[:n_paths]) * 1e-6 * grid.B).astype(np.int64)
+    # beyond the six Veh-A paths, extra taps model fractional-Doppler leakage:
+    # the same delays one Doppler bin away, 25 dB down (analysis / stress only)
+    base = np.asarray(VEHA_DELAYS_US)
+    idx = np.arange(n_paths) % len(base)
+    delays = np.round(base[idx] * 1e-6 * grid.B).astype(np.int64)
     if delays.max() >= grid.M:
         raise ValueError("Veh-A delay spread exceeds the delay period; increase M")
-    powers = 10.0 ** (np.asarray(VEHA_POWERS_DB[:n_paths]) / 10.0)
+    pdb = np.where(np.arange(n_paths) < len(base), np.asarray(VEHA_POWERS_DB)[idx], -25.0)
+    powers = 10.0 ** (pdb / 10.0)
     mags = torch.as_tensor(np.sqrt(powers / powers.sum()), device=device, dtype=torch.float64)
     phase = torch.rand(B, n_paths, generator=gen, device=device, dtype=torch.float64) * 2 * np.pi
     u = torch.rand(B, n_paths, generator=gen, device=device, dtype=torch.float64)
     dop = torch.round(nu_max_hz * torch.cos(2 * np.pi * u) / grid.delta_nu).to(torch.int64)
-    dop = dop.clamp(-(grid.N // 2) + 1, grid.N // 2 - 1)
+    leak = torch.as_tensor((np.arange(n_paths) >= len(base)).astype(np.int64), device=device)
+    dop = (dop + leak[None, :]).clamp(-(grid.N // 2) + 1, grid.N // 2 - 1)
     k = (grid.K0 + torch.as_tensor(delays, device=device)[None, :]).expand(B, n_paths) % grid.M
     l = (grid.L0 + dop) % grid.N
     gain = torch.polar(mags[None, :].expand(B, n_paths), phase)
