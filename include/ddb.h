@@ -37,7 +37,7 @@
 extern "C" {
 #endif
 
-#define DDB_ABI_VERSION 1
+#define DDB_ABI_VERSION 2
 
 typedef enum {
   DDB_OK = 0,
@@ -96,7 +96,9 @@ typedef struct {
   int32_t threads;           /* threads per CTA                                     */
   int32_t smem_bytes;        /* dynamic shared memory per CTA                       */
   int32_t ctas_per_sm;       /* occupancy reported by the CUDA runtime (0 on CPU)   */
-  int32_t halo_rows;         /* quasi-periodic extension rows kept around p and u   */
+  int32_t halo_rows;         /* quasi-periodic extension rows kept around c and u   */
+  int32_t kernel;            /* 0: row-slice kernel, 1: TMEM-operand kernel (fp32)  */
+  int32_t rows_per_thread;   /* delay rows per thread (TMEM-operand kernel), else 1 */
 } ddb_plan;
 
 /* ---- library ------------------------------------------------------------ */

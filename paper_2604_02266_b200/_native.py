@@ -54,11 +54,14 @@ class Outputs(C.Structure):
     ]
 
 
+ABI_VERSION = 2  # include/ddb.h DDB_ABI_VERSION
+
+
 class Plan(C.Structure):
     _fields_ = [
         ("cluster", C.c_int32), ("cols_per_cta", C.c_int32), ("cols_per_thread", C.c_int32),
         ("threads", C.c_int32), ("smem_bytes", C.c_int32), ("ctas_per_sm", C.c_int32),
-        ("halo_rows", C.c_int32),
+        ("halo_rows", C.c_int32), ("kernel", C.c_int32), ("rows_per_thread", C.c_int32),
     ]
 
 
@@ -115,7 +118,7 @@ def load(build_if_missing: bool = False):
             fn = getattr(lib, name)
             fn.restype = res
             fn.argtypes = args
-        if lib.ddb_abi_version() != 1:
+        if lib.ddb_abi_version() != ABI_VERSION:
             raise RuntimeError("libddb ABI version mismatch")
         _lib = lib
         return lib

@@ -155,7 +155,8 @@ class SsCgaSolver:
         p = self._plan
         return {"cluster": p.cluster, "cols_per_cta": p.cols_per_cta,
                 "cols_per_thread": p.cols_per_thread, "threads": p.threads,
-                "smem_bytes": p.smem_bytes, "ctas_per_sm": p.ctas_per_sm, "halo_rows": p.halo_rows}
+                "smem_bytes": p.smem_bytes, "ctas_per_sm": p.ctas_per_sm, "halo_rows": p.halo_rows,
+                "kernel": "tmem" if p.kernel == 1 else "rows", "rows_per_thread": p.rows_per_thread}
 
     # -- buffers -------------------------------------------------------------
     def alloc(self, B: int, *, llr: bool = False, labels: bool = True, trace: bool = True,

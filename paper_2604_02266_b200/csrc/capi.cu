@@ -49,10 +49,84 @@ int smem_optin() {
   return v;
 }
 
+// TMEM-operand kernel (sscga_tm.cu, fp32): 128 TMEM lanes = Lcta columns x
+// S segments of G = M / S delay rows, G <= 64 so that c | u | p | x fit the
+// 512 lane columns; WQ warps per lane quarter, R = G / WQ rows per thread.
+// Smallest cluster that fits, most warps first; the extended column-major
+// slices of c and u take the rest of shared memory as halo (up to M rows).
+bool make_plan_tm(int32_t M, int32_t N, ddb::LaunchShape* s) {
+  const char* env_k = getenv("DDB_KERNEL");
+  if (env_k && env_k[0] == 'r') return false;  // DDB_KERNEL=row: force the row-slice kernel
+  const int cap = smem_optin();
+  const int pcap = 64;
+  int TL = 0, TH = 0;
+  ddb::twiddle_split(M * N, &TL, &TH);
+  const int hmin = M < 64 ? M : 64;
+  const char* env_c = getenv("DDB_PLAN_C");
+  const int cmin = env_c ? atoi(env_c) : 1;
+  for (int C = 1; C <= 16; C *= 2) {
+    if (N % C || C < cmin) continue;
+    const int lcta = N / C;
+    if (128 % lcta) continue;
+    const int S = 128 / lcta;
+    if (M % S) continue;
+    const int G = M / S;
+    if (G > 64 || G % 2) continue;
+    int wq = 0, R = 0;
+    const char* env_wq = getenv("DDB_PLAN_WQ");
+    for (int w = env_wq ? 8 : 4; w >= 1; w /= 2) {  // 1024-thread CTAs (WQ = 8) only on request
+      if (G % w || (env_wq && atoi(env_wq) != w)) continue;
+      const int r = G / w;
+      if (r == 4 || r == 8 || (r == 16 && w <= 4)) { wq = w; R = r; break; }
+    }
+    if (!wq) continue;
+    auto cs_of = [&](int h) { int cs = M + 2 * h + 2; return cs % 4 == 2 ? cs : cs + 2; };
+    auto smem_of = [&](int h) { return ddb::sscga_tm_layout(M, lcta, N, cs_of(h), TL, TH, pcap).total; };
+    if (smem_of(hmin) > (size_t)cap) continue;
+    int h = M;
+    while (h > hmin && smem_of(h) > (size_t)cap) h -= 2;
+    if (const char* env_h = getenv("DDB_PLAN_H")) h = h < atoi(env_h) ? h : atoi(env_h);
+    h &= ~1;
+    s->kind = 1;
+    s->cluster = C;
+    s->lcta = lcta;
+    s->lc = 1;
+    s->g = G;
+    s->wq = wq;
+    s->rows = R;
+    s->threads = 128 * wq;
+    s->halo = h;
+    s->cs = cs_of(h);
+    s->tl = TL;
+    s->th = TH;
+    s->pcap = pcap;
+    int tc = 32;
+    while (tc < 8 * G) tc *= 2;
+    s->tcols = tc;
+    // keep (CTAs per SM) x (TMEM columns per CTA) <= 512 so tcgen05.alloc never
+    // waits on a co-resident CTA (228 KiB per SM, 1 KiB reserved per CTA)
+    const int max_ctas = 512 / tc;
+    int floor_smem = 233472 / (max_ctas + 1) - 1024 + 16;
+    if (floor_smem > cap) floor_smem = cap;
+    s->smem = (int)smem_of(h);
+    if (const char* env_h = getenv("DDB_PLAN_SMEM_CAP")) {  // tuning: cap the halo so more CTAs fit
+      while (h > hmin && smem_of(h) > (size_t)atoi(env_h)) h -= 2;
+      s->halo = h;
+      s->cs = cs_of(h);
+      s->smem = (int)smem_of(h);
+    }
+    if (s->smem < floor_smem) s->smem = floor_smem;
+    return true;
+  }
+  return false;
+}
+
 // Smallest cluster whose CTAs can hold their column slice of p, u and x in
 // shared memory; then the widest per-thread column run that keeps at least
 // 256 threads per CTA within the register file.
 int32_t make_plan(int32_t M, int32_t N, int32_t dtype, ddb::LaunchShape* s) {
+  *s = ddb::LaunchShape{};
+  if (dtype == DDB_F32 && make_plan_tm(M, N, s)) return DDB_OK;
   const int eb = dtype == DDB_F64 ? 8 : 4;
   const int cap = smem_optin();
   const int lcmax = dtype == DDB_F64 ? 8 : 16;
@@ -144,10 +218,14 @@ int32_t ddb_sscga_plan(int32_t M, int32_t N, int32_t dtype, ddb_plan* out) {
   out->smem_bytes = s.smem;
   out->ctas_per_sm = 0;
   out->halo_rows = s.halo;
+  out->kernel = s.kind;
+  out->rows_per_thread = s.kind == 1 ? s.rows : 1;
   int n = 0;
   int dev_count = 0;
   if (cudaGetDeviceCount(&dev_count) == cudaSuccess && dev_count > 0) {
-    cudaError_t e = dtype == DDB_F64 ? ddb::sscga_occupancy<double>(s, &n) : ddb::sscga_occupancy<float>(s, &n);
+    cudaError_t e = s.kind == 1          ? ddb::sscga_tm_occupancy(s, &n)
+                    : dtype == DDB_F64 ? ddb::sscga_occupancy<double>(s, &n)
+                                       : ddb::sscga_occupancy<float>(s, &n);
     if (e == cudaSuccess) out->ctas_per_sm = n;
   }
   cudaGetLastError();
@@ -200,6 +278,10 @@ static int32_t solve_impl(const ddb_sscga_problem* prob, const ddb_sscga_outputs
   a.TH = s.th;
   a.pcap = s.pcap;
   a.tcols = s.tcols;
+  a.G = s.g;
+  a.WQ = s.wq;
+  a.CS = s.cs;
+  if (s.kind == 1) a.active_threads = s.threads;
   a.off = prob->path_offsets;
   a.pk = prob->path_k;
   a.pl = prob->path_l;
@@ -219,7 +301,9 @@ static int32_t solve_impl(const ddb_sscga_problem* prob, const ddb_sscga_outputs
   a.berr = out->bit_errors;
   a.prof = prof;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  cudaError_t e = prob->dtype == DDB_F64 ? ddb::launch_sscga<double>(a, s, st) : ddb::launch_sscga<float>(a, s, st);
+  cudaError_t e = s.kind == 1                ? ddb::launch_sscga_tm(a, s, st)
+                  : prob->dtype == DDB_F64 ? ddb::launch_sscga<double>(a, s, st)
+                                           : ddb::launch_sscga<float>(a, s, st);
   if (e != cudaSuccess) return cuda_fail(e, "sscga launch");
   return ok();
 }

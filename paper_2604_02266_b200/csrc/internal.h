@@ -20,6 +20,10 @@ struct SolveArgs {
   int TL, TH;         // two-level W_MN twiddle tables: e = hi * TL + lo
   int pcap;           // per-frame tap table capacity in shared memory
   int tcols;          // TMEM columns allocated per CTA (x lives in TMEM)
+  // TMEM-operand kernel (sscga_tm.cu) only
+  int G;              // delay rows per TMEM lane segment (M / segments per column)
+  int WQ;             // warps per TMEM lane quarter (threads = 128 WQ)
+  int CS;             // column stride (complex elements) of the column-major extended slices
   const int* off;
   const int* pk;
   const int* pl;
@@ -44,6 +48,8 @@ constexpr int kProfPhases = 12;
 
 struct LaunchShape {
   int cluster, lcta, lc, threads, smem, halo, tl, th, pcap, tcols;
+  int kind;        // 0: row-slice kernel (sscga.cu), 1: TMEM-operand kernel (sscga_tm.cu)
+  int g, wq, rows, cs;  // kind 1: segment rows, warps per lane quarter, rows per thread, column stride
 };
 
 // TMEM columns for the thread-private runs of x, p and the own-element copies
@@ -78,6 +84,11 @@ void twiddle_split(int MN, int* TL, int* TH);
 
 template <typename T>
 cudaError_t launch_sscga(SolveArgs a, const LaunchShape& s, cudaStream_t st);
+
+// TMEM-operand kernel (fp32): layout of its shared memory and launch.
+SmemLayout sscga_tm_layout(int M, int Lcta, int N, int CS, int TL, int TH, int pcap);
+cudaError_t launch_sscga_tm(SolveArgs a, const LaunchShape& s, cudaStream_t st);
+cudaError_t sscga_tm_occupancy(const LaunchShape& s, int* ctas_per_sm);
 
 template <typename T>
 cudaError_t sscga_occupancy(const LaunchShape& s, int* ctas_per_sm);

@@ -41,35 +41,12 @@
 // partials in the same order, so all CTAs take identical branches.
 #include <climits>
 
+#include "cg.cuh"
 #include "common.cuh"
 #include "demod.cuh"
 #include "internal.h"
 
 namespace ddb {
-
-// Per-frame tap entry: offsets and both direction's row-invariant gain factor,
-// hf = h W_MN^{-d_l d_k} (forward) and hh = conj(h) (hermitian), so a thread
-// only adds its own row's W_MN^{-+d_l k} (skipped when d_l == 0).  off is the
-// tap's shift in the row-major on-chip slices, d_k RS + d_l elements: the
-// forward gather of row k reads thread_base + off, the hermitian one - off.
-template <typename T> struct PathEnt;
-template <> struct __align__(16) PathEnt<double> {
-  int dk, dl, off, pad;
-  double2 hf, hh;
-  __device__ double2 coef(bool herm) const { return herm ? hh : hf; }
-};
-// fp32: gains stored as FFMA2-ready quads (g.x, g.x, -g.y, g.y), so a 128-bit
-// load yields the register pairs of both packed MACs directly.
-template <> struct __align__(16) PathEnt<float> {
-  int dk, dl, off, pad;
-  float4 hf, hh;
-  __device__ float2 coef(bool herm) const {
-    const float4 q = herm ? hh : hf;
-    return make_float2(q.x, q.w);
-  }
-};
-__device__ __forceinline__ float4 quad(float2 g) { return make_float4(g.x, g.x, -g.y, g.y); }
-__device__ __forceinline__ double2 quad(double2 g) { return g; }
 
 // Dense per-frame list of the d_l == 0 taps (the hot loop): slice offset and
 // both direction's gains, 48 bytes, read with two broadcast 128-bit loads.
@@ -117,12 +94,6 @@ __device__ __forceinline__ Vec<T> twid(const Sm<T>& sm, int e) {
   return cmul(sm.thi[e >> sm.tlb], sm.tlo[e & ((1 << sm.tlb) - 1)]);
 }
 
-// (x mod m) for x in (-m, 2m)
-__device__ __forceinline__ int wrap1(int x, int m) {
-  x = x < 0 ? x + m : x;
-  return x >= m ? x - m : x;
-}
-
 template <typename T>
 __device__ __forceinline__ PathEnt<T> make_path(const SolveArgs& a, const Sm<T>& sm, int kp, int lp, Vec<T> h) {
   PathEnt<T> e;
@@ -141,51 +112,6 @@ __device__ __forceinline__ PathEnt<T> get_path(const SolveArgs& a, const Sm<T>& 
   if (fc.in_smem) return sm.ptab[p];
   return make_path(a, sm, __ldg(a.pk + fc.P0 + p), __ldg(a.pl + fc.P0 + p),
                    __ldg(reinterpret_cast<const Vec<T>*>(a.ph) + fc.P0 + p));
-}
-
-// Contiguous run of LC source columns starting at rp (16-byte aligned row,
-// offset `odd` elements): 128-bit loads, two complex values each; an odd start
-// loads one extra aligned chunk and uses the other halves (register naming only).
-// acc += c v with c given as the FFMA2 operand pairs X = (c.x, c.x), Y = (-c.y, c.y)
-__device__ __forceinline__ void cmacxy(unsigned long long& acc, unsigned long long X, unsigned long long Y,
-                                       float a, float b) {
-  asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(acc) : "l"(X), "l"(pack2(a, b)));
-  asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(acc) : "l"(Y), "l"(pack2(b, a)));
-}
-template <int LC>
-__device__ __forceinline__ void gather_run(const float2* rp, bool odd, unsigned long long X, unsigned long long Y,
-                                           unsigned long long (&acc)[LC]) {
-  if constexpr (LC == 1) {
-    const float2 v = rp[0];
-    cmacxy(acc[0], X, Y, v.x, v.y);
-  } else {
-    if (!odd) {
-      const float4* q = reinterpret_cast<const float4*>(rp);
-#pragma unroll
-      for (int m = 0; m < LC / 2; ++m) {
-        const float4 w = q[m];
-        cmacxy(acc[2 * m], X, Y, w.x, w.y);
-        cmacxy(acc[2 * m + 1], X, Y, w.z, w.w);
-      }
-    } else {
-      const float4* q = reinterpret_cast<const float4*>(rp - 1);
-      float4 w = q[0];
-      cmacxy(acc[0], X, Y, w.z, w.w);
-#pragma unroll
-      for (int m = 1; m < LC / 2; ++m) {
-        w = q[m];
-        cmacxy(acc[2 * m - 1], X, Y, w.x, w.y);
-        cmacxy(acc[2 * m], X, Y, w.z, w.w);
-      }
-      w = q[LC / 2];
-      cmacxy(acc[LC - 1], X, Y, w.x, w.y);
-    }
-  }
-}
-template <int LC>
-__device__ __forceinline__ void gather_run(const double2* rp, bool, double2 c, double2 (&acc)[LC]) {
-#pragma unroll
-  for (int j = 0; j < LC; ++j) Acc<double>::mac(acc[j], c, rp[j]);
 }
 
 // The MVM runs in two passes around a split cluster barrier:
@@ -452,94 +378,6 @@ __device__ __forceinline__ void put_ext(Vec<T>* buf, int RS, int lo, int hi, int
   }
 }
 
-template <typename T>
-__device__ __forceinline__ void cl_sync(int C) {
-  if (C > 1) cluster_sync_all();
-  else __syncthreads();
-}
-
-// Deterministic cluster-wide sum of a pair of partials.  slot: this CTA's [32]
-// pair array for the reduction kind / parity in use.  Contains the barrier.
-// Lane i of every warp sums the per-warp pairs i, i+32, ... of the whole
-// cluster (rank-major), then the warp butterflies: every warp of every CTA
-// gets bit-identical totals.  (r0, w0): lane's first (rank, warp) slot.
-//
-// Small clusters (C * nwarps <= kPushSlots) push: lane r of every warp stores
-// the warp's pair into slot[rank * nwarps + warp] of CTA r before the barrier
-// (remote stores are released by barrier.cluster.arrive.release), so after it
-// every read is a local shared-memory load.  Larger clusters pull the peers'
-// per-warp pairs through DSMEM after the barrier.
-constexpr int kPushSlots = 64;
-
-// Publish this warp's pair (before the cluster barrier's arrive).
-template <typename T>
-__device__ __forceinline__ void red_push(Vec<T> part, Vec<T>* slot, int C, int nwarps, int lane, int warp, int rank) {
-  part.x = warp_sum(part.x);
-  part.y = warp_sum(part.y);
-  if (C * nwarps <= kPushSlots) {
-    const int idx = rank * nwarps + warp;
-    if (C == 1) {
-      if (lane == 0) slot[idx] = part;
-    } else if (lane < C) {
-      st_cluster(map_rank(smem_addr(slot + idx), lane), part);
-    }
-  } else if (lane == 0) {
-    slot[warp] = part;
-  }
-}
-
-// Cluster-wide total (after the cluster barrier's wait); identical in every warp.
-template <typename T>
-__device__ __forceinline__ Vec<T> red_read(const Vec<T>* slot, int C, int nwarps, int lane, int r0, int w0) {
-  using V = Vec<T>;
-  const int total = C * nwarps;
-  V s = czero<V>();
-  if (total <= kPushSlots) {
-    for (int i = lane; i < total; i += 32) s = cadd(s, slot[i]);
-  } else {
-    const uint32_t base = smem_addr(slot);
-    for (int r = r0, w = w0; r < C;) {
-      s = cadd(s, ld_cluster(static_cast<V*>(nullptr), map_rank(base + w * (int)sizeof(V), r)));
-      w += 32;
-      while (w >= nwarps) { w -= nwarps; ++r; }
-    }
-  }
-  s.x = warp_sum(s.x);
-  s.y = warp_sum(s.y);
-  return s;
-}
-
-// Split cluster barrier: arrive (release) -> CTA barrier -> ... -> wait (acquire).
-__device__ __forceinline__ void cl_arrive(int C) {
-  if (C > 1) asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
-  __syncthreads();
-}
-__device__ __forceinline__ void cl_wait(int C) {
-  if (C > 1) asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
-}
-
-// ---- packed elementwise CG arithmetic (FFMA2 for fp32)
-// y + a x (a real, broadcast)
-__device__ __forceinline__ float2 axpy(float2 y, float a, float2 x) {
-  unsigned long long r = pack2(y.x, y.y);
-  asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(r) : "l"(pack2(a, a)), "l"(pack2(x.x, x.y)));
-  return unpack2(r);
-}
-__device__ __forceinline__ double2 axpy(double2 y, double a, double2 x) {
-  return make_double2(fma(a, x.x, y.x), fma(a, x.y, y.y));
-}
-// n += (v.x^2, v.y^2); the norm is n.x + n.y
-__device__ __forceinline__ void nacc(float2& n, float2 v) {
-  unsigned long long r = pack2(n.x, n.y);
-  const unsigned long long p = pack2(v.x, v.y);
-  asm("fma.rn.f32x2 %0, %1, %1, %0;" : "+l"(r) : "l"(p));
-  n = unpack2(r);
-}
-__device__ __forceinline__ void nacc(double2& n, double2 v) {
-  n.x = fma(v.x, v.x, n.x);
-  n.y = fma(v.y, v.y, n.y);
-}
-
 __host__ __device__ static inline size_t align16(size_t v) { return (v + 15) & ~size_t(15); }
 
 __host__ __device__ static inline SmemLayout layout_impl(int M, int N, int C, int eb, int H, int TL, int TH,
@@ -556,7 +394,7 @@ __host__ __device__ static inline SmemLayout layout_impl(int M, int N, int C, in
   L.tw = o; o = align16(o + (size_t)N * vb);
   // tap table (pcap PathEnt) followed by the dense d_l == 0 list (kTap0Cap Tap0), 48 B each
   L.ptab = o; o = align16(o + (size_t)(pcap + kTap0Cap) * 48);
-  L.red = o; o = align16(o + 2 * 2 * 64 * vb + kProfPhases * 8);  // [2][2][kPushSlots] pairs + prof
+  L.red = o; o = align16(o + 2 * 2 * 64 * vb + sizeof(ProfSm));  // [2][2][kPushSlots] pairs + prof
   L.total = o;
   return L;
 }
@@ -571,23 +409,6 @@ void twiddle_split(int MN, int* TL, int* TH) {
   *TL = tl;
   *TH = (MN + tl - 1) / tl;
 }
-
-// Phase timer (measurement builds of a launch only: SolveArgs::prof != null):
-// thread 0 of each CTA attributes clock64 intervals to the phase being run.
-enum Phase { kSetup, kArrive, kMvmLocal, kWait, kMvmRemote, kRead, kStep1, kStep3, kEpilogue, kTail };
-struct Prof {
-  long long* acc;  // shared [kProfPhases] on thread 0, nullptr elsewhere
-  long long t;
-  int cur;
-  __device__ __forceinline__ void mark(int next) {
-    if (acc) {
-      const long long now = clock64();
-      acc[cur] += now - t;
-      t = now;
-      cur = next;
-    }
-  }
-};
 
 // Epilogue for XC equalized symbols at global indices q0 + j M: x_hat, hard
 // labels, max-log LLRs (vector stores) and the bit-error count vs TX labels.
@@ -665,9 +486,6 @@ __global__ void __launch_bounds__(sscga_max_threads(sizeof(T), LC), 1) sscga_ker
   const uint32_t cta = xta + (uint32_t)(2 * XW);
   const uint32_t uta = xta + (uint32_t)(3 * XW);
   // reduction lane mapping: lane i starts at cluster slot i = (rank, warp)
-  const int rtot = a.C * nwarps;
-  const int r0 = lane < rtot ? lane / nwarps : a.C;
-  const int w0 = lane < rtot ? lane - (lane / nwarps) * nwarps : 0;
   V* red = reinterpret_cast<V*>(sm.red);  // [2 kinds][2 parities][32 warps] pairs
 
   const V* y = reinterpret_cast<const V*>(a.y);
@@ -679,15 +497,8 @@ __global__ void __launch_bounds__(sscga_max_threads(sizeof(T), LC), 1) sscga_ker
   const bool lead = (cx.rank == 0 && tid == 0);
   const int stride = a.iters + 1;
   int par[2] = {0, 0};  // 0: (||u||^2, ||p||^2), 1: (||c||^2, -)
-  Prof pf;
-  pf.acc = nullptr;
-  pf.t = 0;
-  pf.cur = kTail;
-  if (a.prof && tid == 0) {
-    pf.acc = reinterpret_cast<long long*>(red + 2 * 2 * kPushSlots);
-    for (int i = 0; i < kProfPhases; ++i) pf.acc[i] = 0;
-    pf.t = clock64();
-  }
+  ProfSm* const psm = reinterpret_cast<ProfSm*>(red + 2 * 2 * kPushSlots);
+  prof_init(a.prof, psm);
 
   for (int f = blockIdx.x / a.C; f < a.B; f += a.n_clusters) {
     FrameCtx fc;
@@ -716,7 +527,7 @@ __global__ void __launch_bounds__(sscga_max_threads(sizeof(T), LC), 1) sscga_ker
     }
 
     // ---- frame setup: tap table, extension halo sizes
-    pf.mark(kSetup);
+    prof_mark(a.prof, psm, kSetup);
     fc.in_smem = fc.P <= a.pcap;
     if (fc.in_smem) {
       const V* gains = reinterpret_cast<const V*>(a.ph);
@@ -789,15 +600,15 @@ __global__ void __launch_bounds__(sscga_max_threads(sizeof(T), LC), 1) sscga_ker
     // Every barrier is split: publish (data + reduction partials), arrive,
     // CTA barrier, the local-tap half of the next MVM, wait, the remote taps.
     typename A::type acc[LC];
-    pf.mark(kArrive);
+    prof_mark(a.prof, psm, kArrive);
     cl_arrive(a.C);  // y published
-    pf.mark(kMvmLocal);
+    prof_mark(a.prof, psm, kMvmLocal);
     Skipped sk = ss_mvm_local<T, LC, true>(a, cx, sm, fc, sm.u, fc.lo_u, acc);  // b = H^H y (equalize.py:52)
-    pf.mark(kWait);
+    prof_mark(a.prof, psm, kWait);
     cl_wait(a.C);
-    pf.mark(kMvmRemote);
+    prof_mark(a.prof, psm, kMvmRemote);
     ss_mvm_remote<T, LC, true>(a, cx, sm, fc, sm.u, fc.lo_u, sk, acc);
-    pf.mark(kStep1);
+    prof_mark(a.prof, psm, kStep1);
     V nrm = czero<V>();
 #pragma unroll
     for (int j = 0; j < LC; ++j) {
@@ -817,14 +628,14 @@ __global__ void __launch_bounds__(sscga_max_threads(sizeof(T), LC), 1) sscga_ker
     V* slot = red + (1 * 2 + par[1]) * kPushSlots;
     par[1] ^= 1;
     red_push<T>(cmake<V>(nrm.x + nrm.y, T(0)), slot, a.C, nwarps, lane, warp, cx.rank);
-    pf.mark(kArrive);
+    prof_mark(a.prof, psm, kArrive);
     cl_arrive(a.C);  // c = b published
-    pf.mark(kMvmLocal);
+    prof_mark(a.prof, psm, kMvmLocal);
     sk = ss_mvm_local<T, LC, false>(a, cx, sm, fc, sm.c, fc.lo_c, acc);
-    pf.mark(kWait);
+    prof_mark(a.prof, psm, kWait);
     cl_wait(a.C);
-    pf.mark(kRead);
-    T cn = red_read<T>(slot, a.C, nwarps, lane, r0, w0).x;
+    prof_mark(a.prof, psm, kRead);
+    T cn = red_read<T>(slot, a.C, nwarps, lane).x;
     T beta = T(0);
     if (lead && cnorm) cnorm[(size_t)f * stride] = cn;
 
@@ -832,9 +643,9 @@ __global__ void __launch_bounds__(sscga_max_threads(sizeof(T), LC), 1) sscga_ker
     bool exact = false;
     for (int it = 0; it < a.iters; ++it) {
       // u = H c + beta u_old, p = c + beta p_old      (= H p, p of equalize.py:60, 72)
-      pf.mark(kMvmRemote);
+      prof_mark(a.prof, psm, kMvmRemote);
       ss_mvm_remote<T, LC, false>(a, cx, sm, fc, sm.c, fc.lo_c, sk, acc);
-      pf.mark(kStep1);
+      prof_mark(a.prof, psm, kStep1);
       V nu = czero<V>(), np = czero<V>();
 #pragma unroll
       for (int c0 = 0; c0 < LC; c0 += XC) {
@@ -871,18 +682,18 @@ __global__ void __launch_bounds__(sscga_max_threads(sizeof(T), LC), 1) sscga_ker
       slot = red + (0 * 2 + par[0]) * kPushSlots;
       par[0] ^= 1;
       red_push<T>(cmake<V>(nu.x + nu.y, np.x + np.y), slot, a.C, nwarps, lane, warp, cx.rank);
-      pf.mark(kArrive);
+      prof_mark(a.prof, psm, kArrive);
       cl_arrive(a.C);  // u published
       // ap = H^H u + lam p;  x += alpha p;  c -= alpha ap      (equalize.py:60-70)
-      pf.mark(kMvmLocal);
+      prof_mark(a.prof, psm, kMvmLocal);
       sk = ss_mvm_local<T, LC, true>(a, cx, sm, fc, sm.u, fc.lo_u, acc);
-      pf.mark(kWait);
+      prof_mark(a.prof, psm, kWait);
       cl_wait(a.C);
-      pf.mark(kMvmRemote);
+      prof_mark(a.prof, psm, kMvmRemote);
       ss_mvm_remote<T, LC, true>(a, cx, sm, fc, sm.u, fc.lo_u, sk, acc);
-      pf.mark(kRead);
-      const V up = red_read<T>(slot, a.C, nwarps, lane, r0, w0);
-      pf.mark(kStep3);
+      prof_mark(a.prof, psm, kRead);
+      const V up = red_read<T>(slot, a.C, nwarps, lane);
+      prof_mark(a.prof, psm, kStep3);
       const T denom = up.x + lam * up.y;  // ||H p||^2 + lam ||p||^2 = Re p^H (H^H H + lam I) p
       if (denom == T(0)) {  // equalize.py:64-67
         exact = true;
@@ -921,14 +732,14 @@ __global__ void __launch_bounds__(sscga_max_threads(sizeof(T), LC), 1) sscga_ker
       slot = red + (1 * 2 + par[1]) * kPushSlots;
       par[1] ^= 1;
       red_push<T>(cmake<V>(nc.x + nc.y, T(0)), slot, a.C, nwarps, lane, warp, cx.rank);
-      pf.mark(kArrive);
+      prof_mark(a.prof, psm, kArrive);
       cl_arrive(a.C);  // c published
-      pf.mark(kMvmLocal);
+      prof_mark(a.prof, psm, kMvmLocal);
       if (it + 1 < a.iters) sk = ss_mvm_local<T, LC, false>(a, cx, sm, fc, sm.c, fc.lo_c, acc);  // next H c
-      pf.mark(kWait);
+      prof_mark(a.prof, psm, kWait);
       cl_wait(a.C);
-      pf.mark(kRead);
-      const T nn = red_read<T>(slot, a.C, nwarps, lane, r0, w0).x;
+      prof_mark(a.prof, psm, kRead);
+      const T nn = red_read<T>(slot, a.C, nwarps, lane).x;
       beta = nn / cn;
       cn = nn;
       done = it + 1;
@@ -941,7 +752,7 @@ __global__ void __launch_bounds__(sscga_max_threads(sizeof(T), LC), 1) sscga_ker
     }
 
     // epilogue: x_hat out, fused hard decisions / LLRs / bit errors
-    pf.mark(kEpilogue);
+    prof_mark(a.prof, psm, kEpilogue);
     T scale = T(1);
     if (a.bps) {
       const T nv = nvar ? nvar[f] : lam;
@@ -967,9 +778,8 @@ __global__ void __launch_bounds__(sscga_max_threads(sizeof(T), LC), 1) sscga_ker
       if (lane == 0 && errs) atomicAdd(a.berr + f, errs);
     }
   }
-  pf.mark(kTail);
-  if (pf.acc)
-    for (int i = 0; i < kProfPhases; ++i) a.prof[(size_t)blockIdx.x * kProfPhases + i] = pf.acc[i];
+  prof_mark(a.prof, psm, kTail);
+  prof_store(a.prof, psm);
   // no CTA may leave while a peer can still read its shared memory (DSMEM)
   tmem_fence_before();
   cl_sync<T>(a.C);
@@ -980,6 +790,8 @@ template <typename T, int LC>
 static cudaError_t launch_lc(SolveArgs a, const LaunchShape& s, cudaStream_t st) {
   auto kern = sscga_kernel<T, LC>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, s.smem);
+  if (e != cudaSuccess) return e;
+  e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
   if (e != cudaSuccess) return e;
   if (s.cluster > 8) {
     e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
@@ -1027,6 +839,8 @@ template <typename T, int LC>
 static cudaError_t occ_lc(const LaunchShape& s, int* n) {
   auto kern = sscga_kernel<T, LC>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, s.smem);
+  if (e != cudaSuccess) return e;
+  e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
   if (e != cudaSuccess) return e;
   return cudaOccupancyMaxActiveBlocksPerMultiprocessor(n, kern, s.threads, s.smem);
 }

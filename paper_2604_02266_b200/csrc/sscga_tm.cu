@@ -1,0 +1,862 @@
+// Fused SS-CGA solve with TMEM-resident operands (fp32, sm_100a).
+//
+// Same algorithm as sscga.cu (cga_equalize, equalize.py:43-77, on the
+// matrix-free operator of sparse.py:91-160, closed forms in that file's
+// header) with a data layout built around tensor memory.  The MVM of the
+// reference is a gather-multiply-reduce: every complex MAC needs one fresh
+// 8-byte operand.  Served from shared memory (128 B/clk/SM) that caps the MVM
+// at half the FP32 FMA rate; tcgen05.ld delivers > 300 B/clk/SM
+// (profiles/ubench_tmem_bw.txt), so here the gathered vectors live in TMEM.
+//
+// TMEM is lane-private: a warp reaches only its quarter of the 128 lanes and a
+// thread only its own lane, but any column of it.  A Doppler-preserving tap
+// (d_l == 0, the bulk of every Veh-A channel) shifts data along the delay axis
+// only, so delay rows go along TMEM columns:
+//   lane L = seg * Lcta + col   holds delay rows [seg G, seg G + G) of the
+//                               CTA's Doppler column col (S = 128 / Lcta
+//                               segments of G = M / S rows per column);
+//   thread (warp w, lane t)     uses TMEM lane 32 (w % 4) + t and owns the
+//                               R = G / WQ rows j R .. j R + R - 1 of that
+//                               segment, j = w / 4 (WQ warps per lane quarter).
+// Per lane the 512 columns hold c | u (the whole segment, 2G words each,
+// gathered by H and H^H) and p | x (the WQ threads' own rows).  A d_l == 0 tap
+// whose source rows stay inside the segment is one tcgen05.ld of 2R words at
+// column 2 (j R + shift) followed by R FFMA2 complex MACs with a warp-uniform
+// gain.  Everything else reads the column-major extended copies of c and u in
+// shared memory (written beside every TMEM update, quasi-periodic halo rows
+// included): d_l == 0 taps that leave the segment take one contiguous run of
+// the lane's own column, other taps gather per element, through DSMEM when the
+// source column lives in a peer CTA of the cluster.
+//
+// CG step (u-recurrence, two cluster barriers per iteration) and the
+// deterministic reductions are those of sscga.cu.
+#include <climits>
+
+#include "cg.cuh"
+#include "common.cuh"
+#include "demod.cuh"
+#include "internal.h"
+
+namespace ddb {
+
+namespace {
+
+using V = float2;
+using U64 = unsigned long long;
+
+// Per-frame state, in shared memory (written at frame setup, read where
+// needed, so none of it occupies registers across the CG loop).  Tap masks
+// (P <= 32, tap table on chip) are per row block j: the TMEM test depends on
+// the warp's rows, so they are warp-uniform.
+struct FrameSm {
+  int P0, P;
+  int in_smem, halo, masks;
+  int lo_c, hi_c, lo_u, hi_u;  // extension rows written for c (gathered by H) and u (by H^H)
+  int pad[3];
+  uint32_t mk[8][6];           // [j][tmF, smF, gnF, tmH, smH, gnH]: TMEM run / shared run / per element
+};
+
+__host__ __device__ inline size_t a16(size_t v) { return (v + 15) & ~size_t(15); }
+
+__host__ __device__ inline SmemLayout tm_layout_impl(int Lcta, int N, int CS, int TL, int TH, int pcap) {
+  SmemLayout L;
+  size_t o = 0;
+  // extended c and u, column-major, each behind a 16-byte guard: odd-aligned
+  // runs read one (unused) element beyond either end of a column
+  o += 16;
+  L.p = o; o = a16(o + (size_t)Lcta * CS * sizeof(V)) + 16;
+  L.u = o; o = a16(o + (size_t)Lcta * CS * sizeof(V));
+  L.x = o; o = a16(o + 16);                             // TMEM base-address slot
+  L.tlo = o; o = a16(o + (size_t)TL * sizeof(V));
+  L.thi = o; o = a16(o + (size_t)TH * sizeof(V));
+  L.tw = o; o = a16(o + (size_t)N * sizeof(V));
+  L.ptab = o; o = a16(o + (size_t)pcap * sizeof(PathEnt<float>));
+  L.red = o; o = a16(o + 2 * 2 * kPushSlots * sizeof(V) + sizeof(ProfSm) + sizeof(FrameSm));
+  L.total = o;
+  return L;
+}
+
+struct TmSm {
+  V* c;  // extended column-major c: column col at c + col CS, row a (in [-H, M + H)) at + H + a
+  V* u;
+  uint32_t* tslot;
+  const V* tlo;
+  const V* thi;
+  const V* tw;
+  PathEnt<float>* ptab;
+  int tlb;
+};
+
+__device__ __forceinline__ V twid_tm(const TmSm& sm, int e) {
+  return cmul(sm.thi[e >> sm.tlb], sm.tlo[e & ((1 << sm.tlb) - 1)]);
+}
+
+// Per-thread geometry (kept small: the kernel runs at 64-128 registers).
+struct TmThr {
+  int col;    // Doppler column inside the CTA (TMEM lane -> column)
+  int colg;   // global Doppler column
+  int jr;     // first owned row inside the segment (j R, j = warp / 4)
+  int r0;     // first owned delay row
+  uint32_t tl;  // TMEM address of this warp's lane quarter, column 0
+};
+
+
+
+__device__ __forceinline__ PathEnt<float> tm_path(const SolveArgs& a, const TmSm& sm, int kp, int lp, V h) {
+  PathEnt<float> e;
+  e.dk = a.K0 - kp;
+  e.dl = a.L0 - lp;
+  e.off = 0;
+  e.pad = 0;
+  e.hf = quad(e.dl ? cmul(h, twid_tm(sm, wrap1(-e.dl * e.dk, a.MN))) : h);
+  e.hh = quad(cconj(h));
+  return e;
+}
+
+__device__ __forceinline__ PathEnt<float> tm_get(const SolveArgs& a, const TmSm& sm, const FrameSm& fs, int p) {
+  if (fs.in_smem) return sm.ptab[p];
+  return tm_path(a, sm, __ldg(a.pk + fs.P0 + p), __ldg(a.pl + fs.P0 + p),
+                 __ldg(reinterpret_cast<const V*>(a.ph) + fs.P0 + p));
+}
+
+// Tap classes for row block jr: 0 = TMEM run, 1 = shared-memory run, 2 = per element.
+template <int R, bool HERM>
+__device__ __forceinline__ int tap_class(const SolveArgs& a, int jr, bool halo, const PathEnt<float>& e) {
+  if (e.dl != 0) return 2;
+  const int s = HERM ? -e.dk : e.dk;
+  if (jr + s >= 0 && jr + s + R <= a.G) return 0;
+  return halo ? 1 : 2;
+}
+
+// ---- gathers ------------------------------------------------------------
+// FFMA2 operand pairs X = (g.x, g.x), Y = (-g.y, g.y) of a tap's gain for one
+// direction: one 128-bit shared load straight into two register pairs.
+template <bool HERM>
+__device__ __forceinline__ ulonglong2 gain_pairs(const PathEnt<float>& e) {
+  return *reinterpret_cast<const ulonglong2*>(HERM ? &e.hh : &e.hf);
+}
+template <int R>
+__device__ __forceinline__ void gather_tmem(uint32_t ta, U64 X, U64 Y, U64 (&acc)[R]) {
+  uint32_t v[2 * R];
+  tmem_ld<2 * R>(ta, v);
+  tmem_wait_ld_tie<2 * R>(v);
+#pragma unroll
+  for (int i = 0; i < R; ++i) cmacxy(acc[i], X, Y, __uint_as_float(v[2 * i]), __uint_as_float(v[2 * i + 1]));
+}
+
+// One tap, per element, from the (possibly remote) extended column of the
+// source Doppler column; row wraps applied in registers when the frame's
+// shifts exceed the halo.
+template <int R, bool HERM>
+__device__ __forceinline__ void tap_elem(const SolveArgs& a, const TmThr& th, const TmSm& sm, bool halo,
+                                         const V* buf, const PathEnt<float>& e, U64 (&acc)[R]) {
+  const int M = a.M, MN = a.MN;
+  const int dl = e.dl;
+  const int s = HERM ? -e.dk : e.dk;
+  const float4 g = HERM ? e.hh : e.hf;
+  const V h0 = make_float2(g.x, g.w);
+  const int ls = wrap1(th.colg + (HERM ? -dl : dl), a.N);  // source Doppler column
+  const int own = ls / a.Lcta;
+  const int lc = ls - own * a.Lcta;
+  const uint32_t colad = map_rank(smem_addr(buf + (size_t)lc * a.CS + a.H), (uint32_t)own);
+#pragma unroll
+  for (int i = 0; i < R; ++i) {
+    const int k = th.r0 + i;
+    const V coef = dl ? cmul(h0, twid_tm(sm, wrap1(HERM ? dl * k : -dl * k, MN))) : h0;
+    int ar = k + s;
+    int nw = 0;
+    if (!halo) {
+      nw = ar < 0 ? -1 : (ar >= M ? 1 : 0);
+      ar -= nw * M;
+    }
+    V v = ld_cluster(static_cast<V*>(nullptr), colad + (uint32_t)(ar * (int)sizeof(V)));
+    if (nw != 0) {
+      V t = sm.tw[ls];
+      if (nw < 0) t = cconj(t);
+      v = cmul(v, t);
+    }
+    Acc<float>::mac(acc[i], coef, v);
+  }
+}
+
+// TMEM taps of a mask, software-pipelined in half runs (R / 2 values): the
+// load of the next half is in flight while the FFMA2s of the current one run
+// (tcgen05.wait::ld covers every outstanding load, so the pipeline is one deep).
+template <int R, bool HERM>
+__device__ __forceinline__ void tmem_taps(int jr, const TmSm& sm, uint32_t tv, uint32_t m, U64 (&acc)[R]) {
+  constexpr int H2 = R / 2;  // complex values per half run
+  constexpr int W = R;       // 32-bit TMEM columns per half run
+  if (!m) return;
+  auto addr = [&](const PathEnt<float>& e) { return tv + (uint32_t)(2 * (jr + (HERM ? -e.dk : e.dk))); };
+  const PathEnt<float>* ent = &sm.ptab[__ffs(m) - 1];
+  m &= m - 1;
+  uint32_t ad = addr(*ent);
+  ulonglong2 g = gain_pairs<HERM>(*ent);
+  uint32_t A[W], B[W];
+  tmem_ld<W>(ad, A);
+  tmem_wait_ld_tie<W>(A);
+  while (true) {
+    tmem_ld<W>(ad + (uint32_t)W, B);
+    const U64 X = g.x, Y = g.y;
+#pragma unroll
+    for (int i = 0; i < H2; ++i) cmacxy(acc[i], X, Y, __uint_as_float(A[2 * i]), __uint_as_float(A[2 * i + 1]));
+    tmem_wait_ld_tie<W>(B);
+    const bool more = m != 0;
+    if (more) {
+      ent = &sm.ptab[__ffs(m) - 1];
+      m &= m - 1;
+      ad = addr(*ent);
+      g = gain_pairs<HERM>(*ent);
+      tmem_ld<W>(ad, A);
+    }
+#pragma unroll
+    for (int i = 0; i < H2; ++i)
+      cmacxy(acc[H2 + i], X, Y, __uint_as_float(B[2 * i]), __uint_as_float(B[2 * i + 1]));
+    if (!more) break;
+    tmem_wait_ld_tie<W>(A);
+  }
+}
+
+// Local pass (after the CTA barrier): TMEM runs and own-column shared runs.
+template <int R, bool HERM>
+__device__ __forceinline__ void mvm_local(const SolveArgs& a, const TmThr& th, const TmSm& sm, const FrameSm& fs,
+                                          uint32_t tv, const V* vcol, U64 (&acc)[R]) {
+#pragma unroll
+  for (int i = 0; i < R; ++i) acc[i] = 0ull;
+  if (fs.masks) {
+    const uint32_t* mk = fs.mk[th.jr / R] + (HERM ? 3 : 0);
+    tmem_taps<R, HERM>(th.jr, sm, tv, mk[0], acc);
+    for (uint32_t m = mk[1]; m; m &= m - 1) {
+      const PathEnt<float>& e = sm.ptab[__ffs(m) - 1];
+      const int s = HERM ? -e.dk : e.dk;
+      const ulonglong2 g = gain_pairs<HERM>(e);
+      gather_run<R>(vcol + th.r0 + s, (s & 1) != 0, g.x, g.y, acc);
+    }
+  } else {
+    const bool halo = fs.halo;
+    for (int p = 0; p < fs.P; ++p) {
+      const PathEnt<float> e = tm_get(a, sm, fs, p);
+      const int cls = tap_class<R, HERM>(a, th.jr, halo, e);
+      const int s = HERM ? -e.dk : e.dk;
+      const float4 g = HERM ? e.hh : e.hf;
+      if (cls == 0) gather_tmem<R>(tv + (uint32_t)(2 * (th.jr + s)), pack2(g.x, g.y), pack2(g.z, g.w), acc);
+      else if (cls == 1) gather_run<R>(vcol + th.r0 + s, (s & 1) != 0, pack2(g.x, g.y), pack2(g.z, g.w), acc);
+    }
+  }
+}
+
+// Remote pass (after the cluster barrier's wait): per-element taps.
+template <int R, bool HERM>
+__device__ __forceinline__ void mvm_remote(const SolveArgs& a, const TmThr& th, const TmSm& sm, const FrameSm& fs,
+                                           const V* buf, U64 (&acc)[R]) {
+  const bool halo = fs.halo;
+  if (fs.masks) {
+    for (uint32_t m = fs.mk[th.jr / R][HERM ? 5 : 2]; m; m &= m - 1)
+      tap_elem<R, HERM>(a, th, sm, halo, buf, sm.ptab[__ffs(m) - 1], acc);
+  } else {
+    for (int p = 0; p < fs.P; ++p) {
+      const PathEnt<float> e = tm_get(a, sm, fs, p);
+      if (tap_class<R, HERM>(a, th.jr, halo, e) == 2) tap_elem<R, HERM>(a, th, sm, halo, buf, e, acc);
+    }
+  }
+}
+
+// ---- TMEM runs of E complex values (2E words) ----------------------------
+template <int E>
+__device__ __forceinline__ void tm_ld(uint32_t ta, uint32_t (&r)[2 * E]) {
+  tmem_ld<2 * E>(ta, r);
+}
+template <int E>
+__device__ __forceinline__ void tm_st(uint32_t ta, const V (&v)[E]) {
+  uint32_t r[2 * E];
+#pragma unroll
+  for (int i = 0; i < E; ++i) {
+    r[2 * i] = __float_as_uint(v[i].x);
+    r[2 * i + 1] = __float_as_uint(v[i].y);
+  }
+  tmem_st<2 * E>(ta, r);
+}
+template <int E>
+__device__ __forceinline__ V tm_get_v(const uint32_t (&r)[2 * E], int i) {
+  return make_float2(__uint_as_float(r[2 * i]), __uint_as_float(r[2 * i + 1]));
+}
+
+// Store E values of rows rr .. rr + E - 1 into the lane's extended column
+// (16-byte stores), plus the quasi-periodic copies a frame's shifts need:
+// ext[r - M] = v W_N^{-l} for r >= M - lo, ext[r + M] = v W_N^{+l} for r < hi.
+template <int E>
+__device__ __forceinline__ void put_col(V* colp, int rr, int M, int lo, int hi, V tw, const V (&v)[E]) {
+  float4* q = reinterpret_cast<float4*>(colp + rr);
+#pragma unroll
+  for (int i = 0; i < E / 2; ++i) q[i] = make_float4(v[2 * i].x, v[2 * i].y, v[2 * i + 1].x, v[2 * i + 1].y);
+  if (rr + E > M - lo) {
+    const V t = cconj(tw);
+#pragma unroll
+    for (int i = 0; i < E; ++i)
+      if (rr + i >= M - lo) colp[rr + i - M] = cmul(v[i], t);
+  }
+  if (rr < hi) {
+#pragma unroll
+    for (int i = 0; i < E; ++i)
+      if (rr + i < hi) colp[rr + i + M] = cmul(v[i], tw);
+  }
+}
+
+// Barrier halves around TMEM traffic: stores of every warp complete and are
+// ordered before the CTA barrier; loads after it see them.
+__device__ __forceinline__ void tm_arrive(int C) {
+  tmem_wait_st();
+  tmem_fence_before();
+  if (C > 1) asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+  __syncthreads();
+  tmem_fence_after();
+}
+
+// Two-level deterministic cluster reduction of a pair (e.g. ||u||^2, ||p||^2).
+// base = this reduction's buffer (kind, parity): base[0 .. 32) per-warp
+// partials of this CTA, base[32 + r] CTA r's total.
+//   red_stage   (before the barrier)  every warp publishes its partial;
+//   tm_arrive_red (the barrier's arrive half) after the CTA barrier warp 0
+//               folds the CTA's partials with a fixed xor-tree (bit-identical
+//               in every lane) and pushes the total to every CTA of the
+//               cluster, then the cluster arrive releases it;
+//   red_total   (after the wait) the C totals summed in rank order, so every
+//               warp of every CTA holds the same bits and takes the same branch.
+// One CTA (C == 1) reads the per-warp partials directly instead.
+__device__ __forceinline__ void red_stage(V part, V* base, int warp, int lane) {
+  part.x = warp_sum(part.x);
+  part.y = warp_sum(part.y);
+  if (lane == 0) base[warp] = part;
+}
+__device__ __forceinline__ void tm_arrive_red(int C, V* base, int nwarps, int warp, int lane, int rank) {
+  tmem_wait_st();
+  tmem_fence_before();
+  __syncthreads();
+  if (C > 1) {
+    if (warp == 0) {
+      V t = lane < nwarps ? base[lane] : make_float2(0.f, 0.f);
+      t.x = warp_sum(t.x);
+      t.y = warp_sum(t.y);
+      if (lane < C) st_cluster(map_rank(smem_addr(base + 32 + rank), (uint32_t)lane), t);
+    }
+    asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+  }
+  tmem_fence_after();
+}
+__device__ __forceinline__ V red_total(int C, const V* base, int nwarps) {
+  if (C == 1) return red_read<float>(base, 1, nwarps, 0);
+  V t = base[32];
+  for (int r = 1; r < C; ++r) t = cadd(t, base[32 + r]);
+  return t;
+}
+
+// Epilogue for E equalized symbols of rows rr.. (contiguous in q): x_hat,
+// hard labels, max-log LLRs and the bit-error count vs TX labels.
+template <int BA, int E>
+__device__ __forceinline__ int tm_epilogue(const SolveArgs& a, const V (&xv)[E], size_t q0, float scale) {
+  V* xo = reinterpret_cast<V*>(a.x) + q0;
+#pragma unroll
+  for (int i = 0; i < E / 2; ++i)
+    reinterpret_cast<float4*>(xo)[i] = make_float4(xv[2 * i].x, xv[2 * i].y, xv[2 * i + 1].x, xv[2 * i + 1].y);
+  if constexpr (BA == 0) {
+    return 0;
+  } else {
+    uint8_t lab[E];
+#pragma unroll
+    for (int i = 0; i < E; ++i) {
+      float l[2 * BA];
+      lab[i] = (uint8_t)qam_symbol<float, BA>(xv[i].x, xv[i].y, scale, a.llr ? l : nullptr);
+      if (a.llr) {
+        float* dst = a.llr + (q0 + i) * (2 * BA);
+        if constexpr (BA == 2) {
+          *reinterpret_cast<float4*>(dst) = make_float4(l[0], l[1], l[2], l[3]);
+        } else {
+#pragma unroll
+          for (int m = 0; m < BA; ++m) reinterpret_cast<float2*>(dst)[m] = make_float2(l[2 * m], l[2 * m + 1]);
+        }
+      }
+    }
+    int errs = 0;
+    static_assert(E % 4 == 0, "label runs are stored in 32-bit words");
+#pragma unroll
+    for (int w = 0; w < E / 4; ++w) {
+      const uint32_t word = (uint32_t)lab[4 * w] | ((uint32_t)lab[4 * w + 1] << 8) |
+                            ((uint32_t)lab[4 * w + 2] << 16) | ((uint32_t)lab[4 * w + 3] << 24);
+      if (a.labels) reinterpret_cast<uint32_t*>(a.labels + q0)[w] = word;
+      if (a.txl) errs += __popc(word ^ __ldg(reinterpret_cast<const uint32_t*>(a.txl + q0) + w));
+    }
+    return errs;
+  }
+}
+
+// Coalesced epilogue pass over the CTA's staged x (column-major, stride M + 2).
+template <int BA>
+__device__ __forceinline__ int epi_pass(const SolveArgs& a, const V* stg, int M, size_t qb, float scale) {
+  const int tot = a.Lcta * M;
+  int errs = 0;
+#pragma unroll 1
+  for (int e = 4 * (int)threadIdx.x; e < tot; e += 4 * (int)blockDim.x) {
+    const int cl = e / M;
+    const float4* sp = reinterpret_cast<const float4*>(stg + cl * (M + 2) + (e - cl * M));
+    const float4 w0 = sp[0], w1 = sp[1];
+    const V xv[4] = {make_float2(w0.x, w0.y), make_float2(w0.z, w0.w), make_float2(w1.x, w1.y),
+                     make_float2(w1.z, w1.w)};
+    errs += tm_epilogue<BA, 4>(a, xv, qb + e, scale);
+  }
+  return errs;
+}
+
+template <int R, int MAXT, bool PROF>
+__global__ void __launch_bounds__(MAXT, 1) sscga_tm_kernel(const SolveArgs a) {
+  constexpr int E = 4;  // elements per TMEM chunk of the elementwise steps
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int M = a.M;
+  const SmemLayout L = tm_layout_impl(a.Lcta, a.N, a.CS, a.TL, a.TH, a.pcap);
+  TmSm sm;
+  sm.c = reinterpret_cast<V*>(smem + L.p);
+  sm.u = reinterpret_cast<V*>(smem + L.u);
+  sm.tslot = reinterpret_cast<uint32_t*>(smem + L.x);
+  V* tlo = reinterpret_cast<V*>(smem + L.tlo);
+  V* thi = reinterpret_cast<V*>(smem + L.thi);
+  V* tw = reinterpret_cast<V*>(smem + L.tw);
+  sm.tlo = tlo;
+  sm.thi = thi;
+  sm.tw = tw;
+  sm.ptab = reinterpret_cast<PathEnt<float>*>(smem + L.ptab);
+  sm.tlb = __ffs(a.TL) - 1;
+  V* red = reinterpret_cast<V*>(smem + L.red);
+  ProfSm* const psm = reinterpret_cast<ProfSm*>(red + 2 * 2 * kPushSlots);
+  FrameSm& fs = *reinterpret_cast<FrameSm*>(psm + 1);
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
+  const int rank = a.C > 1 ? (int)cluster_rank() : 0;
+  TmThr th;
+  {
+    const int ln = 32 * (warp & 3) + lane;  // TMEM lane of this thread
+    const int seg = ln / a.Lcta;
+    th.col = ln - seg * a.Lcta;
+    th.colg = rank * a.Lcta + th.col;
+    th.jr = (warp >> 2) * R;
+    th.r0 = seg * a.G + th.jr;
+  }
+
+  for (int i = tid; i < a.TL; i += blockDim.x) tlo[i] = twiddle(0.f, i, a.MN);
+  for (int i = tid; i < a.TH; i += blockDim.x) thi[i] = twiddle(0.f, (int)(((long long)i * a.TL) % a.MN), a.MN);
+  for (int l = tid; l < a.N; l += blockDim.x) tw[l] = twiddle(0.f, l, a.N);
+  if (warp == 0) tmem_alloc(sm.tslot, (uint32_t)a.tcols);
+  tmem_fence_before();
+  __syncthreads();
+  tmem_fence_after();
+  const uint32_t tbase = *sm.tslot;
+  th.tl = tbase + ((uint32_t)(32 * (warp & 3)) << 16);
+  // TMEM regions of this lane: c | u (segment rows 0..G-1) | p | x (own runs)
+  auto tC = [&](int c0) { return th.tl + (uint32_t)(2 * (th.jr + c0)); };
+  auto tU = [&](int c0) { return th.tl + (uint32_t)(2 * (a.G + th.jr + c0)); };
+  auto tP = [&](int c0) { return th.tl + (uint32_t)(2 * (2 * a.G + th.jr + c0)); };
+  auto tX = [&](int c0) { return th.tl + (uint32_t)(2 * (3 * a.G + th.jr + c0)); };
+  V* const ccol = sm.c + (size_t)th.col * a.CS + a.H;  // this lane's extended columns (row 0)
+  V* const ucol = sm.u + (size_t)th.col * a.CS + a.H;
+
+  const bool lead = (rank == 0 && tid == 0);
+  const int stride = a.iters + 1;
+  int par0 = 0, par1 = 0;
+  if constexpr (PROF) prof_init(a.prof, psm);
+
+  for (int f = blockIdx.x / a.C; f < a.B; f += a.n_clusters) {
+    const size_t fo = (size_t)f * a.MN;
+    const size_t qown = fo + (size_t)th.colg * M + th.r0;  // first owned element of the frame
+    const int P0 = __ldg(a.off + f);
+    const int P = __ldg(a.off + f + 1) - P0;
+
+    if (P <= 0) {  // EmptyChannel (sparse.py:126-127): flag it, no NaNs
+#pragma unroll 1
+      for (int i = 0; i < R; ++i) {
+        reinterpret_cast<V*>(a.x)[qown + i] = make_float2(0.f, 0.f);
+        if (a.labels) a.labels[qown + i] = 0;
+        if (a.llr)
+          for (int b = 0; b < a.bps; ++b) a.llr[(qown + i) * a.bps + b] = 0.f;
+      }
+      if (lead) {
+        float* cnorm = reinterpret_cast<float*>(a.cnorm);
+        if (cnorm) for (int i = 0; i < stride; ++i) cnorm[(size_t)f * stride + i] = 0.f;
+        if (a.itdone) a.itdone[f] = 0;
+        if (a.status) a.status[f] = 1;
+        if (a.berr) a.berr[f] = a.bps * a.MN / 2;  // harness.py:173 scoring of a failed packet
+      }
+      continue;
+    }
+
+    // ---- frame setup: tap table, halo extents, per-row-block tap classes
+    if constexpr (PROF) prof_mark(a.prof, psm, kSetup);
+    const bool in_smem = P <= a.pcap;
+    if (in_smem) {
+      const V* gains = reinterpret_cast<const V*>(a.ph);
+      for (int i = tid; i < P; i += blockDim.x)
+        sm.ptab[i] = tm_path(a, sm, __ldg(a.pk + P0 + i), __ldg(a.pl + P0 + i), __ldg(gains + P0 + i));
+    }
+    if (tid == 0) {
+      int dmin = INT_MAX, dmax = INT_MIN;
+      for (int p = 0; p < P; ++p) {
+        const int dk = a.K0 - __ldg(a.pk + P0 + p);
+        dmin = min(dmin, dk);
+        dmax = max(dmax, dk);
+      }
+      const int lo = max(0, -dmin), hi = max(0, dmax);
+      const bool halo = lo <= a.H && hi <= a.H;
+      fs.P0 = P0;
+      fs.P = P;
+      fs.in_smem = in_smem;
+      fs.halo = halo;
+      fs.masks = in_smem && P <= 32;
+      fs.lo_c = halo ? lo : 0;
+      fs.hi_c = halo ? hi : 0;
+      fs.lo_u = fs.hi_c;
+      fs.hi_u = fs.lo_c;
+    }
+    __syncthreads();
+    if (fs.masks && tid < a.WQ) {  // thread j classifies the taps for row block j
+      uint32_t mk[6] = {0u, 0u, 0u, 0u, 0u, 0u};
+      const bool halo = fs.halo;
+      for (int p = 0; p < P; ++p) {
+        const PathEnt<float>& e = sm.ptab[p];
+        const uint32_t bit = 1u << p;
+        const int cf = tap_class<R, false>(a, tid * R, halo, e);
+        const int ch = tap_class<R, true>(a, tid * R, halo, e);
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          mk[c] |= cf == c ? bit : 0u;
+          mk[3 + c] |= ch == c ? bit : 0u;
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < 6; ++i) fs.mk[tid][i] = mk[i];
+    }
+    const float lam = reinterpret_cast<const float*>(a.lam)[f];
+
+    // y -> u (TMEM own rows + extended shared column); b = H^H y is gathered from it
+    {
+      const int lo_u = fs.lo_u, hi_u = fs.hi_u;
+      const V twl = tw[th.colg];
+      const V* y = reinterpret_cast<const V*>(a.y);
+#pragma unroll
+      for (int c0 = 0; c0 < R; c0 += E) {
+        V w[E];
+        const float4* yq = reinterpret_cast<const float4*>(y + qown + c0);
+#pragma unroll
+        for (int i = 0; i < E / 2; ++i) {
+          const float4 t = __ldg(yq + i);
+          w[2 * i] = make_float2(t.x, t.y);
+          w[2 * i + 1] = make_float2(t.z, t.w);
+        }
+        tm_st<E>(tU(c0), w);
+        put_col<E>(ucol, th.r0 + c0, M, lo_u, hi_u, twl, w);
+        V z[E];
+#pragma unroll
+        for (int i = 0; i < E; ++i) z[i] = make_float2(0.f, 0.f);
+        tm_st<E>(tX(c0), z);  // x = 0
+      }
+      // warm L2 with this cluster's next frame (y, TX labels) while this one solves
+      if (f + a.n_clusters < a.B) {
+        const size_t qn = qown + (size_t)a.n_clusters * a.MN;
+#pragma unroll
+        for (int c0 = 0; c0 < R; c0 += 16) asm volatile("prefetch.global.L2 [%0];" :: "l"(y + qn + c0));
+        if (a.txl) asm volatile("prefetch.global.L2 [%0];" :: "l"(a.txl + qn));
+      }
+    }
+    if (lead && a.berr) a.berr[f] = 0;
+
+    U64 acc[R];
+    if constexpr (PROF) prof_mark(a.prof, psm, kArrive);
+    tm_arrive(a.C);  // y and the tap classes published
+    if constexpr (PROF) prof_mark(a.prof, psm, kMvmLocal);
+    mvm_local<R, true>(a, th, sm, fs, tU(0) - 2 * th.jr, ucol, acc);  // b = H^H y (equalize.py:52)
+    if constexpr (PROF) prof_mark(a.prof, psm, kWait);
+    cl_wait(a.C);
+    if constexpr (PROF) prof_mark(a.prof, psm, kMvmRemote);
+    mvm_remote<R, true>(a, th, sm, fs, sm.u, acc);
+    if constexpr (PROF) prof_mark(a.prof, psm, kStep1);
+    {
+      V nrm = make_float2(0.f, 0.f);
+      const int lo_c = fs.lo_c, hi_c = fs.hi_c;
+      const V twl = tw[th.colg];
+#pragma unroll
+      for (int c0 = 0; c0 < R; c0 += E) {
+        V w[E];
+#pragma unroll
+        for (int i = 0; i < E; ++i) {
+          w[i] = unpack2(acc[c0 + i]);
+          nacc(nrm, w[i]);
+        }
+        tm_st<E>(tC(c0), w);  // c = b
+        put_col<E>(ccol, th.r0 + c0, M, lo_c, hi_c, twl, w);
+      }
+      red_stage(make_float2(nrm.x + nrm.y, 0.f), red + (2 + par1) * kPushSlots, warp, lane);
+    }
+    if constexpr (PROF) prof_mark(a.prof, psm, kArrive);
+    tm_arrive_red(a.C, red + (2 + par1) * kPushSlots, nwarps, warp, lane, rank);  // c = b published
+    if constexpr (PROF) prof_mark(a.prof, psm, kMvmLocal);
+    mvm_local<R, false>(a, th, sm, fs, tC(0) - 2 * th.jr, ccol, acc);
+    if constexpr (PROF) prof_mark(a.prof, psm, kWait);
+    cl_wait(a.C);
+    if constexpr (PROF) prof_mark(a.prof, psm, kRead);
+    float cn = red_total(a.C, red + (2 + par1) * kPushSlots, nwarps).x;
+    par1 ^= 1;
+    float beta = 0.f;
+    if (lead && a.cnorm) reinterpret_cast<float*>(a.cnorm)[(size_t)f * stride] = cn;
+
+    int done = 0;
+    bool exact = false;
+    for (int it = 0; it < a.iters; ++it) {
+      // u = H c + beta u_old, p = c + beta p_old      (= H p, p of equalize.py:60, 72)
+      if constexpr (PROF) prof_mark(a.prof, psm, kMvmRemote);
+      mvm_remote<R, false>(a, th, sm, fs, sm.c, acc);
+      if constexpr (PROF) prof_mark(a.prof, psm, kStep1);
+      {
+        V nu = make_float2(0.f, 0.f), np = make_float2(0.f, 0.f);
+        const int lo_u = fs.lo_u, hi_u = fs.hi_u;
+        const V twl = tw[th.colg];
+#pragma unroll
+        for (int c0 = 0; c0 < R; c0 += E) {
+          uint32_t ru[2 * E], rc[2 * E], rp[2 * E];
+          tm_ld<E>(tC(c0), rc);
+          if (it > 0) {
+            tm_ld<E>(tU(c0), ru);
+            tm_ld<E>(tP(c0), rp);
+            tmem_wait_ld_tie<2 * E>(ru);
+            tmem_wait_ld_tie<2 * E>(rp);
+          }
+          tmem_wait_ld_tie<2 * E>(rc);
+          V w[E], pv[E];
+#pragma unroll
+          for (int i = 0; i < E; ++i) {
+            const V hc = unpack2(acc[c0 + i]);
+            const V cr = tm_get_v<E>(rc, i);
+            w[i] = it == 0 ? hc : axpy(hc, beta, tm_get_v<E>(ru, i));
+            pv[i] = it == 0 ? cr : axpy(cr, beta, tm_get_v<E>(rp, i));
+            nacc(nu, w[i]);
+            nacc(np, pv[i]);
+          }
+          tm_st<E>(tU(c0), w);
+          tm_st<E>(tP(c0), pv);
+          put_col<E>(ucol, th.r0 + c0, M, lo_u, hi_u, twl, w);
+        }
+        red_stage(make_float2(nu.x + nu.y, np.x + np.y), red + par0 * kPushSlots, warp, lane);
+      }
+      if constexpr (PROF) prof_mark(a.prof, psm, kArrive);
+      tm_arrive_red(a.C, red + par0 * kPushSlots, nwarps, warp, lane, rank);  // u published
+      // ap = H^H u + lam p;  x += alpha p;  c -= alpha ap      (equalize.py:60-70)
+      if constexpr (PROF) prof_mark(a.prof, psm, kMvmLocal);
+      mvm_local<R, true>(a, th, sm, fs, tU(0) - 2 * th.jr, ucol, acc);
+      if constexpr (PROF) prof_mark(a.prof, psm, kWait);
+      cl_wait(a.C);
+      if constexpr (PROF) prof_mark(a.prof, psm, kMvmRemote);
+      mvm_remote<R, true>(a, th, sm, fs, sm.u, acc);
+      if constexpr (PROF) prof_mark(a.prof, psm, kRead);
+      const V up = red_total(a.C, red + par0 * kPushSlots, nwarps);
+      par0 ^= 1;
+      if constexpr (PROF) prof_mark(a.prof, psm, kStep3);
+      const float denom = up.x + lam * up.y;  // ||H p||^2 + lam ||p||^2 = Re p^H (H^H H + lam I) p
+      if (denom == 0.f) {  // equalize.py:64-67
+        exact = true;
+        // peers may still be reading this CTA's u: one more full barrier
+        tm_arrive(a.C);
+        cl_wait(a.C);
+        break;
+      }
+      const float alpha = cn / denom;
+      {
+        V nc = make_float2(0.f, 0.f);
+        const int lo_c = fs.lo_c, hi_c = fs.hi_c;
+        const V twl = tw[th.colg];
+#pragma unroll
+        for (int c0 = 0; c0 < R; c0 += E) {
+          uint32_t rx[2 * E], rp[2 * E], rc[2 * E];
+          tm_ld<E>(tX(c0), rx);
+          tm_ld<E>(tP(c0), rp);
+          tm_ld<E>(tC(c0), rc);
+          tmem_wait_ld_tie<2 * E>(rx);
+          tmem_wait_ld_tie<2 * E>(rp);
+          tmem_wait_ld_tie<2 * E>(rc);
+          V xv[E], cv[E];
+#pragma unroll
+          for (int i = 0; i < E; ++i) {
+            const V pv = tm_get_v<E>(rp, i);
+            const V ap = axpy(unpack2(acc[c0 + i]), lam, pv);
+            xv[i] = axpy(tm_get_v<E>(rx, i), alpha, pv);
+            cv[i] = axpy(tm_get_v<E>(rc, i), -alpha, ap);
+            nacc(nc, cv[i]);
+          }
+          tm_st<E>(tX(c0), xv);
+          tm_st<E>(tC(c0), cv);
+          put_col<E>(ccol, th.r0 + c0, M, lo_c, hi_c, twl, cv);
+          if (a.snaps) {
+            V* sp = reinterpret_cast<V*>(a.snaps) + ((size_t)f * a.iters + it) * a.MN + (qown - fo) + c0;
+#pragma unroll
+            for (int i = 0; i < E; ++i) sp[i] = xv[i];
+          }
+        }
+        red_stage(make_float2(nc.x + nc.y, 0.f), red + (2 + par1) * kPushSlots, warp, lane);
+      }
+      if constexpr (PROF) prof_mark(a.prof, psm, kArrive);
+      tm_arrive_red(a.C, red + (2 + par1) * kPushSlots, nwarps, warp, lane, rank);  // c published
+      if constexpr (PROF) prof_mark(a.prof, psm, kMvmLocal);
+      if (it + 1 < a.iters) mvm_local<R, false>(a, th, sm, fs, tC(0) - 2 * th.jr, ccol, acc);  // next H c
+      if constexpr (PROF) prof_mark(a.prof, psm, kWait);
+      cl_wait(a.C);
+      if constexpr (PROF) prof_mark(a.prof, psm, kRead);
+      const float nn = red_total(a.C, red + (2 + par1) * kPushSlots, nwarps).x;
+      par1 ^= 1;
+      beta = nn / cn;
+      cn = nn;
+      done = it + 1;
+      if (lead && a.cnorm) reinterpret_cast<float*>(a.cnorm)[(size_t)f * stride + done] = cn;
+    }
+    if (lead) {
+      float* cnorm = reinterpret_cast<float*>(a.cnorm);
+      if (cnorm) for (int i = done + 1; i < stride; ++i) cnorm[(size_t)f * stride + i] = 0.f;
+      if (a.itdone) a.itdone[f] = done;
+      if (a.status) a.status[f] = exact ? 2 : 0;
+    }
+
+    // epilogue: x_hat out, fused hard decisions / LLRs / bit errors
+    if constexpr (PROF) prof_mark(a.prof, psm, kEpilogue);
+    float scale = 1.f;
+    if (a.bps) {
+      const float nv = a.nvar ? reinterpret_cast<const float*>(a.nvar)[f] : lam;
+      scale = nv > 0.f ? 1.f / nv : 1.f;
+    }
+    // x -> shared staging in q order (column-major, stride M + 2: conflict-free
+    // 16-byte stores), then every thread takes 4 consecutive symbols at a time
+    // so the x_hat / LLR / label stores and TX label loads are coalesced.  The
+    // c slice is free: all gathers of this frame are behind the last barrier.
+    {
+      const int SS = M + 2;
+#pragma unroll
+      for (int c0 = 0; c0 < R; c0 += E) {
+        uint32_t rx[2 * E];
+        tm_ld<E>(tX(c0), rx);
+        tmem_wait_ld_tie<2 * E>(rx);
+        float4* d = reinterpret_cast<float4*>(sm.c + th.col * SS + th.r0 + c0);
+#pragma unroll
+        for (int i = 0; i < E / 2; ++i)
+          d[i] = make_float4(__uint_as_float(rx[4 * i]), __uint_as_float(rx[4 * i + 1]),
+                             __uint_as_float(rx[4 * i + 2]), __uint_as_float(rx[4 * i + 3]));
+      }
+    }
+    __syncthreads();
+    int errs = 0;
+    {
+      const size_t qb = fo + (size_t)rank * a.Lcta * M;
+      switch (a.bps) {
+        case 0: epi_pass<0>(a, sm.c, M, qb, scale); break;
+        case 2: errs = epi_pass<1>(a, sm.c, M, qb, scale); break;
+        case 4: errs = epi_pass<2>(a, sm.c, M, qb, scale); break;
+        default: errs = epi_pass<3>(a, sm.c, M, qb, scale); break;
+      }
+    }
+    if (a.berr) {
+      errs = warp_sum(errs);
+      if (lane == 0 && errs) atomicAdd(a.berr + f, errs);
+    }
+  }
+  if constexpr (PROF) prof_mark(a.prof, psm, kTail);
+  if constexpr (PROF) prof_store(a.prof, psm);
+  // no CTA may leave while a peer can still read its shared memory (DSMEM)
+  tmem_fence_before();
+  cl_sync<float>(a.C);
+  if (warp == 0) tmem_dealloc(tbase, (uint32_t)a.tcols);
+}
+
+template <int R, int MAXT, bool PROF = false>
+cudaError_t launch_r(SolveArgs a, const LaunchShape& s, cudaStream_t st) {
+  auto kern = sscga_tm_kernel<R, MAXT, PROF>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, s.smem);
+  if (e != cudaSuccess) return e;
+  e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+  if (e != cudaSuccess) return e;
+  if (s.cluster > 8) {
+    e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    if (e != cudaSuccess) return e;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.blockDim = dim3(s.threads);
+  cfg.dynamicSmemBytes = s.smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = s.cluster;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cfg.gridDim = dim3(s.cluster);
+  int max_clusters = 0;
+  e = cudaOccupancyMaxActiveClusters(&max_clusters, kern, &cfg);
+  if (e != cudaSuccess) return e;
+  if (max_clusters < 1) return cudaErrorInvalidConfiguration;
+  const int nclu = a.B < max_clusters ? a.B : max_clusters;
+  a.n_clusters = nclu;
+  cfg.gridDim = dim3(nclu * s.cluster);
+  return cudaLaunchKernelEx(&cfg, kern, a);
+}
+
+template <int R, int MAXT>
+cudaError_t occ_r(const LaunchShape& s, int* n) {
+  auto kern = sscga_tm_kernel<R, MAXT, false>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, s.smem);
+  if (e != cudaSuccess) return e;
+  e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+  if (e != cudaSuccess) return e;
+  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(n, kern, s.threads, s.smem);
+}
+
+}  // namespace
+
+SmemLayout sscga_tm_layout(int M, int Lcta, int N, int CS, int TL, int TH, int pcap) {
+  (void)M;
+  return tm_layout_impl(Lcta, N, CS, TL, TH, pcap);
+}
+
+cudaError_t launch_sscga_tm(SolveArgs a, const LaunchShape& s, cudaStream_t st) {
+  if (a.B == 0) return cudaSuccess;
+  // 1024-thread CTAs (8 warps per lane quarter) run at <= 64 registers
+  if (s.threads > 512) {
+    switch (s.rows) {
+      case 4: return launch_r<4, 1024>(a, s, st);
+      case 8: return launch_r<8, 1024>(a, s, st);
+      default: return cudaErrorInvalidValue;
+    }
+  }
+  if (a.prof) {  // clock64 phase profile (measurement launches only)
+    switch (s.rows) {
+      case 4: return launch_r<4, 512, true>(a, s, st);
+      case 8: return launch_r<8, 512, true>(a, s, st);
+      case 16: return launch_r<16, 512, true>(a, s, st);
+      default: return cudaErrorInvalidValue;
+    }
+  }
+  switch (s.rows) {
+    case 4: return launch_r<4, 512>(a, s, st);
+    case 8: return launch_r<8, 512>(a, s, st);
+    case 16: return launch_r<16, 512>(a, s, st);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+cudaError_t sscga_tm_occupancy(const LaunchShape& s, int* n) {
+  if (s.threads > 512) {
+    switch (s.rows) {
+      case 4: return occ_r<4, 1024>(s, n);
+      case 8: return occ_r<8, 1024>(s, n);
+      default: return cudaErrorInvalidValue;
+    }
+  }
+  switch (s.rows) {
+    case 4: return occ_r<4, 512>(s, n);
+    case 8: return occ_r<8, 512>(s, n);
+    case 16: return occ_r<16, 512>(s, n);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+}  // namespace ddb

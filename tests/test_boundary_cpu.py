@@ -18,7 +18,7 @@ def test_exports_every_header_symbol(lib):
     assert len(names) >= 12
     for n in names:
         assert hasattr(lib, n), n
-    assert lib.ddb_abi_version() == 1
+    assert lib.ddb_abi_version() == nat.ABI_VERSION == 2
     assert b"sm_100a" in lib.ddb_build_info()
 
 

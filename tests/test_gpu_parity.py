@@ -28,6 +28,18 @@ def pkg():
     return p
 
 
+@pytest.fixture(params=["tmem", "rows"])
+def fp32_kernel(request, monkeypatch):
+    """Run an fp32 test on both fused kernels: the TMEM-operand kernel (the
+    planner's default wherever its layout applies) and the row-slice kernel
+    (DDB_KERNEL=row)."""
+    if request.param == "rows":
+        monkeypatch.setenv("DDB_KERNEL", "row")
+    else:
+        monkeypatch.delenv("DDB_KERNEL", raising=False)
+    return request.param
+
+
 def frame_taps(d, f):
     a, b = int(d["path_off"][f]), int(d["path_off"][f + 1])
     return [orc.Tap(int(k), int(l), complex(g)) for k, l, g in zip(d["path_k"][a:b], d["path_l"][a:b], d["path_g"][a:b])]
@@ -196,7 +208,7 @@ def _oracle_frames(d, const):
 
 
 @pytest.mark.parametrize("name", ["frames_cfg1", "frames_cfg2", "frames_cfg3", "frames_sweep", "frames_cfg4"])
-def test_batched_fp32_parity(pkg, name):
+def test_batched_fp32_parity(pkg, name, fp32_kernel):
     d = load_golden(name)
     M, N, iters, b = (int(v) for v in d["meta"])
     const = orc.qam({2: "qpsk", 4: "qam16"}[b])
@@ -316,10 +328,23 @@ def _random_problem(M, N, B, P, rng, anywhere=True):
     return off, k, l, g, y
 
 
-@pytest.mark.parametrize("M,N,P", [(8, 2, 3), (2, 2, 1), (12, 6, 4), (48, 32, 5), (64, 6, 3),
-                                   (512, 32, 6), (256, 64, 7), (1024, 64, 8), (2048, 32, 6)])
+SHAPES = [(8, 2, 3), (2, 2, 1), (12, 6, 4), (48, 32, 5), (64, 6, 3), (512, 32, 6), (256, 64, 7), (1024, 64, 8),
+          (2048, 32, 6), (64, 16, 4), (128, 8, 5), (128, 32, 6), (256, 16, 40)]
+
+
+@pytest.mark.parametrize("M,N,P", SHAPES)
 @pytest.mark.parametrize("precision", ["fp32", "fp64"])
-def test_random_taps_all_cluster_shapes(pkg, M, N, P, precision):
+def test_random_taps_all_cluster_shapes(pkg, M, N, P, precision, monkeypatch):
+    _random_taps_case(pkg, M, N, P, precision)
+
+
+@pytest.mark.parametrize("M,N,P", SHAPES)
+def test_random_taps_row_kernel_fp32(pkg, M, N, P, monkeypatch):
+    monkeypatch.setenv("DDB_KERNEL", "row")
+    _random_taps_case(pkg, M, N, P, "fp32")
+
+
+def _random_taps_case(pkg, M, N, P, precision):
     """Arbitrary tap positions exercise the DSMEM (remote column) and wrap-twist
     paths of every cluster shape the planner picks."""
     rng = np.random.default_rng(M * 7 + N + P)
