@@ -230,6 +230,12 @@ __device__ __forceinline__ float2 ld_cluster(float2*, uint32_t caddr) {
   asm volatile("ld.shared::cluster.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "r"(caddr) : "memory");
   return v;
 }
+__device__ __forceinline__ float4 ld_cluster4(uint32_t caddr) {
+  float4 v;
+  asm volatile("ld.shared::cluster.v4.f32 {%0, %1, %2, %3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(caddr) : "memory");
+  return v;
+}
 __device__ __forceinline__ double2 ld_cluster(double2*, uint32_t caddr) {
   double2 v;
   asm volatile("ld.shared::cluster.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(caddr) : "memory");

@@ -144,9 +144,13 @@ __device__ __forceinline__ void gather_tmem(uint32_t ta, U64 X, U64 Y, U64 (&acc
   for (int i = 0; i < R; ++i) cmacxy(acc[i], X, Y, __uint_as_float(v[2 * i]), __uint_as_float(v[2 * i + 1]));
 }
 
-// One tap, per element, from the (possibly remote) extended column of the
-// source Doppler column; row wraps applied in registers when the frame's
-// shifts exceed the halo.
+// One tap with a Doppler shift (d_l != 0), or any tap when the frame's shifts
+// exceed the halo, from the (possibly remote) extended column of the source
+// Doppler column.  With the halo the R source rows are one contiguous run:
+// 16-byte DSMEM loads, and the row-dependent coefficient h W^{-+d_l k} of the
+// forward / hermitian closed form (sparse.py:107-121) advanced by one complex
+// multiply per row from an exact table value every 8 rows.  Without the halo
+// rows wrap the delay period individually (twist applied in registers).
 template <int R, bool HERM>
 __device__ __forceinline__ void tap_elem(const SolveArgs& a, const TmThr& th, const TmSm& sm, bool halo,
                                          const V* buf, const PathEnt<float>& e, U64 (&acc)[R]) {
@@ -159,16 +163,49 @@ __device__ __forceinline__ void tap_elem(const SolveArgs& a, const TmThr& th, co
   const int own = ls / a.Lcta;
   const int lc = ls - own * a.Lcta;
   const uint32_t colad = map_rank(smem_addr(buf + (size_t)lc * a.CS + a.H), (uint32_t)own);
+  const int sg = HERM ? dl : -dl;  // coefficient phase exponent per row
+  if (halo) {
+    constexpr int BS = R < 8 ? R : 8;  // rows per exact re-anchor
+    const V step = twid_tm(sm, wrap1(sg, MN));
+    const uint32_t run = colad + (uint32_t)((th.r0 + s) * (int)sizeof(V));
+    V v[R];
+    if ((s & 1) == 0) {
+#pragma unroll
+      for (int m = 0; m < R / 2; ++m) {
+        const float4 w = ld_cluster4(run + 16u * m);
+        v[2 * m] = make_float2(w.x, w.y);
+        v[2 * m + 1] = make_float2(w.z, w.w);
+      }
+    } else {
+      float4 w = ld_cluster4(run - 8u);
+      v[0] = make_float2(w.z, w.w);
+#pragma unroll
+      for (int m = 1; m < R / 2; ++m) {
+        w = ld_cluster4(run - 8u + 16u * m);
+        v[2 * m - 1] = make_float2(w.x, w.y);
+        v[2 * m] = make_float2(w.z, w.w);
+      }
+      w = ld_cluster4(run - 8u + 16u * (R / 2));
+      v[R - 1] = make_float2(w.x, w.y);
+    }
+#pragma unroll
+    for (int b = 0; b < R; b += BS) {
+      V c = cmul(h0, twid_tm(sm, wrap1(sg * (th.r0 + b) % MN, MN)));
+#pragma unroll
+      for (int i = 0; i < BS; ++i) {
+        Acc<float>::mac(acc[b + i], c, v[b + i]);
+        c = cmul(c, step);
+      }
+    }
+    return;
+  }
 #pragma unroll
   for (int i = 0; i < R; ++i) {
     const int k = th.r0 + i;
-    const V coef = dl ? cmul(h0, twid_tm(sm, wrap1(HERM ? dl * k : -dl * k, MN))) : h0;
+    const V coef = dl ? cmul(h0, twid_tm(sm, wrap1(sg * k, MN))) : h0;
     int ar = k + s;
-    int nw = 0;
-    if (!halo) {
-      nw = ar < 0 ? -1 : (ar >= M ? 1 : 0);
-      ar -= nw * M;
-    }
+    const int nw = ar < 0 ? -1 : (ar >= M ? 1 : 0);
+    ar -= nw * M;
     V v = ld_cluster(static_cast<V*>(nullptr), colad + (uint32_t)(ar * (int)sizeof(V)));
     if (nw != 0) {
       V t = sm.tw[ls];

@@ -37,14 +37,15 @@ def main():
                        device="cuda")
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
-    s.solve(fb.y, fb.paths, fb.lam, tx_labels=fb.tx_labels, out=out, phase_cycles=prof)
+    res = s.solve(fb.y, fb.paths, fb.lam, tx_labels=fb.tx_labels, out=out, phase_cycles=prof)
     e1.record()
     torch.cuda.synchronize()
+    it_done = res.iterations_done.float().mean().item() if res.iterations_done is not None else None
     p = prof.cpu()
     rows = p[p.sum(dim=1) > 0]
     tot = rows.sum(dim=0).double()
     frames_per_cta = args.batch / (rows.shape[0] / s.plan()["cluster"])
-    res = {"plan": s.plan(), "ms": e0.elapsed_time(e1), "ctas": int(rows.shape[0]),
+    res = {"plan": s.plan(), "ms": e0.elapsed_time(e1), "ctas": int(rows.shape[0]), "mean_iterations": it_done,
            "cycles_per_frame": float(tot.sum() / rows.shape[0] / frames_per_cta),
            "phases_pct": {name: round(100 * float(tot[i] / tot.sum()), 2) for i, name in enumerate(nat.PHASES)},
            "phase_cycles_per_frame": {name: round(float(tot[i] / rows.shape[0] / frames_per_cta))
