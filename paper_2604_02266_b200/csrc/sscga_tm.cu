@@ -431,7 +431,7 @@ template <int BA>
 __device__ __forceinline__ int epi_pass(const SolveArgs& a, const V* stg, int M, size_t qb, float scale) {
   const int tot = a.Lcta * M;
   int errs = 0;
-#pragma unroll 1
+#pragma unroll 2
   for (int e = 4 * (int)threadIdx.x; e < tot; e += 4 * (int)blockDim.x) {
     const int cl = e / M;
     const float4* sp = reinterpret_cast<const float4*>(stg + cl * (M + 2) + (e - cl * M));
@@ -525,30 +525,36 @@ __global__ void __launch_bounds__(MAXT, 1) sscga_tm_kernel(const SolveArgs a) {
 
     // ---- frame setup: tap table, halo extents, per-row-block tap classes
     if constexpr (PROF) prof_mark(a.prof, psm, kSetup);
+    // this frame's y first: the 16-byte loads are in flight during the tap-table work
+    const V* y = reinterpret_cast<const V*>(a.y);
+    float4 yv[R / 2];
+#pragma unroll
+    for (int i = 0; i < R / 2; ++i) yv[i] = __ldg(reinterpret_cast<const float4*>(y + qown) + i);
     const bool in_smem = P <= a.pcap;
-    if (in_smem) {
+    if (warp == 0) {  // tap table and shift extents, lanes over taps
       const V* gains = reinterpret_cast<const V*>(a.ph);
-      for (int i = tid; i < P; i += blockDim.x)
-        sm.ptab[i] = tm_path(a, sm, __ldg(a.pk + P0 + i), __ldg(a.pl + P0 + i), __ldg(gains + P0 + i));
-    }
-    if (tid == 0) {
       int dmin = INT_MAX, dmax = INT_MIN;
-      for (int p = 0; p < P; ++p) {
-        const int dk = a.K0 - __ldg(a.pk + P0 + p);
-        dmin = min(dmin, dk);
-        dmax = max(dmax, dk);
+      for (int i = lane; i < P; i += 32) {
+        const int kp = __ldg(a.pk + P0 + i);
+        if (in_smem) sm.ptab[i] = tm_path(a, sm, kp, __ldg(a.pl + P0 + i), __ldg(gains + P0 + i));
+        dmin = min(dmin, a.K0 - kp);
+        dmax = max(dmax, a.K0 - kp);
       }
-      const int lo = max(0, -dmin), hi = max(0, dmax);
-      const bool halo = lo <= a.H && hi <= a.H;
-      fs.P0 = P0;
-      fs.P = P;
-      fs.in_smem = in_smem;
-      fs.halo = halo;
-      fs.masks = in_smem && P <= 32;
-      fs.lo_c = halo ? lo : 0;
-      fs.hi_c = halo ? hi : 0;
-      fs.lo_u = fs.hi_c;
-      fs.hi_u = fs.lo_c;
+      dmin = __reduce_min_sync(0xffffffffu, dmin);
+      dmax = __reduce_max_sync(0xffffffffu, dmax);
+      if (lane == 0) {
+        const int lo = max(0, -dmin), hi = max(0, dmax);
+        const bool halo = lo <= a.H && hi <= a.H;
+        fs.P0 = P0;
+        fs.P = P;
+        fs.in_smem = in_smem;
+        fs.halo = halo;
+        fs.masks = in_smem && P <= 32;
+        fs.lo_c = halo ? lo : 0;
+        fs.hi_c = halo ? hi : 0;
+        fs.lo_u = fs.hi_c;
+        fs.hi_u = fs.lo_c;
+      }
     }
     __syncthreads();
     if (fs.masks && tid < a.WQ) {  // thread j classifies the taps for row block j
@@ -574,14 +580,12 @@ __global__ void __launch_bounds__(MAXT, 1) sscga_tm_kernel(const SolveArgs a) {
     {
       const int lo_u = fs.lo_u, hi_u = fs.hi_u;
       const V twl = tw[th.colg];
-      const V* y = reinterpret_cast<const V*>(a.y);
 #pragma unroll
       for (int c0 = 0; c0 < R; c0 += E) {
         V w[E];
-        const float4* yq = reinterpret_cast<const float4*>(y + qown + c0);
 #pragma unroll
         for (int i = 0; i < E / 2; ++i) {
-          const float4 t = __ldg(yq + i);
+          const float4 t = yv[c0 / 2 + i];
           w[2 * i] = make_float2(t.x, t.y);
           w[2 * i + 1] = make_float2(t.z, t.w);
         }
