@@ -12,7 +12,7 @@ timeout 300 python tools/phase_profile.py > gpurun_out/${TAG}_phase.log 2>&1
 if [ -z "$SKIP_NCU" ]; then
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/${TAG}_launches.csv \
   python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu --no-latency > gpurun_out/${TAG}_ncu_bench.log 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:sscga_kernel -s 3 -c 1 \
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:sscga -s 3 -c 1 \
   -o gpurun_out/${TAG}_full -f python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu --no-latency > gpurun_out/${TAG}_ncu_full.log 2>&1
 fi
-tail -3 gpurun_out/${TAG}_*.log
+for f in gpurun_out/${TAG}_*.log; do tail -n 3 "$f"; done
