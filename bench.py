@@ -59,6 +59,7 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-latency", action="store_true")
+    ap.add_argument("--no-frontend", action="store_true")
     ap.add_argument("--lat-runs", type=int, default=2000)
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     return ap.parse_args()
@@ -349,6 +350,38 @@ def main():
         per_frame = json.loads(ncu_sum.read_text()).get("dram_bytes_per_frame")
         traffic = per_frame * B if per_frame else None
 
+    # ---- receiver front end (row f1): batched DZT of time-domain data frames
+    #      (HBM-bound: 8 B read + 8 B written per symbol at fp32) and the pilot
+    #      path (fp64 DZT + estimate fused, detect_paths) on the same batch
+    frontend = None
+    if not args.no_frontend:
+        from paper_2604_02266_b200.zak import dzt_device
+        y_time = torch.randn(B, MN, dtype=torch.complex64, device="cuda")
+        y_dd = torch.empty_like(y_time)
+        for _ in range(3):
+            dzt_device(y_time, M, N, out=y_dd)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        reps = 10
+        a.record(stream)
+        for _ in range(reps):
+            dzt_device(y_time, M, N, out=y_dd)
+        b.record(stream)
+        b.synchronize()
+        dzt_ms = a.elapsed_time(b) / reps
+        dzt_gbs = B * MN * 16 / (dzt_ms * 1e-3) / 1e9
+        pil = torch.zeros(B, MN, dtype=torch.complex128, device="cuda")
+        pil[:, (N // 2) * M + M // 2] = math.sqrt(MN)  # an identity channel's pilot frame, time domain
+        s.detect(pil, 0.08)
+        torch.cuda.synchronize()
+        a.record(stream)
+        s.detect(pil, 0.08)
+        b.record(stream)
+        b.synchronize()
+        frontend = {"dzt_ms": dzt_ms, "dzt_gbs": dzt_gbs, "dzt_hbm_frac": dzt_gbs / hbm_peak,
+                    "dzt_bytes_per_frame": MN * 16, "detect_ms_per_batch": a.elapsed_time(b),
+                    "what": "ddb_dzt fp32 batch (zak.py:50-55) vs HBM peak; pilot path = fp64 DZT + estimate_heff "
+                            "+ detect_paths + CSR for the batch (pilot.py:40-49, sparse.py:69-88)"}
+
     # ---- single-frame latency: CUDA graph of a batch-1 solve, replayed
     latency = None
     if not args.no_latency and rank == 0:
@@ -437,6 +470,7 @@ def main():
                              "frac": hbm_gbs / hbm_peak, "bytes_per_frame": io_bytes / B},
             "cpu_baseline": cpu,
             "e2e": e2e,
+            "frontend": frontend,
             "gpu_launches": args.steps,
             "clocks": clocks,
             "plan": s.plan(),

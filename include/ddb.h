@@ -19,6 +19,9 @@
  *   ddb_ss_mvm_tables    sparse.py:147-160   ss_mvm / ss_mvm_hermitian on explicit tables
  *   ddb_hard_demod       grid.py:172-183     hard_demod (nearest point, lowest label on ties)
  *   ddb_qam_demod        grid.py:98-183      Gray-QAM slicer + max-log LLR (build-defined)
+ *   ddb_dzt              zak.py:50-55        dzt_gemm (kernel of zak.py:33-47 or caller's),
+ *                        fused with pilot.py:40-49 estimate_heff (twist of pilot.py:29-37)
+ *   ddb_estimate_heff    pilot.py:40-49      estimate_heff on a DD frame
  *   ddb_detect_paths     sparse.py:69-88     detect_paths (strict relative threshold,
  *                                            stable descending-magnitude order)
  *
@@ -151,11 +154,47 @@ int32_t ddb_detect_paths(int32_t batch, int32_t M, int32_t N, const void* heff, 
                          int32_t max_paths, int32_t* count, int32_t* path_k,
                          int32_t* path_l, void* path_gain, void* stream);
 
+/* ---- receiver front end.
+ *      ddb_dzt: y_time complex [B, M*N] received samples (time index k + i*M,
+ *      grid.py check_signal); kernel complex [N, N] row-major (i, l) or NULL for
+ *      build_zak_kernel(N) = e^{-j2pi i l/N}/sqrt(N) (zak.py:33-47); out complex
+ *      [B, M*N].  flags: DDB_DZT_COLMAJOR writes the flattened vector
+ *      q = l*M + k (grid.py:86-95), else the (M, N) frame row-major as dzt_gemm
+ *      returns it; DDB_DZT_PILOT also multiplies by the twist kernel
+ *      e^{-j2pi K0 (l-L0)/(MN)} and divides by `amplitude` (estimate_heff). */
+#define DDB_DZT_COLMAJOR 1
+#define DDB_DZT_PILOT 2
+int32_t ddb_dzt(int32_t batch, int32_t M, int32_t N, int32_t dtype, const void* y_time, const void* kernel,
+                int32_t flags, double amplitude, void* out, void* stream);
+
+/* ---- estimate_heff (pilot.py:40-49) on DD frames: heff = y_dd * twist / amplitude
+ *      elementwise over `count` complex values of the dtype (amplitude > 0). */
+int32_t ddb_estimate_heff(int64_t count, int32_t dtype, const void* y_dd, const void* twist, double amplitude,
+                          void* heff, void* stream);
+
 /* ---- measurement helper (not a reference interface): FP32 FMA throughput
  *      probe used by bench.py to state the measured FP32 roofline.  Launches
  *      blocks x 256 threads, each doing iters x 256 FMAs (mode 0: FFMA,
  *      mode 1: packed FFMA2).  scratch: device float[blocks]. */
 int32_t ddb_probe_fp32(int32_t mode, int32_t blocks, int32_t iters, float* scratch, void* stream);
+
+/* ---- receiver front end.
+ *      ddb_dzt: y_time complex [B, M*N] received samples (time index k + i*M,
+ *      grid.py check_signal); kernel complex [N, N] row-major (i, l) or NULL for
+ *      build_zak_kernel(N) = e^{-j2pi i l/N}/sqrt(N) (zak.py:33-47); out complex
+ *      [B, M*N].  flags: DDB_DZT_COLMAJOR writes the flattened vector
+ *      q = l*M + k (grid.py:86-95), else the (M, N) frame row-major as dzt_gemm
+ *      returns it; DDB_DZT_PILOT also multiplies by the twist kernel
+ *      e^{-j2pi K0 (l-L0)/(MN)} and divides by `amplitude` (estimate_heff). */
+#define DDB_DZT_COLMAJOR 1
+#define DDB_DZT_PILOT 2
+int32_t ddb_dzt(int32_t batch, int32_t M, int32_t N, int32_t dtype, const void* y_time, const void* kernel,
+                int32_t flags, double amplitude, void* out, void* stream);
+
+/* ---- estimate_heff (pilot.py:40-49) on DD frames: heff = y_dd * twist / amplitude
+ *      elementwise over `count` complex values of the dtype (amplitude > 0). */
+int32_t ddb_estimate_heff(int64_t count, int32_t dtype, const void* y_dd, const void* twist, double amplitude,
+                          void* heff, void* stream);
 
 /* ---- measurement helper (not a reference interface): ddb_sscga_solve with
  *      clock64 phase accounting on thread 0 of every CTA.  phase_cycles:

@@ -14,6 +14,8 @@ reference's own worked examples (tests/test_sparse.py:49-55 of the reference).
 Each function cites the reference file:line it restates.  The hot path
  is:
     detect_paths -> build_tables -> cga -> hard_demod
+and the receiver front end before it (section 8f row f1):
+    dzt_gemm (pilot, data) -> estimate_heff
 """
 
 from __future__ import annotations
@@ -140,6 +142,37 @@ def llr_maxlog(x_vec: np.ndarray, const: Qam, noise_var: float) -> np.ndarray:
         out[:, i] = dist[:, one].min(axis=1) - dist[:, ~one].min(axis=1)
     scale = 1.0 / noise_var if noise_var > 0 else 1.0
     return out * scale
+
+
+# --------------------------------------------------------------------------
+# receiver front end (zak.py:33-55, pilot.py:13-49) — SURVEY.md 8f row f1
+
+
+def zak_kernel(N: int, half_shift: bool = False) -> np.ndarray:
+    """kernel[i, l] = e^{-j2pi i l/N} / sqrt(N), optional (-1)^l columns (zak.py:33-47)."""
+    n = np.arange(N)
+    k = np.exp(-2j * np.pi * np.outer(n, n) / N) / np.sqrt(N)
+    if half_shift:
+        k = k * np.where(n % 2, -1.0, 1.0)[None, :]
+    return k
+
+
+def dzt_gemm(y: np.ndarray, M: int, N: int, kernel: np.ndarray | None = None) -> np.ndarray:
+    """Received samples (index k + i*M) -> (M, N) DD frame, one GEMM (zak.py:50-55)."""
+    kernel = zak_kernel(N) if kernel is None else kernel
+    return np.asarray(y).reshape(M, N, order="F") @ kernel
+
+
+def twist_kernel(M: int, N: int) -> np.ndarray:
+    """e^{-j2pi K0 (l - L0) / MN}, constant along delay (pilot.py:29-37)."""
+    l = np.arange(N)
+    return np.broadcast_to(np.exp(-2j * np.pi * (M // 2) * (l - N // 2) / (M * N)), (M, N))
+
+
+def estimate_heff(Y_dd: np.ndarray, M: int, N: int, amplitude: float | None = None) -> np.ndarray:
+    """Y_dd * twist / amplitude, amplitude defaulting to sqrt(MN) (pilot.py:13-15, 40-49)."""
+    amp = math.sqrt(M * N) if amplitude is None else amplitude
+    return Y_dd * twist_kernel(M, N) / amp
 
 
 # --------------------------------------------------------------------------

@@ -8,6 +8,7 @@ in include/ddb.h).  `SsCgaSolver` is the batched device API.
 
 from .batch import HostPipeline, PathBatch, SolveResult, SsCgaSolver, bits_per_symbol
 from .equalize import CgaConfig, CgaTrace, cga_equalize, get_precision, set_precision
+from .pilot import build_twist_kernel, default_pilot_amplitude, estimate_heff, make_pilot_frame
 from .grid import (
     Constellation,
     GridConfig,
@@ -33,6 +34,7 @@ from .sparse import (
     ss_mvm,
     ss_mvm_hermitian,
 )
+from .zak import build_zak_kernel, dzt_device, dzt_gemm
 
 __all__ = [
     "HostPipeline", "PathBatch", "SolveResult", "SsCgaSolver", "bits_per_symbol",
@@ -41,6 +43,8 @@ __all__ = [
     "make_constellation", "make_constellation_ext", "modulate", "unflatten",
     "DominantPath", "EmptyChannel", "StructuredSparseChannel", "build_ss_channel", "coefficient",
     "detect_paths", "forward_index", "inverse_index", "ss_mvm", "ss_mvm_hermitian",
+    "build_twist_kernel", "default_pilot_amplitude", "estimate_heff", "make_pilot_frame",
+    "build_zak_kernel", "dzt_device", "dzt_gemm",
 ]
 
 __version__ = "0.1.0"

@@ -55,6 +55,8 @@ class Outputs(C.Structure):
 
 
 ABI_VERSION = 2  # include/ddb.h DDB_ABI_VERSION
+DDB_DZT_COLMAJOR = 1
+DDB_DZT_PILOT = 2
 
 
 class Plan(C.Structure):
@@ -84,6 +86,10 @@ _SIGNATURES = {
                                   C.c_void_p, C.c_void_p]),
     "ddb_detect_paths": (C.c_int32, [C.c_int32, C.c_int32, C.c_int32, C.c_void_p, C.c_double, C.c_int32,
                                      C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
+    "ddb_dzt": (C.c_int32, [C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p, C.c_int32,
+                            C.c_double, C.c_void_p, C.c_void_p]),
+    "ddb_estimate_heff": (C.c_int32, [C.c_int64, C.c_int32, C.c_void_p, C.c_void_p, C.c_double, C.c_void_p,
+                                      C.c_void_p]),
     "ddb_probe_fp32": (C.c_int32, [C.c_int32, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p]),
     "ddb_sscga_profile_phases": (C.c_int32, [C.POINTER(Problem), C.POINTER(Outputs), C.c_void_p, C.c_void_p]),
 }

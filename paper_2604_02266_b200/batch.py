@@ -241,6 +241,64 @@ class SsCgaSolver:
                       "ddb_sscga_solve")
         return out
 
+    # -- receiver front end ---------------------------
+    def detect(self, pilot_rx: torch.Tensor, theta: float = 0.08, *, max_paths: int = 64,
+               amplitude: Optional[float] = None, stream=None) -> PathBatch:
+        """Taps of every frame from its received pilot frame, on the device.
+
+        pilot_rx: complex [B, M*N] time-domain samples of the point-pilot frame.
+        Zak transform fused with the pilot estimate (dzt_gemm + estimate_heff,
+        zak.py:50-55, pilot.py:40-49) in fp64, then detect_paths
+        (sparse.py:69-88); the result is the solver's CSR tap batch.  A frame
+        with more than max_paths taps raises (truncation would change the
+        operator); theta < 0 raises as in the reference.
+        """
+        from .zak import dzt_device
+        if theta < 0:
+            raise ValueError("theta must be nonnegative")
+        B = pilot_rx.shape[0]
+        amp = float(np.sqrt(self.MN)) if amplitude is None else float(amplitude)
+        heff = dzt_device(pilot_rx.to(device=self.device, dtype=torch.complex128), self.M, self.N,
+                          colmajor=False, pilot_amplitude=amp, stream=stream)
+        cnt = torch.empty(B, dtype=torch.int32, device=self.device)
+        kk = torch.empty(B, max_paths, dtype=torch.int32, device=self.device)
+        ll = torch.empty(B, max_paths, dtype=torch.int32, device=self.device)
+        gg = torch.empty(B, max_paths, dtype=torch.complex128, device=self.device)
+        nat.check(self.lib.ddb_detect_paths(B, self.M, self.N, _ptr(heff), float(theta), max_paths, _ptr(cnt),
+                                            _ptr(kk), _ptr(ll), _ptr(gg), _stream_handle(stream)),
+                  "ddb_detect_paths")
+        cmin, cmax = int(cnt.min().item()), int(cnt.max().item())
+        if cmin < 0:
+            raise nat.DdbError(nat.DDB_ERR_UNSUPPORTED, "ddb_detect_paths",
+                               "candidate list exceeds the per-frame shared-memory capacity")
+        if cmax > max_paths:
+            raise ValueError(f"a frame has {cmax} taps above threshold > max_paths={max_paths}")
+        # CSR by an exclusive scan of the counts (device tensors, no host round trip of taps)
+        off = torch.zeros(B + 1, dtype=torch.int32, device=self.device)
+        off[1:] = torch.cumsum(cnt, 0)
+        keep = torch.arange(max_paths, device=self.device)[None, :] < cnt[:, None]
+        k = kk[keep].contiguous()
+        l = ll[keep].contiguous()
+        g = gg[keep].to(self.cdtype).contiguous()
+        if k.numel() == 0:  # all frames empty: keep valid device pointers
+            k = torch.zeros(1, dtype=torch.int32, device=self.device)
+            l = torch.zeros(1, dtype=torch.int32, device=self.device)
+            g = torch.zeros(1, dtype=self.cdtype, device=self.device)
+        return PathBatch(off, k, l, g)
+
+    def receive(self, pilot_rx: torch.Tensor, data_rx: torch.Tensor, lam, theta: float = 0.08, *,
+                max_paths: int = 64, tx_labels: Optional[torch.Tensor] = None, llr: bool = False,
+                trace: bool = True, stream=None) -> SolveResult:
+        """The whole receiver of run_packet (harness.py:156-194) on the device for a batch:
+        pilot DZT + estimate + detect_paths -> taps; data DZT -> y_dd; fused SS-CGA
+        solve with hard decisions (and LLRs / bit errors).  data_rx: complex
+        [B, M*N] time-domain samples of the data frame."""
+        from .zak import dzt_device
+        paths = self.detect(pilot_rx, theta, max_paths=max_paths, stream=stream)
+        y = dzt_device(data_rx.to(device=self.device, dtype=self.cdtype), self.M, self.N, colmajor=True,
+                       stream=stream)
+        return self.solve(y, paths, lam, tx_labels=tx_labels, llr=llr, trace=trace, stream=stream)
+
     # -- matrix-free operator -------------------------------------------------
     def apply(self, v: torch.Tensor, paths: PathBatch, hermitian: bool = False,
               out: Optional[torch.Tensor] = None, stream=None) -> torch.Tensor:

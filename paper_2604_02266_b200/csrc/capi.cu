@@ -409,6 +409,40 @@ int32_t ddb_detect_paths(int32_t batch, int32_t M, int32_t N, const void* heff, 
   return ok();
 }
 
+int32_t ddb_dzt(int32_t batch, int32_t M, int32_t N, int32_t dtype, const void* y_time, const void* kernel,
+                int32_t flags, double amplitude, void* out, void* stream) {
+  if (batch < 0) return fail(DDB_ERR_INVALID, "negative batch");
+  if (dtype != DDB_F32 && dtype != DDB_F64) return fail(DDB_ERR_INVALID, "bad dtype %d", dtype);
+  if (M < 1 || N < 1) return fail(DDB_ERR_SHAPE, "grid must be positive, got (%d,%d)", M, N);
+  if ((long long)M * N >= (1LL << 29)) return fail(DDB_ERR_UNSUPPORTED, "grid too large");
+  if (N > 256) return fail(DDB_ERR_UNSUPPORTED, "N=%d > 256 (kernel matrix exceeds shared memory)", N);
+  if (flags & ~(DDB_DZT_COLMAJOR | DDB_DZT_PILOT)) return fail(DDB_ERR_INVALID, "bad flags %d", flags);
+  if ((flags & DDB_DZT_PILOT) && !(amplitude > 0))
+    return fail(DDB_ERR_INVALID, "pilot amplitude must be positive");  // pilot.py:45-46
+  if ((flags & DDB_DZT_PILOT) && ((M & 1) || (N & 1)))
+    return fail(DDB_ERR_SHAPE, "M and N must be even for the pilot estimate");  // grid.py:25-29
+  if (batch == 0) return ok();
+  if (!y_time || !out) return fail(DDB_ERR_INVALID, "null pointer");
+  cudaError_t e = ddb::launch_dzt(dtype == DDB_F64, batch, M, N, y_time, kernel, flags & DDB_DZT_COLMAJOR,
+                                  flags & DDB_DZT_PILOT, (flags & DDB_DZT_PILOT) ? amplitude : 1.0, out,
+                                  static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "dzt launch");
+  return ok();
+}
+
+int32_t ddb_estimate_heff(int64_t count, int32_t dtype, const void* y_dd, const void* twist, double amplitude,
+                          void* heff, void* stream) {
+  if (count < 0) return fail(DDB_ERR_INVALID, "negative count");
+  if (dtype != DDB_F32 && dtype != DDB_F64) return fail(DDB_ERR_INVALID, "bad dtype %d", dtype);
+  if (!(amplitude > 0)) return fail(DDB_ERR_INVALID, "pilot amplitude must be positive");  // pilot.py:45-46
+  if (count == 0) return ok();
+  if (!y_dd || !twist || !heff) return fail(DDB_ERR_INVALID, "null pointer");
+  cudaError_t e = ddb::launch_estimate_heff(dtype == DDB_F64, count, y_dd, twist, amplitude, heff,
+                                            static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "estimate_heff launch");
+  return ok();
+}
+
 int32_t ddb_probe_fp32(int32_t mode, int32_t blocks, int32_t iters, float* scratch, void* stream) {
   if ((mode != 0 && mode != 1) || blocks < 1 || iters < 1 || !scratch)
     return fail(DDB_ERR_INVALID, "bad probe arguments");

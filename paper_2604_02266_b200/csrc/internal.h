@@ -112,6 +112,13 @@ cudaError_t launch_detect_paths(int B, int M, int N, const void* heff, double th
                                 int max_paths, int* count, int* pk, int* pl, void* ph,
                                 cudaStream_t st);
 
+// Receiver front end (frontend.cu): Zak transform (+ fused pilot estimate),
+// elementwise pilot estimate on a DD frame.
+cudaError_t launch_dzt(int dtype_f64, int B, int M, int N, const void* y, const void* kern, int colmajor, int pilot,
+                       double amp, void* out, cudaStream_t st);
+cudaError_t launch_estimate_heff(int dtype_f64, long long count, const void* ydd, const void* twist, double amp,
+                                 void* heff, cudaStream_t st);
+
 // FP32 FMA throughput probe: blocks x 256 threads x iters x 256 FMAs.
 cudaError_t launch_fp32_probe(int mode, int blocks, int iters, float* out, cudaStream_t st);
 

@@ -11,8 +11,10 @@ the test modules import their names:
 Rebinds the names the reference binds at import time:
 ddlink.sparse.{detect_paths, build_ss_channel, ss_mvm, ss_mvm_hermitian,
 forward_index, inverse_index, coefficient}, ddlink.equalize.cga_equalize,
-ddlink.harness.cga_equalize (bound by name, harness.py:23), ddlink.grid.hard_demod
-and the package-level re-exports (__init__.py:14-63).  EmptyChannel stays the
+ddlink.harness.cga_equalize (bound by name, harness.py:23), ddlink.grid.hard_demod,
+the receiver front end ddlink.zak.dzt_gemm / ddlink.harness.dzt_gemm (bound by
+name, harness.py:24) and ddlink.pilot.estimate_heff (called through the module,
+harness.py:157), and the package-level re-exports (__init__.py:14-63).  EmptyChannel stays the
 reference's class so run_packet's handler (harness.py:170) still catches it.
 """
 
@@ -22,7 +24,9 @@ import importlib
 
 from . import equalize as _eq
 from . import grid as _gr
+from . import pilot as _pi
 from . import sparse as _sp
+from . import zak as _zk
 
 _SPARSE = ("detect_paths", "build_ss_channel", "ss_mvm", "ss_mvm_hermitian",
            "forward_index", "inverse_index", "coefficient")
@@ -35,6 +39,8 @@ def install(ddlink_module=None, precision: str = "fp64") -> dict:
     equalize = importlib.import_module(d.__name__ + ".equalize")
     grid = importlib.import_module(d.__name__ + ".grid")
     harness = importlib.import_module(d.__name__ + ".harness")
+    zak = importlib.import_module(d.__name__ + ".zak")
+    pilot = importlib.import_module(d.__name__ + ".pilot")
     _eq.set_precision(precision)
     _sp.EmptyChannel = sparse.EmptyChannel  # keep the reference's exception type
     saved = {}
@@ -51,6 +57,10 @@ def install(ddlink_module=None, precision: str = "fp64") -> dict:
     bind(d, "cga_equalize", _eq.cga_equalize)
     bind(grid, "hard_demod", _gr.hard_demod)
     bind(d, "hard_demod", _gr.hard_demod)
+    for mod in (zak, harness, d):
+        bind(mod, "dzt_gemm", _zk.dzt_gemm)
+    for mod in (pilot, d):
+        bind(mod, "estimate_heff", _pi.estimate_heff)
     return saved
 
 

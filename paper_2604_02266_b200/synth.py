@@ -67,7 +67,7 @@ def make_frames(solver: SsCgaSolver, B: int, snr_db: float = 25.0, nu_max_hz: fl
     gen = torch.Generator(device=dev)
     gen.manual_seed(seed)
     const = make_constellation_ext(modulation)
-    pts = torch.as_tensor(const.points, device=dev).to(solver.cdtype)
+    pts = torch.as_tensor(np.array(const.points), device=dev).to(solver.cdtype)
     labels = torch.randint(0, len(const.points), (B, solver.MN), generator=gen, device=dev, dtype=torch.int64)
     x = pts[labels].contiguous()
     paths = veha_paths(B, grid, nu_max_hz, gen, dev, solver.cdtype, n_paths)

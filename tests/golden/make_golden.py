@@ -272,13 +272,66 @@ def detect_fixture(d):
     np.savez_compressed(OUT / "detect.npz", **out)
 
 
+def frontend_fixture(d):
+    """Receiver front end: run_packet's time-domain pilot
+    and data frames with the reference's dzt_gemm / estimate_heff /
+    detect_paths outputs and the full receive (harness.py:141-194), on the
+    unrounded fp64 data path."""
+    from ddlink.harness import Workspace
+    out = {}
+    cases = [("c1", 64, 16, "qpsk", 25.0, 300.0, 0.08, 31, 3), ("c3", 512, 32, "qam16", 25.0, 100.0, 0.08, 33, 1)]
+    for tag, M, N, mod, snr, nu, theta, seed, count in cases:
+        cfg = d.SimConfig(m=M, n=N, mod=mod, snr_db=snr, nu_max_hz=nu, theta=theta, iters=10, packets=count,
+                          seed=seed)
+        ws = Workspace(cfg)
+        grid, const = ws.grid, ws.const
+        rec = {k: [] for k in ("pilot_rx", "data_rx", "ypil", "heff", "y", "tx", "rx", "x", "taps")}
+        for idx in range(count):
+            rng = np.random.default_rng([seed, idx])
+            pset = d.draw_veha(cfg.nu_max_hz, grid, rng)
+            tx_bits = rng.integers(0, 2, size=const.bits_per_symbol * grid.size)
+            data_tx = d.idzt(d.modulate(tx_bits, const, grid), grid)
+            pilot_rx = d.add_awgn(d.apply_channel(ws.pilot_tx, pset, grid), cfg.snr_db, rng)
+            data_rx = d.add_awgn(d.apply_channel(data_tx, pset, grid), cfg.snr_db, rng)
+            ypil = d.dzt_gemm(pilot_rx, ws.zak_kernel, grid)
+            heff = d.estimate_heff(ypil, ws.twist, grid)
+            taps = d.detect_paths(heff, cfg.theta, grid)
+            y = d.flatten(d.dzt_gemm(data_rx, ws.zak_kernel, grid), grid)
+            lam = 1.0 / cfg.snr_linear
+            x, _ = d.cga_equalize(d.build_ss_channel(taps, grid), y, d.CgaConfig(iterations=cfg.iters, lam=lam))
+            _, rx_bits = d.hard_demod(d.unflatten(x, grid), const, grid)
+            for key, v in (("pilot_rx", pilot_rx), ("data_rx", data_rx), ("ypil", ypil), ("heff", heff), ("y", y),
+                           ("tx", tx_bits), ("rx", rx_bits), ("x", x), ("taps", taps)):
+                rec[key].append(v)
+        b = const.bits_per_symbol
+        wts = 1 << np.arange(b - 1, -1, -1)
+        off, k, l, g = pack_taps(rec["taps"])
+        out[tag + "_meta"] = np.array([M, N, 10, b], np.int64)
+        out[tag + "_theta"] = np.array(theta)
+        out[tag + "_lam"] = np.full(count, 1.0 / cfg.snr_linear)
+        for key in ("pilot_rx", "data_rx", "ypil", "heff", "y"):
+            out[f"{tag}_{key}"] = np.stack(rec[key])
+        out[tag + "_x"] = np.stack(rec["x"]).astype(np.complex64)
+        out[tag + "_tx_labels"] = np.stack([t.reshape(-1, b) @ wts for t in rec["tx"]]).astype(np.uint8)
+        out[tag + "_rx_labels"] = np.stack([t.reshape(-1, b) @ wts for t in rec["rx"]]).astype(np.uint8)
+        out[tag + "_path_off"], out[tag + "_path_k"], out[tag + "_path_l"], out[tag + "_path_g"] = off, k, l, g
+        # the reference kernel / twist tables and one half-shift kernel case for dzt_gemm
+        out[tag + "_ypil_half"] = d.dzt_gemm(rec["pilot_rx"][0], d.build_zak_kernel(N, half_shift=True), grid)
+    np.savez_compressed(OUT / "frontend.npz", **out)
+
+
 def main():
     d = _ref()
+    if len(sys.argv) > 1:  # regenerate selected fixtures only, e.g. `make_golden.py frontend`
+        for name in sys.argv[1:]:
+            globals()[f"{name}_fixture"](d)
+        return
     tables_fixture(d)
     cga_fixture(d)
     demod_fixture(d)
     detect_fixture(d)
     frames_fixtures(d)
+    frontend_fixture(d)
     for p in sorted(OUT.glob("*.npz")):
         print(f"{p.name:24s} {p.stat().st_size / 1024:8.1f} KiB")
 

@@ -456,3 +456,81 @@ def test_host_pipeline_matches_device_solve(pkg):
              pin(fb.lam), pin(fb.tx_labels), labels, errs)
     assert torch.equal(labels, ref.labels.cpu())
     assert torch.equal(errs, ref.bit_errors.cpu())
+
+
+# ---------------------------------------------------------------- receiver front end (row f1)
+class TestFrontEnd:
+    """ddb_dzt / ddb_estimate_heff / the batched device receiver against the
+    reference's outputs (tests/golden/frontend.npz) and the oracle."""
+
+    @pytest.mark.parametrize("tag", ["c1", "c3"])
+    def test_drop_in_dzt_and_estimate(self, pkg, tag):
+        from paper_2604_02266_b200 import pilot, zak
+        d = load_golden("frontend")
+        M, N, _, _ = (int(v) for v in d[tag + "_meta"])
+        g = pkg.GridConfig(M, N)
+        K = zak.build_zak_kernel(N)
+        for i in range(d[tag + "_pilot_rx"].shape[0]):
+            yp = zak.dzt_gemm(d[tag + "_pilot_rx"][i], K, g)
+            np.testing.assert_allclose(yp, d[tag + "_ypil"][i], rtol=0, atol=1e-12)
+            h = pilot.estimate_heff(yp, pilot.build_twist_kernel(g), g)
+            np.testing.assert_allclose(h, d[tag + "_heff"][i], rtol=0, atol=1e-13)
+        half = zak.dzt_gemm(d[tag + "_pilot_rx"][0], zak.build_zak_kernel(N, half_shift=True), g)
+        np.testing.assert_allclose(half, d[tag + "_ypil_half"], rtol=0, atol=1e-12)
+        with pytest.raises(ValueError):
+            zak.dzt_gemm(d[tag + "_pilot_rx"][0][:-1], K, g)
+        with pytest.raises(ValueError):
+            pilot.estimate_heff(yp, pilot.build_twist_kernel(g), g, amplitude=0.0)
+
+    @pytest.mark.parametrize("tag", ["c1", "c3"])
+    @pytest.mark.parametrize("precision", ["fp32", "fp64"])
+    def test_batched_dzt(self, pkg, tag, precision):
+        from paper_2604_02266_b200.zak import dzt_device
+        d = load_golden("frontend")
+        M, N, _, _ = (int(v) for v in d[tag + "_meta"])
+        cd = torch.complex128 if precision == "fp64" else torch.complex64
+        yt = torch.as_tensor(d[tag + "_data_rx"], device="cuda").to(cd)
+        y = dzt_device(yt, M, N, colmajor=True).cpu().numpy()
+        ref = d[tag + "_y"]
+        tol = 1e-12 if precision == "fp64" else 2e-6
+        for i in range(ref.shape[0]):
+            assert rel_l2(y[i], ref[i]) < tol
+        hp = dzt_device(torch.as_tensor(d[tag + "_pilot_rx"], device="cuda").to(cd), M, N, colmajor=False,
+                        pilot_amplitude=float(np.sqrt(M * N))).cpu().numpy()
+        for i in range(ref.shape[0]):
+            assert rel_l2(hp[i], d[tag + "_heff"][i].reshape(-1)) < tol
+
+    @pytest.mark.parametrize("tag", ["c1", "c3"])
+    def test_device_detect_matches_reference_taps(self, pkg, tag):
+        d = load_golden("frontend")
+        M, N, iters, b = (int(v) for v in d[tag + "_meta"])
+        s = solver_for(pkg, M, N, iters, "fp32", b)
+        paths = s.detect(torch.as_tensor(d[tag + "_pilot_rx"], device="cuda"), float(d[tag + "_theta"]))
+        np.testing.assert_array_equal(paths.offsets.cpu().numpy(), d[tag + "_path_off"])
+        np.testing.assert_array_equal(paths.k.cpu().numpy(), d[tag + "_path_k"])
+        np.testing.assert_array_equal(paths.l.cpu().numpy(), d[tag + "_path_l"])
+        np.testing.assert_allclose(paths.gain.cpu().numpy(), d[tag + "_path_g"], rtol=1e-6, atol=1e-7)
+        with pytest.raises(ValueError):
+            s.detect(torch.as_tensor(d[tag + "_pilot_rx"], device="cuda"), -0.1)
+
+    @pytest.mark.parametrize("tag", ["c1", "c3"])
+    def test_device_receiver_end_to_end(self, pkg, tag, fp32_kernel):
+        """run_packet's receiver (harness.py:156-194) from time-domain pilot and data
+        frames, entirely on the device, vs the reference's x_hat and decisions."""
+        d = load_golden("frontend")
+        M, N, iters, b = (int(v) for v in d[tag + "_meta"])
+        const = orc.qam({2: "qpsk", 4: "qam16"}[b])
+        s = solver_for(pkg, M, N, iters, "fp32", b)
+        tx = torch.as_tensor(d[tag + "_tx_labels"], device="cuda")
+        res = s.receive(torch.as_tensor(d[tag + "_pilot_rx"], device="cuda"),
+                        torch.as_tensor(d[tag + "_data_rx"], device="cuda"), torch.as_tensor(d[tag + "_lam"]),
+                        float(d[tag + "_theta"]), tx_labels=tx, llr=True)
+        x = res.x.cpu().numpy()
+        labels = res.labels.cpu().numpy()
+        for f in range(x.shape[0]):
+            xr = d[tag + "_x"][f].astype(np.complex128)
+            assert rel_l2(x[f], xr) < REL_L2_FP32
+            mism = labels[f] != d[tag + "_rx_labels"][f]
+            assert np.all(orc.decision_margin(xr, const)[mism] < TIE_BAND)
+            want = int(np.unpackbits((labels[f] ^ d[tag + "_tx_labels"][f])[:, None], axis=1).sum())
+            assert int(res.bit_errors[f]) == want

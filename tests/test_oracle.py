@@ -156,3 +156,27 @@ def test_frames_reproduce_reference(name):
         assert np.linalg.norm(x - ref) <= 1e-9 * np.linalg.norm(ref)
         np.testing.assert_allclose(tr.c_norm, d["c_norm"][f], rtol=1e-9)
         np.testing.assert_array_equal(lab, d["rx_labels"][f])
+
+
+class TestFrontEnd:
+    """Receiver front end pinned to the reference's own
+    dzt_gemm / estimate_heff / detect_paths outputs (tests/golden/frontend.npz)."""
+
+    @pytest.mark.parametrize("tag", ["c1", "c3"])
+    def test_dzt_estimate_detect(self, tag):
+        d = load_golden("frontend")
+        M, N, _, _ = (int(v) for v in d[tag + "_meta"])
+        theta = float(d[tag + "_theta"])
+        off = d[tag + "_path_off"]
+        for i in range(d[tag + "_pilot_rx"].shape[0]):
+            yp = orc.dzt_gemm(d[tag + "_pilot_rx"][i], M, N)
+            np.testing.assert_allclose(yp, d[tag + "_ypil"][i], rtol=0, atol=1e-12)
+            h = orc.estimate_heff(yp, M, N)
+            np.testing.assert_allclose(h, d[tag + "_heff"][i], rtol=0, atol=1e-13)
+            taps = orc.detect_paths(h, theta)
+            a, e = int(off[i]), int(off[i + 1])
+            assert [(t.k, t.l) for t in taps] == list(zip(d[tag + "_path_k"][a:e], d[tag + "_path_l"][a:e]))
+            y = orc.to_vector(orc.dzt_gemm(d[tag + "_data_rx"][i], M, N))
+            np.testing.assert_allclose(y, d[tag + "_y"][i], rtol=0, atol=1e-12)
+        half = orc.dzt_gemm(d[tag + "_pilot_rx"][0], M, N, orc.zak_kernel(N, half_shift=True))
+        np.testing.assert_allclose(half, d[tag + "_ypil_half"], rtol=0, atol=1e-12)

@@ -27,6 +27,8 @@ def test_install_and_uninstall(ddlink):
         assert ddlink.sparse.build_ss_channel is b200.build_ss_channel
         assert ddlink.grid.hard_demod is b200.hard_demod
         assert ddlink.detect_paths is b200.detect_paths
+        assert ddlink.harness.dzt_gemm is b200.dzt_gemm and ddlink.zak.dzt_gemm is b200.dzt_gemm
+        assert ddlink.pilot.estimate_heff is b200.estimate_heff
         # the reference's EmptyChannel is what the drop-in raises (harness.py:170)
         with pytest.raises(ddlink.EmptyChannel):
             b200.build_ss_channel([], ddlink.GridConfig(8, 4))
@@ -35,3 +37,4 @@ def test_install_and_uninstall(ddlink):
         import paper_2604_02266_b200.sparse as sp
         sp.EmptyChannel = b200.EmptyChannel
     assert ddlink.harness.cga_equalize is orig_cga
+    assert ddlink.harness.dzt_gemm is not b200.dzt_gemm
