@@ -320,6 +320,42 @@ def frontend_fixture(d):
     np.savez_compressed(OUT / "frontend.npz", **out)
 
 
+def harness_fixture(d):
+    """Acceptance criterion 6 of the reference (tests/test_acceptance.py:179-192):
+    run_packets(SimConfig(m=32, n=32, packets=200, seed=11)), i.e. 200 QPSK
+    packets at 25 dB, nu_max 100 Hz, theta 0.08, Xi 10.  Stores every packet's
+    time-domain pilot and data frames in run_packet's draw order
+    (harness.py:141-149), the TX labels, and the reference's own per-packet
+    results from run_packets, so the device receiver can be scored against
+    the reference's BER known answer (3.491e-4, test_output.txt:234)."""
+    from ddlink.harness import Workspace
+    cfg = d.SimConfig(m=32, n=32, packets=200, seed=11)
+    ws = Workspace(cfg)
+    grid, const = ws.grid, ws.const
+    pil, dat, tx = [], [], []
+    for idx in range(cfg.packets):
+        rng = np.random.default_rng([cfg.seed, idx])
+        pset = d.draw_veha(cfg.nu_max_hz, grid, rng)
+        tx_bits = rng.integers(0, 2, size=const.bits_per_symbol * grid.size)
+        data_tx = d.idzt(d.modulate(tx_bits, const, grid), grid)
+        pil.append(d.add_awgn(d.apply_channel(ws.pilot_tx, pset, grid), cfg.snr_db, rng))
+        dat.append(d.add_awgn(d.apply_channel(data_tx, pset, grid), cfg.snr_db, rng))
+        tx.append(tx_bits)
+    res = d.run_packets(cfg)
+    b = const.bits_per_symbol
+    wts = 1 << np.arange(b - 1, -1, -1)
+    np.savez_compressed(
+        OUT / "harness_c6.npz",
+        meta=np.array([cfg.m, cfg.n, cfg.iters, b, cfg.packets], np.int64),
+        snr_db=np.array(cfg.snr_db), theta=np.array(cfg.theta),
+        pilot_rx=np.stack(pil), data_rx=np.stack(dat),
+        tx_labels=np.stack([t.reshape(-1, b) @ wts for t in tx]).astype(np.uint8),
+        bit_errors=np.array([r.bit_errors for r in res], np.int64),
+        failed=np.array([r.failed for r in res], bool),
+        ber=np.array([r.ber for r in res]),
+    )
+
+
 def main():
     d = _ref()
     if len(sys.argv) > 1:  # regenerate selected fixtures only, e.g. `make_golden.py frontend`
@@ -332,6 +368,7 @@ def main():
     detect_fixture(d)
     frames_fixtures(d)
     frontend_fixture(d)
+    harness_fixture(d)
     for p in sorted(OUT.glob("*.npz")):
         print(f"{p.name:24s} {p.stat().st_size / 1024:8.1f} KiB")
 

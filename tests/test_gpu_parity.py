@@ -534,3 +534,26 @@ class TestFrontEnd:
             assert np.all(orc.decision_margin(xr, const)[mism] < TIE_BAND)
             want = int(np.unpackbits((labels[f] ^ d[tag + "_tx_labels"][f])[:, None], axis=1).sum())
             assert int(res.bit_errors[f]) == want
+
+
+# ---------------------------------------------------------------- harness known answer (row f3)
+@pytest.mark.parametrize("precision", ["fp64", "fp32"])
+def test_acceptance_criterion6_ber_known_answer(pkg, precision):
+    """The reference's acceptance criterion 6 run (tests/test_acceptance.py:179-192:
+    200 QPSK packets at (32, 32), 25 dB, seed 11) received entirely on the device
+    from its time-domain pilot and data frames, batch of 200: the mean BER is the
+    reference's published 3.491e-4 (143 bit errors, test_output.txt:234)."""
+    d = load_golden("harness_c6")
+    M, N, iters, b, P = (int(v) for v in d["meta"])
+    s = solver_for(pkg, M, N, iters, precision, b)
+    lam = 1.0 / 10 ** (float(d["snr_db"]) / 10)
+    res = s.receive(torch.as_tensor(d["pilot_rx"], device="cuda"), torch.as_tensor(d["data_rx"], device="cuda"),
+                    lam, float(d["theta"]), tx_labels=torch.as_tensor(d["tx_labels"], device="cuda"))
+    errs = res.bit_errors.cpu().numpy().astype(np.int64)
+    failed = (res.status.cpu().numpy() & 1).astype(bool)
+    np.testing.assert_array_equal(failed, d["failed"])
+    if precision == "fp64":
+        np.testing.assert_array_equal(errs, d["bit_errors"])
+        assert abs(errs.mean() / (b * M * N) - 3.491e-4) < 5e-8
+    else:  # fp32 decisions may differ only inside the fp64 tie band: a handful of bits at most
+        assert abs(int(errs.sum()) - int(d["bit_errors"].sum())) <= 3

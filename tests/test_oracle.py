@@ -180,3 +180,22 @@ class TestFrontEnd:
             np.testing.assert_allclose(y, d[tag + "_y"][i], rtol=0, atol=1e-12)
         half = orc.dzt_gemm(d[tag + "_pilot_rx"][0], M, N, orc.zak_kernel(N, half_shift=True))
         np.testing.assert_allclose(half, d[tag + "_ypil_half"], rtol=0, atol=1e-12)
+
+
+def test_oracle_receiver_reproduces_criterion6():
+    """The oracle's receive chain (dzt_gemm -> estimate_heff -> detect_paths ->
+    tables -> CG -> hard_demod) on the stored criterion-6 packets gives the
+    reference run_packets' per-packet bit errors (143 in 200 packets)."""
+    d = load_golden("harness_c6")
+    M, N, iters, b, P = (int(v) for v in d["meta"])
+    const = orc.qam("qpsk")
+    lam = 1.0 / 10 ** (float(d["snr_db"]) / 10)
+    errs = []
+    for i in range(P):
+        h = orc.estimate_heff(orc.dzt_gemm(d["pilot_rx"][i], M, N), M, N)
+        taps = orc.detect_paths(h, float(d["theta"]))
+        y = orc.to_vector(orc.dzt_gemm(d["data_rx"][i], M, N))
+        _, _, lab, _ = orc.receive(taps, y, M, N, iters, lam, const)
+        diff = (lab ^ d["tx_labels"][i]).astype(np.uint8)
+        errs.append(int(np.unpackbits(diff[:, None], axis=1).sum()))
+    np.testing.assert_array_equal(np.array(errs), d["bit_errors"])
