@@ -60,6 +60,8 @@ def parse():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-latency", action="store_true")
     ap.add_argument("--no-frontend", action="store_true")
+    ap.add_argument("--e2e-chunk", type=int, default=444, help="frames per HostPipeline chunk (6 waves of 74 clusters)")
+    ap.add_argument("--e2e-depth", type=int, default=2)
     ap.add_argument("--lat-runs", type=int, default=2000)
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     return ap.parse_args()
@@ -414,7 +416,7 @@ def main():
     # ---- end to end from pinned host buffers (HostPipeline)
     e2e = None
     if not args.no_e2e:
-        pipe = pkg.HostPipeline(s, chunk=512, depth=2)
+        pipe = pkg.HostPipeline(s, chunk=args.e2e_chunk, depth=args.e2e_depth)
         hy = fb.y.cpu().pin_memory()
         hl = fb.lam.cpu().pin_memory()
         ht = fb.tx_labels.cpu().pin_memory()

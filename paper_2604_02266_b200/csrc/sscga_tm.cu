@@ -262,8 +262,9 @@ __device__ __forceinline__ void mvm_local(const SolveArgs& a, const TmThr& th, c
   for (int i = 0; i < R; ++i) acc[i] = 0ull;
   if (fs.masks) {
     const uint32_t* mk = fs.mk[th.jr / R] + (HERM ? 3 : 0);
-    tmem_taps<R, HERM>(th.jr, sm, tv, mk[0], acc);
-    for (uint32_t m = mk[1]; m; m &= m - 1) {
+    const uint32_t mt = mk[0], ms = mk[1];
+    tmem_taps<R, HERM>(th.jr, sm, tv, mt, acc);
+    for (uint32_t m = ms; m; m &= m - 1) {
       const PathEnt<float>& e = sm.ptab[__ffs(m) - 1];
       const int s = HERM ? -e.dk : e.dk;
       const ulonglong2 g = gain_pairs<HERM>(e);
@@ -560,11 +561,14 @@ __global__ void __launch_bounds__(MAXT, 1) sscga_tm_kernel(const SolveArgs a) {
     if (fs.masks && tid < a.WQ) {  // thread j classifies the taps for row block j
       uint32_t mk[6] = {0u, 0u, 0u, 0u, 0u, 0u};
       const bool halo = fs.halo;
+      int nf = 0, nh = 0;  // TMEM-run taps so far (capped at a.tmcap per direction)
       for (int p = 0; p < P; ++p) {
         const PathEnt<float>& e = sm.ptab[p];
         const uint32_t bit = 1u << p;
-        const int cf = tap_class<R, false>(a, tid * R, halo, e);
-        const int ch = tap_class<R, true>(a, tid * R, halo, e);
+        int cf = tap_class<R, false>(a, tid * R, halo, e);
+        int ch = tap_class<R, true>(a, tid * R, halo, e);
+        if (cf == 0 && a.tmcap > 0 && nf++ >= a.tmcap) cf = halo ? 1 : 2;
+        if (ch == 0 && a.tmcap > 0 && nh++ >= a.tmcap) ch = halo ? 1 : 2;
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
           mk[c] |= cf == c ? bit : 0u;
