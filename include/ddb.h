@@ -100,7 +100,8 @@ typedef struct {
   int32_t smem_bytes;        /* dynamic shared memory per CTA                       */
   int32_t ctas_per_sm;       /* occupancy reported by the CUDA runtime (0 on CPU)   */
   int32_t halo_rows;         /* quasi-periodic extension rows kept around c and u   */
-  int32_t kernel;            /* 0: row-slice kernel, 1: TMEM-operand kernel (fp32)  */
+  int32_t kernel;            /* 0: row-slice kernel, 1: TMEM-operand kernel (fp32),
+                                2: workspace-backed kernels (grids beyond a cluster) */
   int32_t rows_per_thread;   /* delay rows per thread (TMEM-operand kernel), else 1 */
 } ddb_plan;
 
@@ -111,6 +112,11 @@ const char* ddb_build_info(void);
 
 /* ---- planning / workspace ----------------------------------------------- */
 int32_t ddb_sscga_plan(int32_t M, int32_t N, int32_t dtype, ddb_plan* out);
+/* Bytes of device workspace ddb_sscga_solve needs for this problem: 0 for the
+ * fused kernels (all CG state on chip); for grids beyond a 16-CTA cluster's
+ * on-chip memory (e.g. the paper's 16384 x 32) the c, u, p vectors of every
+ * frame plus per-block partials.  Pass it as `workspace` (DDB_ERR_WORKSPACE
+ * if missing or too small). */
 size_t ddb_sscga_workspace_bytes(const ddb_sscga_problem* prob);
 
 /* ---- fused solve: coefficients on the fly + fixed-Xi CG + demod ---------- */

@@ -156,7 +156,7 @@ class SsCgaSolver:
         return {"cluster": p.cluster, "cols_per_cta": p.cols_per_cta,
                 "cols_per_thread": p.cols_per_thread, "threads": p.threads,
                 "smem_bytes": p.smem_bytes, "ctas_per_sm": p.ctas_per_sm, "halo_rows": p.halo_rows,
-                "kernel": "tmem" if p.kernel == 1 else "rows", "rows_per_thread": p.rows_per_thread}
+                "kernel": {0: "rows", 1: "tmem", 2: "workspace"}[p.kernel], "rows_per_thread": p.rows_per_thread}
 
     # -- buffers -------------------------------------------------------------
     def alloc(self, B: int, *, llr: bool = False, labels: bool = True, trace: bool = True,
@@ -237,9 +237,21 @@ class SsCgaSolver:
             nat.check(self.lib.ddb_sscga_profile_phases(C.byref(prob), C.byref(outs), _ptr(phase_cycles),
                                                         _stream_handle(stream)), "ddb_sscga_profile_phases")
         else:
-            nat.check(self.lib.ddb_sscga_solve(C.byref(prob), C.byref(outs), None, 0, _stream_handle(stream)),
-                      "ddb_sscga_solve")
+            ws_bytes = int(self.lib.ddb_sscga_workspace_bytes(C.byref(prob)))
+            ws = self._workspace(ws_bytes)
+            nat.check(self.lib.ddb_sscga_solve(C.byref(prob), C.byref(outs), _ptr(ws), ws_bytes,
+                                               _stream_handle(stream)), "ddb_sscga_solve")
         return out
+
+    def _workspace(self, nbytes: int) -> Optional[torch.Tensor]:
+        """Device workspace of the workspace-backed path (grown, never shrunk)."""
+        if nbytes == 0:
+            return None
+        ws = getattr(self, "_ws", None)
+        if ws is None or ws.numel() < nbytes:
+            ws = torch.empty(nbytes, dtype=torch.uint8, device=self.device)
+            self._ws = ws
+        return ws
 
     # -- receiver front end (SURVEY.md §8f row f1) ---------------------------
     def detect(self, pilot_rx: torch.Tensor, theta: float = 0.08, *, max_paths: int = 64,

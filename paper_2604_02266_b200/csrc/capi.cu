@@ -128,11 +128,26 @@ bool make_plan_tm(int32_t M, int32_t N, ddb::LaunchShape* s) {
   return false;
 }
 
+// Workspace-backed kernels (sscga_global.cu): any grid; the CG vectors live in
+// a caller-provided workspace (ddb_sscga_workspace_bytes).
+int32_t plan_global(int32_t M, int32_t N, ddb::LaunchShape* s) {
+  *s = ddb::LaunchShape{};
+  s->kind = 2;
+  s->cluster = 1;
+  s->lcta = N;
+  s->lc = 1;
+  s->threads = 256;
+  ddb::twiddle_split(M * N, &s->tl, &s->th);
+  return DDB_OK;
+}
+
 // Smallest cluster whose CTAs can hold their column slice of p, u and x in
 // shared memory; then the widest per-thread column run that keeps at least
 // 256 threads per CTA within the register file.
 int32_t make_plan(int32_t M, int32_t N, int32_t dtype, ddb::LaunchShape* s) {
   *s = ddb::LaunchShape{};
+  const char* env_k = getenv("DDB_KERNEL");
+  if (env_k && env_k[0] == 'g') return plan_global(M, N, s);  // DDB_KERNEL=global (tests / A-B)
   if (dtype == DDB_F32 && make_plan_tm(M, N, s)) return DDB_OK;
   const int eb = dtype == DDB_F64 ? 8 : 4;
   const int cap = smem_optin();
@@ -189,9 +204,7 @@ int32_t make_plan(int32_t M, int32_t N, int32_t dtype, ddb::LaunchShape* s) {
       return DDB_OK;
     }
   }
-  return fail(DDB_ERR_UNSUPPORTED,
-              "grid (%d,%d) %s: CG state does not fit a 16-CTA cluster's shared memory", M, N,
-              dtype == DDB_F64 ? "fp64" : "fp32");
+  return plan_global(M, N, s);
 }
 
 }  // namespace
@@ -230,7 +243,8 @@ int32_t ddb_sscga_plan(int32_t M, int32_t N, int32_t dtype, ddb_plan* out) {
   int n = 0;
   int dev_count = 0;
   if (cudaGetDeviceCount(&dev_count) == cudaSuccess && dev_count > 0) {
-    cudaError_t e = s.kind == 1          ? ddb::sscga_tm_occupancy(s, &n)
+    cudaError_t e = s.kind == 2          ? (n = 0, cudaSuccess)
+                    : s.kind == 1        ? ddb::sscga_tm_occupancy(s, &n)
                     : dtype == DDB_F64 ? ddb::sscga_occupancy<double>(s, &n)
                                        : ddb::sscga_occupancy<float>(s, &n);
     if (e == cudaSuccess) out->ctas_per_sm = n;
@@ -240,12 +254,16 @@ int32_t ddb_sscga_plan(int32_t M, int32_t N, int32_t dtype, ddb_plan* out) {
 }
 
 size_t ddb_sscga_workspace_bytes(const ddb_sscga_problem* prob) {
-  (void)prob;
-  return 0;  // the fused solve keeps all state on chip
+  if (!prob || prob->batch <= 0 || (prob->dtype != DDB_F32 && prob->dtype != DDB_F64)) return 0;
+  if (check_grid(prob->M, prob->N)) return 0;
+  ddb::LaunchShape s;
+  if (make_plan(prob->M, prob->N, prob->dtype, &s)) return 0;
+  // the fused kernels keep all CG state on chip; the workspace path keeps c, u, p in HBM
+  return s.kind == 2 ? ddb::sscga_global_workspace(prob->dtype == DDB_F64, prob->batch, prob->M, prob->N) : 0;
 }
 
 static int32_t solve_impl(const ddb_sscga_problem* prob, const ddb_sscga_outputs* out, long long* prof,
-                          void* stream) {
+                          void* workspace, size_t workspace_bytes, void* stream) {
   if (!prob || !out) return fail(DDB_ERR_INVALID, "null problem/outputs");
   if (prob->batch < 0) return fail(DDB_ERR_INVALID, "negative batch");
   if (prob->iterations < 1) return fail(DDB_ERR_INVALID, "need at least one iteration");  // equalize.py:26-27
@@ -309,7 +327,16 @@ static int32_t solve_impl(const ddb_sscga_problem* prob, const ddb_sscga_outputs
   a.berr = out->bit_errors;
   a.prof = prof;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  cudaError_t e = s.kind == 1                ? ddb::launch_sscga_tm(a, s, st)
+  if (s.kind == 2) {
+    const size_t need = ddb::sscga_global_workspace(prob->dtype == DDB_F64, a.B, a.M, a.N);
+    if (!workspace || workspace_bytes < need)
+      return fail(DDB_ERR_WORKSPACE, "grid (%d,%d) needs a %zu-byte workspace (ddb_sscga_workspace_bytes), got %zu",
+                  a.M, a.N, need, workspace ? workspace_bytes : (size_t)0);
+    if (prof) return fail(DDB_ERR_UNSUPPORTED, "phase profiling is a fused-kernel feature");
+  }
+  cudaError_t e = s.kind == 2                ? (prob->dtype == DDB_F64 ? ddb::launch_sscga_global<double>(a, workspace, st)
+                                                                       : ddb::launch_sscga_global<float>(a, workspace, st))
+                  : s.kind == 1              ? ddb::launch_sscga_tm(a, s, st)
                   : prob->dtype == DDB_F64 ? ddb::launch_sscga<double>(a, s, st)
                                            : ddb::launch_sscga<float>(a, s, st);
   if (e != cudaSuccess) return cuda_fail(e, "sscga launch");
@@ -318,15 +345,13 @@ static int32_t solve_impl(const ddb_sscga_problem* prob, const ddb_sscga_outputs
 
 int32_t ddb_sscga_solve(const ddb_sscga_problem* prob, const ddb_sscga_outputs* out, void* workspace,
                         size_t workspace_bytes, void* stream) {
-  (void)workspace;
-  (void)workspace_bytes;
-  return solve_impl(prob, out, nullptr, stream);
+  return solve_impl(prob, out, nullptr, workspace, workspace_bytes, stream);
 }
 
 int32_t ddb_sscga_profile_phases(const ddb_sscga_problem* prob, const ddb_sscga_outputs* out,
                                  long long* phase_cycles, void* stream) {
   if (!phase_cycles) return fail(DDB_ERR_INVALID, "null phase buffer");
-  return solve_impl(prob, out, phase_cycles, stream);
+  return solve_impl(prob, out, phase_cycles, nullptr, 0, stream);
 }
 
 int32_t ddb_ss_apply(const ddb_sscga_problem* prob, void* outp, int32_t hermitian, void* stream) {

@@ -49,7 +49,8 @@ constexpr int kProfPhases = 12;
 
 struct LaunchShape {
   int cluster, lcta, lc, threads, smem, halo, tl, th, pcap, tcols;
-  int kind;        // 0: row-slice kernel (sscga.cu), 1: TMEM-operand kernel (sscga_tm.cu)
+  int kind;        // 0: row-slice kernel (sscga.cu), 1: TMEM-operand kernel (sscga_tm.cu),
+                   // 2: workspace-backed kernels (sscga_global.cu)
   int g, wq, rows, cs;  // kind 1: segment rows, warps per lane quarter, rows per thread, column stride
   int tmcap;            // kind 1: TMEM-run taps per warp and MVM (0: all eligible)
 };
@@ -91,6 +92,12 @@ cudaError_t launch_sscga(SolveArgs a, const LaunchShape& s, cudaStream_t st);
 SmemLayout sscga_tm_layout(int M, int Lcta, int N, int CS, int TL, int TH, int pcap);
 cudaError_t launch_sscga_tm(SolveArgs a, const LaunchShape& s, cudaStream_t st);
 cudaError_t sscga_tm_occupancy(const LaunchShape& s, int* ctas_per_sm);
+
+// Workspace-backed path for grids beyond a cluster's on-chip memory (sscga_global.cu).
+size_t align_up(size_t v, size_t a);
+size_t sscga_global_workspace(int dtype_f64, int B, int M, int N);
+template <typename T>
+cudaError_t launch_sscga_global(const SolveArgs& a, void* workspace, cudaStream_t st);
 
 template <typename T>
 cudaError_t sscga_occupancy(const LaunchShape& s, int* ctas_per_sm);

@@ -1,0 +1,420 @@
+// SS-CGA for grids whose CG state does not fit a cluster's on-chip memory
+// (e.g. the paper's (16384, 32): 4 MB per complex64 vector).  Same algorithm
+// as the fused kernels (cga_equalize, equalize.py:43-77, u-recurrence form,
+// matrix-free operator of sparse.py:91-160), with the CG vectors c, u, p in a
+// caller-provided workspace and x in the output buffer, one kernel per CG
+// phase over all frames of the batch:
+//
+//   init:  b = H^H y -> c, x = 0, block partials of ||c||^2
+//   fold:  per-frame deterministic sum of the block partials -> scalars
+//   fwd:   u = H c + beta u, p = c + beta p, partials (||u||^2, ||p||^2)
+//   herm:  ap = H^H u + lam p, x += alpha p, c -= alpha ap, partials ||c||^2
+//   demod: hard labels, max-log LLRs, bit errors from x
+//
+// The launch sequence is fixed (no host synchronisation), so it is CUDA-graph
+// capturable; per-frame exact convergence (equalize.py:64-67) is a device
+// flag the update kernels honour.  Every gather recomputes its coefficient
+// from the exact integer phase (two-level twiddle table in shared memory);
+// the vectors stream through L2 / HBM, so the path is memory-bound.
+#include <cmath>
+
+#include "cg.cuh"
+#include "common.cuh"
+#include "demod.cuh"
+#include "internal.h"
+
+namespace ddb {
+
+size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
+
+namespace {
+
+constexpr int kGThreads = 256;
+constexpr int kGPerThread = 4;                      // elements per thread
+constexpr int kGBlock = kGThreads * kGPerThread;    // elements per block (one frame)
+constexpr int kGTaps = 64;                          // taps per frame staged in shared memory
+
+// Per-frame scalars in the workspace.
+template <typename T> struct FrameScal {
+  T cn;       // current ||c||^2
+  T beta;     // beta for the next forward phase
+  T alpha;    // alpha of the current hermitian phase
+  int state;  // 0 running, 1 exact convergence reached (stop updating)
+  int done;   // iterations completed
+};
+
+template <typename T> struct GArgs {
+  int B, M, N, MN, K0, L0, iters, nblk, TL, TH;
+  const int* off;
+  const int* pk;
+  const int* pl;
+  const Vec<T>* ph;
+  const Vec<T>* y;
+  const T* lam;
+  Vec<T>* x;
+  Vec<T>* c;
+  Vec<T>* u;
+  Vec<T>* p;
+  Vec<T>* part;   // [B][nblk] pairs
+  FrameScal<T>* sc;
+  T* cnorm;
+  int* itdone;
+  uint8_t* status;
+  Vec<T>* snaps;
+};
+
+template <typename T> struct GTap {
+  int dk, dl;
+  Vec<T> hf, hh;  // forward gain h W^{-d_l d_k}, hermitian conj(h)
+};
+
+template <typename T>
+__device__ __forceinline__ Vec<T> gtwid(const Vec<T>* tlo, const Vec<T>* thi, int tl_bits, int e) {
+  return cmul(thi[e >> tl_bits], tlo[e & ((1 << tl_bits) - 1)]);
+}
+
+// Shared setup of a gather kernel: twiddle tables and the frame's taps.
+template <typename T>
+__device__ __forceinline__ int g_setup(const GArgs<T>& a, int f, Vec<T>* tlo, Vec<T>* thi, Vec<T>* tw, GTap<T>* taps,
+                                       int& P0) {
+  for (int i = threadIdx.x; i < a.TL; i += blockDim.x) tlo[i] = twiddle(T(0), i, a.MN);
+  for (int i = threadIdx.x; i < a.TH; i += blockDim.x)
+    thi[i] = twiddle(T(0), (int)(((long long)i * a.TL) % a.MN), a.MN);
+  for (int l = threadIdx.x; l < a.N; l += blockDim.x) tw[l] = twiddle(T(0), l, a.N);
+  P0 = a.off[f];
+  const int P = a.off[f + 1] - P0;
+  __syncthreads();
+  const int tlb = __ffs(a.TL) - 1;
+  for (int i = threadIdx.x; i < P && i < kGTaps; i += blockDim.x) {
+    GTap<T> t;
+    t.dk = a.K0 - a.pk[P0 + i];
+    t.dl = a.L0 - a.pl[P0 + i];
+    const Vec<T> h = a.ph[P0 + i];
+    t.hf = t.dl ? cmul(h, gtwid<T>(tlo, thi, tlb, wrap1(-t.dl * t.dk, a.MN))) : h;
+    t.hh = cconj(h);
+    taps[i] = t;
+  }
+  __syncthreads();
+  return P;
+}
+
+// (H v)[q] (HERM false) or (H^H v)[q] (HERM true) for one element q = l M + k
+// of frame f, v in global memory (closed forms in sscga.cu's header).
+template <typename T, bool HERM>
+__device__ __forceinline__ Vec<T> g_apply(const GArgs<T>& a, const Vec<T>* v, int k, int l, int P, int P0,
+                                          const GTap<T>* taps, const Vec<T>* tlo, const Vec<T>* thi, const Vec<T>* tw) {
+  using V = Vec<T>;
+  const int M = a.M, N = a.N, MN = a.MN;
+  const int tlb = __ffs(a.TL) - 1;
+  V acc = czero<V>();
+  for (int p = 0; p < P; ++p) {
+    GTap<T> t;
+    if (p < kGTaps) {
+      t = taps[p];
+    } else {
+      t.dk = a.K0 - a.pk[P0 + p];
+      t.dl = a.L0 - a.pl[P0 + p];
+      const V h = a.ph[P0 + p];
+      t.hf = t.dl ? cmul(h, gtwid<T>(tlo, thi, tlb, wrap1(-t.dl * t.dk, MN))) : h;
+      t.hh = cconj(h);
+    }
+    const int ar = HERM ? k - t.dk : k + t.dk;
+    const int nw = ar < 0 ? -1 : (ar >= M ? 1 : 0);
+    const int ks = ar - nw * M;
+    int ls = l + (HERM ? -t.dl : t.dl);
+    ls = ls < 0 ? ls + N : (ls >= N ? ls - N : ls);
+    V coef = HERM ? t.hh : t.hf;
+    if (t.dl) coef = cmul(coef, gtwid<T>(tlo, thi, tlb, wrap1(HERM ? t.dl * k : -t.dl * k, MN)));
+    V s = __ldg(reinterpret_cast<const V*>(v) + (size_t)ls * M + ks);
+    if (nw != 0) s = cmul(s, nw < 0 ? cconj(tw[ls]) : tw[ls]);
+    cfma(acc, coef, s);
+  }
+  return acc;
+}
+
+template <typename T>
+__device__ __forceinline__ void block_pair_sum(Vec<T> v, Vec<T>* dst) {
+  __shared__ Vec<T> red[kGThreads / 32];
+  v.x = warp_sum(v.x);
+  v.y = warp_sum(v.y);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (lane == 0) red[warp] = v;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    Vec<T> s = red[0];
+    for (int w = 1; w < kGThreads / 32; ++w) s = cadd(s, red[w]);
+    *dst = s;
+  }
+}
+
+#define G_SMEM_DECL                                        \
+  extern __shared__ __align__(16) unsigned char gsm[];     \
+  Vec<T>* tlo = reinterpret_cast<Vec<T>*>(gsm);            \
+  Vec<T>* thi = tlo + a.TL;                                \
+  Vec<T>* tw = thi + a.TH;                                 \
+  GTap<T>* taps = reinterpret_cast<GTap<T>*>(tw + a.N);
+
+// b = H^H y -> c (equalize.py:52-57), x = 0, partial ||c||^2.
+template <typename T>
+__global__ void __launch_bounds__(kGThreads) g_init(const GArgs<T> a) {
+  using V = Vec<T>;
+  G_SMEM_DECL
+  const int f = blockIdx.y, blk = blockIdx.x;
+  int P0 = 0;
+  const int P = g_setup(a, f, tlo, thi, tw, taps, P0);
+  const size_t fo = (size_t)f * a.MN;
+  V nrm = czero<V>();
+  for (int e = 0; e < kGPerThread; ++e) {
+    const int q = blk * kGBlock + e * kGThreads + threadIdx.x;
+    if (q >= a.MN) break;
+    const int l = q / a.M, k = q - l * a.M;
+    V b = P > 0 ? g_apply<T, true>(a, a.y + fo, k, l, P, P0, taps, tlo, thi, tw) : czero<V>();
+    a.c[fo + q] = b;
+    a.x[fo + q] = czero<V>();
+    nrm.x += b.x * b.x + b.y * b.y;
+  }
+  block_pair_sum<T>(nrm, a.part + (size_t)f * a.nblk + blk);
+}
+
+// u = H c + beta u_old, p = c + beta p_old (u-recurrence), partials (||u||^2, ||p||^2).
+template <typename T>
+__global__ void __launch_bounds__(kGThreads) g_fwd(const GArgs<T> a, int it) {
+  using V = Vec<T>;
+  G_SMEM_DECL
+  const int f = blockIdx.y, blk = blockIdx.x;
+  if (a.sc[f].state) return;
+  int P0 = 0;
+  const int P = g_setup(a, f, tlo, thi, tw, taps, P0);
+  const T beta = a.sc[f].beta;
+  const size_t fo = (size_t)f * a.MN;
+  V nu = czero<V>();
+  for (int e = 0; e < kGPerThread; ++e) {
+    const int q = blk * kGBlock + e * kGThreads + threadIdx.x;
+    if (q >= a.MN) break;
+    const int l = q / a.M, k = q - l * a.M;
+    const V hc = g_apply<T, false>(a, a.c + fo, k, l, P, P0, taps, tlo, thi, tw);
+    const V cq = a.c[fo + q];
+    const V uq = it == 0 ? hc : cadd(hc, cscale(a.u[fo + q], beta));
+    const V pq = it == 0 ? cq : cadd(cq, cscale(a.p[fo + q], beta));
+    a.u[fo + q] = uq;
+    a.p[fo + q] = pq;
+    nu.x += uq.x * uq.x + uq.y * uq.y;
+    nu.y += pq.x * pq.x + pq.y * pq.y;
+  }
+  block_pair_sum<T>(nu, a.part + (size_t)f * a.nblk + blk);
+}
+
+// ap = H^H u + lam p; x += alpha p; c -= alpha ap; partial ||c||^2.
+template <typename T>
+__global__ void __launch_bounds__(kGThreads) g_herm(const GArgs<T> a, int it) {
+  using V = Vec<T>;
+  G_SMEM_DECL
+  const int f = blockIdx.y, blk = blockIdx.x;
+  if (a.sc[f].state) return;
+  int P0 = 0;
+  const int P = g_setup(a, f, tlo, thi, tw, taps, P0);
+  const T alpha = a.sc[f].alpha, lam = a.lam[f];
+  const size_t fo = (size_t)f * a.MN;
+  V nc = czero<V>();
+  for (int e = 0; e < kGPerThread; ++e) {
+    const int q = blk * kGBlock + e * kGThreads + threadIdx.x;
+    if (q >= a.MN) break;
+    const int l = q / a.M, k = q - l * a.M;
+    const V pq = a.p[fo + q];
+    const V ap = cadd(g_apply<T, true>(a, a.u + fo, k, l, P, P0, taps, tlo, thi, tw), cscale(pq, lam));
+    const V xq = cadd(a.x[fo + q], cscale(pq, alpha));
+    const V cq = csub(a.c[fo + q], cscale(ap, alpha));
+    a.x[fo + q] = xq;
+    a.c[fo + q] = cq;
+    if (a.snaps) a.snaps[((size_t)f * a.iters + it) * a.MN + q] = xq;
+    nc.x += cq.x * cq.x + cq.y * cq.y;
+  }
+  block_pair_sum<T>(nc, a.part + (size_t)f * a.nblk + blk);
+}
+
+// Per-frame fixed-order sum of the block partials, then the CG scalar logic.
+// kind 0: ||c||^2 of b (start); 1: (||u||^2, ||p||^2) -> alpha or exact
+// convergence; 2: ||c||^2 after an iteration -> beta.
+template <typename T>
+__global__ void __launch_bounds__(kGThreads) g_fold(const GArgs<T> a, int kind, int it) {
+  using V = Vec<T>;
+  const int f = blockIdx.x;
+  FrameScal<T>& s = a.sc[f];
+  if (kind != 0 && s.state) return;
+  const V* pp = a.part + (size_t)f * a.nblk;
+  V v = czero<V>();
+  for (int i = threadIdx.x; i < a.nblk; i += blockDim.x) v = cadd(v, pp[i]);
+  __shared__ V tot;
+  block_pair_sum<T>(v, &tot);
+  __syncthreads();
+  if (threadIdx.x != 0) return;
+  const int stride = a.iters + 1;
+  const V t = tot;
+  if (kind == 0) {
+    s.cn = t.x;
+    s.beta = T(0);
+    s.state = 0;
+    s.done = 0;
+    if (a.cnorm) a.cnorm[(size_t)f * stride] = t.x;
+  } else if (kind == 1) {
+    const T denom = t.x + a.lam[f] * t.y;  // ||H p||^2 + lam ||p||^2 (equalize.py:60-64)
+    if (denom == T(0)) {
+      s.state = 1;  // equalize.py:64-67
+    } else {
+      s.alpha = s.cn / denom;
+    }
+  } else {
+    s.beta = t.x / s.cn;
+    s.cn = t.x;
+    s.done = it + 1;
+    if (a.cnorm) a.cnorm[(size_t)f * stride + it + 1] = t.x;
+  }
+}
+
+// Trace tail and status after the last iteration.
+template <typename T>
+__global__ void g_finish(const GArgs<T> a) {
+  const int f = blockIdx.x * blockDim.x + threadIdx.x;
+  if (f >= a.B) return;
+  const FrameScal<T>& s = a.sc[f];
+  const int P = a.off[f + 1] - a.off[f];
+  const int stride = a.iters + 1;
+  if (P <= 0) {
+    if (a.cnorm) for (int i = 0; i < stride; ++i) a.cnorm[(size_t)f * stride + i] = T(0);
+    if (a.itdone) a.itdone[f] = 0;
+    if (a.status) a.status[f] = 1;
+    return;
+  }
+  if (a.cnorm) for (int i = s.done + 1; i < stride; ++i) a.cnorm[(size_t)f * stride + i] = T(0);
+  if (a.itdone) a.itdone[f] = s.done;
+  if (a.status) a.status[f] = s.state ? 2 : 0;
+}
+
+// Hard labels, LLRs and bit errors from x (EmptyChannel frames: zeros and the
+// harness.py:173 scoring of a failed packet).
+template <typename T, int BA>
+__global__ void __launch_bounds__(kGThreads) g_demod(const GArgs<T> a, uint8_t* labels, float* llr, const T* nvar,
+                                                      const uint8_t* txl, int* berr) {
+  const int f = blockIdx.y;
+  const size_t fo = (size_t)f * a.MN;
+  const int P = a.off[f + 1] - a.off[f];
+  const T nv = nvar ? nvar[f] : a.lam[f];
+  const T scale = nv > T(0) ? T(1) / nv : T(1);
+  int errs = 0;
+  const bool any = labels || llr || txl;
+  for (int e = 0; e < kGPerThread; ++e) {
+    const int q = blockIdx.x * kGBlock + e * kGThreads + threadIdx.x;
+    if (q >= a.MN) break;
+    if (P <= 0) {
+      a.x[fo + q] = czero<Vec<T>>();
+      if (labels) labels[fo + q] = 0;
+      if (llr) for (int b = 0; b < 2 * BA; ++b) llr[(fo + q) * (2 * BA) + b] = 0.f;
+      continue;
+    }
+    if (!any) continue;
+    const Vec<T> xv = a.x[fo + q];
+    float l[2 * BA];
+    const int lab = qam_symbol<T, BA>(xv.x, xv.y, scale, llr ? l : nullptr);
+    if (llr)
+      for (int b = 0; b < 2 * BA; ++b) llr[(fo + q) * (2 * BA) + b] = l[b];
+    if (labels) labels[fo + q] = (uint8_t)lab;
+    if (txl) errs += __popc((unsigned)(lab ^ txl[fo + q]));
+  }
+  if (berr) {
+    if (P <= 0) {
+      if (blockIdx.x == 0 && threadIdx.x == 0) berr[f] = a.MN * BA;  // bps * MN / 2
+      return;
+    }
+    errs = warp_sum(errs);
+    if ((threadIdx.x & 31) == 0 && errs) atomicAdd(berr + f, errs);
+  }
+}
+
+template <typename T>
+__global__ void g_zero_int(int* p, int n) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) p[i] = 0;
+}
+
+template <typename T>
+size_t g_workspace(int B, int MN) {
+  const int nblk = (MN + kGBlock - 1) / kGBlock;
+  return align_up(3 * (size_t)B * MN * sizeof(Vec<T>), 256) + align_up((size_t)B * nblk * sizeof(Vec<T>), 256) +
+         align_up((size_t)B * sizeof(FrameScal<T>), 256);
+}
+
+}  // namespace
+
+size_t sscga_global_workspace(int dtype_f64, int B, int M, int N) {
+  return dtype_f64 ? g_workspace<double>(B, M * N) : g_workspace<float>(B, M * N);
+}
+
+template <typename T>
+cudaError_t launch_sscga_global(const SolveArgs& s, void* ws, cudaStream_t st) {
+  using V = Vec<T>;
+  GArgs<T> a = {};
+  a.B = s.B;
+  a.M = s.M;
+  a.N = s.N;
+  a.MN = s.MN;
+  a.K0 = s.K0;
+  a.L0 = s.L0;
+  a.iters = s.iters;
+  a.nblk = (s.MN + kGBlock - 1) / kGBlock;
+  a.TL = s.TL;
+  a.TH = s.TH;
+  a.off = s.off;
+  a.pk = s.pk;
+  a.pl = s.pl;
+  a.ph = reinterpret_cast<const V*>(s.ph);
+  a.y = reinterpret_cast<const V*>(s.y);
+  a.lam = reinterpret_cast<const T*>(s.lam);
+  a.x = reinterpret_cast<V*>(s.x);
+  unsigned char* w = static_cast<unsigned char*>(ws);
+  const size_t vb = (size_t)s.B * s.MN * sizeof(V);
+  a.c = reinterpret_cast<V*>(w);
+  a.u = reinterpret_cast<V*>(w + vb);
+  a.p = reinterpret_cast<V*>(w + 2 * vb);
+  w += align_up(3 * vb, 256);
+  a.part = reinterpret_cast<V*>(w);
+  w += align_up((size_t)s.B * a.nblk * sizeof(V), 256);
+  a.sc = reinterpret_cast<FrameScal<T>*>(w);
+  a.cnorm = reinterpret_cast<T*>(s.cnorm);
+  a.itdone = s.itdone;
+  a.status = s.status;
+  a.snaps = reinterpret_cast<V*>(s.snaps);
+  if (s.B == 0) return cudaSuccess;
+  const size_t smem = (size_t)(a.TL + a.TH + a.N) * sizeof(V) + kGTaps * sizeof(GTap<T>);
+  cudaError_t e;
+  if ((e = cudaFuncSetAttribute(g_init<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem))) return e;
+  if ((e = cudaFuncSetAttribute(g_fwd<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem))) return e;
+  if ((e = cudaFuncSetAttribute(g_herm<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem))) return e;
+  const dim3 grid(a.nblk, s.B);
+  g_init<T><<<grid, kGThreads, smem, st>>>(a);
+  g_fold<T><<<s.B, kGThreads, 0, st>>>(a, 0, 0);
+  for (int it = 0; it < s.iters; ++it) {
+    g_fwd<T><<<grid, kGThreads, smem, st>>>(a, it);
+    g_fold<T><<<s.B, kGThreads, 0, st>>>(a, 1, it);
+    g_herm<T><<<grid, kGThreads, smem, st>>>(a, it);
+    g_fold<T><<<s.B, kGThreads, 0, st>>>(a, 2, it);
+  }
+  g_finish<T><<<(s.B + 127) / 128, 128, 0, st>>>(a);
+  if (s.berr) g_zero_int<T><<<(s.B + 255) / 256, 256, 0, st>>>(s.berr, s.B);
+  if (s.bps) {
+    const T* nvar = reinterpret_cast<const T*>(s.nvar);
+    switch (s.bps) {
+      case 2: g_demod<T, 1><<<grid, kGThreads, 0, st>>>(a, s.labels, s.llr, nvar, s.txl, s.berr); break;
+      case 4: g_demod<T, 2><<<grid, kGThreads, 0, st>>>(a, s.labels, s.llr, nvar, s.txl, s.berr); break;
+      default: g_demod<T, 3><<<grid, kGThreads, 0, st>>>(a, s.labels, s.llr, nvar, s.txl, s.berr); break;
+    }
+  } else {
+    // EmptyChannel frames still need x = 0
+    g_demod<T, 1><<<grid, kGThreads, 0, st>>>(a, nullptr, nullptr, nullptr, nullptr, nullptr);
+  }
+  return cudaGetLastError();
+}
+
+template cudaError_t launch_sscga_global<float>(const SolveArgs&, void*, cudaStream_t);
+template cudaError_t launch_sscga_global<double>(const SolveArgs&, void*, cudaStream_t);
+
+}  // namespace ddb

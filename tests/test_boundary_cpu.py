@@ -48,9 +48,22 @@ def test_plan_without_gpu(lib, M, N, dt, cluster):
 def test_plan_large_grid_uses_bigger_clusters(lib):
     p = nat.plan(1024, 64, nat.DDB_F32)
     assert p.cluster in (8, 16)
-    with pytest.raises(nat.DdbError) as e:
-        nat.plan(16384, 32, nat.DDB_F32)
-    assert e.value.status == nat.DDB_ERR_UNSUPPORTED
+    assert p.kernel == 1 and p.rows_per_thread == 16  # TMEM-operand kernel
+    p = nat.plan(512, 32, nat.DDB_F32)
+    assert (p.kernel, p.cluster, p.rows_per_thread, p.threads) == (1, 2, 16, 512)
+    assert nat.plan(512, 32, nat.DDB_F64).kernel == 0  # fp64: row-slice kernel
+
+
+def test_paper_grid_uses_workspace_path(lib):
+    """(16384, 32) exceeds a 16-CTA cluster's on-chip memory: the
+    planner picks the workspace-backed kernels and sizes their workspace."""
+    for dt, eb in ((nat.DDB_F32, 8), (nat.DDB_F64, 16)):
+        p = nat.plan(16384, 32, dt)
+        assert p.kernel == 2
+        prob = _prob(batch=3, M=16384, N=32, dtype=dt)
+        ws = lib.ddb_sscga_workspace_bytes(C.byref(prob))
+        assert ws >= 3 * 3 * 16384 * 32 * eb  # c, u, p of every frame
+    assert lib.ddb_sscga_workspace_bytes(C.byref(_prob(M=512, N=32))) == 0  # fused: state on chip
 
 
 def _prob(**kw):

@@ -28,13 +28,16 @@ def pkg():
     return p
 
 
-@pytest.fixture(params=["tmem", "rows"])
+@pytest.fixture(params=["tmem", "rows", "workspace"])
 def fp32_kernel(request, monkeypatch):
-    """Run an fp32 test on both fused kernels: the TMEM-operand kernel (the
-    planner's default wherever its layout applies) and the row-slice kernel
-    (DDB_KERNEL=row)."""
+    """Run an fp32 test on every solve path: the TMEM-operand kernel (the
+    planner's default wherever its layout applies), the row-slice kernel
+    (DDB_KERNEL=row) and the workspace-backed kernels (DDB_KERNEL=global, the
+    path of grids beyond a cluster's on-chip memory)."""
     if request.param == "rows":
         monkeypatch.setenv("DDB_KERNEL", "row")
+    elif request.param == "workspace":
+        monkeypatch.setenv("DDB_KERNEL", "global")
     else:
         monkeypatch.delenv("DDB_KERNEL", raising=False)
     return request.param
@@ -244,7 +247,10 @@ def test_batched_fp32_parity(pkg, name, fp32_kernel):
 
 
 @pytest.mark.parametrize("name", ["frames_cfg1", "frames_cfg2", "frames_cfg3"])
-def test_batched_fp64_identical_decisions(pkg, name):
+@pytest.mark.parametrize("path", ["fused", "workspace"])
+def test_batched_fp64_identical_decisions(pkg, name, path, monkeypatch):
+    if path == "workspace":
+        monkeypatch.setenv("DDB_KERNEL", "global")
     d = load_golden(name)
     M, N, iters, b = (int(v) for v in d["meta"])
     s = solver_for(pkg, M, N, iters, "fp64", b)
@@ -342,6 +348,20 @@ def test_random_taps_all_cluster_shapes(pkg, M, N, P, precision, monkeypatch):
 def test_random_taps_row_kernel_fp32(pkg, M, N, P, monkeypatch):
     monkeypatch.setenv("DDB_KERNEL", "row")
     _random_taps_case(pkg, M, N, P, "fp32")
+
+
+@pytest.mark.parametrize("M,N,P", SHAPES + [(8192, 32, 6), (16384, 32, 6)])
+@pytest.mark.parametrize("precision", ["fp32", "fp64"])
+def test_random_taps_workspace_path(pkg, M, N, P, precision, monkeypatch):
+    """The workspace-backed kernels on every shape, and the paper's large grids
+    (16384 x 32), which only this path can hold."""
+    if M * N > 200000:
+        monkeypatch.delenv("DDB_KERNEL", raising=False)  # the planner must pick it by itself
+        s = solver_for(pkg, M, N, 10, precision)
+        assert s.plan()["kernel"] == "workspace"
+    else:
+        monkeypatch.setenv("DDB_KERNEL", "global")
+    _random_taps_case(pkg, M, N, P, precision)
 
 
 def _random_taps_case(pkg, M, N, P, precision):
