@@ -267,12 +267,10 @@ def main():
     import torch
     import torch.distributed as dist
 
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
+    from paper_2604_02266_b200 import dist as ddist
+    rank, local, world = ddist.world()
     torch.cuda.set_device(local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    ddist.init("nccl")
 
     import ctypes as C
     import paper_2604_02266_b200 as pkg
@@ -284,19 +282,15 @@ def main():
     B = args.batch or cfg["batch"]
     bps = BPS[cfg["mod"]]
     s = pkg.SsCgaSolver(M, N, args.iters, precision="fp32", modulation=cfg["mod"])
-    fb = make_frames(s, B, snr_db=args.snr, nu_max_hz=cfg["nu"], modulation=cfg["mod"], seed=1000 + rank,
-                     n_paths=P)
+    fb = make_frames(s, B, snr_db=args.snr, nu_max_hz=cfg["nu"], modulation=cfg["mod"],
+                     seed=ddist.rank_seed(1000, rank), n_paths=P)
     out = s.alloc(B, llr=True, trace=True, bit_errors=True)
     stream = torch.cuda.current_stream()
 
     def step():
         s.solve(fb.y, fb.paths, fb.lam, tx_labels=fb.tx_labels, out=out)
 
-    def barrier():
-        torch.cuda.synchronize()
-        if world > 1:
-            dist.barrier()
-        torch.cuda.synchronize()
+    barrier = ddist.barrier
 
     for _ in range(max(3, args.warmup)):
         step()
@@ -312,15 +306,11 @@ def main():
     e1.record(stream)
     barrier()
     clocks = sampler.stop()
-    ms = e0.elapsed_time(e1)
-    if world > 1:
-        t = torch.tensor([ms], device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
+    ms = ddist.max_over_ranks(e0.elapsed_time(e1))
     ms_step = ms / args.steps
     value = world * B * MN * args.steps / (ms * 1e-3)
-    bit_errors = int(out.bit_errors.sum().item())
-    ber = bit_errors / (B * MN * bps)
+    bit_errors = ddist.sum_over_ranks(int(out.bit_errors.sum().item()))
+    ber = bit_errors / (world * B * MN * bps)
 
     # ---- FP32 peak of this box (FFMA / FFMA2 probe), HBM peak from MEASURED_PEAKS
     scratch = torch.empty(148 * 8, dtype=torch.float32, device="cuda")
@@ -436,11 +426,7 @@ def main():
             pipe.run(hy, hp, hl, ht, lab_h, err_h)
         b.record(pipe.d2h)
         b.synchronize()
-        ems = a.elapsed_time(b)
-        if world > 1:
-            t = torch.tensor([ems], device="cuda")
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            ems = float(t.item())
+        ems = ddist.max_over_ranks(a.elapsed_time(b))
         h2d = hy.numel() * hy.element_size() + hl.numel() * hl.element_size() + ht.numel() + \
             sum(t.numel() * t.element_size() for t in hp)
         d2h = lab_h.numel() + err_h.numel() * 4
