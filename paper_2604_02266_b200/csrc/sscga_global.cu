@@ -98,15 +98,24 @@ __device__ __forceinline__ int g_setup(const GArgs<T>& a, int f, Vec<T>* tlo, Ve
   return P;
 }
 
-// (H v)[q] (HERM false) or (H^H v)[q] (HERM true) for one element q = l M + k
-// of frame f, v in global memory (closed forms in sscga.cu's header).
+// (H v)[q] (HERM false) or (H^H v)[q] (HERM true), v in global memory (closed
+// forms in sscga.cu's header), for the kGPerThread elements of this thread (q = q0 + e kGThreads),
+// tap-major so the element gathers of one tap are in flight together.
 template <typename T, bool HERM>
-__device__ __forceinline__ Vec<T> g_apply(const GArgs<T>& a, const Vec<T>* v, int k, int l, int P, int P0,
-                                          const GTap<T>* taps, const Vec<T>* tlo, const Vec<T>* thi, const Vec<T>* tw) {
+__device__ __forceinline__ void g_apply4(const GArgs<T>& a, const Vec<T>* v, int q0, int P, int P0,
+                                         const GTap<T>* taps, const Vec<T>* tlo, const Vec<T>* thi, const Vec<T>* tw,
+                                         Vec<T> (&acc)[kGPerThread]) {
   using V = Vec<T>;
   const int M = a.M, N = a.N, MN = a.MN;
   const int tlb = __ffs(a.TL) - 1;
-  V acc = czero<V>();
+  int kk[kGPerThread], ll[kGPerThread];
+#pragma unroll
+  for (int e = 0; e < kGPerThread; ++e) {
+    const int q = min(q0 + e * kGThreads, MN - 1);
+    ll[e] = q / M;
+    kk[e] = q - ll[e] * M;
+    acc[e] = czero<V>();
+  }
   for (int p = 0; p < P; ++p) {
     GTap<T> t;
     if (p < kGTaps) {
@@ -118,18 +127,25 @@ __device__ __forceinline__ Vec<T> g_apply(const GArgs<T>& a, const Vec<T>* v, in
       t.hf = t.dl ? cmul(h, gtwid<T>(tlo, thi, tlb, wrap1(-t.dl * t.dk, MN))) : h;
       t.hh = cconj(h);
     }
-    const int ar = HERM ? k - t.dk : k + t.dk;
-    const int nw = ar < 0 ? -1 : (ar >= M ? 1 : 0);
-    const int ks = ar - nw * M;
-    int ls = l + (HERM ? -t.dl : t.dl);
-    ls = ls < 0 ? ls + N : (ls >= N ? ls - N : ls);
-    V coef = HERM ? t.hh : t.hf;
-    if (t.dl) coef = cmul(coef, gtwid<T>(tlo, thi, tlb, wrap1(HERM ? t.dl * k : -t.dl * k, MN)));
-    V s = __ldg(reinterpret_cast<const V*>(v) + (size_t)ls * M + ks);
-    if (nw != 0) s = cmul(s, nw < 0 ? cconj(tw[ls]) : tw[ls]);
-    cfma(acc, coef, s);
+    V s[kGPerThread];
+    int nw[kGPerThread], ls[kGPerThread];
+#pragma unroll
+    for (int e = 0; e < kGPerThread; ++e) {
+      const int ar = HERM ? kk[e] - t.dk : kk[e] + t.dk;
+      nw[e] = ar < 0 ? -1 : (ar >= M ? 1 : 0);
+      int l2 = ll[e] + (HERM ? -t.dl : t.dl);
+      ls[e] = l2 < 0 ? l2 + N : (l2 >= N ? l2 - N : l2);
+      s[e] = __ldg(v + (size_t)ls[e] * M + (ar - nw[e] * M));
+    }
+#pragma unroll
+    for (int e = 0; e < kGPerThread; ++e) {
+      V coef = HERM ? t.hh : t.hf;
+      if (t.dl) coef = cmul(coef, gtwid<T>(tlo, thi, tlb, wrap1(HERM ? t.dl * kk[e] : -t.dl * kk[e], MN)));
+      V x = s[e];
+      if (nw[e] != 0) x = cmul(x, nw[e] < 0 ? cconj(tw[ls[e]]) : tw[ls[e]]);
+      cfma(acc[e], coef, x);
+    }
   }
-  return acc;
 }
 
 template <typename T>
@@ -164,11 +180,12 @@ __global__ void __launch_bounds__(kGThreads) g_init(const GArgs<T> a) {
   const int P = g_setup(a, f, tlo, thi, tw, taps, P0);
   const size_t fo = (size_t)f * a.MN;
   V nrm = czero<V>();
+  V bb[kGPerThread];
+  g_apply4<T, true>(a, a.y + fo, blk * kGBlock + threadIdx.x, P, P0, taps, tlo, thi, tw, bb);
   for (int e = 0; e < kGPerThread; ++e) {
     const int q = blk * kGBlock + e * kGThreads + threadIdx.x;
     if (q >= a.MN) break;
-    const int l = q / a.M, k = q - l * a.M;
-    V b = P > 0 ? g_apply<T, true>(a, a.y + fo, k, l, P, P0, taps, tlo, thi, tw) : czero<V>();
+    const V b = bb[e];
     a.c[fo + q] = b;
     a.x[fo + q] = czero<V>();
     nrm.x += b.x * b.x + b.y * b.y;
@@ -188,11 +205,12 @@ __global__ void __launch_bounds__(kGThreads) g_fwd(const GArgs<T> a, int it) {
   const T beta = a.sc[f].beta;
   const size_t fo = (size_t)f * a.MN;
   V nu = czero<V>();
+  V hcv[kGPerThread];
+  g_apply4<T, false>(a, a.c + fo, blk * kGBlock + threadIdx.x, P, P0, taps, tlo, thi, tw, hcv);
   for (int e = 0; e < kGPerThread; ++e) {
     const int q = blk * kGBlock + e * kGThreads + threadIdx.x;
     if (q >= a.MN) break;
-    const int l = q / a.M, k = q - l * a.M;
-    const V hc = g_apply<T, false>(a, a.c + fo, k, l, P, P0, taps, tlo, thi, tw);
+    const V hc = hcv[e];
     const V cq = a.c[fo + q];
     const V uq = it == 0 ? hc : cadd(hc, cscale(a.u[fo + q], beta));
     const V pq = it == 0 ? cq : cadd(cq, cscale(a.p[fo + q], beta));
@@ -216,12 +234,13 @@ __global__ void __launch_bounds__(kGThreads) g_herm(const GArgs<T> a, int it) {
   const T alpha = a.sc[f].alpha, lam = a.lam[f];
   const size_t fo = (size_t)f * a.MN;
   V nc = czero<V>();
+  V hu[kGPerThread];
+  g_apply4<T, true>(a, a.u + fo, blk * kGBlock + threadIdx.x, P, P0, taps, tlo, thi, tw, hu);
   for (int e = 0; e < kGPerThread; ++e) {
     const int q = blk * kGBlock + e * kGThreads + threadIdx.x;
     if (q >= a.MN) break;
-    const int l = q / a.M, k = q - l * a.M;
     const V pq = a.p[fo + q];
-    const V ap = cadd(g_apply<T, true>(a, a.u + fo, k, l, P, P0, taps, tlo, thi, tw), cscale(pq, lam));
+    const V ap = cadd(hu[e], cscale(pq, lam));
     const V xq = cadd(a.x[fo + q], cscale(pq, alpha));
     const V cq = csub(a.c[fo + q], cscale(ap, alpha));
     a.x[fo + q] = xq;
