@@ -402,8 +402,11 @@ def main():
             b.record()
         torch.cuda.synchronize()
         lat = sorted(a.elapsed_time(b) for a, b in ev)
+        n_clu = max(1, sms // max(1, s.plan()["cluster"]))  # persistent clusters (1 CTA per SM)
         latency = {"p50_ms": lat[len(lat) // 2], "p99_ms": lat[int(len(lat) * 0.99)],
                    "max_ms": lat[-1], "runs": len(lat), "frame_duration_ms": 1e3 * N / 30e3,
+                   # in a full batch every cluster solves B / clusters frames back to back
+                   "in_batch_frame_residency_ms": ms_step * n_clu / B if s.plan()["kernel"] != "workspace" else None,
                    "what": ("batch-1 solve (one fused launch" if s.plan()["kernel"] != "workspace" else
                             "batch-1 solve (workspace-backed kernels, one graph") + ", CUDA graph replay), device events"}
 

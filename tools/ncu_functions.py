@@ -1,3 +1,10 @@
+#!/usr/bin/env python
+"""Per-function view of an ncu --set full capture: executed warp instructions
+and stall samples attributed to the device function (file:function) each
+source line belongs to.
+
+    python tools/ncu_functions.py gpurun_out/x.ncu-rep <frames in the launch>
+"""
 import subprocess, csv, io, collections, re, sys
 rep=sys.argv[1]; nfr=float(sys.argv[2])
 out = subprocess.run(["ncu","-i",rep,"--page","source","--csv","--print-source","cuda,sass"],capture_output=True,text=True).stdout
