@@ -577,3 +577,22 @@ def test_acceptance_criterion6_ber_known_answer(pkg, precision):
         assert abs(errs.mean() / (b * M * N) - 3.491e-4) < 5e-8
     else:  # fp32 decisions may differ only inside the fp64 tie band: a handful of bits at most
         assert abs(int(errs.sum()) - int(d["bit_errors"].sum())) <= 3
+
+
+@pytest.mark.parametrize("M,N", [(12, 6), (8, 2), (100, 10), (64, 64)])
+@pytest.mark.parametrize("colmajor", [True, False])
+def test_dzt_any_grid_vs_oracle(pkg, M, N, colmajor):
+    """ddb_dzt on grids whose N is not a multiple of 4 (unblocked kernel), partial
+    delay tiles (M not a multiple of 64) and N = 64, with the fused pilot estimate."""
+    from paper_2604_02266_b200.zak import dzt_device
+    rng = np.random.default_rng(M + N)
+    y = rng.normal(size=(3, M * N)) + 1j * rng.normal(size=(3, M * N))
+    for pilot in (False, True):
+        out = dzt_device(torch.as_tensor(y, device="cuda"), M, N, colmajor=colmajor,
+                         pilot_amplitude=2.5 if pilot else None).cpu().numpy()
+        for f in range(3):
+            want = orc.dzt_gemm(y[f], M, N)
+            if pilot:
+                want = orc.estimate_heff(want, M, N, 2.5)
+            want = orc.to_vector(want) if colmajor else want.reshape(-1)
+            assert rel_l2(out[f], want) < 1e-12
