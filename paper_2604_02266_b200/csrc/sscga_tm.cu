@@ -52,7 +52,8 @@ struct FrameSm {
   int P0, P;
   int in_smem, halo, masks;
   int lo_c, hi_c, lo_u, hi_u;  // extension rows written for c (gathered by H) and u (by H^H)
-  int pad[3];
+  int remote;                  // some warp gathers per element (DSMEM): publish c / u with release
+  int pad[2];
   uint32_t mk[8][6];           // [j][tmF, smF, gnF, tmH, smH, gnH]: TMEM run / shared run / per element
 };
 
@@ -342,10 +343,17 @@ __device__ __forceinline__ void put_col(V* colp, int rr, int M, int lo, int hi, 
 
 // Barrier halves around TMEM traffic: stores of every warp complete and are
 // ordered before the CTA barrier; loads after it see them.
-__device__ __forceinline__ void tm_arrive(int C) {
+// relaxed: no peer reads this CTA's shared memory in the current phase (the
+// frame has no DSMEM taps), so only warp 0 (the reduction push) needs release
+// semantics at cluster scope; the other warps skip the cluster-scope fence.
+__device__ __forceinline__ void cl_arrive_sem(bool release) {
+  if (release) asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+  else asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void tm_arrive(int C, bool relaxed = false) {
   tmem_wait_st();
   tmem_fence_before();
-  if (C > 1) asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+  if (C > 1) cl_arrive_sem(!relaxed || (threadIdx.x >> 5) == 0);
   __syncthreads();
   tmem_fence_after();
 }
@@ -366,7 +374,8 @@ __device__ __forceinline__ void red_stage(V part, V* base, int warp, int lane) {
   part.y = warp_sum(part.y);
   if (lane == 0) base[warp] = part;
 }
-__device__ __forceinline__ void tm_arrive_red(int C, V* base, int nwarps, int warp, int lane, int rank) {
+__device__ __forceinline__ void tm_arrive_red(int C, V* base, int nwarps, int warp, int lane, int rank,
+                                              bool relaxed = false) {
   tmem_wait_st();
   tmem_fence_before();
   __syncthreads();
@@ -377,7 +386,7 @@ __device__ __forceinline__ void tm_arrive_red(int C, V* base, int nwarps, int wa
       t.y = warp_sum(t.y);
       if (lane < C) st_cluster(map_rank(smem_addr(base + 32 + rank), (uint32_t)lane), t);
     }
-    asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+    cl_arrive_sem(!relaxed || warp == 0);
   }
   tmem_fence_after();
 }
@@ -555,6 +564,7 @@ __global__ void __launch_bounds__(MAXT, 1) sscga_tm_kernel(const SolveArgs a) {
         fs.hi_c = halo ? hi : 0;
         fs.lo_u = fs.hi_c;
         fs.hi_u = fs.lo_c;
+        fs.remote = !fs.masks;  // without per-warp masks assume DSMEM taps
       }
     }
     __syncthreads();
@@ -577,6 +587,7 @@ __global__ void __launch_bounds__(MAXT, 1) sscga_tm_kernel(const SolveArgs a) {
       }
 #pragma unroll
       for (int i = 0; i < 6; ++i) fs.mk[tid][i] = mk[i];
+      if (mk[2] | mk[5]) atomicOr(&fs.remote, 1);
     }
     const float lam = reinterpret_cast<const float*>(a.lam)[f];
 
@@ -638,7 +649,7 @@ __global__ void __launch_bounds__(MAXT, 1) sscga_tm_kernel(const SolveArgs a) {
       red_stage(make_float2(nrm.x + nrm.y, 0.f), red + (2 + par1) * kPushSlots, warp, lane);
     }
     if constexpr (PROF) prof_mark(a.prof, psm, kArrive);
-    tm_arrive_red(a.C, red + (2 + par1) * kPushSlots, nwarps, warp, lane, rank);  // c = b published
+    tm_arrive_red(a.C, red + (2 + par1) * kPushSlots, nwarps, warp, lane, rank, !fs.remote);  // c = b published
     if constexpr (PROF) prof_mark(a.prof, psm, kMvmLocal);
     mvm_local<R, false>(a, th, sm, fs, tC(0) - 2 * th.jr, ccol, acc);
     if constexpr (PROF) prof_mark(a.prof, psm, kWait);
@@ -688,7 +699,7 @@ __global__ void __launch_bounds__(MAXT, 1) sscga_tm_kernel(const SolveArgs a) {
         red_stage(make_float2(nu.x + nu.y, np.x + np.y), red + par0 * kPushSlots, warp, lane);
       }
       if constexpr (PROF) prof_mark(a.prof, psm, kArrive);
-      tm_arrive_red(a.C, red + par0 * kPushSlots, nwarps, warp, lane, rank);  // u published
+      tm_arrive_red(a.C, red + par0 * kPushSlots, nwarps, warp, lane, rank, !fs.remote);  // u published
       // ap = H^H u + lam p;  x += alpha p;  c -= alpha ap      (equalize.py:60-70)
       if constexpr (PROF) prof_mark(a.prof, psm, kMvmLocal);
       mvm_local<R, true>(a, th, sm, fs, tU(0) - 2 * th.jr, ucol, acc);
@@ -743,7 +754,7 @@ __global__ void __launch_bounds__(MAXT, 1) sscga_tm_kernel(const SolveArgs a) {
         red_stage(make_float2(nc.x + nc.y, 0.f), red + (2 + par1) * kPushSlots, warp, lane);
       }
       if constexpr (PROF) prof_mark(a.prof, psm, kArrive);
-      tm_arrive_red(a.C, red + (2 + par1) * kPushSlots, nwarps, warp, lane, rank);  // c published
+      tm_arrive_red(a.C, red + (2 + par1) * kPushSlots, nwarps, warp, lane, rank, !fs.remote);  // c published
       if constexpr (PROF) prof_mark(a.prof, psm, kMvmLocal);
       if (it + 1 < a.iters) mvm_local<R, false>(a, th, sm, fs, tC(0) - 2 * th.jr, ccol, acc);  // next H c
       if constexpr (PROF) prof_mark(a.prof, psm, kWait);
