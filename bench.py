@@ -416,7 +416,9 @@ def main():
         pipe = pkg.HostPipeline(s, chunk=args.e2e_chunk, depth=args.e2e_depth)
         hy = fb.y.cpu().pin_memory()
         hl = fb.lam.cpu().pin_memory()
-        ht = fb.tx_labels.cpu().pin_memory()
+        # transmitted labels as bits (bps bits per symbol, packed) like the reference's tx_bits
+        tx_in = pkg.pack_labels(fb.tx_labels, bps) if bps in (2, 4) else fb.tx_labels
+        ht = tx_in.cpu().pin_memory()
         hp = tuple(t.cpu().pin_memory() for t in (fb.paths.offsets, fb.paths.k, fb.paths.l, fb.paths.gain))
         lab_h = torch.empty(B, MN, dtype=torch.uint8).pin_memory()
         err_h = torch.empty(B, dtype=torch.int32).pin_memory()
@@ -435,7 +437,8 @@ def main():
         d2h = lab_h.numel() + err_h.numel() * 4
         e2e = {"value": world * B * MN * k2 / (ems * 1e-3), "unit": "symbols/s", "h2d_bytes_per_step": h2d,
                "d2h_bytes_per_step": d2h, "steps": k2, "ms_per_step": ems / k2,
-               "what": "HostPipeline: pinned H2D of y/taps/lam/tx labels, fused solve, D2H labels + bit errors"}
+               "what": "HostPipeline: pinned H2D of y/taps/lam/tx labels (bps bits per symbol), fused solve, "
+                       "D2H labels + bit errors"}
         assert torch.equal(err_h, out.bit_errors.cpu())
 
     # ---- CPU baseline (oracle port on the host cores), rank 0 at N=1 only

@@ -40,7 +40,7 @@
 extern "C" {
 #endif
 
-#define DDB_ABI_VERSION 2
+#define DDB_ABI_VERSION 3
 
 typedef enum {
   DDB_OK = 0,
@@ -89,6 +89,9 @@ typedef struct {
   const void* noise_var;    /* [B] real LLR noise variance, or NULL (-> lam; 1 if 0) */
   const uint8_t* tx_labels; /* [B, M*N] transmitted labels, or NULL                 */
   int32_t* bit_errors;      /* [B] Hamming distance rx vs tx bits (needs tx_labels) */
+  int32_t tx_labels_packed; /* 1: tx_labels carry bits_per_symbol bits per symbol,
+                               LSB-first within bytes ([B, M*N*bps/8] bytes; bps 2 or 4),
+                               0: one byte per symbol                              */
 } ddb_sscga_outputs;
 
 /* Launch plan chosen for a grid/dtype (exposed for tests and tooling). */

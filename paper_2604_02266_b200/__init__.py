@@ -6,7 +6,7 @@ their arithmetic runs in hand-written sm_100a CUDA kernels (libddb.so, C ABI
 in include/ddb.h).  `SsCgaSolver` is the batched device API.
 """
 
-from .batch import HostPipeline, PathBatch, SolveResult, SsCgaSolver, bits_per_symbol
+from .batch import HostPipeline, PathBatch, SolveResult, SsCgaSolver, bits_per_symbol, pack_labels
 from .equalize import CgaConfig, CgaTrace, cga_equalize, get_precision, set_precision
 from .pilot import build_twist_kernel, default_pilot_amplitude, estimate_heff, make_pilot_frame
 from .grid import (
@@ -37,7 +37,7 @@ from .sparse import (
 from .zak import build_zak_kernel, dzt_device, dzt_gemm
 
 __all__ = [
-    "HostPipeline", "PathBatch", "SolveResult", "SsCgaSolver", "bits_per_symbol",
+    "HostPipeline", "PathBatch", "SolveResult", "SsCgaSolver", "bits_per_symbol", "pack_labels",
     "CgaConfig", "CgaTrace", "cga_equalize", "get_precision", "set_precision",
     "Constellation", "GridConfig", "ber", "check_frame", "check_signal", "flatten", "hard_demod",
     "make_constellation", "make_constellation_ext", "modulate", "unflatten",

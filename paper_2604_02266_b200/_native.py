@@ -50,11 +50,11 @@ class Outputs(C.Structure):
         ("status", C.c_void_p), ("snapshots", C.c_void_p),
         ("bits_per_symbol", C.c_int32),
         ("labels", C.c_void_p), ("llr", C.c_void_p), ("noise_var", C.c_void_p),
-        ("tx_labels", C.c_void_p), ("bit_errors", C.c_void_p),
+        ("tx_labels", C.c_void_p), ("bit_errors", C.c_void_p), ("tx_labels_packed", C.c_int32),
     ]
 
 
-ABI_VERSION = 2  # include/ddb.h DDB_ABI_VERSION
+ABI_VERSION = 3  # include/ddb.h DDB_ABI_VERSION
 DDB_DZT_COLMAJOR = 1
 DDB_DZT_PILOT = 2
 

@@ -219,9 +219,11 @@ class SsCgaSolver:
         self._check_inputs(y, paths, lam)
         if out is None:
             out = self.alloc(B, llr=llr, trace=trace, bit_errors=tx_labels is not None, profile=profile)
+        packed = 0
         if tx_labels is not None:
-            if tx_labels.shape != (B, self.MN) or tx_labels.dtype != torch.uint8:
-                raise ValueError(f"tx_labels must be uint8 [{B}, {self.MN}]")
+            packed = int(self.bps in (2, 4) and tuple(tx_labels.shape) == (B, self.MN * self.bps // 8))
+            if (not packed and tuple(tx_labels.shape) != (B, self.MN)) or tx_labels.dtype != torch.uint8:
+                raise ValueError(f"tx_labels must be uint8 [{B}, {self.MN}] (or packed by pack_labels)")
             if out.bit_errors is None:
                 out.bit_errors = torch.empty(B, dtype=torch.int32, device=self.device)
         if noise_var is not None:
@@ -232,7 +234,7 @@ class SsCgaSolver:
             _ptr(out.snapshots), self.bps if (out.labels is not None or out.llr is not None
                                               or tx_labels is not None) else 0,
             _ptr(out.labels), _ptr(out.llr), _ptr(noise_var), _ptr(tx_labels),
-            _ptr(out.bit_errors if tx_labels is not None else None))
+            _ptr(out.bit_errors if tx_labels is not None else None), packed)
         if phase_cycles is not None:
             nat.check(self.lib.ddb_sscga_profile_phases(C.byref(prob), C.byref(outs), _ptr(phase_cycles),
                                                         _stream_handle(stream)), "ddb_sscga_profile_phases")
@@ -331,6 +333,22 @@ class SsCgaSolver:
         return out
 
 
+def pack_labels(labels: torch.Tensor, bps: int) -> torch.Tensor:
+    """[B, MN] uint8 labels -> [B, MN * bps / 8] bytes, bps bits per symbol LSB-first
+    (QPSK 4 and 16-QAM 2 symbols per byte): the tx_labels_packed layout of
+    include/ddb.h, which halves (16-QAM) the transmitted-label bytes an
+    end-to-end run moves over PCIe."""
+    if bps not in (2, 4):
+        raise ValueError("packing needs 2 or 4 bits per symbol")
+    per = 8 // bps
+    B, MN = labels.shape
+    if MN % per:
+        raise ValueError("M*N must be a multiple of the symbols per byte")
+    v = labels.reshape(B, MN // per, per).to(torch.int32)
+    shifts = torch.arange(per, device=labels.device, dtype=torch.int32) * bps
+    return (v << shifts).sum(dim=2).to(torch.uint8)
+
+
 class HostPipeline:
     """End-to-end solve from host buffers (the call a user with numpy data makes).
 
@@ -353,7 +371,7 @@ class HostPipeline:
             self.slots.append(dict(
                 y=torch.empty(self.chunk, MN, dtype=solver.cdtype, device=dev),
                 lam=torch.empty(self.chunk, dtype=solver.rdtype, device=dev),
-                tx=torch.empty(self.chunk, MN, dtype=torch.uint8, device=dev),
+                tx=None,  # allocated at the first run with the host labels' width (packed or not)
                 res=solver.alloc(self.chunk, trace=False, bit_errors=True),
                 loaded=torch.cuda.Event(), solved=torch.cuda.Event(), drained=torch.cuda.Event(),
             ))
@@ -365,6 +383,10 @@ class HostPipeline:
         B = y_host.shape[0]
         off, kk, ll, gg = paths_host
         dev = s.device
+        for slot in self.slots:  # TX labels one byte per symbol, or packed (pack_labels)
+            if slot["tx"] is None or slot["tx"].shape[1] != tx_host.shape[1]:
+                torch.cuda.synchronize(dev)
+                slot["tx"] = torch.empty(self.chunk, tx_host.shape[1], dtype=torch.uint8, device=dev)
         # taps are tiny: one copy for the whole batch, rebased per chunk on the device
         with torch.cuda.stream(self.h2d):
             d_off = off.to(dev, non_blocking=True)

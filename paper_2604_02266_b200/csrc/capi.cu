@@ -282,6 +282,8 @@ static int32_t solve_impl(const ddb_sscga_problem* prob, const ddb_sscga_outputs
     return fail(DDB_ERR_INVALID, "bit_errors needs tx_labels and bits_per_symbol > 0");
   if ((out->labels || out->llr) && bps == 0)
     return fail(DDB_ERR_INVALID, "labels/llr need bits_per_symbol > 0");
+  if (out->tx_labels_packed && bps != 2 && bps != 4)
+    return fail(DDB_ERR_INVALID, "packed tx labels need bits_per_symbol 2 or 4, got %d", bps);
   ddb::LaunchShape s;
   r = make_plan(prob->M, prob->N, prob->dtype, &s);
   if (r) return r;
@@ -324,6 +326,7 @@ static int32_t solve_impl(const ddb_sscga_problem* prob, const ddb_sscga_outputs
   a.llr = out->llr;
   a.nvar = out->noise_var;
   a.txl = out->tx_labels;
+  a.txpk = out->tx_labels_packed ? 1 : 0;
   a.berr = out->bit_errors;
   a.prof = prof;
   cudaStream_t st = static_cast<cudaStream_t>(stream);

@@ -72,6 +72,17 @@ __device__ __forceinline__ float np_cabs(float re, float im) {
   return __fmul_rn(big, __fsqrt_rn(__fmaf_rn(r, r, 1.f)));
 }
 
+// Transmitted label of symbol q: one byte per symbol, or bps bits per symbol
+// packed LSB-first within bytes (bps 2 or 4, so a symbol never straddles bytes).
+__device__ __forceinline__ unsigned tx_label_at(const uint8_t* txl, size_t q, int bps, int packed) {
+  if (!packed) return txl[q];
+  const size_t bit = q * (size_t)bps;
+  return (txl[bit >> 3] >> (bit & 7)) & ((1u << bps) - 1u);
+}
+__device__ __forceinline__ const uint8_t* tx_label_ptr(const uint8_t* txl, size_t q, int bps, int packed) {
+  return txl + (packed ? (q * (size_t)bps >> 3) : q);
+}
+
 // ---- packed complex MAC on sm_100 FFMA2: acc (re, im) += c * v as two
 //      fma.rn.f32x2; ptxas folds the broadcast of c.re / c.im and the swapped,
 //      partially negated v into the FFMA2 operand modifiers.

@@ -41,6 +41,7 @@ struct SolveArgs {
   float* llr;
   const void* nvar;
   const uint8_t* txl;
+  int txpk;          // tx labels packed bps bits per symbol (bps 2 or 4)
   int* berr;
   long long* prof;  // optional per-CTA phase cycle counters [gridDim.x][kProfPhases]
 };

@@ -433,7 +433,7 @@ __device__ __forceinline__ int epilogue(const SolveArgs& a, const Vec<T> (&xv)[X
         }
       }
       if (a.labels) a.labels[q] = (uint8_t)lab;
-      if (a.txl) errs += __popc((unsigned)(lab ^ a.txl[q]));
+      if (a.txl) errs += __popc((unsigned)lab ^ tx_label_at(a.txl, q, a.bps, a.txpk));
     }
   }
   return errs;
@@ -590,7 +590,7 @@ __global__ void __launch_bounds__(sscga_max_threads(sizeof(T), LC), 1) sscga_ker
       for (int j = 0; j < LC; ++j) {
         const size_t q = fn + (size_t)(cx.colbase + j) * M + cx.k;
         asm volatile("prefetch.global.L2 [%0];" :: "l"(y + q));
-        if (a.txl && (cx.k & 31) == 0) asm volatile("prefetch.global.L2 [%0];" :: "l"(a.txl + q));
+        if (a.txl && (cx.k & 31) == 0) asm volatile("prefetch.global.L2 [%0];" :: "l"(tx_label_ptr(a.txl, q, a.bps, a.txpk)));
       }
     }
     // CG in the "u recurrence" form: with u = H p kept from the previous step,

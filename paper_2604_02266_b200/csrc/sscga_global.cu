@@ -313,7 +313,7 @@ __global__ void g_finish(const GArgs<T> a) {
 // harness.py:173 scoring of a failed packet).
 template <typename T, int BA>
 __global__ void __launch_bounds__(kGThreads) g_demod(const GArgs<T> a, uint8_t* labels, float* llr, const T* nvar,
-                                                      const uint8_t* txl, int* berr) {
+                                                      const uint8_t* txl, int txpk, int* berr) {
   const int f = blockIdx.y;
   const size_t fo = (size_t)f * a.MN;
   const int P = a.off[f + 1] - a.off[f];
@@ -337,7 +337,7 @@ __global__ void __launch_bounds__(kGThreads) g_demod(const GArgs<T> a, uint8_t* 
     if (llr)
       for (int b = 0; b < 2 * BA; ++b) llr[(fo + q) * (2 * BA) + b] = l[b];
     if (labels) labels[fo + q] = (uint8_t)lab;
-    if (txl) errs += __popc((unsigned)(lab ^ txl[fo + q]));
+    if (txl) errs += __popc((unsigned)lab ^ tx_label_at(txl, fo + q, 2 * BA, txpk));
   }
   if (berr) {
     if (P <= 0) {
@@ -422,13 +422,13 @@ cudaError_t launch_sscga_global(const SolveArgs& s, void* ws, cudaStream_t st) {
   if (s.bps) {
     const T* nvar = reinterpret_cast<const T*>(s.nvar);
     switch (s.bps) {
-      case 2: g_demod<T, 1><<<grid, kGThreads, 0, st>>>(a, s.labels, s.llr, nvar, s.txl, s.berr); break;
-      case 4: g_demod<T, 2><<<grid, kGThreads, 0, st>>>(a, s.labels, s.llr, nvar, s.txl, s.berr); break;
-      default: g_demod<T, 3><<<grid, kGThreads, 0, st>>>(a, s.labels, s.llr, nvar, s.txl, s.berr); break;
+      case 2: g_demod<T, 1><<<grid, kGThreads, 0, st>>>(a, s.labels, s.llr, nvar, s.txl, s.txpk, s.berr); break;
+      case 4: g_demod<T, 2><<<grid, kGThreads, 0, st>>>(a, s.labels, s.llr, nvar, s.txl, s.txpk, s.berr); break;
+      default: g_demod<T, 3><<<grid, kGThreads, 0, st>>>(a, s.labels, s.llr, nvar, s.txl, s.txpk, s.berr); break;
     }
   } else {
     // EmptyChannel frames still need x = 0
-    g_demod<T, 1><<<grid, kGThreads, 0, st>>>(a, nullptr, nullptr, nullptr, nullptr, nullptr);
+    g_demod<T, 1><<<grid, kGThreads, 0, st>>>(a, nullptr, nullptr, nullptr, nullptr, 0, nullptr);
   }
   return cudaGetLastError();
 }

@@ -430,7 +430,19 @@ __device__ __forceinline__ int tm_epilogue(const SolveArgs& a, const V (&xv)[E],
       const uint32_t word = (uint32_t)lab[4 * w] | ((uint32_t)lab[4 * w + 1] << 8) |
                             ((uint32_t)lab[4 * w + 2] << 16) | ((uint32_t)lab[4 * w + 3] << 24);
       if (a.labels) reinterpret_cast<uint32_t*>(a.labels + q0)[w] = word;
-      if (a.txl) errs += __popc(word ^ __ldg(reinterpret_cast<const uint32_t*>(a.txl + q0) + w));
+      if (a.txl) {
+        if (!a.txpk) {
+          errs += __popc(word ^ __ldg(reinterpret_cast<const uint32_t*>(a.txl + q0) + w));
+        } else if constexpr (BA <= 2) {  // four symbols = 2 BA bits each, LSB-first: 8 or 16 bits
+          constexpr int SB = 2 * BA;
+          const uint32_t mine = (uint32_t)lab[4 * w] | ((uint32_t)lab[4 * w + 1] << SB) |
+                                ((uint32_t)lab[4 * w + 2] << (2 * SB)) | ((uint32_t)lab[4 * w + 3] << (3 * SB));
+          const size_t q = q0 + 4 * w;
+          const uint32_t tx = SB == 4 ? (uint32_t)__ldg(reinterpret_cast<const uint16_t*>(a.txl + (q >> 1)))
+                                      : (uint32_t)__ldg(a.txl + (q >> 2));
+          errs += __popc(mine ^ tx);
+        }  // (64-QAM labels are never packed: the ABI rejects it)
+      }
     }
     return errs;
   }
@@ -616,7 +628,7 @@ __global__ void __launch_bounds__(MAXT, 1) sscga_tm_kernel(const SolveArgs a) {
         const size_t qn = qown + (size_t)a.n_clusters * a.MN;
 #pragma unroll
         for (int c0 = 0; c0 < R; c0 += 16) asm volatile("prefetch.global.L2 [%0];" :: "l"(y + qn + c0));
-        if (a.txl) asm volatile("prefetch.global.L2 [%0];" :: "l"(a.txl + qn));
+        if (a.txl) asm volatile("prefetch.global.L2 [%0];" :: "l"(tx_label_ptr(a.txl, qn, a.bps, a.txpk)));
       }
     }
     if (lead && a.berr) a.berr[f] = 0;

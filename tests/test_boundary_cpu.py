@@ -18,7 +18,7 @@ def test_exports_every_header_symbol(lib):
     assert len(names) >= 12
     for n in names:
         assert hasattr(lib, n), n
-    assert lib.ddb_abi_version() == nat.ABI_VERSION == 2
+    assert lib.ddb_abi_version() == nat.ABI_VERSION == 3
     assert b"sm_100a" in lib.ddb_build_info()
 
 
@@ -159,3 +159,13 @@ class TestHostMirror:
         pkg = pathlib.Path(nat.__file__).parent
         for f in pkg.rglob("*.py"):
             assert "oracle" not in f.read_text().replace("oracle_check", ""), f
+
+
+def test_pack_labels_layout():
+    import torch
+    from paper_2604_02266_b200 import pack_labels
+    lab = torch.tensor([[1, 2, 3, 0, 15, 14, 13, 12]], dtype=torch.uint8)
+    assert pack_labels(lab & 3, 2).tolist() == [[1 | 2 << 2 | 3 << 4, 3 | 2 << 2 | 1 << 4]]
+    assert pack_labels(lab, 4).tolist() == [[0x21, 0x03, 0xEF, 0xCD]]
+    with pytest.raises(ValueError):
+        pack_labels(lab, 6)

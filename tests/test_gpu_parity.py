@@ -239,6 +239,9 @@ def test_batched_fp32_parity(pkg, name, fp32_kernel):
         # fused bit-error count == Hamming distance of the fused labels
         want = int(np.unpackbits((labels[f] ^ d["tx_labels"][f])[:, None], axis=1).sum())
         assert int(res.bit_errors[f]) == want
+    # TX labels packed bps bits per symbol (include/ddb.h tx_labels_packed) count the same errors
+    res_p = s.solve(y, paths, torch.as_tensor(d["lam"]), tx_labels=pkg.pack_labels(tx, b))
+    assert torch.equal(res_p.bit_errors.cpu(), res.bit_errors.cpu())
     # LLR signs reproduce the fused hard decisions
     llr = res.llr.cpu().numpy()
     bits = ((labels[..., None] >> np.arange(b - 1, -1, -1)) & 1).astype(bool)
