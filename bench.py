@@ -372,10 +372,27 @@ def main():
         s.detect(pil, 0.08)
         b.record(stream)
         b.synchronize()
+        det_ms = a.elapsed_time(b)
+        # the whole receiver from time-domain pilot and data frames (SsCgaSolver.receive)
+        from paper_2604_02266_b200.synth import time_domain_frames
+        pil_rx, dat_rx = time_domain_frames(s, fb)
+        for _ in range(2):
+            rres = s.receive(pil_rx, dat_rx, fb.lam, 0.08, tx_labels=fb.tx_labels, trace=False)
+        torch.cuda.synchronize()
+        a.record(stream)
+        rres = s.receive(pil_rx, dat_rx, fb.lam, 0.08, tx_labels=fb.tx_labels, trace=False)
+        b.record(stream)
+        b.synchronize()
+        rx_ms = a.elapsed_time(b)
+        rx_ber = int(rres.bit_errors.sum().item()) / (B * MN * bps)
+        del pil_rx, dat_rx, rres
         frontend = {"dzt_ms": dzt_ms, "dzt_gbs": dzt_gbs, "dzt_hbm_frac": dzt_gbs / hbm_peak,
-                    "dzt_bytes_per_frame": MN * 16, "detect_ms_per_batch": a.elapsed_time(b),
+                    "receiver_ms": rx_ms, "receiver_sym_s": B * MN / (rx_ms * 1e-3), "receiver_ber": rx_ber,
+                    "dzt_bytes_per_frame": MN * 16, "detect_ms_per_batch": det_ms,
                     "what": "ddb_dzt fp32 batch (zak.py:50-55) vs HBM peak; pilot path = fp64 DZT + estimate_heff "
-                            "+ detect_paths + CSR for the batch (pilot.py:40-49, sparse.py:69-88)"}
+                            "+ detect_paths + CSR for the batch (pilot.py:40-49, sparse.py:69-88); receiver = "
+                            "SsCgaSolver.receive on time-domain pilot + data frames (harness.py:156-194): pilot "
+                            "path, data DZT, fused solve + demod + bit errors"}
 
     # ---- single-frame latency: CUDA graph of a batch-1 solve, replayed
     latency = None

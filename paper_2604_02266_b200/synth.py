@@ -85,3 +85,29 @@ def make_frames(solver: SsCgaSolver, B: int, snr_db: float = 25.0, nu_max_hz: fl
         lam = torch.full((B,), 1.0 / snr, dtype=solver.rdtype, device=dev)
     return FrameBatch(y=y, x=x, tx_labels=labels.to(torch.uint8).contiguous(), paths=paths, lam=lam,
                       snr_db=snr_db)
+
+
+def time_domain_frames(solver: SsCgaSolver, fb: FrameBatch, seed: int = 1) -> tuple[torch.Tensor, torch.Tensor]:
+    """Received pilot and data frames in the time domain for the batched receiver
+    (`SsCgaSolver.receive`), from a DD-domain FrameBatch: the point pilot of
+    pilot.py:18-26 through the same channel plus AWGN at the frame's SNR, and
+    both frames taken to the time domain by the inverse Zak transform
+    x[k + nM] = (1/sqrt N) sum_l X[k, l] e^{+j2pi n l/N} (zak.py:14-21), i.e.
+    ddb_dzt with the conjugate kernel.  The transform is unitary, so the AWGN
+    statistics are the DD domain's.  Benchmark input generation only."""
+    from .zak import build_zak_kernel, dzt_device
+    dev, B, M, N, MN = solver.device, fb.y.shape[0], solver.M, solver.N, solver.MN
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(seed)
+    pil = torch.zeros(B, MN, dtype=solver.cdtype, device=dev)
+    pil[:, (N // 2) * M + M // 2] = float(np.sqrt(MN))
+    hp = solver.apply(pil, fb.paths)
+    if not np.isinf(fb.snr_db):
+        snr = 10.0 ** (fb.snr_db / 10.0)
+        sigma = torch.sqrt((hp.real ** 2 + hp.imag ** 2).mean(dim=1, keepdim=True) / snr / 2)
+        hp = hp + sigma * torch.complex(torch.randn(B, MN, generator=gen, device=dev, dtype=solver.rdtype),
+                                        torch.randn(B, MN, generator=gen, device=dev, dtype=solver.rdtype))
+    kinv = torch.as_tensor(np.conj(build_zak_kernel(N)), device=dev).to(solver.cdtype)
+    pilot_rx = dzt_device(hp.contiguous(), M, N, kernel=kinv, colmajor=True)
+    data_rx = dzt_device(fb.y, M, N, kernel=kinv, colmajor=True)
+    return pilot_rx, data_rx
