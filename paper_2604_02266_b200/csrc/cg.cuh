@@ -92,35 +92,10 @@ __device__ __forceinline__ void cl_sync(int C) {
   else __syncthreads();
 }
 
-// Deterministic cluster-wide sum of a pair of partials.  slot: this CTA's [32]
-// pair array for the reduction kind / parity in use.  Contains the barrier.
-// Lane i of every warp sums the per-warp pairs i, i+32, ... of the whole
-// cluster (rank-major), then the warp butterflies: every warp of every CTA
-// gets bit-identical totals.  (r0, w0): lane's first (rank, warp) slot.
-//
-// Small clusters (C * nwarps <= kPushSlots) push: lane r of every warp stores
-// the warp's pair into slot[rank * nwarps + warp] of CTA r before the barrier
-// (remote stores are released by barrier.cluster.arrive.release), so after it
-// every read is a local shared-memory load.  Larger clusters pull the peers'
-// per-warp pairs through DSMEM after the barrier.
+// Reduction buffers: [2 kinds][2 parities][kPushSlots] pairs.  red_read sums
+// `total` per-warp pairs of slot in a fixed order (the one-CTA case of the
+// two-level reduction below, and the pull of peers' pairs for large clusters).
 constexpr int kPushSlots = 64;
-
-// Publish this warp's pair (before the cluster barrier's arrive).
-template <typename T>
-__device__ __forceinline__ void red_push(Vec<T> part, Vec<T>* slot, int C, int nwarps, int lane, int warp, int rank) {
-  part.x = warp_sum(part.x);
-  part.y = warp_sum(part.y);
-  if (C * nwarps <= kPushSlots) {
-    const int idx = rank * nwarps + warp;
-    if (C == 1) {
-      if (lane == 0) slot[idx] = part;
-    } else if (lane < C) {
-      st_cluster(map_rank(smem_addr(slot + idx), lane), part);
-    }
-  } else if (lane == 0) {
-    slot[warp] = part;
-  }
-}
 
 // Cluster-wide total (after the cluster barrier's wait); identical in every warp.
 template <typename T>
@@ -173,6 +148,57 @@ __device__ __forceinline__ Vec<T> red_read(const Vec<T>* slot, int C, int nwarps
   s.x = warp_sum(s.x);
   s.y = warp_sum(s.y);
   return s;
+}
+
+// Two-level deterministic cluster reduction of a pair (e.g. ||u||^2, ||p||^2).
+// base = this reduction's buffer (kind, parity): base[0 .. 32) per-warp
+// partials of this CTA, base[32 + r] CTA r's total.
+//   red_stage       (before the barrier)  every warp publishes its partial;
+//   cl_arrive_red   (the barrier's arrive half) after the CTA barrier warp 0
+//                   folds the CTA's partials with a fixed xor-tree (bit-identical
+//                   in every lane) and pushes the total to every CTA of the
+//                   cluster, then the cluster arrive releases it.  relaxed: no
+//                   peer reads this CTA's shared memory in this phase, so only
+//                   warp 0 needs release semantics (cluster-scope fences are the
+//                   most expensive part of a cluster barrier);
+//   red_total       (after the wait) the C totals summed in rank order, so every
+//                   warp of every CTA holds the same bits and takes the same branch.
+// One CTA (C == 1) reads the per-warp partials directly instead.
+template <typename T>
+__device__ __forceinline__ void red_stage(Vec<T> part, Vec<T>* base, int warp, int lane) {
+  part.x = warp_sum(part.x);
+  part.y = warp_sum(part.y);
+  if (lane == 0) base[warp] = part;
+}
+__device__ __forceinline__ void cl_arrive_sem(bool release) {
+  if (release) asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+  else asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
+}
+template <typename T, bool TMEM_FENCES>
+__device__ __forceinline__ void cl_arrive_red(int C, Vec<T>* base, int nwarps, int warp, int lane, int rank,
+                                              bool relaxed) {
+  if constexpr (TMEM_FENCES) {
+    tmem_wait_st();
+    tmem_fence_before();
+  }
+  __syncthreads();
+  if (C > 1) {
+    if (warp == 0) {
+      Vec<T> t = lane < nwarps ? base[lane] : czero<Vec<T>>();
+      t.x = warp_sum(t.x);
+      t.y = warp_sum(t.y);
+      if (lane < C) st_cluster(map_rank(smem_addr(base + 32 + rank), (uint32_t)lane), t);
+    }
+    cl_arrive_sem(!relaxed || warp == 0);
+  }
+  if constexpr (TMEM_FENCES) tmem_fence_after();
+}
+template <typename T>
+__device__ __forceinline__ Vec<T> red_total(int C, const Vec<T>* base, int nwarps) {
+  if (C == 1) return red_read<T>(base, 1, nwarps, 0);
+  Vec<T> t = base[32];
+  for (int r = 1; r < C; ++r) t = cadd(t, base[32 + r]);
+  return t;
 }
 
 // Split cluster barrier: arrive (release) -> CTA barrier -> ... -> wait (acquire).

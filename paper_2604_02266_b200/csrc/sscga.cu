@@ -569,6 +569,9 @@ __global__ void __launch_bounds__(sscga_max_threads(sizeof(T), LC), 1) sscga_ker
       }
       __syncthreads();
     }
+    // every tap of the frame is local (d_l == 0 inside the halo): no peer reads
+    // this CTA's shared memory, so the cluster arrives can be relaxed
+    const bool relaxed = fc.split && fc.m1 == 0u;
 
     const int RS = a.RS;
     const int gcol = cx.g * LC;
@@ -627,15 +630,15 @@ __global__ void __launch_bounds__(sscga_max_threads(sizeof(T), LC), 1) sscga_ker
     }
     V* slot = red + (1 * 2 + par[1]) * kPushSlots;
     par[1] ^= 1;
-    red_push<T>(cmake<V>(nrm.x + nrm.y, T(0)), slot, a.C, nwarps, lane, warp, cx.rank);
+    red_stage<T>(cmake<V>(nrm.x + nrm.y, T(0)), slot, warp, lane);
     prof_mark(a.prof, psm, kArrive);
-    cl_arrive(a.C);  // c = b published
+    cl_arrive_red<T, false>(a.C, slot, nwarps, warp, lane, cx.rank, relaxed);  // c = b published
     prof_mark(a.prof, psm, kMvmLocal);
     sk = ss_mvm_local<T, LC, false>(a, cx, sm, fc, sm.c, fc.lo_c, acc);
     prof_mark(a.prof, psm, kWait);
     cl_wait(a.C);
     prof_mark(a.prof, psm, kRead);
-    T cn = red_read<T>(slot, a.C, nwarps, lane).x;
+    T cn = red_total<T>(a.C, slot, nwarps).x;
     T beta = T(0);
     if (lead && cnorm) cnorm[(size_t)f * stride] = cn;
 
@@ -681,9 +684,9 @@ __global__ void __launch_bounds__(sscga_max_threads(sizeof(T), LC), 1) sscga_ker
       if (!cx.active) nu = np = czero<V>();
       slot = red + (0 * 2 + par[0]) * kPushSlots;
       par[0] ^= 1;
-      red_push<T>(cmake<V>(nu.x + nu.y, np.x + np.y), slot, a.C, nwarps, lane, warp, cx.rank);
+      red_stage<T>(cmake<V>(nu.x + nu.y, np.x + np.y), slot, warp, lane);
       prof_mark(a.prof, psm, kArrive);
-      cl_arrive(a.C);  // u published
+      cl_arrive_red<T, false>(a.C, slot, nwarps, warp, lane, cx.rank, relaxed);  // u published
       // ap = H^H u + lam p;  x += alpha p;  c -= alpha ap      (equalize.py:60-70)
       prof_mark(a.prof, psm, kMvmLocal);
       sk = ss_mvm_local<T, LC, true>(a, cx, sm, fc, sm.u, fc.lo_u, acc);
@@ -692,7 +695,7 @@ __global__ void __launch_bounds__(sscga_max_threads(sizeof(T), LC), 1) sscga_ker
       prof_mark(a.prof, psm, kMvmRemote);
       ss_mvm_remote<T, LC, true>(a, cx, sm, fc, sm.u, fc.lo_u, sk, acc);
       prof_mark(a.prof, psm, kRead);
-      const V up = red_read<T>(slot, a.C, nwarps, lane);
+      const V up = red_total<T>(a.C, slot, nwarps);
       prof_mark(a.prof, psm, kStep3);
       const T denom = up.x + lam * up.y;  // ||H p||^2 + lam ||p||^2 = Re p^H (H^H H + lam I) p
       if (denom == T(0)) {  // equalize.py:64-67
@@ -731,15 +734,15 @@ __global__ void __launch_bounds__(sscga_max_threads(sizeof(T), LC), 1) sscga_ker
       else nc = czero<V>();
       slot = red + (1 * 2 + par[1]) * kPushSlots;
       par[1] ^= 1;
-      red_push<T>(cmake<V>(nc.x + nc.y, T(0)), slot, a.C, nwarps, lane, warp, cx.rank);
+      red_stage<T>(cmake<V>(nc.x + nc.y, T(0)), slot, warp, lane);
       prof_mark(a.prof, psm, kArrive);
-      cl_arrive(a.C);  // c published
+      cl_arrive_red<T, false>(a.C, slot, nwarps, warp, lane, cx.rank, relaxed);  // c published
       prof_mark(a.prof, psm, kMvmLocal);
       if (it + 1 < a.iters) sk = ss_mvm_local<T, LC, false>(a, cx, sm, fc, sm.c, fc.lo_c, acc);  // next H c
       prof_mark(a.prof, psm, kWait);
       cl_wait(a.C);
       prof_mark(a.prof, psm, kRead);
-      const T nn = red_read<T>(slot, a.C, nwarps, lane).x;
+      const T nn = red_total<T>(a.C, slot, nwarps).x;
       beta = nn / cn;
       cn = nn;
       done = it + 1;

@@ -344,12 +344,7 @@ __device__ __forceinline__ void put_col(V* colp, int rr, int M, int lo, int hi, 
 // Barrier halves around TMEM traffic: stores of every warp complete and are
 // ordered before the CTA barrier; loads after it see them.
 // relaxed: no peer reads this CTA's shared memory in the current phase (the
-// frame has no DSMEM taps), so only warp 0 (the reduction push) needs release
-// semantics at cluster scope; the other warps skip the cluster-scope fence.
-__device__ __forceinline__ void cl_arrive_sem(bool release) {
-  if (release) asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
-  else asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
-}
+// frame has no DSMEM taps): see cl_arrive_red (cg.cuh).
 __device__ __forceinline__ void tm_arrive(int C, bool relaxed = false) {
   tmem_wait_st();
   tmem_fence_before();
@@ -358,43 +353,9 @@ __device__ __forceinline__ void tm_arrive(int C, bool relaxed = false) {
   tmem_fence_after();
 }
 
-// Two-level deterministic cluster reduction of a pair (e.g. ||u||^2, ||p||^2).
-// base = this reduction's buffer (kind, parity): base[0 .. 32) per-warp
-// partials of this CTA, base[32 + r] CTA r's total.
-//   red_stage   (before the barrier)  every warp publishes its partial;
-//   tm_arrive_red (the barrier's arrive half) after the CTA barrier warp 0
-//               folds the CTA's partials with a fixed xor-tree (bit-identical
-//               in every lane) and pushes the total to every CTA of the
-//               cluster, then the cluster arrive releases it;
-//   red_total   (after the wait) the C totals summed in rank order, so every
-//               warp of every CTA holds the same bits and takes the same branch.
-// One CTA (C == 1) reads the per-warp partials directly instead.
-__device__ __forceinline__ void red_stage(V part, V* base, int warp, int lane) {
-  part.x = warp_sum(part.x);
-  part.y = warp_sum(part.y);
-  if (lane == 0) base[warp] = part;
-}
 __device__ __forceinline__ void tm_arrive_red(int C, V* base, int nwarps, int warp, int lane, int rank,
                                               bool relaxed = false) {
-  tmem_wait_st();
-  tmem_fence_before();
-  __syncthreads();
-  if (C > 1) {
-    if (warp == 0) {
-      V t = lane < nwarps ? base[lane] : make_float2(0.f, 0.f);
-      t.x = warp_sum(t.x);
-      t.y = warp_sum(t.y);
-      if (lane < C) st_cluster(map_rank(smem_addr(base + 32 + rank), (uint32_t)lane), t);
-    }
-    cl_arrive_sem(!relaxed || warp == 0);
-  }
-  tmem_fence_after();
-}
-__device__ __forceinline__ V red_total(int C, const V* base, int nwarps) {
-  if (C == 1) return red_read<float>(base, 1, nwarps, 0);
-  V t = base[32];
-  for (int r = 1; r < C; ++r) t = cadd(t, base[32 + r]);
-  return t;
+  cl_arrive_red<float, true>(C, base, nwarps, warp, lane, rank, relaxed);
 }
 
 // Epilogue for E equalized symbols of rows rr.. (contiguous in q): x_hat,
@@ -658,7 +619,7 @@ __global__ void __launch_bounds__(MAXT, 1) sscga_tm_kernel(const SolveArgs a) {
         tm_st<E>(tC(c0), w);  // c = b
         put_col<E>(ccol, th.r0 + c0, M, lo_c, hi_c, twl, w);
       }
-      red_stage(make_float2(nrm.x + nrm.y, 0.f), red + (2 + par1) * kPushSlots, warp, lane);
+      red_stage<float>(make_float2(nrm.x + nrm.y, 0.f), red + (2 + par1) * kPushSlots, warp, lane);
     }
     if constexpr (PROF) prof_mark(a.prof, psm, kArrive);
     tm_arrive_red(a.C, red + (2 + par1) * kPushSlots, nwarps, warp, lane, rank, !fs.remote);  // c = b published
@@ -667,7 +628,7 @@ __global__ void __launch_bounds__(MAXT, 1) sscga_tm_kernel(const SolveArgs a) {
     if constexpr (PROF) prof_mark(a.prof, psm, kWait);
     cl_wait(a.C);
     if constexpr (PROF) prof_mark(a.prof, psm, kRead);
-    float cn = red_total(a.C, red + (2 + par1) * kPushSlots, nwarps).x;
+    float cn = red_total<float>(a.C, red + (2 + par1) * kPushSlots, nwarps).x;
     par1 ^= 1;
     float beta = 0.f;
     if (lead && a.cnorm) reinterpret_cast<float*>(a.cnorm)[(size_t)f * stride] = cn;
@@ -708,7 +669,7 @@ __global__ void __launch_bounds__(MAXT, 1) sscga_tm_kernel(const SolveArgs a) {
           tm_st<E>(tP(c0), pv);
           put_col<E>(ucol, th.r0 + c0, M, lo_u, hi_u, twl, w);
         }
-        red_stage(make_float2(nu.x + nu.y, np.x + np.y), red + par0 * kPushSlots, warp, lane);
+        red_stage<float>(make_float2(nu.x + nu.y, np.x + np.y), red + par0 * kPushSlots, warp, lane);
       }
       if constexpr (PROF) prof_mark(a.prof, psm, kArrive);
       tm_arrive_red(a.C, red + par0 * kPushSlots, nwarps, warp, lane, rank, !fs.remote);  // u published
@@ -720,7 +681,7 @@ __global__ void __launch_bounds__(MAXT, 1) sscga_tm_kernel(const SolveArgs a) {
       if constexpr (PROF) prof_mark(a.prof, psm, kMvmRemote);
       mvm_remote<R, true>(a, th, sm, fs, sm.u, acc);
       if constexpr (PROF) prof_mark(a.prof, psm, kRead);
-      const V up = red_total(a.C, red + par0 * kPushSlots, nwarps);
+      const V up = red_total<float>(a.C, red + par0 * kPushSlots, nwarps);
       par0 ^= 1;
       if constexpr (PROF) prof_mark(a.prof, psm, kStep3);
       const float denom = up.x + lam * up.y;  // ||H p||^2 + lam ||p||^2 = Re p^H (H^H H + lam I) p
@@ -763,7 +724,7 @@ __global__ void __launch_bounds__(MAXT, 1) sscga_tm_kernel(const SolveArgs a) {
             for (int i = 0; i < E; ++i) sp[i] = xv[i];
           }
         }
-        red_stage(make_float2(nc.x + nc.y, 0.f), red + (2 + par1) * kPushSlots, warp, lane);
+        red_stage<float>(make_float2(nc.x + nc.y, 0.f), red + (2 + par1) * kPushSlots, warp, lane);
       }
       if constexpr (PROF) prof_mark(a.prof, psm, kArrive);
       tm_arrive_red(a.C, red + (2 + par1) * kPushSlots, nwarps, warp, lane, rank, !fs.remote);  // c published
@@ -772,7 +733,7 @@ __global__ void __launch_bounds__(MAXT, 1) sscga_tm_kernel(const SolveArgs a) {
       if constexpr (PROF) prof_mark(a.prof, psm, kWait);
       cl_wait(a.C);
       if constexpr (PROF) prof_mark(a.prof, psm, kRead);
-      const float nn = red_total(a.C, red + (2 + par1) * kPushSlots, nwarps).x;
+      const float nn = red_total<float>(a.C, red + (2 + par1) * kPushSlots, nwarps).x;
       par1 ^= 1;
       beta = nn / cn;
       cn = nn;
