@@ -466,7 +466,8 @@ def test_ber_decreases_with_snr(pkg):
     assert all(b2 <= b1 for b1, b2 in zip(bers, bers[1:])), bers
 
 
-def test_host_pipeline_matches_device_solve(pkg):
+@pytest.mark.parametrize("packed", [False, True])
+def test_host_pipeline_matches_device_solve(pkg, packed):
     from paper_2604_02266_b200.synth import make_frames
     s = solver_for(pkg, 256, 16, 10, "fp32", 4)
     fb = make_frames(s, 40, snr_db=20.0, seed=2)
@@ -475,10 +476,29 @@ def test_host_pipeline_matches_device_solve(pkg):
     pin = lambda t: t.cpu().pin_memory()  # noqa: E731
     labels = torch.empty(40, s.MN, dtype=torch.uint8).pin_memory()
     errs = torch.empty(40, dtype=torch.int32).pin_memory()
+    tx = pkg.pack_labels(fb.tx_labels, 4) if packed else fb.tx_labels
     pipe.run(pin(fb.y), tuple(pin(t) for t in (fb.paths.offsets, fb.paths.k, fb.paths.l, fb.paths.gain)),
-             pin(fb.lam), pin(fb.tx_labels), labels, errs)
+             pin(fb.lam), pin(tx), labels, errs)
     assert torch.equal(labels, ref.labels.cpu())
     assert torch.equal(errs, ref.bit_errors.cpu())
+
+
+def test_receiver_flags_frames_without_pilot_energy(pkg):
+    """A frame whose received pilot is all zeros has no taps (detect_paths returns
+    [] when the peak is 0, sparse.py:81-82): EmptyChannel semantics on the device,
+    status 1, no NaNs, and run_packet's scoring of a failed packet (harness.py:170-178)."""
+    d = load_golden("frontend")
+    M, N, iters, b = (int(v) for v in d["c1_meta"])
+    s = solver_for(pkg, M, N, iters, "fp32", b)
+    pil = torch.as_tensor(d["c1_pilot_rx"], device="cuda").clone()
+    pil[1] = 0
+    res = s.receive(pil, torch.as_tensor(d["c1_data_rx"], device="cuda"), torch.as_tensor(d["c1_lam"]),
+                    float(d["c1_theta"]), tx_labels=torch.as_tensor(d["c1_tx_labels"], device="cuda"))
+    status = res.status.cpu().numpy()
+    assert status[1] & 1 and not (status[0] & 1) and not (status[2] & 1)
+    assert torch.isfinite(torch.view_as_real(res.x)).all()
+    assert int(res.bit_errors[1]) == b * M * N // 2
+    assert float(res.x[1].abs().max()) == 0.0
 
 
 # ---------------------------------------------------------------- receiver front end (row f1)
