@@ -173,6 +173,8 @@ int32_t ddb_detect_paths(int32_t batch, int32_t M, int32_t N, const void* heff, 
  *      e^{-j2pi K0 (l-L0)/(MN)} and divides by `amplitude` (estimate_heff). */
 #define DDB_DZT_COLMAJOR 1
 #define DDB_DZT_PILOT 2
+#define DDB_DZT_INPUT_F32 4  /* dtype f64 with complex64 y_time (fp64 arithmetic on
+                                single-precision samples); default kernel, power-of-two N */
 int32_t ddb_dzt(int32_t batch, int32_t M, int32_t N, int32_t dtype, const void* y_time, const void* kernel,
                 int32_t flags, double amplitude, void* out, void* stream);
 
@@ -197,6 +199,8 @@ int32_t ddb_probe_fp32(int32_t mode, int32_t blocks, int32_t iters, float* scrat
  *      e^{-j2pi K0 (l-L0)/(MN)} and divides by `amplitude` (estimate_heff). */
 #define DDB_DZT_COLMAJOR 1
 #define DDB_DZT_PILOT 2
+#define DDB_DZT_INPUT_F32 4  /* dtype f64 with complex64 y_time (fp64 arithmetic on
+                                single-precision samples); default kernel, power-of-two N */
 int32_t ddb_dzt(int32_t batch, int32_t M, int32_t N, int32_t dtype, const void* y_time, const void* kernel,
                 int32_t flags, double amplitude, void* out, void* stream);
 

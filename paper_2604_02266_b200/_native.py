@@ -57,6 +57,7 @@ class Outputs(C.Structure):
 ABI_VERSION = 3  # include/ddb.h DDB_ABI_VERSION
 DDB_DZT_COLMAJOR = 1
 DDB_DZT_PILOT = 2
+DDB_DZT_INPUT_F32 = 4
 
 
 class Plan(C.Structure):

@@ -272,8 +272,8 @@ class SsCgaSolver:
             raise ValueError("theta must be nonnegative")
         B = pilot_rx.shape[0]
         amp = float(np.sqrt(self.MN)) if amplitude is None else float(amplitude)
-        heff = dzt_device(pilot_rx.to(device=self.device, dtype=torch.complex128), self.M, self.N,
-                          colmajor=False, pilot_amplitude=amp, stream=stream)
+        heff = dzt_device(pilot_rx.to(device=self.device), self.M, self.N, colmajor=False, pilot_amplitude=amp,
+                          stream=stream, fp64=True)
         cnt = torch.empty(B, dtype=torch.int32, device=self.device)
         kk = torch.empty(B, max_paths, dtype=torch.int32, device=self.device)
         ll = torch.empty(B, max_paths, dtype=torch.int32, device=self.device)

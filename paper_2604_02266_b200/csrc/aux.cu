@@ -163,81 +163,73 @@ __device__ __forceinline__ double block_max(double v, double* scratch) {
   return v;
 }
 
-// exclusive block scan of ints; returns the block total through *total
-__device__ __forceinline__ int block_exscan(int v, int* scratch, int* total) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  int incl = v;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const int t = __shfl_up_sync(0xffffffffu, incl, o);
-    if (lane >= o) incl += t;
-  }
-  if (lane == 31) scratch[warp] = incl;
-  __syncthreads();
-  if (warp == 0) {
-    int w = lane < nw ? scratch[lane] : 0;
-    int wi = w;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const int t = __shfl_up_sync(0xffffffffu, wi, o);
-      if (lane >= o) wi += t;
-    }
-    if (lane < nw) scratch[lane] = wi - w;
-    if (lane == nw - 1) scratch[32] = wi;
-  }
-  __syncthreads();
-  const int res = scratch[warp] + incl - v;
-  *total = scratch[32];
-  __syncthreads();
-  return res;
-}
-
+// |h| is evaluated once per bin into shared memory when the frame fits (else
+// re-read), candidates are compacted in row-major order with warp ballots over
+// coalesced bin ranges, then ranked.
 __global__ void __launch_bounds__(kDetectThreads) detect_paths_kernel(
-    int M, int N, const double2* __restrict__ heff, double theta, int max_paths, int cap,
+    int M, int N, const double2* __restrict__ heff, double theta, int max_paths, int cap, int mag_smem,
     int* count, int* pk, int* pl, double2* ph) {
   extern __shared__ __align__(16) unsigned char smem[];
-  double* cmag = reinterpret_cast<double*>(smem);          // [cap]
-  int* cidx = reinterpret_cast<int*>(cmag + cap);           // [cap]
-  __shared__ double dscratch[32];
-  __shared__ int iscratch[33];
-  const int f = blockIdx.x;
   const int n = M * N;
+  double* mag = reinterpret_cast<double*>(smem);                        // [n] when mag_smem
+  int* cidx = reinterpret_cast<int*>(mag + (mag_smem ? n : 0));         // [cap]
+  __shared__ double dscratch[32];
+  __shared__ int wcount[32];
+  __shared__ int running;
+  const int f = blockIdx.x;
   const double2* h = heff + (size_t)f * n;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   double peak = 0.0;
-  for (int i = threadIdx.x; i < n; i += blockDim.x) peak = fmax(peak, np_cabs(h[i].x, h[i].y));
-  peak = block_max(peak, dscratch);
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    const double m = np_cabs(h[i].x, h[i].y);
+    if (mag_smem) mag[i] = m;
+    peak = fmax(peak, m);
+  }
+  peak = block_max(peak, dscratch);  // (contains the barriers that publish mag)
   if (peak == 0.0) {  // sparse.py:81-82
     if (threadIdx.x == 0) count[f] = 0;
     return;
   }
   const double thr = theta * peak;
-  const int chunk = (n + blockDim.x - 1) / blockDim.x;
-  const int i0 = threadIdx.x * chunk;
-  const int i1 = min(n, i0 + chunk);
-  int mine = 0;
-  for (int i = i0; i < i1; ++i) mine += np_cabs(h[i].x, h[i].y) > thr;
-  int total = 0;
-  int pos = block_exscan(mine, iscratch, &total);
+  if (threadIdx.x == 0) running = 0;
+  __syncthreads();
+  // order-preserving compaction of {i : |h_i| > thr} (np.nonzero on the (M, N) frame)
+  for (int base = 0; base < n; base += blockDim.x) {
+    const int i = base + threadIdx.x;
+    const bool keep = i < n && (mag_smem ? mag[i] : np_cabs(h[i].x, h[i].y)) > thr;
+    const unsigned bal = __ballot_sync(0xffffffffu, keep);
+    if (lane == 0) wcount[warp] = __popc(bal);
+    __syncthreads();
+    int before = running;
+    for (int w = 0; w < warp; ++w) before += wcount[w];
+    const int pos = before + __popc(bal & ((1u << lane) - 1u));
+    if (keep && pos < cap) cidx[pos] = i;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int t = running;
+      for (int w = 0; w < nw; ++w) t += wcount[w];
+      running = t;
+    }
+    __syncthreads();
+  }
+  const int total = running;
   if (threadIdx.x == 0) count[f] = total > cap ? -1 : total;
   if (total > cap) return;  // -1: candidate list exceeds shared memory; host reports it
-  for (int i = i0; i < i1; ++i) {
-    const double m = np_cabs(h[i].x, h[i].y);
-    if (m > thr) { cmag[pos] = m; cidx[pos] = i; ++pos; }
-  }
-  __syncthreads();
+  // descending |h|, ties in row-major order (argsort kind="stable")
   for (int c = threadIdx.x; c < total; c += blockDim.x) {
-    const double m = cmag[c];
+    const int ic = cidx[c];
+    const double m = mag_smem ? mag[ic] : np_cabs(h[ic].x, h[ic].y);
     int rank = 0;
     for (int o = 0; o < total; ++o) {
-      const double mo = cmag[o];
+      const int io = cidx[o];
+      const double mo = mag_smem ? mag[io] : np_cabs(h[io].x, h[io].y);
       rank += (mo > m) || (mo == m && o < c);
     }
     if (rank < max_paths) {
-      const int i = cidx[c];
       const size_t out = (size_t)f * max_paths + rank;
-      pk[out] = i / N;
-      pl[out] = i - (i / N) * N;
-      ph[out] = h[i];
+      pk[out] = ic / N;
+      pl[out] = ic - (ic / N) * N;
+      ph[out] = h[ic];
     }
   }
 }
@@ -249,13 +241,16 @@ cudaError_t launch_detect_paths(int B, int M, int N, const void* heff, double th
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
   const int n = M * N;
-  int cap = (optin - 1024) / (int)(sizeof(double) + sizeof(int));
+  const int budget = optin - 2048;  // static shared memory of the kernel
+  // keep the frame's magnitudes on chip when they leave room for a candidate list
+  const int mag_smem = (size_t)n * sizeof(double) + 4096 * sizeof(int) <= (size_t)budget ? 1 : 0;
+  int cap = (budget - (mag_smem ? n * (int)sizeof(double) : 0)) / (int)sizeof(int);
   if (cap > n) cap = n;
-  const size_t smem = (size_t)cap * (sizeof(double) + sizeof(int));
+  const size_t smem = (mag_smem ? (size_t)n * sizeof(double) : 0) + (size_t)cap * sizeof(int);
   cudaError_t e = cudaFuncSetAttribute(detect_paths_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)smem);
   if (e != cudaSuccess) return e;
-  detect_paths_kernel<<<B, kDetectThreads, smem, st>>>(M, N, (const double2*)heff, theta, max_paths, cap,
+  detect_paths_kernel<<<B, kDetectThreads, smem, st>>>(M, N, (const double2*)heff, theta, max_paths, cap, mag_smem,
                                                        count, pk, pl, (double2*)ph);
   return cudaGetLastError();
 }

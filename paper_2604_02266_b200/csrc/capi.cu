@@ -452,16 +452,21 @@ int32_t ddb_dzt(int32_t batch, int32_t M, int32_t N, int32_t dtype, const void* 
   if (M < 1 || N < 1) return fail(DDB_ERR_SHAPE, "grid must be positive, got (%d,%d)", M, N);
   if ((long long)M * N >= (1LL << 29)) return fail(DDB_ERR_UNSUPPORTED, "grid too large");
   if (N > 256) return fail(DDB_ERR_UNSUPPORTED, "N=%d > 256 (kernel matrix exceeds shared memory)", N);
-  if (flags & ~(DDB_DZT_COLMAJOR | DDB_DZT_PILOT)) return fail(DDB_ERR_INVALID, "bad flags %d", flags);
+  if (flags & ~(DDB_DZT_COLMAJOR | DDB_DZT_PILOT | DDB_DZT_INPUT_F32)) return fail(DDB_ERR_INVALID, "bad flags %d", flags);
+  if ((flags & DDB_DZT_INPUT_F32) && (dtype != DDB_F64 || kernel || N < 2 || (N & (N - 1))))
+    return fail(DDB_ERR_UNSUPPORTED, "complex64 input needs dtype f64, the default kernel and a power-of-two N");
   if ((flags & DDB_DZT_PILOT) && !(amplitude > 0))
     return fail(DDB_ERR_INVALID, "pilot amplitude must be positive");  // pilot.py:45-46
   if ((flags & DDB_DZT_PILOT) && ((M & 1) || (N & 1)))
     return fail(DDB_ERR_SHAPE, "M and N must be even for the pilot estimate");  // grid.py:25-29
   if (batch == 0) return ok();
   if (!y_time || !out) return fail(DDB_ERR_INVALID, "null pointer");
-  cudaError_t e = ddb::launch_dzt(dtype == DDB_F64, batch, M, N, y_time, kernel, flags & DDB_DZT_COLMAJOR,
-                                  flags & DDB_DZT_PILOT, (flags & DDB_DZT_PILOT) ? amplitude : 1.0, out,
-                                  static_cast<cudaStream_t>(stream));
+  const double amp = (flags & DDB_DZT_PILOT) ? amplitude : 1.0;
+  cudaError_t e = (flags & DDB_DZT_INPUT_F32)
+                      ? ddb::launch_dzt_mixed(batch, M, N, y_time, flags & DDB_DZT_COLMAJOR, flags & DDB_DZT_PILOT, amp,
+                                              out, static_cast<cudaStream_t>(stream))
+                      : ddb::launch_dzt(dtype == DDB_F64, batch, M, N, y_time, kernel, flags & DDB_DZT_COLMAJOR,
+                                        flags & DDB_DZT_PILOT, amp, out, static_cast<cudaStream_t>(stream));
   if (e != cudaSuccess) return cuda_fail(e, "dzt launch");
   return ok();
 }

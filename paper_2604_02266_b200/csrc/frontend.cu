@@ -128,6 +128,67 @@ __global__ void __launch_bounds__(kDztThreads) dzt_blk_kernel(int M, int N, cons
   }
 }
 
+// Default kernel (build_zak_kernel(N), N a power of two): the same transform
+// as a radix-2 FFT along the N time blocks of every delay row, log2 N stages
+// of N/2 butterflies in shared memory instead of N complex MACs per element
+// (the GEMM form is kept for caller-supplied kernels).  The input is stored in
+// bit-reversed block order while it is loaded, so the decimation-in-time
+// stages leave the Doppler columns in natural order; twiddles come from exact
+// integer phases.  Same result to rounding (parity tolerances 1e-12 fp64).
+template <typename T, bool COLMAJOR, bool PILOT, typename VIN = Vec<T>>
+__global__ void __launch_bounds__(kDztThreads) dzt_fft_kernel(int M, int N, int logn, const VIN* __restrict__ y,
+                                                              T inv_amp, Vec<T>* __restrict__ out) {
+  using V = Vec<T>;
+  extern __shared__ __align__(16) unsigned char smem[];
+  V* xs = reinterpret_cast<V*>(smem);  // [N][kTk], block index bit-reversed
+  V* wn = xs + (size_t)N * kTk;        // [N/2]: W_N^{-e}
+  const int f = blockIdx.y;
+  const int k0 = blockIdx.x * kTk;
+  const int MN = M * N;
+  const VIN* yf = y + (size_t)f * MN;
+  for (int e = threadIdx.x; e < N / 2; e += blockDim.x) wn[e] = twiddle(T(0), mod_pos(-e, N), N);
+  for (int idx = threadIdx.x; idx < N * kTk; idx += blockDim.x) {
+    const int i = idx / kTk, kl = idx - i * kTk;
+    const int k = k0 + kl;
+    const int ir = (int)(__brev((unsigned)i) >> (32 - logn));
+    V v = czero<V>();
+    if (k < M) {
+      const VIN t = yf[k + (size_t)i * M];
+      v = cmake<V>(t.x, t.y);
+    }
+    xs[ir * kTk + kl] = v;
+  }
+  __syncthreads();
+  const int kl = threadIdx.x % kTk;
+  const int g0 = threadIdx.x / kTk, groups = blockDim.x / kTk;
+  for (int st = 0; st < logn; ++st) {
+    const int half = 1 << st;
+    for (int bf = g0; bf < N / 2; bf += groups) {
+      const int grp = bf >> st, pos = bf & (half - 1);
+      const int i0 = (grp << (st + 1)) + pos, i1 = i0 + half;
+      const V w = wn[pos << (logn - 1 - st)];
+      const V a0 = xs[i0 * kTk + kl];
+      const V t = cmul(w, xs[i1 * kTk + kl]);
+      xs[i0 * kTk + kl] = cadd(a0, t);
+      xs[i1 * kTk + kl] = csub(a0, t);
+    }
+    __syncthreads();
+  }
+  const T rs = T(1) / sqrt(T(N));
+  const int k = k0 + kl;
+  if (k >= M) return;
+  for (int l = g0; l < N; l += groups) {
+    V r = cscale(xs[l * kTk + kl], rs);
+    if constexpr (PILOT) {
+      const long long e = (long long)(M / 2) * (l - N / 2);
+      const int er = (int)(((-e) % MN + MN) % MN);
+      r = cscale(cmul(r, twiddle(T(0), er, MN)), inv_amp);
+    }
+    if constexpr (COLMAJOR) out[(size_t)f * MN + (size_t)l * M + k] = r;
+    else out[(size_t)f * MN + (size_t)k * N + l] = r;
+  }
+}
+
 template <typename T, bool COLMAJOR, bool PILOT>
 cudaError_t launch_dzt_t(int B, int M, int N, const void* y, const void* kern, double amp, void* out,
                          cudaStream_t st) {
@@ -141,6 +202,17 @@ cudaError_t launch_dzt_t(int B, int M, int N, const void* y, const void* kern, d
     kfn<<<grid, kDztThreads, smem, st>>>(M, N, (const V*)y, (const V*)kern, T(1.0 / amp), (V*)out);
     return cudaGetLastError();
   };
+  if (!kern && N >= 2 && (N & (N - 1)) == 0) {  // default kernel, power-of-two N: FFT
+    int logn = 0;
+    while ((1 << logn) < N) ++logn;
+    const size_t fsmem = ((size_t)N * kTk + N / 2) * sizeof(V);
+    cudaError_t e = cudaFuncSetAttribute(dzt_fft_kernel<T, COLMAJOR, PILOT>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fsmem);
+    if (e != cudaSuccess) return e;
+    dzt_fft_kernel<T, COLMAJOR, PILOT><<<grid, kDztThreads, fsmem, st>>>(M, N, logn, (const V*)y, T(1.0 / amp),
+                                                                        (V*)out);
+    return cudaGetLastError();
+  }
   if (N % groups == 0) {
     switch (N / groups) {
       case 1: return run(dzt_blk_kernel<T, COLMAJOR, PILOT, 1>);
@@ -163,6 +235,34 @@ __global__ void estimate_heff_kernel(long long count, const Vec<T>* __restrict__
 }
 
 }  // namespace
+
+// fp64 arithmetic on complex64 samples (the pilot path: no separate widening
+// pass); default kernel, power-of-two N.
+template <bool COLMAJOR, bool PILOT>
+cudaError_t launch_dzt_mixed_t(int B, int M, int N, const void* y, double amp, void* out, cudaStream_t st) {
+  int logn = 0;
+  while ((1 << logn) < N) ++logn;
+  const size_t fsmem = ((size_t)N * kTk + N / 2) * sizeof(double2);
+  auto kfn = dzt_fft_kernel<double, COLMAJOR, PILOT, float2>;
+  cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fsmem);
+  if (e != cudaSuccess) return e;
+  dim3 grid((M + kTk - 1) / kTk, B);
+  kfn<<<grid, kDztThreads, fsmem, st>>>(M, N, logn, (const float2*)y, 1.0 / amp, (double2*)out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_dzt_mixed(int B, int M, int N, const void* y, int colmajor, int pilot, double amp, void* out,
+                             cudaStream_t st) {
+  if (B == 0) return cudaSuccess;
+  if (N < 2 || (N & (N - 1))) return cudaErrorInvalidValue;
+  const int sel = (colmajor ? 1 : 0) | (pilot ? 2 : 0);
+  switch (sel) {
+    case 0: return launch_dzt_mixed_t<false, false>(B, M, N, y, amp, out, st);
+    case 1: return launch_dzt_mixed_t<true, false>(B, M, N, y, amp, out, st);
+    case 2: return launch_dzt_mixed_t<false, true>(B, M, N, y, amp, out, st);
+    default: return launch_dzt_mixed_t<true, true>(B, M, N, y, amp, out, st);
+  }
+}
 
 cudaError_t launch_dzt(int dtype_f64, int B, int M, int N, const void* y, const void* kern, int colmajor, int pilot,
                        double amp, void* out, cudaStream_t st) {

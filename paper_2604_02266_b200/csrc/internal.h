@@ -126,6 +126,8 @@ cudaError_t launch_detect_paths(int B, int M, int N, const void* heff, double th
 // elementwise pilot estimate on a DD frame.
 cudaError_t launch_dzt(int dtype_f64, int B, int M, int N, const void* y, const void* kern, int colmajor, int pilot,
                        double amp, void* out, cudaStream_t st);
+cudaError_t launch_dzt_mixed(int B, int M, int N, const void* y, int colmajor, int pilot, double amp, void* out,
+                             cudaStream_t st);
 cudaError_t launch_estimate_heff(int dtype_f64, long long count, const void* ydd, const void* twist, double amp,
                                  void* heff, cudaStream_t st);
 

@@ -36,29 +36,36 @@ def build_zak_kernel(N, half_shift=False):
 
 def dzt_device(y_time: torch.Tensor, M: int, N: int, *, kernel: torch.Tensor | None = None,
                colmajor: bool = True, pilot_amplitude: float | None = None, out: torch.Tensor | None = None,
-               stream: torch.cuda.Stream | None = None) -> torch.Tensor:
+               stream: torch.cuda.Stream | None = None, fp64: bool = False) -> torch.Tensor:
     """Batched Zak transform of received frames on the device.
 
     y_time: complex64/complex128 [B, M*N] (time index k + i*M).  Returns [B, M*N]
-    of the same dtype: flattened q = l*M + k when colmajor (the solver's input
-    layout), else the (M, N) frame row-major (dzt_gemm's).  With
-    pilot_amplitude the point-pilot estimate of pilot.py:40-49 is fused in.
+    of the same dtype (complex128 with fp64=True): flattened q = l*M + k when
+    colmajor (the solver's input layout), else the (M, N) frame row-major
+    (dzt_gemm's).  With pilot_amplitude the point-pilot estimate of
+    pilot.py:40-49 is fused in.
     """
     if y_time.dim() != 2 or y_time.shape[1] != M * N:
         raise ValueError(f"y_time must be [B, {M * N}], got {tuple(y_time.shape)}")
     if y_time.dtype not in (torch.complex64, torch.complex128):
         raise ValueError("y_time must be complex64 or complex128")
     y_time = y_time.contiguous()
-    dtype = nat.DDB_F64 if y_time.dtype == torch.complex128 else nat.DDB_F32
+    # fp64 on complex64 samples without a widening pass (default kernel, power-of-two N)
+    mixed = fp64 and y_time.dtype == torch.complex64 and kernel is None and N >= 2 and N & (N - 1) == 0
+    if fp64 and y_time.dtype == torch.complex64 and not mixed:
+        y_time = y_time.to(torch.complex128)
+    dtype = nat.DDB_F64 if (mixed or y_time.dtype == torch.complex128) else nat.DDB_F32
     if out is None:
-        out = torch.empty_like(y_time)
+        out = torch.empty(y_time.shape, dtype=torch.complex128 if dtype == nat.DDB_F64 else torch.complex64,
+                          device=y_time.device)
     kptr = None
     if kernel is not None:
         kernel = kernel.to(device=y_time.device, dtype=y_time.dtype).contiguous()
         if kernel.shape != (N, N):
             raise ValueError(f"kernel shape {tuple(kernel.shape)} does not match N={N}")
         kptr = _p(kernel)
-    flags = (nat.DDB_DZT_COLMAJOR if colmajor else 0) | (nat.DDB_DZT_PILOT if pilot_amplitude is not None else 0)
+    flags = ((nat.DDB_DZT_COLMAJOR if colmajor else 0) | (nat.DDB_DZT_PILOT if pilot_amplitude is not None else 0)
+             | (nat.DDB_DZT_INPUT_F32 if mixed else 0))
     st = stream.cuda_stream if stream is not None else torch.cuda.current_stream(y_time.device).cuda_stream
     import ctypes as C
     nat.check(nat.load().ddb_dzt(int(y_time.shape[0]), M, N, dtype, _p(y_time), kptr, flags,
@@ -74,7 +81,7 @@ def dzt_gemm(y, kernel, cfg):
         raise ValueError(f"kernel shape {kernel.shape} does not match N={cfg.N}")
     dev = _dev()
     yt = torch.as_tensor(np.ascontiguousarray(y, dtype=np.complex128), device=dev)[None, :]
-    kt = torch.as_tensor(np.ascontiguousarray(kernel, dtype=np.complex128), device=dev)
+    kt = torch.as_tensor(np.array(kernel, dtype=np.complex128), device=dev)
     out = dzt_device(yt, cfg.M, cfg.N, kernel=kt, colmajor=False)
     torch.cuda.current_stream().synchronize()
     return out[0].cpu().numpy().reshape(cfg.M, cfg.N)

@@ -619,3 +619,17 @@ def test_dzt_any_grid_vs_oracle(pkg, M, N, colmajor):
                 want = orc.estimate_heff(want, M, N, 2.5)
             want = orc.to_vector(want) if colmajor else want.reshape(-1)
             assert rel_l2(out[f], want) < 1e-12
+
+
+@pytest.mark.parametrize("colmajor,pilot", [(True, False), (False, True)])
+def test_dzt_fp64_on_complex64_samples(pkg, colmajor, pilot):
+    """ddb_dzt's DDB_DZT_INPUT_F32 (the pilot path's fp64 transform of complex64
+    samples) equals widening the samples first, bit for bit."""
+    from paper_2604_02266_b200.zak import dzt_device
+    rng = np.random.default_rng(5)
+    y = torch.as_tensor(rng.normal(size=(4, 512 * 32)) + 1j * rng.normal(size=(4, 512 * 32)),
+                        device="cuda").to(torch.complex64)
+    amp = 128.0 if pilot else None
+    a = dzt_device(y, 512, 32, colmajor=colmajor, pilot_amplitude=amp, fp64=True)
+    b = dzt_device(y.to(torch.complex128), 512, 32, colmajor=colmajor, pilot_amplitude=amp)
+    assert a.dtype == torch.complex128 and torch.equal(a, b)
