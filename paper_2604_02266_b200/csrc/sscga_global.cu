@@ -172,7 +172,7 @@ __device__ __forceinline__ void block_pair_sum(Vec<T> v, Vec<T>* dst) {
 
 // b = H^H y -> c (equalize.py:52-57), x = 0, partial ||c||^2.
 template <typename T>
-__global__ void __launch_bounds__(kGThreads) g_init(const GArgs<T> a) {
+__global__ void __launch_bounds__(kGThreads, 6) g_init(const GArgs<T> a) {
   using V = Vec<T>;
   G_SMEM_DECL
   const int f = blockIdx.y, blk = blockIdx.x;
@@ -195,7 +195,7 @@ __global__ void __launch_bounds__(kGThreads) g_init(const GArgs<T> a) {
 
 // u = H c + beta u_old, p = c + beta p_old (u-recurrence), partials (||u||^2, ||p||^2).
 template <typename T>
-__global__ void __launch_bounds__(kGThreads) g_fwd(const GArgs<T> a, int it) {
+__global__ void __launch_bounds__(kGThreads, 6) g_fwd(const GArgs<T> a, int it) {
   using V = Vec<T>;
   G_SMEM_DECL
   const int f = blockIdx.y, blk = blockIdx.x;
@@ -224,7 +224,7 @@ __global__ void __launch_bounds__(kGThreads) g_fwd(const GArgs<T> a, int it) {
 
 // ap = H^H u + lam p; x += alpha p; c -= alpha ap; partial ||c||^2.
 template <typename T>
-__global__ void __launch_bounds__(kGThreads) g_herm(const GArgs<T> a, int it) {
+__global__ void __launch_bounds__(kGThreads, 6) g_herm(const GArgs<T> a, int it) {
   using V = Vec<T>;
   G_SMEM_DECL
   const int f = blockIdx.y, blk = blockIdx.x;
