@@ -54,11 +54,6 @@ int smem_optin() {
 // 512 lane columns; WQ warps per lane quarter, R = G / WQ rows per thread.
 // Smallest cluster that fits, most warps first; the extended column-major
 // slices of c and u take the rest of shared memory as halo (up to M rows).
-// TMEM-run taps per warp and MVM before the rest go to shared memory: a TMEM
-// load is ~200 cycles deep, so a warp with many TMEM taps is the MVM's
-// critical path while its neighbours' shared-memory taps finish early.
-constexpr int kTmCapDefault = 0;
-
 bool make_plan_tm(int32_t M, int32_t N, ddb::LaunchShape* s) {
   const char* env_k = getenv("DDB_KERNEL");
   if (env_k && env_k[0] == 'r') return false;  // DDB_KERNEL=row: force the row-slice kernel
@@ -79,10 +74,10 @@ bool make_plan_tm(int32_t M, int32_t N, ddb::LaunchShape* s) {
     if (G > 64 || G % 2) continue;
     int wq = 0, R = 0;
     const char* env_wq = getenv("DDB_PLAN_WQ");
-    for (int w = env_wq ? 8 : 4; w >= 1; w /= 2) {  // 1024-thread CTAs (WQ = 8) only on request
+    for (int w = 4; w >= 1; w /= 2) {
       if (G % w || (env_wq && atoi(env_wq) != w)) continue;
       const int r = G / w;
-      if (r == 4 || r == 8 || (r == 16 && w <= 4)) { wq = w; R = r; break; }
+      if (r == 4 || r == 8 || r == 16) { wq = w; R = r; break; }
     }
     if (!wq) continue;
     auto cs_of = [&](int h) { int cs = M + 2 * h + 2; return cs % 4 == 2 ? cs : cs + 2; };
@@ -108,8 +103,6 @@ bool make_plan_tm(int32_t M, int32_t N, ddb::LaunchShape* s) {
     int tc = 32;
     while (tc < 8 * G) tc *= 2;
     s->tcols = tc;
-    s->tmcap = kTmCapDefault;
-    if (const char* env_cap = getenv("DDB_TM_CAP")) s->tmcap = atoi(env_cap);
     // keep (CTAs per SM) x (TMEM columns per CTA) <= 512 so tcgen05.alloc never
     // waits on a co-resident CTA (228 KiB per SM, 1 KiB reserved per CTA)
     const int max_ctas = 512 / tc;
@@ -308,7 +301,6 @@ static int32_t solve_impl(const ddb_sscga_problem* prob, const ddb_sscga_outputs
   a.G = s.g;
   a.WQ = s.wq;
   a.CS = s.cs;
-  a.tmcap = s.tmcap;
   if (s.kind == 1) a.active_threads = s.threads;
   a.off = prob->path_offsets;
   a.pk = prob->path_k;

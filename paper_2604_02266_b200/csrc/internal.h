@@ -24,7 +24,6 @@ struct SolveArgs {
   int G;              // delay rows per TMEM lane segment (M / segments per column)
   int WQ;             // warps per TMEM lane quarter (threads = 128 WQ)
   int CS;             // column stride (complex elements) of the column-major extended slices
-  int tmcap;          // at most this many TMEM-run taps per warp and MVM (0: no cap); the rest read shared memory
   const int* off;
   const int* pk;
   const int* pl;
@@ -53,7 +52,6 @@ struct LaunchShape {
   int kind;        // 0: row-slice kernel (sscga.cu), 1: TMEM-operand kernel (sscga_tm.cu),
                    // 2: workspace-backed kernels (sscga_global.cu)
   int g, wq, rows, cs;  // kind 1: segment rows, warps per lane quarter, rows per thread, column stride
-  int tmcap;            // kind 1: TMEM-run taps per warp and MVM (0: all eligible)
 };
 
 // TMEM columns for the thread-private runs of x, p and the own-element copies

@@ -544,14 +544,11 @@ __global__ void __launch_bounds__(MAXT, 1) sscga_tm_kernel(const SolveArgs a) {
     if (fs.masks && tid < a.WQ) {  // thread j classifies the taps for row block j
       uint32_t mk[6] = {0u, 0u, 0u, 0u, 0u, 0u};
       const bool halo = fs.halo;
-      int nf = 0, nh = 0;  // TMEM-run taps so far (capped at a.tmcap per direction)
       for (int p = 0; p < P; ++p) {
         const PathEnt<float>& e = sm.ptab[p];
         const uint32_t bit = 1u << p;
-        int cf = tap_class<R, false>(a, tid * R, halo, e);
-        int ch = tap_class<R, true>(a, tid * R, halo, e);
-        if (cf == 0 && a.tmcap > 0 && nf++ >= a.tmcap) cf = halo ? 1 : 2;
-        if (ch == 0 && a.tmcap > 0 && nh++ >= a.tmcap) ch = halo ? 1 : 2;
+        const int cf = tap_class<R, false>(a, tid * R, halo, e);
+        const int ch = tap_class<R, true>(a, tid * R, halo, e);
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
           mk[c] |= cf == c ? bit : 0u;
@@ -848,14 +845,6 @@ SmemLayout sscga_tm_layout(int M, int Lcta, int N, int CS, int TL, int TH, int p
 
 cudaError_t launch_sscga_tm(SolveArgs a, const LaunchShape& s, cudaStream_t st) {
   if (a.B == 0) return cudaSuccess;
-  // 1024-thread CTAs (8 warps per lane quarter) run at <= 64 registers
-  if (s.threads > 512) {
-    switch (s.rows) {
-      case 4: return launch_r<4, 1024>(a, s, st);
-      case 8: return launch_r<8, 1024>(a, s, st);
-      default: return cudaErrorInvalidValue;
-    }
-  }
   if (a.prof) {  // clock64 phase profile (measurement launches only)
     switch (s.rows) {
       case 4: return launch_r<4, 512, true>(a, s, st);
@@ -873,13 +862,6 @@ cudaError_t launch_sscga_tm(SolveArgs a, const LaunchShape& s, cudaStream_t st) 
 }
 
 cudaError_t sscga_tm_occupancy(const LaunchShape& s, int* n) {
-  if (s.threads > 512) {
-    switch (s.rows) {
-      case 4: return occ_r<4, 1024>(s, n);
-      case 8: return occ_r<8, 1024>(s, n);
-      default: return cudaErrorInvalidValue;
-    }
-  }
   switch (s.rows) {
     case 4: return occ_r<4, 512>(s, n);
     case 8: return occ_r<8, 512>(s, n);
