@@ -20,16 +20,24 @@ numpy oracle port of ddlink, oracle/ddlink_oracle.py) on all host cores.
 
 from __future__ import annotations
 
-import argparse
-import json
-import math
 import os
-import statistics
-import subprocess
-import sys
-import tempfile
-import time
-from pathlib import Path
+
+# The CPU reference legs run one single-threaded numpy process per core, as
+# run_packets does with OPENBLAS_NUM_THREADS=1 (harness.py:217-232; SURVEY.md
+# 8c: multithreaded OpenBLAS makes cga_equalize ~10x slower).  BLAS pools are
+# sized when numpy first loads, so this has to precede every import.
+for _v in ("OPENBLAS_NUM_THREADS", "OMP_NUM_THREADS", "MKL_NUM_THREADS"):
+    os.environ.setdefault(_v, "1")
+
+import argparse  # noqa: E402
+import json  # noqa: E402
+import math  # noqa: E402
+import statistics  # noqa: E402
+import subprocess  # noqa: E402
+import sys  # noqa: E402
+import tempfile  # noqa: E402
+import time  # noqa: E402
+from pathlib import Path  # noqa: E402
 
 ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
@@ -152,9 +160,19 @@ def _cpu_frames(cfg, S, snr_db, iters, seed):
 _WORK = None
 
 
+def _single_thread_blas():
+    """Pin every BLAS / OpenMP pool of this process to one thread (the parent may
+    already have loaded numpy with the default pool, e.g. under torch)."""
+    try:
+        from threadpoolctl import threadpool_limits
+        threadpool_limits(1)
+    except ImportError:
+        pass
+
+
 def _init_worker(frames, cfg, iters):
     global _WORK
-    os.environ["OPENBLAS_NUM_THREADS"] = "1"
+    _single_thread_blas()
     _WORK = (frames, cfg, iters)
 
 
@@ -184,6 +202,7 @@ class CpuArm:
                                                 initargs=(frames, cfg, iters))
         self.pool.map(_solve_chunk, [[0]] * self.cores)  # warm every worker
         t0 = time.perf_counter()
+        _single_thread_blas()
         _solve_chunk_local(frames, cfg, iters, 2)
         self.frame_s = (time.perf_counter() - t0) / 2
 
