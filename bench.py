@@ -49,6 +49,10 @@ CONFIGS = {
     "cfg2": dict(M=256, N=16, P=4, mod="qam16", batch=1024, nu=300.0),
     "cfg3": dict(M=512, N=32, P=6, mod="qam16", batch=4096, nu=100.0),
     "cfg4": dict(M=1024, N=64, P=6, mod="qam16", batch=1024, nu=1000.0),
+    # cfg3 grid with the taps the reference's detect_paths finds on fractional-Doppler
+    # Veh-A channels (tests/golden/frames_sweep.npz: 8-10 taps per frame, 2-4 of them
+    # Doppler-leakage taps at l = L0 +- 1), cycled over the batch
+    "cfg3det": dict(M=512, N=32, P=0, mod="qam16", batch=4096, nu=100.0, taps="frames_sweep"),
     # the paper's real-time grid: beyond a cluster's on-chip
     # memory, so the workspace-backed kernels run it
     "paper": dict(M=16384, N=32, P=6, mod="qam16", batch=128, nu=100.0),
@@ -139,12 +143,13 @@ def _cpu_frames(cfg, S, snr_db, iters, seed):
     M, N = cfg["M"], cfg["N"]
     const = orc.qam(cfg["mod"])
     B = M * 30e3
-    delays = np.round(np.array([0.0, 0.31, 0.71, 1.09, 1.73, 2.51])[:cfg["P"]] * 1e-6 * B).astype(int)
-    pw = 10 ** (np.array([0.0, -1.0, -9.0, -10.0, -15.0, -20.0])[:cfg["P"]] / 10)
+    P = cfg["P"] or 6
+    delays = np.round(np.array([0.0, 0.31, 0.71, 1.09, 1.73, 2.51])[:P] * 1e-6 * B).astype(int)
+    pw = 10 ** (np.array([0.0, -1.0, -9.0, -10.0, -15.0, -20.0])[:P] / 10)
     mags = np.sqrt(pw / pw.sum())
     frames = []
     for _ in range(S):
-        dop = np.round(cfg["nu"] * np.cos(2 * np.pi * rng.random(cfg["P"])) / (30e3 / N)).astype(int)
+        dop = np.round(cfg["nu"] * np.cos(2 * np.pi * rng.random(P)) / (30e3 / N)).astype(int)
         taps = [orc.Tap(int((M // 2 + d) % M), int((N // 2 + o) % N), complex(m * np.exp(2j * np.pi * rng.random())))
                 for d, o, m in zip(delays, dop, mags)]
         lab = rng.integers(0, len(const.points), M * N)
@@ -266,7 +271,8 @@ def run_reference(args, cfg):
 
 def _config_json(args, cfg):
     B = args.batch or cfg["batch"]
-    return {"workload": f"{args.config}: OTFS M={cfg['M']} N={cfg['N']} P={cfg['P']} {cfg['mod']} "
+    ptxt = f"P={cfg['P']}" if cfg["P"] else f"P=detect_paths taps of {cfg['taps']}"
+    return {"workload": f"{args.config}: OTFS M={cfg['M']} N={cfg['N']} {ptxt} {cfg['mod']} "
                         f"batch {B} frames/GPU, Xi={args.iters}, {args.snr:g} dB",
             "M": cfg["M"], "N": cfg["N"], "P": cfg["P"], "modulation": cfg["mod"], "batch_per_gpu": B,
             "iterations": args.iters, "snr_db": args.snr, "nu_max_hz": cfg["nu"],
@@ -301,8 +307,14 @@ def main():
     B = args.batch or cfg["batch"]
     bps = BPS[cfg["mod"]]
     s = pkg.SsCgaSolver(M, N, args.iters, precision="fp32", modulation=cfg["mod"])
+    given = None
+    if cfg.get("taps"):
+        import numpy as np
+        from paper_2604_02266_b200.synth import cycle_paths
+        with np.load(ROOT / "tests" / "golden" / f"{cfg['taps']}.npz") as z:
+            given = cycle_paths(B, z["path_off"], z["path_k"], z["path_l"], z["path_g"], "cuda", s.cdtype)
     fb = make_frames(s, B, snr_db=args.snr, nu_max_hz=cfg["nu"], modulation=cfg["mod"],
-                     seed=ddist.rank_seed(1000, rank), n_paths=P)
+                     seed=ddist.rank_seed(1000, rank), n_paths=P or 6, paths=given)
     out = s.alloc(B, llr=True, trace=True, bit_errors=True)
     stream = torch.cuda.current_stream()
 

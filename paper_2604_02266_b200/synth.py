@@ -60,8 +60,26 @@ def veha_paths(B: int, grid: GridConfig, nu_max_hz: float, gen: torch.Generator,
                      gain.reshape(-1).to(cdtype).contiguous())
 
 
+def cycle_paths(B: int, offsets, k, l, gain, device, cdtype) -> PathBatch:
+    """B frames whose tap sets cycle through the given CSR tap sets (e.g. the
+    reference's detect_paths output on fractional-Doppler Veh-A channels)."""
+    offsets, k, l, gain = (np.asarray(v) for v in (offsets, k, l, gain))
+    F = len(offsets) - 1
+    sets = [slice(int(offsets[i]), int(offsets[i + 1])) for i in range(F)]
+    ks, ls, gs, off = [], [], [], [0]
+    for b in range(B):
+        sl = sets[b % F]
+        ks.append(k[sl])
+        ls.append(l[sl])
+        gs.append(gain[sl])
+        off.append(off[-1] + (sl.stop - sl.start))
+    return PathBatch.from_arrays(off, np.concatenate(ks), np.concatenate(ls), np.concatenate(gs), device, cdtype)
+
+
 def make_frames(solver: SsCgaSolver, B: int, snr_db: float = 25.0, nu_max_hz: float = 100.0,
-                modulation: str = "qam16", seed: int = 0, n_paths: int = 6, delta_f: float = 30e3) -> FrameBatch:
+                modulation: str = "qam16", seed: int = 0, n_paths: int = 6, delta_f: float = 30e3,
+                paths: PathBatch | None = None) -> FrameBatch:
+    """paths: use these taps instead of drawing Veh-A ones."""
     dev = solver.device
     grid = GridConfig(solver.M, solver.N, delta_f)
     gen = torch.Generator(device=dev)
@@ -70,7 +88,8 @@ def make_frames(solver: SsCgaSolver, B: int, snr_db: float = 25.0, nu_max_hz: fl
     pts = torch.as_tensor(np.array(const.points), device=dev).to(solver.cdtype)
     labels = torch.randint(0, len(const.points), (B, solver.MN), generator=gen, device=dev, dtype=torch.int64)
     x = pts[labels].contiguous()
-    paths = veha_paths(B, grid, nu_max_hz, gen, dev, solver.cdtype, n_paths)
+    if paths is None:
+        paths = veha_paths(B, grid, nu_max_hz, gen, dev, solver.cdtype, n_paths)
     hx = solver.apply(x, paths)
     if np.isinf(snr_db):
         y = hx
