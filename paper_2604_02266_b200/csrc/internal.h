@@ -46,6 +46,7 @@ struct SolveArgs {
 };
 
 constexpr int kProfPhases = 12;
+constexpr int kProfWarpBase = 4096;  // per-warp timers of measurement builds: prof[4096 + (cta * 16 + warp) * 8 + k]
 
 struct LaunchShape {
   int cluster, lcta, lc, threads, smem, halo, tl, th, pcap, tcols;

@@ -57,6 +57,8 @@ struct FrameSm {
   uint32_t mk[8][6];           // [j][tmF, smF, gnF, tmH, smH, gnH]: TMEM run / shared run / per element
 };
 
+constexpr int kWarpTimers = 8;
+
 __host__ __device__ inline size_t a16(size_t v) { return (v + 15) & ~size_t(15); }
 
 __host__ __device__ inline SmemLayout tm_layout_impl(int Lcta, int N, int CS, int TL, int TH, int pcap) {
@@ -353,9 +355,34 @@ __device__ __forceinline__ void tm_arrive(int C, bool relaxed = false) {
   tmem_fence_after();
 }
 
+// Timed variant (measurement builds): wt[4] TMEM store wait + fence, wt[5] CTA
+// barrier, wt[6] fold + push, wt[7] cluster arrive.  BAR.SYNC defers blocking,
+// so the CTA-barrier wait mostly lands in wt[6].
+template <bool PROF>
 __device__ __forceinline__ void tm_arrive_red(int C, V* base, int nwarps, int warp, int lane, int rank,
-                                              bool relaxed = false) {
-  cl_arrive_red<float, true>(C, base, nwarps, warp, lane, rank, relaxed);
+                                              bool relaxed, long long* wt) {
+  if constexpr (!PROF) {
+    cl_arrive_red<float, true>(C, base, nwarps, warp, lane, rank, relaxed);
+  } else {
+    long long t = clock64(), u;
+    tmem_wait_st();
+    tmem_fence_before();
+    u = clock64(); wt[4] += u - t; t = u;
+    __syncthreads();
+    u = clock64(); wt[5] += u - t; t = u;
+    if (C > 1) {
+      if (warp == 0) {
+        V v = lane < nwarps ? base[lane] : make_float2(0.f, 0.f);
+        v.x = warp_sum(v.x);
+        v.y = warp_sum(v.y);
+        if (lane < C) st_cluster(map_rank(smem_addr(base + 32 + rank), (uint32_t)lane), v);
+      }
+      u = clock64(); wt[6] += u - t; t = u;
+      cl_arrive_sem(!relaxed || warp == 0);
+    }
+    tmem_fence_after();
+    u = clock64(); wt[7] += u - t;
+  }
 }
 
 // Epilogue for E equalized symbols of rows rr.. (contiguous in q): x_hat,
@@ -426,6 +453,20 @@ __device__ __forceinline__ int epi_pass(const SolveArgs& a, const V* stg, int M,
   return errs;
 }
 
+// Measurement builds: per-warp cycles of a call (wt[0] forward / wt[1]
+// hermitian local MVM, wt[2] reduction arrive, wt[3] cluster wait), stored by
+// lane 0 of every warp at prof[kProfWarpBase + (cta * 16 + warp) * kWarpTimers].
+#define TM_WT(k, ...)                                  \
+  do {                                                 \
+    if constexpr (PROF) {                              \
+      const long long t0_ = clock64();                 \
+      __VA_ARGS__;                                     \
+      wt[k] += clock64() - t0_;                        \
+    } else {                                           \
+      __VA_ARGS__;                                     \
+    }                                                  \
+  } while (0)
+
 template <int R, int MAXT, bool PROF>
 __global__ void __launch_bounds__(MAXT, 1) sscga_tm_kernel(const SolveArgs a) {
   constexpr int E = 4;  // elements per TMEM chunk of the elementwise steps
@@ -481,6 +522,7 @@ __global__ void __launch_bounds__(MAXT, 1) sscga_tm_kernel(const SolveArgs a) {
   const int stride = a.iters + 1;
   int par0 = 0, par1 = 0;
   if constexpr (PROF) prof_init(a.prof, psm);
+  long long wt[kWarpTimers] = {0, 0, 0, 0, 0, 0, 0, 0};
 
   for (int f = blockIdx.x / a.C; f < a.B; f += a.n_clusters) {
     const size_t fo = (size_t)f * a.MN;
@@ -595,7 +637,7 @@ __global__ void __launch_bounds__(MAXT, 1) sscga_tm_kernel(const SolveArgs a) {
     if constexpr (PROF) prof_mark(a.prof, psm, kArrive);
     tm_arrive(a.C);  // y and the tap classes published
     if constexpr (PROF) prof_mark(a.prof, psm, kMvmLocal);
-    mvm_local<R, true>(a, th, sm, fs, tU(0) - 2 * th.jr, ucol, acc);  // b = H^H y (equalize.py:52)
+    TM_WT(1, mvm_local<R, true>(a, th, sm, fs, tU(0) - 2 * th.jr, ucol, acc));  // b = H^H y (equalize.py:52)
     if constexpr (PROF) prof_mark(a.prof, psm, kWait);
     cl_wait(a.C);
     if constexpr (PROF) prof_mark(a.prof, psm, kMvmRemote);
@@ -619,9 +661,9 @@ __global__ void __launch_bounds__(MAXT, 1) sscga_tm_kernel(const SolveArgs a) {
       red_stage<float>(make_float2(nrm.x + nrm.y, 0.f), red + (2 + par1) * kPushSlots, warp, lane);
     }
     if constexpr (PROF) prof_mark(a.prof, psm, kArrive);
-    tm_arrive_red(a.C, red + (2 + par1) * kPushSlots, nwarps, warp, lane, rank, !fs.remote);  // c = b published
+    TM_WT(2, tm_arrive_red<PROF>(a.C, red + (2 + par1) * kPushSlots, nwarps, warp, lane, rank, !fs.remote, wt));  // c = b published
     if constexpr (PROF) prof_mark(a.prof, psm, kMvmLocal);
-    mvm_local<R, false>(a, th, sm, fs, tC(0) - 2 * th.jr, ccol, acc);
+    TM_WT(0, mvm_local<R, false>(a, th, sm, fs, tC(0) - 2 * th.jr, ccol, acc));
     if constexpr (PROF) prof_mark(a.prof, psm, kWait);
     cl_wait(a.C);
     if constexpr (PROF) prof_mark(a.prof, psm, kRead);
@@ -669,12 +711,12 @@ __global__ void __launch_bounds__(MAXT, 1) sscga_tm_kernel(const SolveArgs a) {
         red_stage<float>(make_float2(nu.x + nu.y, np.x + np.y), red + par0 * kPushSlots, warp, lane);
       }
       if constexpr (PROF) prof_mark(a.prof, psm, kArrive);
-      tm_arrive_red(a.C, red + par0 * kPushSlots, nwarps, warp, lane, rank, !fs.remote);  // u published
+      TM_WT(2, tm_arrive_red<PROF>(a.C, red + par0 * kPushSlots, nwarps, warp, lane, rank, !fs.remote, wt));  // u published
       // ap = H^H u + lam p;  x += alpha p;  c -= alpha ap      (equalize.py:60-70)
       if constexpr (PROF) prof_mark(a.prof, psm, kMvmLocal);
-      mvm_local<R, true>(a, th, sm, fs, tU(0) - 2 * th.jr, ucol, acc);
+      TM_WT(1, mvm_local<R, true>(a, th, sm, fs, tU(0) - 2 * th.jr, ucol, acc));
       if constexpr (PROF) prof_mark(a.prof, psm, kWait);
-      cl_wait(a.C);
+      TM_WT(3, cl_wait(a.C));
       if constexpr (PROF) prof_mark(a.prof, psm, kMvmRemote);
       mvm_remote<R, true>(a, th, sm, fs, sm.u, acc);
       if constexpr (PROF) prof_mark(a.prof, psm, kRead);
@@ -724,11 +766,11 @@ __global__ void __launch_bounds__(MAXT, 1) sscga_tm_kernel(const SolveArgs a) {
         red_stage<float>(make_float2(nc.x + nc.y, 0.f), red + (2 + par1) * kPushSlots, warp, lane);
       }
       if constexpr (PROF) prof_mark(a.prof, psm, kArrive);
-      tm_arrive_red(a.C, red + (2 + par1) * kPushSlots, nwarps, warp, lane, rank, !fs.remote);  // c published
+      TM_WT(2, tm_arrive_red<PROF>(a.C, red + (2 + par1) * kPushSlots, nwarps, warp, lane, rank, !fs.remote, wt));  // c published
       if constexpr (PROF) prof_mark(a.prof, psm, kMvmLocal);
-      if (it + 1 < a.iters) mvm_local<R, false>(a, th, sm, fs, tC(0) - 2 * th.jr, ccol, acc);  // next H c
+      if (it + 1 < a.iters) TM_WT(0, mvm_local<R, false>(a, th, sm, fs, tC(0) - 2 * th.jr, ccol, acc));  // next H c
       if constexpr (PROF) prof_mark(a.prof, psm, kWait);
-      cl_wait(a.C);
+      TM_WT(3, cl_wait(a.C));
       if constexpr (PROF) prof_mark(a.prof, psm, kRead);
       const float nn = red_total<float>(a.C, red + (2 + par1) * kPushSlots, nwarps).x;
       par1 ^= 1;
@@ -787,6 +829,11 @@ __global__ void __launch_bounds__(MAXT, 1) sscga_tm_kernel(const SolveArgs a) {
   }
   if constexpr (PROF) prof_mark(a.prof, psm, kTail);
   if constexpr (PROF) prof_store(a.prof, psm);
+  if constexpr (PROF) {
+    if (a.prof != nullptr && lane == 0)
+      for (int k = 0; k < kWarpTimers; ++k)
+        a.prof[kProfWarpBase + ((size_t)blockIdx.x * 16 + warp) * kWarpTimers + k] = wt[k];
+  }
   // no CTA may leave while a peer can still read its shared memory (DSMEM)
   tmem_fence_before();
   cl_sync<float>(a.C);

@@ -41,15 +41,21 @@ def main():
     e1.record()
     torch.cuda.synchronize()
     it_done = res.iterations_done.float().mean().item() if res.iterations_done is not None else None
-    p = prof.cpu()
+    flat = prof.cpu().reshape(-1)
+    p = flat[:4096 - 4096 % 12].reshape(-1, 12)
     rows = p[p.sum(dim=1) > 0]
+    # per-warp timers [cta][warp][fwd MVM, herm MVM, arrive, wait, arrive parts] (kProfWarpBase)
+    wt = flat[4096:4096 + rows.shape[0] * 16 * 8].reshape(rows.shape[0], 16, 8).double()
     tot = rows.sum(dim=0).double()
     frames_per_cta = args.batch / (rows.shape[0] / s.plan()["cluster"])
     res = {"plan": s.plan(), "ms": e0.elapsed_time(e1), "ctas": int(rows.shape[0]), "mean_iterations": it_done,
            "cycles_per_frame": float(tot.sum() / rows.shape[0] / frames_per_cta),
            "phases_pct": {name: round(100 * float(tot[i] / tot.sum()), 2) for i, name in enumerate(nat.PHASES)},
            "phase_cycles_per_frame": {name: round(float(tot[i] / rows.shape[0] / frames_per_cta))
-                                      for i, name in enumerate(nat.PHASES)}}
+                                      for i, name in enumerate(nat.PHASES)},
+           "per_warp_cycles_per_frame": {
+               k: [round(float(v)) for v in (wt[:, :, i].mean(dim=0) / frames_per_cta)]
+               for i, k in enumerate(("mvm_fwd", "mvm_herm", "arrive", "wait", "a_tmem_st", "a_cta_bar", "a_fold", "a_arrive"))}}
     print(json.dumps(res, indent=1))
 
 
