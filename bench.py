@@ -82,6 +82,23 @@ def parse():
     return ap.parse_args()
 
 
+def median_ms(fn, stream, reps: int = 5) -> float:
+    """Median device time of fn() over reps calls (CUDA events on `stream`,
+    synchronised on both sides): robust to one-off host stalls in calls that
+    include host round trips (the receiver's tap CSR)."""
+    import torch
+    times = []
+    for _ in range(reps):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        a.record(stream)
+        fn()
+        b.record(stream)
+        b.synchronize()
+        times.append(a.elapsed_time(b))
+    return sorted(times)[len(times) // 2]
+
+
 def flops_per_frame(P, MN, iters):
     return 8 * P * MN * (2 * iters + 1) + 24 * MN * iters + 4 * MN
 
@@ -409,21 +426,52 @@ def main():
         pil_rx, dat_rx = time_domain_frames(s, fb)
         for _ in range(2):
             rres = s.receive(pil_rx, dat_rx, fb.lam, 0.08, tx_labels=fb.tx_labels, trace=False)
-        torch.cuda.synchronize()
-        a.record(stream)
+        rx_ms = median_ms(lambda: s.receive(pil_rx, dat_rx, fb.lam, 0.08, tx_labels=fb.tx_labels, trace=False),
+                          stream)
         rres = s.receive(pil_rx, dat_rx, fb.lam, 0.08, tx_labels=fb.tx_labels, trace=False)
-        b.record(stream)
-        b.synchronize()
-        rx_ms = a.elapsed_time(b)
         rx_ber = int(rres.bit_errors.sum().item()) / (B * MN * bps)
         del pil_rx, dat_rx, rres
+        # frame synthesis on the device (row f2) and the receiver on those
+        # continuous-Doppler packets (fractional Doppler leaks into extra taps)
+        from paper_2604_02266_b200.channel import apply_channel_device
+        from paper_2604_02266_b200.synth import synthesize_packets
+        pb = synthesize_packets(s, B, snr_db=args.snr, nu_max_hz=cfg["nu"], modulation=cfg["mod"],
+                                seed=ddist.rank_seed(2000, rank), cdtype=s.cdtype)
+        torch.cuda.synchronize()
+        a.record(stream)
+        pb = synthesize_packets(s, B, snr_db=args.snr, nu_max_hz=cfg["nu"], modulation=cfg["mod"],
+                                seed=ddist.rank_seed(2000, rank), cdtype=s.cdtype)
+        b.record(stream)
+        b.synchronize()
+        synth_ms = a.elapsed_time(b)
+        ych = torch.empty_like(pb.data_rx)
+        apply_channel_device(pb.data_rx, pb.channel, pkg.GridConfig(M, N), out=ych)
+        a.record(stream)
+        for _ in range(reps):
+            apply_channel_device(pb.data_rx, pb.channel, pkg.GridConfig(M, N), out=ych)
+        b.record(stream)
+        b.synchronize()
+        ch_ms = a.elapsed_time(b) / reps
+        del ych
+        rres = s.receive(pb.pilot_rx, pb.data_rx, pb.lam, 0.08, tx_labels=pb.tx_labels, trace=False)
+        frx_ms = median_ms(lambda: s.receive(pb.pilot_rx, pb.data_rx, pb.lam, 0.08, tx_labels=pb.tx_labels,
+                                             trace=False), stream)
+        frx_ber = int(rres.bit_errors.sum().item()) / (B * MN * bps)
+        del pb, rres
         frontend = {"dzt_ms": dzt_ms, "dzt_gbs": dzt_gbs, "dzt_hbm_frac": dzt_gbs / hbm_peak,
+                    "synth_ms": synth_ms, "apply_channel_ms": ch_ms,
+                    "apply_channel_gbs": B * MN * 16 / (ch_ms * 1e-3) / 1e9,
+                    "fracdop_receiver_ms": frx_ms, "fracdop_receiver_sym_s": B * MN / (frx_ms * 1e-3),
+                    "fracdop_receiver_ber": frx_ber,
                     "receiver_ms": rx_ms, "receiver_sym_s": B * MN / (rx_ms * 1e-3), "receiver_ber": rx_ber,
                     "dzt_bytes_per_frame": MN * 16, "detect_ms_per_batch": det_ms,
                     "what": "ddb_dzt fp32 batch (zak.py:50-55) vs HBM peak; pilot path = fp64 DZT + estimate_heff "
                             "+ detect_paths + CSR for the batch (pilot.py:40-49, sparse.py:69-88); receiver = "
-                            "SsCgaSolver.receive on time-domain pilot + data frames (harness.py:156-194): pilot "
-                            "path, data DZT, fused solve + demod + bit errors"}
+                            "SsCgaSolver.receive (median of 5 calls) on time-domain pilot + data frames (harness.py:156-194): pilot "
+                            "path, data DZT, fused solve + demod + bit errors; synth = synthesize_packets "
+                            "(modulate, idzt, Veh-A apply_channel with continuous Doppler, AWGN; pilot + data, "
+                            "channel.py:62-119, harness.py:141-149) on the device; fracdop_receiver = receive on "
+                            "those packets (detected taps include Doppler leakage)"}
 
     # ---- single-frame latency: CUDA graph of a batch-1 solve, replayed
     latency = None

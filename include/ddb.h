@@ -24,6 +24,10 @@
  *   ddb_estimate_heff    pilot.py:40-49      estimate_heff on a DD frame
  *   ddb_detect_paths     sparse.py:69-88     detect_paths (strict relative threshold,
  *                                            stable descending-magnitude order)
+ *   ddb_dzt + INVERSE    zak.py:14-21        idzt (transmit side, frame synthesis)
+ *   ddb_modulate         grid.py:157-169     modulate (labels -> constellation points)
+ *   ddb_apply_channel    channel.py:95-103   apply_channel (delay shift + Doppler ramp)
+ *   ddb_add_awgn         channel.py:106-119  add_awgn (own counter-based RNG)
  *
  * Layouts (identical to the reference's numpy layouts):
  *   complex values are interleaved (re, im) of the problem dtype;
@@ -175,6 +179,9 @@ int32_t ddb_detect_paths(int32_t batch, int32_t M, int32_t N, const void* heff, 
 #define DDB_DZT_PILOT 2
 #define DDB_DZT_INPUT_F32 4  /* dtype f64 with complex64 y_time (fp64 arithmetic on
                                 single-precision samples); default kernel, power-of-two N */
+#define DDB_DZT_INVERSE 8    /* idzt (zak.py:14-21): x[k + nM] = (1/sqrt N) sum_l X[k,l] e^{+j2pi n l/N};
+                                y_time is then the flattened DD vector q = l*M + k and out the
+                                time samples (needs DDB_DZT_COLMAJOR, the default kernel) */
 int32_t ddb_dzt(int32_t batch, int32_t M, int32_t N, int32_t dtype, const void* y_time, const void* kernel,
                 int32_t flags, double amplitude, void* out, void* stream);
 
@@ -182,32 +189,38 @@ int32_t ddb_dzt(int32_t batch, int32_t M, int32_t N, int32_t dtype, const void* 
  *      elementwise over `count` complex values of the dtype (amplitude > 0). */
 int32_t ddb_estimate_heff(int64_t count, int32_t dtype, const void* y_dd, const void* twist, double amplitude,
                           void* heff, void* stream);
+
+/* ---- frame synthesis on the device: the transmit
+ *      side and channel of one packet (harness.py:141-149) for a batch.
+ *      ddb_modulate        grid.py:157-169  labels [count] (bits MSB first,
+ *                          as `groups @ weights`) -> points of
+ *                          make_constellation (grid.py:126-154), complex dtype.
+ *      ddb_apply_channel   channel.py:95-103 on time-domain frames x [B, M*N]:
+ *                          y[i] = sum_p h_p x[(i - k_p) mod MN]
+ *                                 e^{j2pi nu_p (i / bandwidth - tau_p)}
+ *                          paths as CSR (path_offsets [B+1]; delay_bin int32,
+ *                          doppler_hz / delay_s float64, gain complex dtype);
+ *                          phases in fp64.  y must not alias x.
+ *      ddb_add_awgn        channel.py:106-119: out = y + sigma/sqrt(2) (n1 + j n2),
+ *                          sigma^2 = mean_frame |y|^2 / 10^(snr_db/10), per frame of
+ *                          frame_len samples; counter-based normals (Philox4x32-10,
+ *                          seed) -- the reference's numpy stream is not reproduced.
+ *                          snr_db = +inf copies (the noiseless sentinel).
+ *                          frame_power: device float64 [batch] scratch (receives
+ *                          the per-frame mean power).  out may alias y. */
+int32_t ddb_modulate(int64_t count, int32_t dtype, const uint8_t* labels, int32_t bits_per_symbol, void* out,
+                     void* stream);
+int32_t ddb_apply_channel(int32_t batch, int32_t M, int32_t N, int32_t dtype, const void* x,
+                          const int32_t* path_offsets, const int32_t* delay_bin, const double* doppler_hz,
+                          const double* delay_s, const void* gain, double bandwidth_hz, void* y, void* stream);
+int32_t ddb_add_awgn(int32_t batch, int64_t frame_len, int32_t dtype, const void* y, double snr_db, uint64_t seed,
+                     double* frame_power, void* out, void* stream);
 
 /* ---- measurement helper (not a reference interface): FP32 FMA throughput
  *      probe used by bench.py to state the measured FP32 roofline.  Launches
  *      blocks x 256 threads, each doing iters x 256 FMAs (mode 0: FFMA,
  *      mode 1: packed FFMA2).  scratch: device float[blocks]. */
 int32_t ddb_probe_fp32(int32_t mode, int32_t blocks, int32_t iters, float* scratch, void* stream);
-
-/* ---- receiver front end.
- *      ddb_dzt: y_time complex [B, M*N] received samples (time index k + i*M,
- *      grid.py check_signal); kernel complex [N, N] row-major (i, l) or NULL for
- *      build_zak_kernel(N) = e^{-j2pi i l/N}/sqrt(N) (zak.py:33-47); out complex
- *      [B, M*N].  flags: DDB_DZT_COLMAJOR writes the flattened vector
- *      q = l*M + k (grid.py:86-95), else the (M, N) frame row-major as dzt_gemm
- *      returns it; DDB_DZT_PILOT also multiplies by the twist kernel
- *      e^{-j2pi K0 (l-L0)/(MN)} and divides by `amplitude` (estimate_heff). */
-#define DDB_DZT_COLMAJOR 1
-#define DDB_DZT_PILOT 2
-#define DDB_DZT_INPUT_F32 4  /* dtype f64 with complex64 y_time (fp64 arithmetic on
-                                single-precision samples); default kernel, power-of-two N */
-int32_t ddb_dzt(int32_t batch, int32_t M, int32_t N, int32_t dtype, const void* y_time, const void* kernel,
-                int32_t flags, double amplitude, void* out, void* stream);
-
-/* ---- estimate_heff (pilot.py:40-49) on DD frames: heff = y_dd * twist / amplitude
- *      elementwise over `count` complex values of the dtype (amplitude > 0). */
-int32_t ddb_estimate_heff(int64_t count, int32_t dtype, const void* y_dd, const void* twist, double amplitude,
-                          void* heff, void* stream);
 
 /* ---- measurement helper (not a reference interface): ddb_sscga_solve with
  *      clock64 phase accounting on thread 0 of every CTA.  phase_cycles:

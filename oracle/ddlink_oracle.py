@@ -16,6 +16,8 @@ Each function cites the reference file:line it restates.  The hot path
     detect_paths -> build_tables -> cga -> hard_demod
 and the receiver front end before it (section 8f row f1):
     dzt_gemm (pilot, data) -> estimate_heff
+and the frame synthesis that feeds it (section 8f row f2):
+    modulate_labels -> idzt -> apply_channel
 """
 
 from __future__ import annotations
@@ -173,6 +175,28 @@ def estimate_heff(Y_dd: np.ndarray, M: int, N: int, amplitude: float | None = No
     """Y_dd * twist / amplitude, amplitude defaulting to sqrt(MN) (pilot.py:13-15, 40-49)."""
     amp = math.sqrt(M * N) if amplitude is None else amplitude
     return Y_dd * twist_kernel(M, N) / amp
+
+
+# --------------------------------------------------------------------------
+# frame synthesis (zak.py:14-21, channel.py:95-103) — SURVEY.md 8f row f2
+
+
+def idzt(X_vec: np.ndarray, M: int, N: int) -> np.ndarray:
+    """Flattened DD vector (q = l*M + k) -> time samples k + n*M:
+    x[k + nM] = (1/sqrt N) sum_l X[k, l] e^{+j2pi n l/N} (zak.py:14-21)."""
+    X = np.asarray(X_vec).reshape(M, N, order="F")
+    return (X @ np.conj(zak_kernel(N))).reshape(M * N, order="F")
+
+
+def apply_channel(x: np.ndarray, gains, delay_s, doppler_hz, delay_bin, bandwidth: float) -> np.ndarray:
+    """Noiseless channel y[i] = sum_p h_p x[(i - k_p) mod MN] e^{j2pi nu_p (i/B - tau_p)}
+    (channel.py:95-103)."""
+    x = np.asarray(x, dtype=np.complex128)
+    i = np.arange(x.size)
+    y = np.zeros(x.size, dtype=np.complex128)
+    for h, tau, nu, k in zip(gains, delay_s, doppler_hz, delay_bin):
+        y += h * np.roll(x, int(k)) * np.exp(2j * np.pi * nu * (i / bandwidth - tau))
+    return y
 
 
 # --------------------------------------------------------------------------

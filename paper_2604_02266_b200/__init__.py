@@ -35,6 +35,21 @@ from .sparse import (
     ss_mvm_hermitian,
 )
 from .zak import build_zak_kernel, dzt_device, dzt_gemm
+from .channel import (
+    ChannelBatch,
+    PathSet,
+    PathSpec,
+    add_awgn,
+    add_awgn_device,
+    apply_channel,
+    apply_channel_device,
+    draw_veha,
+    draw_veha_batch,
+    idzt,
+    idzt_device,
+    make_path,
+    modulate_device,
+)
 
 __all__ = [
     "HostPipeline", "PathBatch", "SolveResult", "SsCgaSolver", "bits_per_symbol", "pack_labels",
@@ -45,6 +60,8 @@ __all__ = [
     "detect_paths", "forward_index", "inverse_index", "ss_mvm", "ss_mvm_hermitian",
     "build_twist_kernel", "default_pilot_amplitude", "estimate_heff", "make_pilot_frame",
     "build_zak_kernel", "dzt_device", "dzt_gemm",
+    "ChannelBatch", "PathSet", "PathSpec", "add_awgn", "add_awgn_device", "apply_channel", "apply_channel_device",
+    "draw_veha", "draw_veha_batch", "idzt", "idzt_device", "make_path", "modulate_device",
 ]
 
 __version__ = "0.1.0"

@@ -58,6 +58,7 @@ ABI_VERSION = 3  # include/ddb.h DDB_ABI_VERSION
 DDB_DZT_COLMAJOR = 1
 DDB_DZT_PILOT = 2
 DDB_DZT_INPUT_F32 = 4
+DDB_DZT_INVERSE = 8
 
 
 class Plan(C.Structure):
@@ -91,6 +92,12 @@ _SIGNATURES = {
                             C.c_double, C.c_void_p, C.c_void_p]),
     "ddb_estimate_heff": (C.c_int32, [C.c_int64, C.c_int32, C.c_void_p, C.c_void_p, C.c_double, C.c_void_p,
                                       C.c_void_p]),
+    "ddb_modulate": (C.c_int32, [C.c_int64, C.c_int32, C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p]),
+    "ddb_apply_channel": (C.c_int32, [C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p,
+                                      C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_double, C.c_void_p,
+                                      C.c_void_p]),
+    "ddb_add_awgn": (C.c_int32, [C.c_int32, C.c_int64, C.c_int32, C.c_void_p, C.c_double, C.c_uint64,
+                                 C.c_void_p, C.c_void_p, C.c_void_p]),
     "ddb_probe_fp32": (C.c_int32, [C.c_int32, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p]),
     "ddb_sscga_profile_phases": (C.c_int32, [C.POINTER(Problem), C.POINTER(Outputs), C.c_void_p, C.c_void_p]),
 }

@@ -16,7 +16,7 @@ PKG_DIR = Path(__file__).resolve().parent
 REPO_DIR = PKG_DIR.parent
 CSRC = PKG_DIR / "csrc"
 LIB_PATH = PKG_DIR / "libddb.so"
-SOURCES = ("sscga.cu", "sscga_tm.cu", "sscga_global.cu", "aux.cu", "frontend.cu", "capi.cu")
+SOURCES = ("sscga.cu", "sscga_tm.cu", "sscga_global.cu", "aux.cu", "frontend.cu", "channel.cu", "capi.cu")
 HEADERS = ("common.cuh", "cg.cuh", "demod.cuh", "internal.h")
 
 NVCC_FLAGS = [
@@ -55,14 +55,21 @@ def build(force: bool = False, verbose: bool = False) -> Path:
     nvcc = nvcc_path()
     objdir = PKG_DIR / "build"
     objdir.mkdir(exist_ok=True)
-    objs = []
+    hdr_mtime = max(p.stat().st_mtime for p in [REPO_DIR / "include" / "ddb.h", *(CSRC / h for h in HEADERS)])
+    objs, cmds = [], []
     for src in SOURCES:
         obj = objdir / (Path(src).stem + ".o")
-        cmd = [nvcc, *NVCC_FLAGS, "-dc" if False else "-c", str(CSRC / src), "-o", str(obj)]
+        objs.append(str(obj))
+        if not force and obj.exists() and obj.stat().st_mtime > max(hdr_mtime, (CSRC / src).stat().st_mtime):
+            continue  # object up to date
+        cmd = [nvcc, *NVCC_FLAGS, "-c", str(CSRC / src), "-o", str(obj)]
         if verbose:
             cmd += ["-Xptxas", "-v"]
-        _run(cmd, verbose)
-        objs.append(str(obj))
+        cmds.append(cmd)
+    from concurrent.futures import ThreadPoolExecutor
+    with ThreadPoolExecutor(max_workers=max(1, min(len(cmds), os.cpu_count() or 1))) as pool:
+        for fut in [pool.submit(_run, c, verbose) for c in cmds]:
+            fut.result()
     tmp = LIB_PATH.with_suffix(".so.tmp")
     _run([nvcc, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-Xcompiler", "-fPIC",
           *objs, "-o", str(tmp)], verbose)

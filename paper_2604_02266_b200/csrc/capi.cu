@@ -7,6 +7,8 @@
 #include "../../include/ddb.h"
 #include "internal.h"
 
+#include <cmath>
+
 namespace {
 
 thread_local std::string g_err;
@@ -444,7 +446,9 @@ int32_t ddb_dzt(int32_t batch, int32_t M, int32_t N, int32_t dtype, const void* 
   if (M < 1 || N < 1) return fail(DDB_ERR_SHAPE, "grid must be positive, got (%d,%d)", M, N);
   if ((long long)M * N >= (1LL << 29)) return fail(DDB_ERR_UNSUPPORTED, "grid too large");
   if (N > 256) return fail(DDB_ERR_UNSUPPORTED, "N=%d > 256 (kernel matrix exceeds shared memory)", N);
-  if (flags & ~(DDB_DZT_COLMAJOR | DDB_DZT_PILOT | DDB_DZT_INPUT_F32)) return fail(DDB_ERR_INVALID, "bad flags %d", flags);
+  if (flags & ~(DDB_DZT_COLMAJOR | DDB_DZT_PILOT | DDB_DZT_INPUT_F32 | DDB_DZT_INVERSE)) return fail(DDB_ERR_INVALID, "bad flags %d", flags);
+  if ((flags & DDB_DZT_INVERSE) && (kernel || (flags & (DDB_DZT_PILOT | DDB_DZT_INPUT_F32)) || !(flags & DDB_DZT_COLMAJOR)))
+    return fail(DDB_ERR_INVALID, "DDB_DZT_INVERSE takes the default kernel, DDB_DZT_COLMAJOR and no pilot / f32 input");
   if ((flags & DDB_DZT_INPUT_F32) && (dtype != DDB_F64 || kernel || N < 2 || (N & (N - 1))))
     return fail(DDB_ERR_UNSUPPORTED, "complex64 input needs dtype f64, the default kernel and a power-of-two N");
   if ((flags & DDB_DZT_PILOT) && !(amplitude > 0))
@@ -458,7 +462,8 @@ int32_t ddb_dzt(int32_t batch, int32_t M, int32_t N, int32_t dtype, const void* 
                       ? ddb::launch_dzt_mixed(batch, M, N, y_time, flags & DDB_DZT_COLMAJOR, flags & DDB_DZT_PILOT, amp,
                                               out, static_cast<cudaStream_t>(stream))
                       : ddb::launch_dzt(dtype == DDB_F64, batch, M, N, y_time, kernel, flags & DDB_DZT_COLMAJOR,
-                                        flags & DDB_DZT_PILOT, amp, out, static_cast<cudaStream_t>(stream));
+                                        flags & DDB_DZT_PILOT, flags & DDB_DZT_INVERSE, amp, out,
+                                        static_cast<cudaStream_t>(stream));
   if (e != cudaSuccess) return cuda_fail(e, "dzt launch");
   return ok();
 }
@@ -473,6 +478,59 @@ int32_t ddb_estimate_heff(int64_t count, int32_t dtype, const void* y_dd, const 
   cudaError_t e = ddb::launch_estimate_heff(dtype == DDB_F64, count, y_dd, twist, amplitude, heff,
                                             static_cast<cudaStream_t>(stream));
   if (e != cudaSuccess) return cuda_fail(e, "estimate_heff launch");
+  return ok();
+}
+
+int32_t ddb_modulate(int64_t count, int32_t dtype, const uint8_t* labels, int32_t bits_per_symbol, void* out,
+                     void* stream) {
+  if (count < 0) return fail(DDB_ERR_INVALID, "negative count");
+  if (dtype != DDB_F32 && dtype != DDB_F64) return fail(DDB_ERR_INVALID, "bad dtype %d", dtype);
+  if (bits_per_symbol != 2 && bits_per_symbol != 4 && bits_per_symbol != 6)
+    return fail(DDB_ERR_INVALID, "bits_per_symbol must be 2, 4 or 6, got %d", bits_per_symbol);
+  if (count == 0) return ok();
+  if (!labels || !out) return fail(DDB_ERR_INVALID, "null pointer");
+  cudaError_t e = ddb::launch_modulate(dtype == DDB_F64, count, labels, bits_per_symbol, out,
+                                       static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "modulate launch");
+  return ok();
+}
+
+int32_t ddb_apply_channel(int32_t batch, int32_t M, int32_t N, int32_t dtype, const void* x,
+                          const int32_t* path_offsets, const int32_t* delay_bin, const double* doppler_hz,
+                          const double* delay_s, const void* gain, double bandwidth_hz, void* y, void* stream) {
+  if (batch < 0) return fail(DDB_ERR_INVALID, "negative batch");
+  if (dtype != DDB_F32 && dtype != DDB_F64) return fail(DDB_ERR_INVALID, "bad dtype %d", dtype);
+  if (M < 1 || N < 1) return fail(DDB_ERR_SHAPE, "grid must be positive, got (%d,%d)", M, N);
+  if ((long long)M * N >= (1LL << 29)) return fail(DDB_ERR_UNSUPPORTED, "grid too large");
+  if (!(bandwidth_hz > 0)) return fail(DDB_ERR_INVALID, "bandwidth must be positive");
+  if (batch == 0) return ok();
+  if (!x || !y || !path_offsets || !delay_bin || !doppler_hz || !delay_s || !gain)
+    return fail(DDB_ERR_INVALID, "null pointer");
+  if (x == y) return fail(DDB_ERR_INVALID, "apply_channel cannot run in place");
+  cudaError_t e = ddb::launch_apply_channel(dtype == DDB_F64, batch, M * N, bandwidth_hz, x, path_offsets, delay_bin,
+                                            doppler_hz, delay_s, gain, y, static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "apply_channel launch");
+  return ok();
+}
+
+int32_t ddb_add_awgn(int32_t batch, int64_t frame_len, int32_t dtype, const void* y, double snr_db, uint64_t seed,
+                     double* frame_power, void* out, void* stream) {
+  if (batch < 0 || frame_len < 0) return fail(DDB_ERR_INVALID, "negative batch/frame_len");
+  if (dtype != DDB_F32 && dtype != DDB_F64) return fail(DDB_ERR_INVALID, "bad dtype %d", dtype);
+  if (snr_db != snr_db) return fail(DDB_ERR_INVALID, "snr_db is NaN");
+  if (batch == 0 || frame_len == 0) return ok();
+  if (!y || !out) return fail(DDB_ERR_INVALID, "null pointer");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (std::isinf(snr_db) && snr_db > 0) {  // noiseless sentinel (channel.py:112-113): a copy
+    if (out == y) return ok();
+    const size_t bytes = (size_t)batch * frame_len * (dtype == DDB_F64 ? 16 : 8);
+    cudaError_t e = cudaMemcpyAsync(out, y, bytes, cudaMemcpyDeviceToDevice, st);
+    if (e != cudaSuccess) return cuda_fail(e, "awgn copy");
+    return ok();
+  }
+  if (!frame_power) return fail(DDB_ERR_INVALID, "frame_power scratch [batch] is required");
+  cudaError_t e = ddb::launch_add_awgn(dtype == DDB_F64, batch, frame_len, y, snr_db, seed, frame_power, out, st);
+  if (e != cudaSuccess) return cuda_fail(e, "awgn launch");
   return ok();
 }
 

@@ -27,7 +27,7 @@ constexpr int kDztThreads = 256;
 
 template <typename T, bool COLMAJOR, bool PILOT>
 __global__ void __launch_bounds__(kDztThreads) dzt_kernel(int M, int N, const Vec<T>* __restrict__ y,
-                                                          const Vec<T>* __restrict__ kern, T inv_amp,
+                                                          const Vec<T>* __restrict__ kern, int sgn, T inv_amp,
                                                           Vec<T>* __restrict__ out) {
   using V = Vec<T>;
   extern __shared__ __align__(16) unsigned char smem[];
@@ -43,7 +43,7 @@ __global__ void __launch_bounds__(kDztThreads) dzt_kernel(int M, int N, const Ve
       kk[idx] = kern[idx];
     } else {
       const int i = idx / N, l = idx - (idx / N) * N;
-      kk[idx] = cscale(twiddle(T(0), mod_pos(-i * l, N), N), rs);
+      kk[idx] = cscale(twiddle(T(0), mod_pos(sgn * ((i * l) % N), N), N), rs);
     }
   }
   for (int idx = threadIdx.x; idx < N * kTk; idx += blockDim.x) {
@@ -76,7 +76,7 @@ __global__ void __launch_bounds__(kDztThreads) dzt_kernel(int M, int N, const Ve
 // traffic per complex MAC drops ~5x and the kernel becomes FMA/HBM bound.
 template <typename T, bool COLMAJOR, bool PILOT, int NB>
 __global__ void __launch_bounds__(kDztThreads) dzt_blk_kernel(int M, int N, const Vec<T>* __restrict__ y,
-                                                              const Vec<T>* __restrict__ kern, T inv_amp,
+                                                              const Vec<T>* __restrict__ kern, int sgn, T inv_amp,
                                                               Vec<T>* __restrict__ out) {
   using V = Vec<T>;
   extern __shared__ __align__(16) unsigned char smem[];
@@ -87,8 +87,8 @@ __global__ void __launch_bounds__(kDztThreads) dzt_blk_kernel(int M, int N, cons
   const int MN = M * N;
   const V* yf = y + (size_t)f * MN;
   const T rs = T(1) / sqrt(T(N));
-  V* wn = kk + (size_t)N * N;  // [N]: W_N^{-e} / sqrt(N), the only distinct kernel values
-  for (int e = threadIdx.x; e < N; e += blockDim.x) wn[e] = cscale(twiddle(T(0), mod_pos(-e, N), N), rs);
+  V* wn = kk + (size_t)N * N;  // [N]: W_N^{sgn e} / sqrt(N), the only distinct kernel values
+  for (int e = threadIdx.x; e < N; e += blockDim.x) wn[e] = cscale(twiddle(T(0), mod_pos(sgn * e, N), N), rs);
   for (int idx = threadIdx.x; idx < N * kTk; idx += blockDim.x) {
     const int i = idx / kTk, kl = idx - i * kTk;
     const int k = k0 + kl;
@@ -137,16 +137,16 @@ __global__ void __launch_bounds__(kDztThreads) dzt_blk_kernel(int M, int N, cons
 // integer phases.  Same result to rounding (parity tolerances 1e-12 fp64).
 template <typename T, bool COLMAJOR, bool PILOT, typename VIN = Vec<T>>
 __global__ void __launch_bounds__(kDztThreads) dzt_fft_kernel(int M, int N, int logn, const VIN* __restrict__ y,
-                                                              T inv_amp, Vec<T>* __restrict__ out) {
+                                                              int sgn, T inv_amp, Vec<T>* __restrict__ out) {
   using V = Vec<T>;
   extern __shared__ __align__(16) unsigned char smem[];
   V* xs = reinterpret_cast<V*>(smem);  // [N][kTk], block index bit-reversed
-  V* wn = xs + (size_t)N * kTk;        // [N/2]: W_N^{-e}
+  V* wn = xs + (size_t)N * kTk;        // [N/2]: W_N^{sgn e} (sgn -1: dzt, +1: idzt)
   const int f = blockIdx.y;
   const int k0 = blockIdx.x * kTk;
   const int MN = M * N;
   const VIN* yf = y + (size_t)f * MN;
-  for (int e = threadIdx.x; e < N / 2; e += blockDim.x) wn[e] = twiddle(T(0), mod_pos(-e, N), N);
+  for (int e = threadIdx.x; e < N / 2; e += blockDim.x) wn[e] = twiddle(T(0), mod_pos(sgn * e, N), N);
   for (int idx = threadIdx.x; idx < N * kTk; idx += blockDim.x) {
     const int i = idx / kTk, kl = idx - i * kTk;
     const int k = k0 + kl;
@@ -190,7 +190,7 @@ __global__ void __launch_bounds__(kDztThreads) dzt_fft_kernel(int M, int N, int 
 }
 
 template <typename T, bool COLMAJOR, bool PILOT>
-cudaError_t launch_dzt_t(int B, int M, int N, const void* y, const void* kern, double amp, void* out,
+cudaError_t launch_dzt_t(int B, int M, int N, const void* y, const void* kern, int sgn, double amp, void* out,
                          cudaStream_t st) {
   using V = Vec<T>;
   const size_t smem = ((size_t)N * kTk + (size_t)N * N + N) * sizeof(V);
@@ -199,7 +199,7 @@ cudaError_t launch_dzt_t(int B, int M, int N, const void* y, const void* kern, d
   auto run = [&](auto kfn) -> cudaError_t {
     cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    kfn<<<grid, kDztThreads, smem, st>>>(M, N, (const V*)y, (const V*)kern, T(1.0 / amp), (V*)out);
+    kfn<<<grid, kDztThreads, smem, st>>>(M, N, (const V*)y, (const V*)kern, sgn, T(1.0 / amp), (V*)out);
     return cudaGetLastError();
   };
   if (!kern && N >= 2 && (N & (N - 1)) == 0) {  // default kernel, power-of-two N: FFT
@@ -209,8 +209,8 @@ cudaError_t launch_dzt_t(int B, int M, int N, const void* y, const void* kern, d
     cudaError_t e = cudaFuncSetAttribute(dzt_fft_kernel<T, COLMAJOR, PILOT>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fsmem);
     if (e != cudaSuccess) return e;
-    dzt_fft_kernel<T, COLMAJOR, PILOT><<<grid, kDztThreads, fsmem, st>>>(M, N, logn, (const V*)y, T(1.0 / amp),
-                                                                        (V*)out);
+    dzt_fft_kernel<T, COLMAJOR, PILOT><<<grid, kDztThreads, fsmem, st>>>(M, N, logn, (const V*)y, sgn,
+                                                                        T(1.0 / amp), (V*)out);
     return cudaGetLastError();
   }
   if (N % groups == 0) {
@@ -247,7 +247,7 @@ cudaError_t launch_dzt_mixed_t(int B, int M, int N, const void* y, double amp, v
   cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fsmem);
   if (e != cudaSuccess) return e;
   dim3 grid((M + kTk - 1) / kTk, B);
-  kfn<<<grid, kDztThreads, fsmem, st>>>(M, N, logn, (const float2*)y, 1.0 / amp, (double2*)out);
+  kfn<<<grid, kDztThreads, fsmem, st>>>(M, N, logn, (const float2*)y, -1, 1.0 / amp, (double2*)out);
   return cudaGetLastError();
 }
 
@@ -265,22 +265,23 @@ cudaError_t launch_dzt_mixed(int B, int M, int N, const void* y, int colmajor, i
 }
 
 cudaError_t launch_dzt(int dtype_f64, int B, int M, int N, const void* y, const void* kern, int colmajor, int pilot,
-                       double amp, void* out, cudaStream_t st) {
+                       int inverse, double amp, void* out, cudaStream_t st) {
+  const int sgn = inverse ? 1 : -1;
   if (B == 0) return cudaSuccess;
   const int sel = (colmajor ? 1 : 0) | (pilot ? 2 : 0);
   if (dtype_f64) {
     switch (sel) {
-      case 0: return launch_dzt_t<double, false, false>(B, M, N, y, kern, amp, out, st);
-      case 1: return launch_dzt_t<double, true, false>(B, M, N, y, kern, amp, out, st);
-      case 2: return launch_dzt_t<double, false, true>(B, M, N, y, kern, amp, out, st);
-      default: return launch_dzt_t<double, true, true>(B, M, N, y, kern, amp, out, st);
+      case 0: return launch_dzt_t<double, false, false>(B, M, N, y, kern, sgn, amp, out, st);
+      case 1: return launch_dzt_t<double, true, false>(B, M, N, y, kern, sgn, amp, out, st);
+      case 2: return launch_dzt_t<double, false, true>(B, M, N, y, kern, sgn, amp, out, st);
+      default: return launch_dzt_t<double, true, true>(B, M, N, y, kern, sgn, amp, out, st);
     }
   }
   switch (sel) {
-    case 0: return launch_dzt_t<float, false, false>(B, M, N, y, kern, amp, out, st);
-    case 1: return launch_dzt_t<float, true, false>(B, M, N, y, kern, amp, out, st);
-    case 2: return launch_dzt_t<float, false, true>(B, M, N, y, kern, amp, out, st);
-    default: return launch_dzt_t<float, true, true>(B, M, N, y, kern, amp, out, st);
+    case 0: return launch_dzt_t<float, false, false>(B, M, N, y, kern, sgn, amp, out, st);
+    case 1: return launch_dzt_t<float, true, false>(B, M, N, y, kern, sgn, amp, out, st);
+    case 2: return launch_dzt_t<float, false, true>(B, M, N, y, kern, sgn, amp, out, st);
+    default: return launch_dzt_t<float, true, true>(B, M, N, y, kern, sgn, amp, out, st);
   }
 }
 

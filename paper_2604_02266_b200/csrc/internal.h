@@ -124,13 +124,20 @@ cudaError_t launch_detect_paths(int B, int M, int N, const void* heff, double th
 // Receiver front end (frontend.cu): Zak transform (+ fused pilot estimate),
 // elementwise pilot estimate on a DD frame.
 cudaError_t launch_dzt(int dtype_f64, int B, int M, int N, const void* y, const void* kern, int colmajor, int pilot,
-                       double amp, void* out, cudaStream_t st);
+                       int inverse, double amp, void* out, cudaStream_t st);
 cudaError_t launch_dzt_mixed(int B, int M, int N, const void* y, int colmajor, int pilot, double amp, void* out,
                              cudaStream_t st);
 cudaError_t launch_estimate_heff(int dtype_f64, long long count, const void* ydd, const void* twist, double amp,
                                  void* heff, cudaStream_t st);
 
 // FP32 FMA throughput probe: blocks x 256 threads x iters x 256 FMAs.
+cudaError_t launch_modulate(int dtype_f64, long long count, const uint8_t* labels, int bps, void* out,
+                            cudaStream_t st);
+cudaError_t launch_apply_channel(int dtype_f64, int B, int MN, double bandwidth, const void* x, const int* off,
+                                 const int* kbin, const double* nu, const double* tau, const void* gain, void* y,
+                                 cudaStream_t st);
+cudaError_t launch_add_awgn(int dtype_f64, int B, long long L, const void* y, double snr_db, unsigned long long seed,
+                            double* power, void* out, cudaStream_t st);
 cudaError_t launch_fp32_probe(int mode, int blocks, int iters, float* out, cudaStream_t st);
 
 }  // namespace ddb

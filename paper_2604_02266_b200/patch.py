@@ -16,12 +16,19 @@ the receiver front end ddlink.zak.dzt_gemm / ddlink.harness.dzt_gemm (bound by
 name, harness.py:24) and ddlink.pilot.estimate_heff (called through the module,
 harness.py:157), and the package-level re-exports (__init__.py:14-63).  EmptyChannel stays the
 reference's class so run_packet's handler (harness.py:170) still catches it.
+
+With synthesis=True the transmit side and channel of run_packet run on the
+device too: ddlink.zak.idzt / ddlink.harness.idzt (bound
+by name, harness.py:24) and ddlink.channel.apply_channel (called through the
+module, harness.py:146-148), fp64 to rounding.  add_awgn keeps the caller's
+numpy generator, so seeded runs draw the reference's noise.
 """
 
 from __future__ import annotations
 
 import importlib
 
+from . import channel as _ch
 from . import equalize as _eq
 from . import grid as _gr
 from . import pilot as _pi
@@ -32,7 +39,7 @@ _SPARSE = ("detect_paths", "build_ss_channel", "ss_mvm", "ss_mvm_hermitian",
            "forward_index", "inverse_index", "coefficient")
 
 
-def install(ddlink_module=None, precision: str = "fp64") -> dict:
+def install(ddlink_module=None, precision: str = "fp64", synthesis: bool = False) -> dict:
     """Patch ddlink in place; returns the original bindings for `uninstall`."""
     d = ddlink_module if ddlink_module is not None else importlib.import_module("ddlink")
     sparse = importlib.import_module(d.__name__ + ".sparse")
@@ -61,6 +68,12 @@ def install(ddlink_module=None, precision: str = "fp64") -> dict:
         bind(mod, "dzt_gemm", _zk.dzt_gemm)
     for mod in (pilot, d):
         bind(mod, "estimate_heff", _pi.estimate_heff)
+    if synthesis:
+        channel = importlib.import_module(d.__name__ + ".channel")
+        for mod in (zak, harness, d):
+            bind(mod, "idzt", _ch.idzt)
+        for mod in (channel, d):
+            bind(mod, "apply_channel", _ch.apply_channel)
     return saved
 
 

@@ -130,3 +130,49 @@ def time_domain_frames(solver: SsCgaSolver, fb: FrameBatch, seed: int = 1) -> tu
     pilot_rx = dzt_device(hp.contiguous(), M, N, kernel=kinv, colmajor=True)
     data_rx = dzt_device(fb.y, M, N, kernel=kinv, colmajor=True)
     return pilot_rx, data_rx
+
+
+@dataclass
+class PacketBatch:
+    """Time-domain received pilot and data frames of a packet batch (the
+    channel side of run_packet, harness.py:141-149), all on the device."""
+
+    pilot_rx: torch.Tensor    # [B, MN] complex, time samples k + n M
+    data_rx: torch.Tensor     # [B, MN] complex
+    tx_labels: torch.Tensor   # uint8 [B, MN] (label of DD symbol q = l M + k)
+    channel: "ChannelBatch"   # physical paths (fractional Doppler)
+    lam: torch.Tensor         # [B] real, 1/SNR (0 when noiseless)
+    snr_db: float
+
+
+def synthesize_packets(solver: SsCgaSolver, B: int, snr_db: float = 25.0, nu_max_hz: float = 100.0,
+                       modulation: str = "qam16", seed: int = 0, delta_f: float = 30e3,
+                       cdtype=torch.complex128) -> PacketBatch:
+    """B packets through Veh-A channels with continuous Doppler, generated on
+    the GPU with the ddb synthesis kernels:
+    labels -> modulate (grid.py:157-169) -> idzt (zak.py:14-21) ->
+    apply_channel (channel.py:95-103) -> add_awgn (channel.py:106-119), and the
+    same channel and noise level for the point pilot (pilot.py:18-26), as
+    run_packet does per packet.  Fractional Doppler leaks into neighbouring
+    Doppler bins, so detect_paths finds more taps than paths, as it does for
+    the reference.  The RNG streams are the device's, not numpy's."""
+    from .channel import add_awgn_device, apply_channel_device, draw_veha_batch, idzt_device, modulate_device
+    from .grid import make_constellation_ext
+    dev = solver.device
+    M, N, MN = solver.M, solver.N, solver.MN
+    grid = GridConfig(M, N, delta_f)
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(seed)
+    bps = make_constellation_ext(modulation).bits_per_symbol
+    labels = torch.randint(0, 1 << bps, (B, MN), generator=gen, device=dev, dtype=torch.uint8)
+    ch = draw_veha_batch(B, grid, nu_max_hz, gen, dev, cdtype)
+    data_tx = idzt_device(modulate_device(labels, bps, cdtype), M, N)
+    pil_dd = torch.zeros(1, MN, dtype=cdtype, device=dev)
+    pil_dd[0, grid.L0 * M + grid.K0] = float(np.sqrt(MN))
+    pilot_tx = idzt_device(pil_dd, M, N).expand(B, MN).contiguous()
+    s0 = int(torch.randint(0, 2 ** 62, (1,), generator=gen, device=dev).item())
+    pilot_rx = add_awgn_device(apply_channel_device(pilot_tx, ch, grid), snr_db, s0)
+    data_rx = add_awgn_device(apply_channel_device(data_tx, ch, grid), snr_db, s0 + 1)
+    lam = torch.full((B,), 0.0 if np.isinf(snr_db) else 10.0 ** (-snr_db / 10.0), dtype=solver.rdtype,
+                     device=dev)
+    return PacketBatch(pilot_rx, data_rx, labels, ch, lam, snr_db)

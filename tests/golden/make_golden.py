@@ -356,6 +356,47 @@ def harness_fixture(d):
     )
 
 
+def channel_fixture(d):
+    """Frame synthesis: the reference's draw_veha on seeded
+    generators (channel.py:62-92), modulate (grid.py:157-169), idzt
+    (zak.py:14-21) and the noiseless apply_channel (channel.py:95-103) on
+    run_packet's data frames, at two grids with continuous Doppler."""
+    out = {}
+    for tag, M, N, mod, nu, seed, count in (("c1", 64, 16, "qpsk", 300.0, 41, 3), ("c3", 512, 32, "qam16", 100.0, 43, 2)):
+        grid = d.GridConfig(M, N)
+        const = d.make_constellation(mod)
+        b = const.bits_per_symbol
+        wts = 1 << np.arange(b - 1, -1, -1)
+        rec = {k: [] for k in ("labels", "X", "x", "y")}
+        pg, pd, pn, pk, off = [], [], [], [], [0]
+        for idx in range(count):
+            rng = np.random.default_rng([seed, idx])
+            pset = d.draw_veha(nu, grid, rng)
+            bits = rng.integers(0, 2, size=b * grid.size)
+            X = d.modulate(bits, const, grid)
+            x = d.idzt(X, grid)
+            rec["labels"].append((bits.reshape(-1, b) @ wts).astype(np.uint8))
+            rec["X"].append(d.flatten(X, grid))
+            rec["x"].append(x)
+            rec["y"].append(d.apply_channel(x, pset, grid))
+            for p in pset.paths:
+                pg.append(p.gain)
+                pd.append(p.delay_s)
+                pn.append(p.doppler_hz)
+                pk.append(p.delay_bin)
+            off.append(len(pg))
+        out[tag + "_meta"] = np.array([M, N, b, seed, count], np.int64)
+        out[tag + "_nu_max"] = np.array(nu)
+        for key in rec:
+            out[f"{tag}_{key}"] = np.stack(rec[key])
+        out[tag + "_path_off"] = np.asarray(off, np.int32)
+        out[tag + "_gain"] = np.asarray(pg, np.complex128)
+        out[tag + "_delay_s"] = np.asarray(pd, np.float64)
+        out[tag + "_doppler_hz"] = np.asarray(pn, np.float64)
+        out[tag + "_delay_bin"] = np.asarray(pk, np.int32)
+    np.savez_compressed(OUT / "channel.npz", **out)
+
+
 def main():
     d = _ref()
     if len(sys.argv) > 1:  # regenerate selected fixtures only, e.g. `make_golden.py frontend`
@@ -369,6 +410,7 @@ def main():
     frames_fixtures(d)
     frontend_fixture(d)
     harness_fixture(d)
+    channel_fixture(d)
     for p in sorted(OUT.glob("*.npz")):
         print(f"{p.name:24s} {p.stat().st_size / 1024:8.1f} KiB")
 

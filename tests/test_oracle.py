@@ -199,3 +199,54 @@ def test_oracle_receiver_reproduces_criterion6():
         diff = (lab ^ d["tx_labels"][i]).astype(np.uint8)
         errs.append(int(np.unpackbits(diff[:, None], axis=1).sum()))
     np.testing.assert_array_equal(np.array(errs), d["bit_errors"])
+
+
+class TestSynthesis:
+    """Frame synthesis pinned to the reference's draw_veha,
+    modulate, idzt and apply_channel outputs (tests/golden/channel.npz)."""
+
+    @pytest.mark.parametrize("tag", ["c1", "c3"])
+    def test_modulate_idzt_apply_channel(self, tag):
+        d = load_golden("channel")
+        M, N, b, _, count = (int(v) for v in d[tag + "_meta"])
+        const = orc.qam({2: "qpsk", 4: "qam16"}[b])
+        off = d[tag + "_path_off"]
+        for f in range(count):
+            X = orc.modulate_labels(d[tag + "_labels"][f], const)
+            np.testing.assert_allclose(X, d[tag + "_X"][f], rtol=0, atol=1e-15)
+            x = orc.idzt(X, M, N)
+            np.testing.assert_allclose(x, d[tag + "_x"][f], rtol=0, atol=1e-12)
+            a, e = int(off[f]), int(off[f + 1])
+            y = orc.apply_channel(x, d[tag + "_gain"][a:e], d[tag + "_delay_s"][a:e], d[tag + "_doppler_hz"][a:e],
+                                  d[tag + "_delay_bin"][a:e], M * 30e3)
+            np.testing.assert_allclose(y, d[tag + "_y"][f], rtol=0, atol=1e-12)
+
+    @pytest.mark.parametrize("tag", ["c1", "c3"])
+    def test_host_draw_veha_reproduces_reference_draws(self, tag):
+        """paper_2604_02266_b200.channel.draw_veha on run_packet's seeded generator
+        draws the reference's paths (same variates, same order)."""
+        from paper_2604_02266_b200.channel import draw_veha
+        from paper_2604_02266_b200.grid import GridConfig
+        d = load_golden("channel")
+        M, N, _, seed, count = (int(v) for v in d[tag + "_meta"])
+        off = d[tag + "_path_off"]
+        for f in range(count):
+            ps = draw_veha(float(d[tag + "_nu_max"]), GridConfig(M, N), np.random.default_rng([seed, f]))
+            a, e = int(off[f]), int(off[f + 1])
+            np.testing.assert_array_equal([p.gain for p in ps.paths], d[tag + "_gain"][a:e])
+            np.testing.assert_array_equal([p.doppler_hz for p in ps.paths], d[tag + "_doppler_hz"][a:e])
+            np.testing.assert_array_equal([p.delay_bin for p in ps.paths], d[tag + "_delay_bin"][a:e])
+            np.testing.assert_array_equal([p.delay_s for p in ps.paths], d[tag + "_delay_s"][a:e])
+
+    def test_make_path_range_errors(self):
+        from paper_2604_02266_b200.channel import draw_veha, make_path
+        from paper_2604_02266_b200.grid import GridConfig
+        g = GridConfig(64, 16)
+        with pytest.raises(ValueError):
+            make_path(1.0, 64 / g.B, 0.0, g)          # delay bin outside the period
+        with pytest.raises(ValueError):
+            make_path(1.0, 0.0, 9 * g.delta_nu, g)     # beyond half the Doppler period
+        with pytest.raises(ValueError):
+            draw_veha(-1.0, g, np.random.default_rng(0))
+        with pytest.raises(ValueError):
+            draw_veha(100.0, GridConfig(8, 16, 1e6), np.random.default_rng(0))  # delay spread > period (1 us)

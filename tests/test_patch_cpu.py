@@ -38,3 +38,21 @@ def test_install_and_uninstall(ddlink):
         sp.EmptyChannel = b200.EmptyChannel
     assert ddlink.harness.cga_equalize is orig_cga
     assert ddlink.harness.dzt_gemm is not b200.dzt_gemm
+
+
+def test_install_with_synthesis(ddlink):
+    import paper_2604_02266_b200 as b200
+    from paper_2604_02266_b200 import channel as pch
+    from paper_2604_02266_b200 import patch
+
+    orig_idzt, orig_apply = ddlink.harness.idzt, ddlink.channel.apply_channel
+    saved = patch.install(ddlink, synthesis=True)
+    try:
+        assert ddlink.harness.idzt is pch.idzt and ddlink.zak.idzt is pch.idzt and ddlink.idzt is pch.idzt
+        assert ddlink.channel.apply_channel is pch.apply_channel and ddlink.apply_channel is pch.apply_channel
+        assert ddlink.channel.add_awgn is not pch.add_awgn  # the reference's noise stream stays
+    finally:
+        patch.uninstall(saved)
+        import paper_2604_02266_b200.sparse as sp
+        sp.EmptyChannel = b200.EmptyChannel
+    assert ddlink.harness.idzt is orig_idzt and ddlink.channel.apply_channel is orig_apply
