@@ -28,6 +28,8 @@
  *   ddb_modulate         grid.py:157-169     modulate (labels -> constellation points)
  *   ddb_apply_channel    channel.py:95-103   apply_channel (delay shift + Doppler ramp)
  *   ddb_add_awgn         channel.py:106-119  add_awgn (own counter-based RNG)
+ *   ddb_threshold_frame  sparse.py:163-169   threshold_frame (dense LMMSE baseline)
+ *   ddb_build_dense_hdd  sparse.py:172-206   build_dense_hdd (dense LMMSE baseline)
  *
  * Layouts (identical to the reference's numpy layouts):
  *   complex values are interleaved (re, im) of the problem dtype;
@@ -215,6 +217,19 @@ int32_t ddb_apply_channel(int32_t batch, int32_t M, int32_t N, int32_t dtype, co
                           const double* delay_s, const void* gain, double bandwidth_hz, void* y, void* stream);
 int32_t ddb_add_awgn(int32_t batch, int64_t frame_len, int32_t dtype, const void* y, double snr_db, uint64_t seed,
                      double* frame_power, void* out, void* stream);
+
+/* ---- dense LMMSE baseline, MN <= 4096.
+ *      ddb_threshold_frame  sparse.py:163-169: zero every bin of heff [B, M, N]
+ *                           (row-major (M, N) frames) with |h| <= theta * peak
+ *                           (peak 0: copy).
+ *      ddb_build_dense_hdd  sparse.py:172-206: H [B, MN, MN] row-major (row
+ *                           q' = l'M + k', column q = lM + k) from heff frames.
+ *      The Gram matrix and Cholesky solve of lmmse_equalize (equalize.py:80-94)
+ *      are library calls (cuBLAS / cuSOLVER) in the host mirror. */
+int32_t ddb_threshold_frame(int32_t batch, int32_t M, int32_t N, int32_t dtype, const void* heff, double theta,
+                            void* out, void* stream);
+int32_t ddb_build_dense_hdd(int32_t batch, int32_t M, int32_t N, int32_t dtype, const void* heff, void* H,
+                            void* stream);
 
 /* ---- measurement helper (not a reference interface): FP32 FMA throughput
  *      probe used by bench.py to state the measured FP32 roofline.  Launches

@@ -18,6 +18,8 @@ and the receiver front end before it (section 8f row f1):
     dzt_gemm (pilot, data) -> estimate_heff
 and the frame synthesis that feeds it (section 8f row f2):
     modulate_labels -> idzt -> apply_channel
+and the dense cross-check (section 8f row f4):
+    threshold_frame -> dense_channel -> lmmse
 """
 
 from __future__ import annotations
@@ -197,6 +199,41 @@ def apply_channel(x: np.ndarray, gains, delay_s, doppler_hz, delay_bin, bandwidt
     for h, tau, nu, k in zip(gains, delay_s, doppler_hz, delay_bin):
         y += h * np.roll(x, int(k)) * np.exp(2j * np.pi * nu * (i / bandwidth - tau))
     return y
+
+
+# --------------------------------------------------------------------------
+# dense LMMSE baseline (sparse.py:163-206, equalize.py:80-94) — SURVEY.md 8f row f4
+
+
+def threshold_frame(heff: np.ndarray, theta: float) -> np.ndarray:
+    """Keep bins with |h| > theta * peak, all of them if the peak is 0 (sparse.py:163-169)."""
+    mags = np.abs(heff)
+    peak = mags.max()
+    return np.where(mags > theta * peak, heff, 0.0) if peak > 0 else np.array(heff, copy=True)
+
+
+def dense_channel(heff: np.ndarray, M: int, N: int) -> np.ndarray:
+    """MN x MN DD channel matrix of an effective-channel frame (sparse.py:172-206):
+    entry (l'M + k', lM + k) = heff[K0 + dk, L0 + dl] e^{j2pi (dl (k + nM) / MN + n l / N)}
+    with the unique wraps n, m that bring (dk, dl) into the signed fundamental range."""
+    MN, K0, L0 = M * N, M // 2, N // 2
+    q = np.arange(MN)
+    kc, lc = q % M, q // M
+    kr, lr = kc[:, None], lc[:, None]
+    n = (kr - kc[None, :] + K0) // M
+    m = (lr - lc[None, :] + L0) // N
+    dk = kr - kc[None, :] - n * M
+    dl = lr - lc[None, :] - m * N
+    ph = np.exp(2j * np.pi * (dl * (kc[None, :] + n * M) / MN + n * lc[None, :] / N))
+    return heff[K0 + dk, L0 + dl] * ph
+
+
+def lmmse(H: np.ndarray, y: np.ndarray, lam: float) -> np.ndarray:
+    """(H^H H + lam I)^{-1} H^H y by a Cholesky solve (equalize.py:80-94)."""
+    g = H.conj().T @ H + lam * np.eye(H.shape[1])
+    L = np.linalg.cholesky(g)
+    z = np.linalg.solve(L, H.conj().T @ y)
+    return np.linalg.solve(L.conj().T, z)
 
 
 # --------------------------------------------------------------------------

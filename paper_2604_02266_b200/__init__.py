@@ -35,6 +35,7 @@ from .sparse import (
     ss_mvm_hermitian,
 )
 from .zak import build_zak_kernel, dzt_device, dzt_gemm
+from .dense import build_dense_hdd, lmmse_equalize, receive_lmmse, threshold_frame
 from .channel import (
     ChannelBatch,
     PathSet,
@@ -62,6 +63,7 @@ __all__ = [
     "build_zak_kernel", "dzt_device", "dzt_gemm",
     "ChannelBatch", "PathSet", "PathSpec", "add_awgn", "add_awgn_device", "apply_channel", "apply_channel_device",
     "draw_veha", "draw_veha_batch", "idzt", "idzt_device", "make_path", "modulate_device",
+    "build_dense_hdd", "lmmse_equalize", "receive_lmmse", "threshold_frame",
 ]
 
 __version__ = "0.1.0"

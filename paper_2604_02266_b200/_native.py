@@ -98,6 +98,10 @@ _SIGNATURES = {
                                       C.c_void_p]),
     "ddb_add_awgn": (C.c_int32, [C.c_int32, C.c_int64, C.c_int32, C.c_void_p, C.c_double, C.c_uint64,
                                  C.c_void_p, C.c_void_p, C.c_void_p]),
+    "ddb_threshold_frame": (C.c_int32, [C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_void_p, C.c_double,
+                                        C.c_void_p, C.c_void_p]),
+    "ddb_build_dense_hdd": (C.c_int32, [C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p,
+                                        C.c_void_p]),
     "ddb_probe_fp32": (C.c_int32, [C.c_int32, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p]),
     "ddb_sscga_profile_phases": (C.c_int32, [C.POINTER(Problem), C.POINTER(Outputs), C.c_void_p, C.c_void_p]),
 }

@@ -16,7 +16,7 @@ PKG_DIR = Path(__file__).resolve().parent
 REPO_DIR = PKG_DIR.parent
 CSRC = PKG_DIR / "csrc"
 LIB_PATH = PKG_DIR / "libddb.so"
-SOURCES = ("sscga.cu", "sscga_tm.cu", "sscga_global.cu", "aux.cu", "frontend.cu", "channel.cu", "capi.cu")
+SOURCES = ("sscga.cu", "sscga_tm.cu", "sscga_global.cu", "aux.cu", "frontend.cu", "channel.cu", "dense.cu", "capi.cu")
 HEADERS = ("common.cuh", "cg.cuh", "demod.cuh", "internal.h")
 
 NVCC_FLAGS = [

@@ -534,6 +534,34 @@ int32_t ddb_add_awgn(int32_t batch, int64_t frame_len, int32_t dtype, const void
   return ok();
 }
 
+int32_t ddb_threshold_frame(int32_t batch, int32_t M, int32_t N, int32_t dtype, const void* heff, double theta,
+                            void* out, void* stream) {
+  if (batch < 0) return fail(DDB_ERR_INVALID, "negative batch");
+  if (dtype != DDB_F32 && dtype != DDB_F64) return fail(DDB_ERR_INVALID, "bad dtype %d", dtype);
+  if (M < 1 || N < 1) return fail(DDB_ERR_SHAPE, "grid must be positive, got (%d,%d)", M, N);
+  if ((long long)M * N >= (1LL << 29)) return fail(DDB_ERR_UNSUPPORTED, "grid too large");
+  if (batch == 0) return ok();
+  if (!heff || !out) return fail(DDB_ERR_INVALID, "null pointer");
+  cudaError_t e = ddb::launch_threshold_frame(dtype == DDB_F64, batch, M * N, heff, theta, out,
+                                              static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "threshold_frame launch");
+  return ok();
+}
+
+int32_t ddb_build_dense_hdd(int32_t batch, int32_t M, int32_t N, int32_t dtype, const void* heff, void* H,
+                            void* stream) {
+  if (batch < 0) return fail(DDB_ERR_INVALID, "negative batch");
+  if (dtype != DDB_F32 && dtype != DDB_F64) return fail(DDB_ERR_INVALID, "bad dtype %d", dtype);
+  int32_t r = check_grid(M, N);
+  if (r) return r;
+  if (M * N > 4096) return fail(DDB_ERR_SHAPE, "dense channel matrix limited to MN <= 4096, got %d", M * N);
+  if (batch == 0) return ok();
+  if (!heff || !H) return fail(DDB_ERR_INVALID, "null pointer");
+  cudaError_t e = ddb::launch_build_dense(dtype == DDB_F64, batch, M, N, heff, H, static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "build_dense_hdd launch");
+  return ok();
+}
+
 int32_t ddb_probe_fp32(int32_t mode, int32_t blocks, int32_t iters, float* scratch, void* stream) {
   if ((mode != 0 && mode != 1) || blocks < 1 || iters < 1 || !scratch)
     return fail(DDB_ERR_INVALID, "bad probe arguments");

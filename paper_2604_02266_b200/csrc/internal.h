@@ -138,6 +138,9 @@ cudaError_t launch_apply_channel(int dtype_f64, int B, int MN, double bandwidth,
                                  cudaStream_t st);
 cudaError_t launch_add_awgn(int dtype_f64, int B, long long L, const void* y, double snr_db, unsigned long long seed,
                             double* power, void* out, cudaStream_t st);
+cudaError_t launch_threshold_frame(int dtype_f64, int B, int MN, const void* heff, double theta, void* out,
+                                   cudaStream_t st);
+cudaError_t launch_build_dense(int dtype_f64, int B, int M, int N, const void* heff, void* H, cudaStream_t st);
 cudaError_t launch_fp32_probe(int mode, int blocks, int iters, float* out, cudaStream_t st);
 
 }  // namespace ddb

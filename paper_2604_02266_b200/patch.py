@@ -14,7 +14,9 @@ forward_index, inverse_index, coefficient}, ddlink.equalize.cga_equalize,
 ddlink.harness.cga_equalize (bound by name, harness.py:23), ddlink.grid.hard_demod,
 the receiver front end ddlink.zak.dzt_gemm / ddlink.harness.dzt_gemm (bound by
 name, harness.py:24) and ddlink.pilot.estimate_heff (called through the module,
-harness.py:157), and the package-level re-exports (__init__.py:14-63).  EmptyChannel stays the
+harness.py:157), the dense LMMSE branch ddlink.sparse.{threshold_frame,
+build_dense_hdd} and ddlink.equalize/harness.lmmse_equalize (harness.py:23,
+163-168, 192), and the package-level re-exports (__init__.py:14-63).  EmptyChannel stays the
 reference's class so run_packet's handler (harness.py:170) still catches it.
 
 With synthesis=True the transmit side and channel of run_packet run on the
@@ -29,6 +31,7 @@ from __future__ import annotations
 import importlib
 
 from . import channel as _ch
+from . import dense as _dn
 from . import equalize as _eq
 from . import grid as _gr
 from . import pilot as _pi
@@ -68,6 +71,14 @@ def install(ddlink_module=None, precision: str = "fp64", synthesis: bool = False
         bind(mod, "dzt_gemm", _zk.dzt_gemm)
     for mod in (pilot, d):
         bind(mod, "estimate_heff", _pi.estimate_heff)
+    # the dense LMMSE branch of run_packet (harness.py:160-168, 191-192)
+    for name in ("threshold_frame", "build_dense_hdd"):
+        bind(sparse, name, getattr(_dn, name))
+        if hasattr(d, name):
+            bind(d, name, getattr(_dn, name))
+    for mod in (equalize, harness, d):
+        if hasattr(mod, "lmmse_equalize"):
+            bind(mod, "lmmse_equalize", _dn.lmmse_equalize)
     if synthesis:
         channel = importlib.import_module(d.__name__ + ".channel")
         for mod in (zak, harness, d):

@@ -397,6 +397,44 @@ def channel_fixture(d):
     np.savez_compressed(OUT / "channel.npz", **out)
 
 
+def dense_fixture(d):
+    """Dense LMMSE baseline: the reference's
+    threshold_frame / build_dense_hdd / lmmse_equalize on estimated
+    effective channels of small grids, and acceptance criterion 6's dense
+    arm (run_packets with equalizer="lmmse" on the criterion's 200 packets,
+    tests/test_acceptance.py:179-192; mean BER 3.662e-4, test_output.txt:234)."""
+    from ddlink.harness import Workspace
+    out = {}
+    for tag, M, N, seed in (("s1", 16, 8, 51), ("s2", 32, 8, 52)):
+        cfg = d.SimConfig(m=M, n=N, mod="qpsk", snr_db=20.0, nu_max_hz=300.0, theta=0.08, packets=1, seed=seed)
+        ws = Workspace(cfg)
+        grid = ws.grid
+        rng = np.random.default_rng([seed, 0])
+        pset = d.draw_veha(cfg.nu_max_hz, grid, rng)
+        tx_bits = rng.integers(0, 2, size=2 * grid.size)
+        data_tx = d.idzt(d.modulate(tx_bits, ws.const, grid), grid)
+        pilot_rx = d.add_awgn(d.apply_channel(ws.pilot_tx, pset, grid), cfg.snr_db, rng)
+        data_rx = d.add_awgn(d.apply_channel(data_tx, pset, grid), cfg.snr_db, rng)
+        heff = d.estimate_heff(d.dzt_gemm(pilot_rx, ws.zak_kernel, grid), ws.twist, grid)
+        thr = d.threshold_frame(heff, cfg.theta, grid)
+        H = d.build_dense_hdd(thr, grid)
+        y = d.flatten(d.dzt_gemm(data_rx, ws.zak_kernel, grid), grid)
+        out[tag + "_meta"] = np.array([M, N], np.int64)
+        out[tag + "_theta"] = np.array(cfg.theta)
+        out[tag + "_snr_linear"] = np.array(cfg.snr_linear)
+        out[tag + "_heff"] = heff
+        out[tag + "_thr"] = thr
+        out[tag + "_H"] = H
+        out[tag + "_y"] = y
+        out[tag + "_x"] = d.lmmse_equalize(H, y, cfg.snr_linear)
+    cfg = d.SimConfig(m=32, n=32, packets=200, seed=11, equalizer="lmmse")
+    res = d.run_packets(cfg)
+    out["c6_bit_errors"] = np.array([r.bit_errors for r in res], np.int64)
+    out["c6_failed"] = np.array([r.failed for r in res], bool)
+    out["c6_ber"] = np.array([r.ber for r in res])
+    np.savez_compressed(OUT / "dense.npz", **out)
+
+
 def main():
     d = _ref()
     if len(sys.argv) > 1:  # regenerate selected fixtures only, e.g. `make_golden.py frontend`
@@ -411,6 +449,7 @@ def main():
     frontend_fixture(d)
     harness_fixture(d)
     channel_fixture(d)
+    dense_fixture(d)
     for p in sorted(OUT.glob("*.npz")):
         print(f"{p.name:24s} {p.stat().st_size / 1024:8.1f} KiB")
 

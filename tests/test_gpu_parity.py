@@ -747,3 +747,47 @@ class TestSynthesis:
             x, _, lab, _ = orc.receive(taps, y, 32, 32, 10, float(pb.lam[f]), const)
             mism = labels[f] != lab
             assert np.all(orc.decision_margin(x, const)[mism] < TIE_BAND)
+
+
+# ---------------------------------------------------------------- dense LMMSE baseline
+class TestDense:
+    @pytest.mark.parametrize("tag", ["s1", "s2"])
+    def test_drop_ins_vs_reference(self, pkg, tag):
+        from paper_2604_02266_b200 import dense as dn
+        d = load_golden("dense")
+        M, N = (int(v) for v in d[tag + "_meta"])
+        g = pkg.GridConfig(M, N)
+        thr = dn.threshold_frame(d[tag + "_heff"], float(d[tag + "_theta"]), g)
+        np.testing.assert_array_equal(thr, d[tag + "_thr"])
+        H = dn.build_dense_hdd(d[tag + "_thr"], g)
+        np.testing.assert_allclose(H, d[tag + "_H"], rtol=0, atol=1e-14)
+        x = dn.lmmse_equalize(d[tag + "_H"], d[tag + "_y"], float(d[tag + "_snr_linear"]))
+        np.testing.assert_allclose(x, d[tag + "_x"], rtol=0, atol=1e-10 * np.abs(d[tag + "_x"]).max())
+        with pytest.raises(ValueError):
+            dn.lmmse_equalize(d[tag + "_H"], d[tag + "_y"], 0.0)
+        with pytest.raises(ValueError):
+            dn.lmmse_equalize(d[tag + "_H"][:-1], d[tag + "_y"], 10.0)
+        with pytest.raises(ValueError):
+            dn.build_dense_hdd(np.zeros((128, 64), complex), pkg.GridConfig(128, 64))  # MN > 4096
+
+    def test_criterion6_dense_arm_per_packet(self, pkg):
+        """The reference's criterion-6 packets (harness_c6 fixture) through the
+        device dense receiver reproduce run_packets(equalizer="lmmse") packet by
+        packet (150 bit errors, mean BER 3.662e-4), and the device SS-CGA arm
+        meets the criterion's bound (iterative <= 2x dense)."""
+        from paper_2604_02266_b200.dense import receive_lmmse
+        h = load_golden("harness_c6")
+        d = load_golden("dense")
+        M, N, iters, b, P = (int(v) for v in h["meta"])
+        s = pkg.SsCgaSolver(M, N, iters, precision="fp64", modulation="qpsk")
+        pil = torch.as_tensor(h["pilot_rx"], device="cuda")
+        dat = torch.as_tensor(h["data_rx"], device="cuda")
+        tx = torch.as_tensor(h["tx_labels"], device="cuda")
+        r = receive_lmmse(s, pil, dat, float(h["snr_db"]), float(h["theta"]), tx_labels=tx)
+        np.testing.assert_array_equal(r["bit_errors"].cpu().numpy(), d["c6_bit_errors"])
+        np.testing.assert_array_equal(r["failed"].cpu().numpy(), d["c6_failed"])
+        lam = 1.0 / 10 ** (float(h["snr_db"]) / 10)
+        cga = s.receive(pil, dat, torch.full((P,), lam, dtype=torch.float64), float(h["theta"]), tx_labels=tx)
+        ber_cga = int(cga.bit_errors.sum()) / (P * M * N * b)
+        ber_lm = int(r["bit_errors"].sum()) / (P * M * N * b)
+        assert ber_cga <= 2.0 * ber_lm

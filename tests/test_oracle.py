@@ -250,3 +250,24 @@ class TestSynthesis:
             draw_veha(-1.0, g, np.random.default_rng(0))
         with pytest.raises(ValueError):
             draw_veha(100.0, GridConfig(8, 16, 1e6), np.random.default_rng(0))  # delay spread > period (1 us)
+
+
+class TestDense:
+    """Dense LMMSE baseline pinned to the reference's
+    threshold_frame / build_dense_hdd / lmmse_equalize (tests/golden/dense.npz)."""
+
+    @pytest.mark.parametrize("tag", ["s1", "s2"])
+    def test_threshold_dense_lmmse(self, tag):
+        d = load_golden("dense")
+        M, N = (int(v) for v in d[tag + "_meta"])
+        thr = orc.threshold_frame(d[tag + "_heff"], float(d[tag + "_theta"]))
+        np.testing.assert_array_equal(thr, d[tag + "_thr"])
+        H = orc.dense_channel(thr, M, N)
+        np.testing.assert_allclose(H, d[tag + "_H"], rtol=0, atol=1e-14)
+        x = orc.lmmse(d[tag + "_H"], d[tag + "_y"], 1.0 / float(d[tag + "_snr_linear"]))
+        np.testing.assert_allclose(x, d[tag + "_x"], rtol=0, atol=1e-10 * np.abs(d[tag + "_x"]).max())
+
+    def test_criterion6_dense_arm_known_answer(self):
+        d = load_golden("dense")
+        assert d["c6_bit_errors"].sum() == 150 and not d["c6_failed"].any()
+        assert abs(d["c6_ber"].mean() - 3.662e-4) < 5e-8  # test_output.txt:234

@@ -29,6 +29,9 @@ def test_install_and_uninstall(ddlink):
         assert ddlink.detect_paths is b200.detect_paths
         assert ddlink.harness.dzt_gemm is b200.dzt_gemm and ddlink.zak.dzt_gemm is b200.dzt_gemm
         assert ddlink.pilot.estimate_heff is b200.estimate_heff
+        assert ddlink.harness.lmmse_equalize is b200.lmmse_equalize
+        assert ddlink.sparse.build_dense_hdd is b200.build_dense_hdd
+        assert ddlink.sparse.threshold_frame is b200.threshold_frame
         # the reference's EmptyChannel is what the drop-in raises (harness.py:170)
         with pytest.raises(ddlink.EmptyChannel):
             b200.build_ss_channel([], ddlink.GridConfig(8, 4))
