@@ -56,6 +56,9 @@ CONFIGS = {
     # the paper's real-time grid: beyond a cluster's on-chip
     # memory, so the workspace-backed kernels run it
     "paper": dict(M=16384, N=32, P=6, mod="qam16", batch=128, nu=100.0),
+    # the grid the paper times its SS-CGA equalization on (PAPER.md:1529, 1627-1629:
+    # (128, 32), QPSK; 0.54-0.78 ms per frame on H200)
+    "paper128": dict(M=128, N=32, P=6, mod="qpsk", batch=4096, nu=100.0),
 }
 BPS = {"qpsk": 2, "qam16": 4, "qam64": 6}
 
@@ -499,12 +502,37 @@ def main():
         torch.cuda.synchronize()
         lat = sorted(a.elapsed_time(b) for a, b in ev)
         n_clu = max(1, sms // max(1, s.plan()["cluster"]))  # persistent clusters (1 CTA per SM)
+        # the whole receiver for one packet from time-domain pilot and data frames
+        # (SsCgaSolver.receive: pilot DZT + detect_paths + CSR, data DZT, solve), as
+        # the paper's full-receiver p99.9; not graph-captured (the
+        # tap CSR is sized on the host), so host round trips are inside the time
+        from paper_2604_02266_b200.synth import synthesize_packets
+        pk1 = synthesize_packets(s, 1, snr_db=args.snr, nu_max_hz=cfg["nu"], modulation=cfg["mod"], seed=7,
+                                 cdtype=s.cdtype)
+        for _ in range(5):
+            s.receive(pk1.pilot_rx, pk1.data_rx, pk1.lam, 0.08, tx_labels=pk1.tx_labels, trace=False)
+        torch.cuda.synchronize()
+        rlat = []
+        for _ in range(min(args.lat_runs, 1000)):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            s.receive(pk1.pilot_rx, pk1.data_rx, pk1.lam, 0.08, tx_labels=pk1.tx_labels, trace=False)
+            b.record()
+            b.synchronize()
+            rlat.append(a.elapsed_time(b))
+        rlat.sort()
+        del pk1
         latency = {"p50_ms": lat[len(lat) // 2], "p99_ms": lat[int(len(lat) * 0.99)],
+                   "p999_ms": lat[int(len(lat) * 0.999)],
                    "max_ms": lat[-1], "runs": len(lat), "frame_duration_ms": 1e3 * N / 30e3,
+                   "receiver_p50_ms": rlat[len(rlat) // 2], "receiver_p99_ms": rlat[int(len(rlat) * 0.99)],
+                   "receiver_p999_ms": rlat[int(len(rlat) * 0.999)], "receiver_runs": len(rlat),
                    # in a full batch every cluster solves B / clusters frames back to back
                    "in_batch_frame_residency_ms": ms_step * n_clu / B if s.plan()["kernel"] != "workspace" else None,
                    "what": ("batch-1 solve (one fused launch" if s.plan()["kernel"] != "workspace" else
-                            "batch-1 solve (workspace-backed kernels, one graph") + ", CUDA graph replay), device events"}
+                            "batch-1 solve (workspace-backed kernels, one graph") + ", CUDA graph replay), device events; "
+                           "receiver_*: one packet through SsCgaSolver.receive from time-domain pilot + data "
+                           "frames (device-synthesised), events around the call"}
 
     # ---- end to end from pinned host buffers (HostPipeline)
     e2e = None

@@ -24,6 +24,7 @@
  *   ddb_estimate_heff    pilot.py:40-49      estimate_heff on a DD frame
  *   ddb_detect_paths     sparse.py:69-88     detect_paths (strict relative threshold,
  *                                            stable descending-magnitude order)
+ *   ddb_paths_csr        harness.py:159-163  taps -> build_ss_channel's input, batched as CSR
  *   ddb_dzt + INVERSE    zak.py:14-21        idzt (transmit side, frame synthesis)
  *   ddb_modulate         grid.py:157-169     modulate (labels -> constellation points)
  *   ddb_apply_channel    channel.py:95-103   apply_channel (delay shift + Doppler ramp)
@@ -168,6 +169,19 @@ int32_t ddb_qam_demod(int64_t count, int32_t dtype, const void* x, int32_t bits_
 int32_t ddb_detect_paths(int32_t batch, int32_t M, int32_t N, const void* heff, double theta,
                          int32_t max_paths, int32_t* count, int32_t* path_k,
                          int32_t* path_l, void* path_gain, void* stream);
+
+/* ---- detected taps -> the solver's CSR, on the device: count [B] and the
+ *      ranked rows [B, max_paths] of ddb_detect_paths become path_offsets
+ *      [B+1] (exclusive scan of the stored rows, clamp(count, 0, max_paths))
+ *      and csr_k / csr_l / csr_gain (gain in `dtype`), each sized for
+ *      B * max_paths.
+ *      stats [3] receives the minimum and maximum count (a negative minimum:
+ *      a frame overflowed the candidate list; maximum > max_paths: truncated)
+ *      and the number of rows stored, so a caller checks and sizes the batch
+ *      with one 12-byte read. */
+int32_t ddb_paths_csr(int32_t batch, int32_t max_paths, const int32_t* count, const int32_t* path_k,
+                      const int32_t* path_l, const void* path_gain, int32_t dtype, int32_t* path_offsets,
+                      int32_t* csr_k, int32_t* csr_l, void* csr_gain, int32_t* stats, void* stream);
 
 /* ---- receiver front end.
  *      ddb_dzt: y_time complex [B, M*N] received samples (time index k + i*M,

@@ -281,24 +281,26 @@ class SsCgaSolver:
         nat.check(self.lib.ddb_detect_paths(B, self.M, self.N, _ptr(heff), float(theta), max_paths, _ptr(cnt),
                                             _ptr(kk), _ptr(ll), _ptr(gg), _stream_handle(stream)),
                   "ddb_detect_paths")
-        cmin, cmax = int(cnt.min().item()), int(cnt.max().item())
+        # CSR on the device (ddb_paths_csr); one 12-byte read checks and sizes the batch
+        cap = max(1, B * max_paths)
+        off = torch.empty(B + 1, dtype=torch.int32, device=self.device)
+        k = torch.empty(cap, dtype=torch.int32, device=self.device)
+        l = torch.empty(cap, dtype=torch.int32, device=self.device)
+        g = torch.empty(cap, dtype=self.cdtype, device=self.device)
+        stats = torch.empty(3, dtype=torch.int32, device=self.device)
+        nat.check(self.lib.ddb_paths_csr(B, max_paths, _ptr(cnt), _ptr(kk), _ptr(ll), _ptr(gg), self.dtype_code,
+                                         _ptr(off), _ptr(k), _ptr(l), _ptr(g), _ptr(stats), _stream_handle(stream)),
+                  "ddb_paths_csr")
+        if stream is not None:
+            stream.synchronize()
+        cmin, cmax, total = (int(v) for v in stats.tolist())
         if cmin < 0:
             raise nat.DdbError(nat.DDB_ERR_UNSUPPORTED, "ddb_detect_paths",
                                "candidate list exceeds the per-frame shared-memory capacity")
         if cmax > max_paths:
             raise ValueError(f"a frame has {cmax} taps above threshold > max_paths={max_paths}")
-        # CSR by an exclusive scan of the counts (device tensors, no host round trip of taps)
-        off = torch.zeros(B + 1, dtype=torch.int32, device=self.device)
-        off[1:] = torch.cumsum(cnt, 0)
-        keep = torch.arange(max_paths, device=self.device)[None, :] < cnt[:, None]
-        k = kk[keep].contiguous()
-        l = ll[keep].contiguous()
-        g = gg[keep].to(self.cdtype).contiguous()
-        if k.numel() == 0:  # all frames empty: keep valid device pointers
-            k = torch.zeros(1, dtype=torch.int32, device=self.device)
-            l = torch.zeros(1, dtype=torch.int32, device=self.device)
-            g = torch.zeros(1, dtype=self.cdtype, device=self.device)
-        return PathBatch(off, k, l, g)
+        n = max(total, 1)  # all frames empty: keep valid device pointers
+        return PathBatch(off, k[:n], l[:n], g[:n])
 
     def receive(self, pilot_rx: torch.Tensor, data_rx: torch.Tensor, lam, theta: float = 0.08, *,
                 max_paths: int = 64, tx_labels: Optional[torch.Tensor] = None, llr: bool = False,

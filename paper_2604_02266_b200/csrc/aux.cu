@@ -3,6 +3,9 @@
 //   K5 table-driven MVM        (sparse.py:147-160 ss_mvm / ss_mvm_hermitian)
 //   K6 demod                   (grid.py:172-183 hard_demod; Gray-QAM max-log LLR)
 //   f1 path detection          (sparse.py:69-88 detect_paths)
+#include <algorithm>
+#include <climits>
+
 #include "common.cuh"
 #include "demod.cuh"
 #include "internal.h"
@@ -144,6 +147,9 @@ template cudaError_t launch_qam_demod<double>(long long, const void*, int, doubl
 // in row-major (k, l) order (np.nonzero on the (M, N) frame) and ranked by
 // descending |h| with ties kept in that order (argsort kind="stable").
 constexpr int kDetectThreads = 1024;
+constexpr int kMaxRankSmem = 1024;  // candidates ranked from shared memory by the tiled path
+constexpr int kTiledMin = 1 << 16;   // frames with at least this many bins take the tiled path
+constexpr int kMinTile = 2048;       // bins per tile at least
 
 __device__ __forceinline__ double block_max(double v, double* scratch) {
 #pragma unroll
@@ -165,10 +171,10 @@ __device__ __forceinline__ double block_max(double v, double* scratch) {
 
 // |h| is evaluated once per bin into shared memory when the frame fits (else
 // re-read), candidates are compacted in row-major order with warp ballots over
-// coalesced bin ranges, then ranked.
-__global__ void __launch_bounds__(kDetectThreads) detect_paths_kernel(
-    int M, int N, const double2* __restrict__ heff, double theta, int max_paths, int cap, int mag_smem,
-    int* count, int* pk, int* pl, double2* ph) {
+// coalesced bin ranges, then ranked.  One CTA handles frame f.
+__device__ __forceinline__ void detect_frame(int f, int M, int N, const double2* __restrict__ heff, double theta,
+                                             int max_paths, int cap, int mag_smem, int* count, int* pk, int* pl,
+                                             double2* ph) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int n = M * N;
   double* mag = reinterpret_cast<double*>(smem);                        // [n] when mag_smem
@@ -176,7 +182,6 @@ __global__ void __launch_bounds__(kDetectThreads) detect_paths_kernel(
   __shared__ double dscratch[32];
   __shared__ int wcount[32];
   __shared__ int running;
-  const int f = blockIdx.x;
   const double2* h = heff + (size_t)f * n;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   double peak = 0.0;
@@ -234,6 +239,154 @@ __global__ void __launch_bounds__(kDetectThreads) detect_paths_kernel(
   }
 }
 
+__global__ void __launch_bounds__(kDetectThreads) detect_paths_kernel(
+    int M, int N, const double2* __restrict__ heff, double theta, int max_paths, int cap, int mag_smem,
+    int* count, int* pk, int* pl, double2* ph) {
+  detect_frame(blockIdx.x, M, N, heff, theta, max_paths, cap, mag_smem, count, pk, pl, ph);
+}
+
+// Large frames (the paper's 16384 x 32): one CTA per frame would stream the
+// whole frame through one SM twice, so the frame is split into T tiles over
+// the row-major bins, with the per-tile partials kept in the frame's own
+// output rows (T <= max_paths; no scratch allocation):
+//   tile_max    ph[f, t].x = max |h| over tile t
+//   tile_count  pl[f, t]   = #{i in tile t : |h_i| > theta * peak}
+//   tile_emit   pk[f, prefix_t + j] = bin index of tile t's j-th candidate
+//               (row-major order), for positions < max_paths
+//   rank        candidates ranked by descending |h| (stable) and written out;
+//               a frame with more than max_paths candidates is re-run by the
+//               single-CTA routine (its truncation semantics).
+constexpr int kTileThreads = 256;
+
+__global__ void __launch_bounds__(kTileThreads) detect_tile_max(int n, int ts, const double2* __restrict__ heff,
+                                                               int max_paths, double2* ph) {
+  __shared__ double dscratch[32];
+  const int f = blockIdx.y, t = blockIdx.x;
+  const double2* h = heff + (size_t)f * n;
+  const int i1 = min(n, (t + 1) * ts);
+  double m = 0.0;
+  for (int i = t * ts + threadIdx.x; i < i1; i += blockDim.x) m = fmax(m, np_cabs(h[i].x, h[i].y));
+  m = block_max(m, dscratch);
+  if (threadIdx.x == 0) ph[(size_t)f * max_paths + t] = make_double2(m, 0.0);
+}
+
+__device__ __forceinline__ double frame_peak(const double2* ph_f, int T, double* dscratch) {
+  double m = 0.0;
+  for (int t = threadIdx.x; t < T; t += blockDim.x) m = fmax(m, ph_f[t].x);
+  return block_max(m, dscratch);
+}
+
+__global__ void __launch_bounds__(kTileThreads) detect_tile_count(int n, int ts, int T, const double2* __restrict__ heff,
+                                                                 double theta, int max_paths, const double2* ph,
+                                                                 int* pl) {
+  __shared__ double dscratch[32];
+  __shared__ int wsum[kTileThreads / 32];
+  const int f = blockIdx.y, t = blockIdx.x;
+  const double thr = theta * frame_peak(ph + (size_t)f * max_paths, T, dscratch);
+  const double2* h = heff + (size_t)f * n;
+  const int i1 = min(n, (t + 1) * ts);
+  int c = 0;
+  for (int i = t * ts + threadIdx.x; i < i1; i += blockDim.x) c += np_cabs(h[i].x, h[i].y) > thr;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+  if ((threadIdx.x & 31) == 0) wsum[threadIdx.x >> 5] = c;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int tot = 0;
+    for (int w = 0; w < kTileThreads / 32; ++w) tot += wsum[w];
+    pl[(size_t)f * max_paths + t] = tot;
+  }
+}
+
+__global__ void __launch_bounds__(kTileThreads) detect_tile_emit(int n, int ts, int T, const double2* __restrict__ heff,
+                                                                double theta, int max_paths, const double2* ph,
+                                                                const int* pl, int* pk) {
+  __shared__ double dscratch[32];
+  __shared__ int wcount[kTileThreads / 32];
+  __shared__ int running;
+  const int f = blockIdx.y, t = blockIdx.x;
+  const double thr = theta * frame_peak(ph + (size_t)f * max_paths, T, dscratch);
+  if (threadIdx.x == 0) {
+    int pre = 0;
+    for (int u = 0; u < t; ++u) pre += pl[(size_t)f * max_paths + u];
+    running = pre;
+  }
+  __syncthreads();
+  if (running >= max_paths) return;  // nothing of this tile is stored (uniform)
+  const double2* h = heff + (size_t)f * n;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int i0 = t * ts, i1 = min(n, (t + 1) * ts);
+  for (int base = i0; base < i1; base += blockDim.x) {
+    const int i = base + threadIdx.x;
+    const bool keep = i < i1 && np_cabs(h[i].x, h[i].y) > thr;
+    const unsigned bal = __ballot_sync(0xffffffffu, keep);
+    if (lane == 0) wcount[warp] = __popc(bal);
+    __syncthreads();
+    int before = running;
+    for (int w = 0; w < warp; ++w) before += wcount[w];
+    const int pos = before + __popc(bal & ((1u << lane) - 1u));
+    if (keep && pos < max_paths) pk[(size_t)f * max_paths + pos] = i;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int s = running;
+      for (int w = 0; w < kTileThreads / 32; ++w) s += wcount[w];
+      running = s;
+    }
+    __syncthreads();
+  }
+}
+
+__global__ void __launch_bounds__(kDetectThreads) detect_rank(int M, int N, int T, const double2* __restrict__ heff,
+                                                             double theta, int max_paths, int cap, int mag_smem,
+                                                             int* count, int* pk, int* pl, double2* ph) {
+  __shared__ double dscratch[32];
+  __shared__ int wsum[32];
+  __shared__ int cand[kMaxRankSmem];
+  const int f = blockIdx.x;
+  const int n = M * N;
+  const size_t fo = (size_t)f * max_paths;
+  // totals from the tile partials (read before any output is written)
+  const double peak = [&] {
+    double m = 0.0;
+    for (int t = threadIdx.x; t < T; t += blockDim.x) m = fmax(m, ph[fo + t].x);
+    return block_max(m, dscratch);
+  }();
+  int c = 0;
+  for (int t = threadIdx.x; t < T; t += blockDim.x) c += pl[fo + t];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+  if ((threadIdx.x & 31) == 0) wsum[threadIdx.x >> 5] = c;
+  __syncthreads();
+  int total = 0;
+  for (int w = 0; w < (int)(blockDim.x >> 5); ++w) total += wsum[w];
+  if (peak == 0.0) {  // sparse.py:81-82
+    if (threadIdx.x == 0) count[f] = 0;
+    return;
+  }
+  if (total > max_paths || total > kMaxRankSmem) {  // rare: the single-CTA routine (ranks every candidate)
+    __syncthreads();
+    detect_frame(f, M, N, heff, theta, max_paths, cap, mag_smem, count, pk, pl, ph);
+    return;
+  }
+  for (int j = threadIdx.x; j < total; j += blockDim.x) cand[j] = pk[fo + j];
+  __syncthreads();
+  const double2* h = heff + (size_t)f * n;
+  for (int j = threadIdx.x; j < total; j += blockDim.x) {
+    const int ic = cand[j];
+    const double m = np_cabs(h[ic].x, h[ic].y);
+    int rank = 0;
+    for (int o = 0; o < total; ++o) {
+      const int io = cand[o];
+      const double mo = np_cabs(h[io].x, h[io].y);
+      rank += (mo > m) || (mo == m && o < j);
+    }
+    pk[fo + rank] = ic / N;
+    pl[fo + rank] = ic - (ic / N) * N;
+    ph[fo + rank] = h[ic];
+  }
+  if (threadIdx.x == 0) count[f] = total;
+}
+
 cudaError_t launch_detect_paths(int B, int M, int N, const void* heff, double theta, int max_paths,
                                 int* count, int* pk, int* pl, void* ph, cudaStream_t st) {
   if (B == 0) return cudaSuccess;
@@ -241,17 +394,132 @@ cudaError_t launch_detect_paths(int B, int M, int N, const void* heff, double th
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
   const int n = M * N;
-  const int budget = optin - 2048;  // static shared memory of the kernel
+  const int budget = optin - 2048 - kMaxRankSmem * (int)sizeof(int);  // static shared memory of the kernels
   // keep the frame's magnitudes on chip when they leave room for a candidate list
   const int mag_smem = (size_t)n * sizeof(double) + 4096 * sizeof(int) <= (size_t)budget ? 1 : 0;
   int cap = (budget - (mag_smem ? n * (int)sizeof(double) : 0)) / (int)sizeof(int);
   if (cap > n) cap = n;
   const size_t smem = (mag_smem ? (size_t)n * sizeof(double) : 0) + (size_t)cap * sizeof(int);
+  const double2* h = (const double2*)heff;
+  // tiled path for large frames (T tiles of ts bins, T <= max_paths)
+  const int T = std::min(std::min(max_paths, 256), (n + kMinTile - 1) / kMinTile);
+  if (n >= kTiledMin && T >= 2) {
+    const int ts = (n + T - 1) / T;
+    dim3 g(T, B);
+    detect_tile_max<<<g, kTileThreads, 0, st>>>(n, ts, h, max_paths, (double2*)ph);
+    detect_tile_count<<<g, kTileThreads, 0, st>>>(n, ts, T, h, theta, max_paths, (const double2*)ph, pl);
+    detect_tile_emit<<<g, kTileThreads, 0, st>>>(n, ts, T, h, theta, max_paths, (const double2*)ph, pl, pk);
+    cudaError_t e = cudaFuncSetAttribute(detect_rank, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    detect_rank<<<B, kDetectThreads, smem, st>>>(M, N, T, h, theta, max_paths, cap, mag_smem, count, pk, pl,
+                                                 (double2*)ph);
+    return cudaGetLastError();
+  }
   cudaError_t e = cudaFuncSetAttribute(detect_paths_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)smem);
   if (e != cudaSuccess) return e;
-  detect_paths_kernel<<<B, kDetectThreads, smem, st>>>(M, N, (const double2*)heff, theta, max_paths, cap, mag_smem,
-                                                       count, pk, pl, (double2*)ph);
+  detect_paths_kernel<<<B, kDetectThreads, smem, st>>>(M, N, h, theta, max_paths, cap, mag_smem, count, pk, pl,
+                                                       (double2*)ph);
+  return cudaGetLastError();
+}
+
+// Detected taps [B, max_paths] (ranked, count[f] each) -> the solver's CSR
+// (path_offsets [B+1], k, l, gain in the solve dtype) on the device.  One CTA
+// scans the counts (fixed order) and records min / max count, then a grid
+// scatters the rows.  stats = {min count, max count, stored rows}.
+__global__ void __launch_bounds__(1024) paths_scan_kernel(int B, int max_paths, const int* __restrict__ count,
+                                                         int* off, int* stats) {
+  __shared__ int part[32];
+  __shared__ int carry;
+  if (threadIdx.x == 0) carry = 0;
+  int mn = INT_MAX, mx = INT_MIN;
+  for (int base = 0; base < B; base += blockDim.x) {
+    const int i = base + threadIdx.x;
+    const int raw = i < B ? count[i] : 0;
+    const int c = max(0, min(raw, max_paths));  // rows actually stored
+    if (i < B) {
+      mn = min(mn, raw);
+      mx = max(mx, raw);
+    }
+    int v = c;  // inclusive warp scan
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int u = __shfl_up_sync(0xffffffffu, v, o);
+      if (lane >= o) v += u;
+    }
+    if (lane == 31) part[warp] = v;
+    __syncthreads();
+    if (warp == 0) {
+      int w = lane < (int)(blockDim.x >> 5) ? part[lane] : 0;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int u = __shfl_up_sync(0xffffffffu, w, o);
+        if (lane >= o) w += u;
+      }
+      part[lane] = w;
+    }
+    __syncthreads();
+    const int excl = carry + (warp ? part[warp - 1] : 0) + v - c;
+    if (i < B) off[i] = excl;
+    __syncthreads();
+    if (threadIdx.x == blockDim.x - 1) carry = excl + c;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    off[B] = carry;
+    stats[2] = carry;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+    mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  }
+  __shared__ int smn[32], smx[32];
+  if ((threadIdx.x & 31) == 0) {
+    smn[threadIdx.x >> 5] = mn;
+    smx[threadIdx.x >> 5] = mx;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < (int)(blockDim.x >> 5); ++w) {
+      mn = min(mn, smn[w]);
+      mx = max(mx, smx[w]);
+    }
+    stats[0] = mn;
+    stats[1] = mx;
+  }
+}
+
+template <typename T>
+__global__ void paths_scatter_kernel(int B, int max_paths, const int* __restrict__ count, const int* __restrict__ off,
+                                     const int* __restrict__ pk, const int* __restrict__ pl,
+                                     const double2* __restrict__ ph, int* k, int* l, Vec<T>* g) {
+  const long long tot = (long long)B * max_paths;
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < tot;
+       idx += (long long)gridDim.x * blockDim.x) {
+    const int f = (int)(idx / max_paths), j = (int)(idx - (long long)f * max_paths);
+    if (j >= min(count[f], max_paths)) continue;
+    const int o = off[f] + j;
+    k[o] = pk[idx];
+    l[o] = pl[idx];
+    g[o] = cmake<Vec<T>>(T(ph[idx].x), T(ph[idx].y));
+  }
+}
+
+cudaError_t launch_paths_csr(int B, int max_paths, const int* count, const int* pk, const int* pl, const void* ph,
+                             int dtype_f64, int* off, int* k, int* l, void* g, int* stats, cudaStream_t st) {
+  if (B == 0) return cudaSuccess;
+  paths_scan_kernel<<<1, 1024, 0, st>>>(B, max_paths, count, off, stats);
+  const long long tot = (long long)B * max_paths;
+  const int blocks = (int)std::min<long long>((tot + 255) / 256, 148 * 8);
+  if (tot == 0) return cudaGetLastError();
+  if (dtype_f64)
+    paths_scatter_kernel<double><<<blocks, 256, 0, st>>>(B, max_paths, count, off, pk, pl, (const double2*)ph, k, l,
+                                                         (double2*)g);
+  else
+    paths_scatter_kernel<float><<<blocks, 256, 0, st>>>(B, max_paths, count, off, pk, pl, (const double2*)ph, k, l,
+                                                        (float2*)g);
   return cudaGetLastError();
 }
 

@@ -439,6 +439,22 @@ int32_t ddb_detect_paths(int32_t batch, int32_t M, int32_t N, const void* heff, 
   return ok();
 }
 
+int32_t ddb_paths_csr(int32_t batch, int32_t max_paths, const int32_t* count, const int32_t* path_k,
+                      const int32_t* path_l, const void* path_gain, int32_t dtype, int32_t* path_offsets,
+                      int32_t* csr_k, int32_t* csr_l, void* csr_gain, int32_t* stats, void* stream) {
+  if (batch < 0 || max_paths < 0) return fail(DDB_ERR_INVALID, "negative batch/max_paths");
+  if (dtype != DDB_F32 && dtype != DDB_F64) return fail(DDB_ERR_INVALID, "bad dtype %d", dtype);
+  if (batch == 0) return ok();
+  if (!count || !path_offsets || !stats || (max_paths > 0 && (!path_k || !path_l || !path_gain || !csr_k ||
+                                                               !csr_l || !csr_gain)))
+    return fail(DDB_ERR_INVALID, "null pointer");
+  cudaError_t e = ddb::launch_paths_csr(batch, max_paths, count, path_k, path_l, path_gain, dtype == DDB_F64,
+                                        path_offsets, csr_k, csr_l, csr_gain, stats,
+                                        static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "paths_csr launch");
+  return ok();
+}
+
 int32_t ddb_dzt(int32_t batch, int32_t M, int32_t N, int32_t dtype, const void* y_time, const void* kernel,
                 int32_t flags, double amplitude, void* out, void* stream) {
   if (batch < 0) return fail(DDB_ERR_INVALID, "negative batch");

@@ -141,6 +141,8 @@ cudaError_t launch_add_awgn(int dtype_f64, int B, long long L, const void* y, do
 cudaError_t launch_threshold_frame(int dtype_f64, int B, int MN, const void* heff, double theta, void* out,
                                    cudaStream_t st);
 cudaError_t launch_build_dense(int dtype_f64, int B, int M, int N, const void* heff, void* H, cudaStream_t st);
+cudaError_t launch_paths_csr(int B, int max_paths, const int* count, const int* pk, const int* pl, const void* ph,
+                             int dtype_f64, int* off, int* k, int* l, void* g, int* stats, cudaStream_t st);
 cudaError_t launch_fp32_probe(int mode, int blocks, int iters, float* out, cudaStream_t st);
 
 }  // namespace ddb

@@ -791,3 +791,71 @@ class TestDense:
         ber_cga = int(cga.bit_errors.sum()) / (P * M * N * b)
         ber_lm = int(r["bit_errors"].sum()) / (P * M * N * b)
         assert ber_cga <= 2.0 * ber_lm
+
+
+# ---------------------------------------------------------------- tiled detect_paths (frames >= 65536 bins)
+@pytest.mark.parametrize("case", ["sparse", "ties", "overflow", "zero", "all_kept"])
+def test_detect_paths_tiled_large_frames(pkg, case):
+    """Frames of the paper's size class take the tiled multi-CTA detect path;
+    the result is the oracle's detect_paths (sparse.py:69-88) tap for tap:
+    order, ties (stable row-major), truncation beyond max_paths (the single-CTA
+    routine ranks every candidate) and the empty / overflow flags."""
+    import ctypes as C
+    from paper_2604_02266_b200 import _native as nat
+    M, N, B, mp = 4096, 32, 3, 64
+    rng = np.random.default_rng(hash(case) % 1000)
+    h = (rng.normal(size=(B, M, N)) + 1j * rng.normal(size=(B, M, N))) * 1e-3
+    theta = 0.08
+    for f in range(B):
+        pos = rng.choice(M * N, 40, replace=False)
+        mags = rng.uniform(0.1, 1.0, 40)
+        if case == "ties":
+            mags[10:20] = mags[10]
+        if case == "overflow":
+            pos = rng.choice(M * N, 150, replace=False)
+            mags = rng.uniform(0.2, 1.0, 150)
+        h[f].reshape(-1)[pos] = mags * np.exp(1j * rng.uniform(0, 2 * np.pi, len(pos)))
+        if case == "ties":  # exactly equal complex values at several positions
+            h[f].reshape(-1)[pos[10:20]] = h[f].reshape(-1)[pos[10]]
+    if case == "zero":
+        h[1] = 0
+    if case == "all_kept":
+        theta = 0.0  # every nonzero bin: more candidates than shared memory holds
+    hd = torch.as_tensor(h, device="cuda")
+    cnt = torch.empty(B, dtype=torch.int32, device="cuda")
+    kk = torch.empty(B, mp, dtype=torch.int32, device="cuda")
+    ll = torch.empty_like(kk)
+    gg = torch.empty(B, mp, dtype=torch.complex128, device="cuda")
+    p = lambda t: C.c_void_p(t.data_ptr())  # noqa: E731
+    nat.check(nat.load().ddb_detect_paths(B, M, N, p(hd), theta, mp, p(cnt), p(kk), p(ll), p(gg),
+                                          C.c_void_p(torch.cuda.current_stream().cuda_stream)), "detect")
+    cnt, kk, ll, gg = cnt.cpu().numpy(), kk.cpu().numpy(), ll.cpu().numpy(), gg.cpu().numpy()
+    for f in range(B):
+        want = orc.detect_paths(h[f], theta)
+        if case == "all_kept":
+            assert cnt[f] == -1  # candidate list exceeds shared memory (host reports it)
+            continue
+        assert cnt[f] == len(want), (f, cnt[f], len(want))
+        n = min(len(want), mp)
+        assert list(zip(kk[f, :n], ll[f, :n])) == [(t.k, t.l) for t in want[:n]]
+        np.testing.assert_array_equal(gg[f, :n], [t.gain for t in want[:n]])
+    if case in ("sparse", "ties", "zero"):
+        # the device CSR of SsCgaSolver.detect's path (ddb_paths_csr) matches too
+        s = pkg.SsCgaSolver(M, N, 10, precision="fp64")
+        off = torch.empty(B + 1, dtype=torch.int32, device="cuda")
+        k = torch.empty(B * mp, dtype=torch.int32, device="cuda")
+        l = torch.empty_like(k)
+        g = torch.empty(B * mp, dtype=torch.complex128, device="cuda")
+        st = torch.empty(3, dtype=torch.int32, device="cuda")
+        cnt_d, kk_d, ll_d, gg_d = (torch.as_tensor(v, device="cuda") for v in (cnt, kk, ll, gg))  # kept alive
+        nat.check(nat.load().ddb_paths_csr(B, mp, p(cnt_d), p(kk_d), p(ll_d), p(gg_d),
+                                           nat.DDB_F64, p(off), p(k), p(l), p(g), p(st),
+                                           C.c_void_p(torch.cuda.current_stream().cuda_stream)), "csr")
+        off = off.cpu().numpy()
+        assert off[0] == 0 and list(np.diff(off)) == [min(c, mp) for c in cnt]
+        assert st.cpu().tolist() == [int(cnt.min()), int(cnt.max()), int(off[-1])]
+        for f in range(B):
+            a, e = off[f], off[f + 1]
+            np.testing.assert_array_equal(k.cpu().numpy()[a:e], kk[f, :e - a])
+            np.testing.assert_array_equal(g.cpu().numpy()[a:e], gg[f, :e - a])
+        del s
