@@ -512,14 +512,18 @@ def main():
         for _ in range(5):
             s.receive(pk1.pilot_rx, pk1.data_rx, pk1.lam, 0.08, tx_labels=pk1.tx_labels, trace=False)
         torch.cuda.synchronize()
+        import gc
+        gc.collect()
+        gc.disable()  # a collector pass inside the loop is host jitter, not receiver time
         rlat = []
-        for _ in range(min(args.lat_runs, 1000)):
+        for _ in range(args.lat_runs):
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             a.record()
             s.receive(pk1.pilot_rx, pk1.data_rx, pk1.lam, 0.08, tx_labels=pk1.tx_labels, trace=False)
             b.record()
             b.synchronize()
             rlat.append(a.elapsed_time(b))
+        gc.enable()
         rlat.sort()
         del pk1
         latency = {"p50_ms": lat[len(lat) // 2], "p99_ms": lat[int(len(lat) * 0.99)],
