@@ -16,7 +16,11 @@
 // flag the update kernels honour.  Every gather recomputes its coefficient
 // from the exact integer phase (two-level twiddle table in shared memory);
 // the vectors stream through L2 / HBM, so the path is memory-bound.
+#include <algorithm>
 #include <cmath>
+#include <cstdlib>
+
+#include <cooperative_groups.h>
 
 #include "cg.cuh"
 #include "common.cuh"
@@ -349,6 +353,219 @@ __global__ void __launch_bounds__(kGThreads) g_demod(const GArgs<T> a, uint8_t* 
   }
 }
 
+// ---- persistent form for small batches (B <= kPersistB): one cooperative
+// launch runs the whole solve, the phases separated by grid barriers instead
+// of kernel boundaries (a batch-1 paper-grid solve is ~45 dependent launches
+// otherwise, each a fraction of the machine).  Every block folds the block
+// partials of every frame itself after a barrier, in the same fixed order as
+// g_fold, so all blocks hold bit-identical CG scalars without a second
+// barrier; block 0 writes the trace.
+constexpr int kPersistB = 8;
+
+template <typename T> struct PScal {
+  T cn, beta, alpha;
+  int state, done;
+};
+
+template <typename T>
+__device__ __forceinline__ Vec<T> p_fold(const GArgs<T>& a, int f) {
+  using V = Vec<T>;
+  const V* pp = a.part + (size_t)f * a.nblk;
+  V v = czero<V>();
+  for (int i = threadIdx.x; i < a.nblk; i += blockDim.x) v = cadd(v, pp[i]);
+  __shared__ V tot;
+  block_pair_sum<T>(v, &tot);
+  __syncthreads();
+  const V t = tot;
+  __syncthreads();
+  return t;
+}
+
+template <typename T, int BA>
+__global__ void __launch_bounds__(kGThreads) g_persist(const GArgs<T> a, uint8_t* labels, float* llr, const T* nvar,
+                                                       const uint8_t* txl, int txpk, int* berr) {
+  using V = Vec<T>;
+  namespace cg = cooperative_groups;
+  cg::grid_group grid = cg::this_grid();
+  extern __shared__ __align__(16) unsigned char gsm[];
+  V* tlo = reinterpret_cast<V*>(gsm);
+  V* thi = tlo + a.TL;
+  V* tw = thi + a.TH;
+  GTap<T>* taps = reinterpret_cast<GTap<T>*>(tw + a.N);  // [B][kGTaps]
+  __shared__ PScal<T> sc[kPersistB];
+  __shared__ int pp0[kPersistB], pcount[kPersistB];
+  for (int i = threadIdx.x; i < a.TL; i += blockDim.x) tlo[i] = twiddle(T(0), i, a.MN);
+  for (int i = threadIdx.x; i < a.TH; i += blockDim.x)
+    thi[i] = twiddle(T(0), (int)(((long long)i * a.TL) % a.MN), a.MN);
+  for (int l = threadIdx.x; l < a.N; l += blockDim.x) tw[l] = twiddle(T(0), l, a.N);
+  if (threadIdx.x < a.B) {
+    pp0[threadIdx.x] = a.off[threadIdx.x];
+    pcount[threadIdx.x] = a.off[threadIdx.x + 1] - a.off[threadIdx.x];
+  }
+  if (berr && blockIdx.x == 0 && threadIdx.x < a.B) berr[threadIdx.x] = 0;
+  __syncthreads();
+  const int tlb = __ffs(a.TL) - 1;
+  for (int f = 0; f < a.B; ++f)
+    for (int i = threadIdx.x; i < pcount[f] && i < kGTaps; i += blockDim.x) {
+      GTap<T> t;
+      t.dk = a.K0 - a.pk[pp0[f] + i];
+      t.dl = a.L0 - a.pl[pp0[f] + i];
+      const V h = a.ph[pp0[f] + i];
+      t.hf = t.dl ? cmul(h, gtwid<T>(tlo, thi, tlb, wrap1(-t.dl * t.dk, a.MN))) : h;
+      t.hh = cconj(h);
+      taps[f * kGTaps + i] = t;
+    }
+  __syncthreads();
+  const int nv = a.nblk * a.B;
+  const int stride = a.iters + 1;
+  const bool lead = blockIdx.x == 0 && threadIdx.x == 0;
+
+  // b = H^H y -> c, x = 0
+  for (int vb = blockIdx.x; vb < nv; vb += gridDim.x) {
+    const int f = vb / a.nblk, blk = vb - f * a.nblk;
+    if (pcount[f] <= 0) continue;
+    const size_t fo = (size_t)f * a.MN;
+    V nrm = czero<V>(), bb[kGPerThread];
+    g_apply4<T, true>(a, a.y + fo, blk * kGBlock + threadIdx.x, pcount[f], pp0[f], taps + f * kGTaps, tlo, thi,
+                      tw, bb);
+    for (int e = 0; e < kGPerThread; ++e) {
+      const int q = blk * kGBlock + e * kGThreads + threadIdx.x;
+      if (q >= a.MN) break;
+      a.c[fo + q] = bb[e];
+      a.x[fo + q] = czero<V>();
+      nrm.x += bb[e].x * bb[e].x + bb[e].y * bb[e].y;
+    }
+    block_pair_sum<T>(nrm, a.part + (size_t)f * a.nblk + blk);
+  }
+  grid.sync();
+  for (int f = 0; f < a.B; ++f) {
+    if (pcount[f] <= 0) continue;
+    const V t = p_fold<T>(a, f);
+    if (threadIdx.x == 0) sc[f] = PScal<T>{t.x, T(0), T(0), 0, 0};
+    if (lead && a.cnorm) a.cnorm[(size_t)f * stride] = t.x;
+  }
+  __syncthreads();
+  for (int it = 0; it < a.iters; ++it) {
+    // u = H c + beta u, p = c + beta p
+    for (int vb = blockIdx.x; vb < nv; vb += gridDim.x) {
+      const int f = vb / a.nblk, blk = vb - f * a.nblk;
+      if (pcount[f] <= 0 || sc[f].state) continue;
+      const size_t fo = (size_t)f * a.MN;
+      const T beta = sc[f].beta;
+      V nu = czero<V>(), hcv[kGPerThread];
+      g_apply4<T, false>(a, a.c + fo, blk * kGBlock + threadIdx.x, pcount[f], pp0[f], taps + f * kGTaps, tlo, thi,
+                         tw, hcv);
+      for (int e = 0; e < kGPerThread; ++e) {
+        const int q = blk * kGBlock + e * kGThreads + threadIdx.x;
+        if (q >= a.MN) break;
+        const V cq = a.c[fo + q];
+        const V uq = it == 0 ? hcv[e] : cadd(hcv[e], cscale(a.u[fo + q], beta));
+        const V pq = it == 0 ? cq : cadd(cq, cscale(a.p[fo + q], beta));
+        a.u[fo + q] = uq;
+        a.p[fo + q] = pq;
+        nu.x += uq.x * uq.x + uq.y * uq.y;
+        nu.y += pq.x * pq.x + pq.y * pq.y;
+      }
+      block_pair_sum<T>(nu, a.part + (size_t)f * a.nblk + blk);
+    }
+    grid.sync();
+    for (int f = 0; f < a.B; ++f) {
+      if (pcount[f] <= 0 || sc[f].state) continue;
+      const V t = p_fold<T>(a, f);
+      if (threadIdx.x == 0) {
+        const T denom = t.x + a.lam[f] * t.y;  // equalize.py:60-67
+        if (denom == T(0)) sc[f].state = 1;
+        else sc[f].alpha = sc[f].cn / denom;
+      }
+    }
+    __syncthreads();
+    // ap = H^H u + lam p; x += alpha p; c -= alpha ap
+    for (int vb = blockIdx.x; vb < nv; vb += gridDim.x) {
+      const int f = vb / a.nblk, blk = vb - f * a.nblk;
+      if (pcount[f] <= 0 || sc[f].state) continue;
+      const size_t fo = (size_t)f * a.MN;
+      const T alpha = sc[f].alpha, lam = a.lam[f];
+      V nc = czero<V>(), hu[kGPerThread];
+      g_apply4<T, true>(a, a.u + fo, blk * kGBlock + threadIdx.x, pcount[f], pp0[f], taps + f * kGTaps, tlo, thi,
+                        tw, hu);
+      for (int e = 0; e < kGPerThread; ++e) {
+        const int q = blk * kGBlock + e * kGThreads + threadIdx.x;
+        if (q >= a.MN) break;
+        const V pq = a.p[fo + q];
+        const V ap = cadd(hu[e], cscale(pq, lam));
+        const V xq = cadd(a.x[fo + q], cscale(pq, alpha));
+        const V cq = csub(a.c[fo + q], cscale(ap, alpha));
+        a.x[fo + q] = xq;
+        a.c[fo + q] = cq;
+        if (a.snaps) a.snaps[((size_t)f * a.iters + it) * a.MN + q] = xq;
+        nc.x += cq.x * cq.x + cq.y * cq.y;
+      }
+      block_pair_sum<T>(nc, a.part + (size_t)f * a.nblk + blk);
+    }
+    grid.sync();
+    for (int f = 0; f < a.B; ++f) {
+      if (pcount[f] <= 0 || sc[f].state) continue;
+      const V t = p_fold<T>(a, f);
+      if (threadIdx.x == 0) {
+        sc[f].beta = t.x / sc[f].cn;
+        sc[f].cn = t.x;
+        sc[f].done = it + 1;
+      }
+      if (lead && a.cnorm) a.cnorm[(size_t)f * stride + it + 1] = t.x;
+    }
+    __syncthreads();
+  }
+  // trace tail and status (g_finish)
+  if (lead) {
+    for (int f = 0; f < a.B; ++f) {
+      if (pcount[f] <= 0) {
+        if (a.cnorm) for (int i = 0; i < stride; ++i) a.cnorm[(size_t)f * stride + i] = T(0);
+        if (a.itdone) a.itdone[f] = 0;
+        if (a.status) a.status[f] = 1;
+        continue;
+      }
+      if (a.cnorm) for (int i = sc[f].done + 1; i < stride; ++i) a.cnorm[(size_t)f * stride + i] = T(0);
+      if (a.itdone) a.itdone[f] = sc[f].done;
+      if (a.status) a.status[f] = sc[f].state ? 2 : 0;
+    }
+  }
+  // demod (g_demod): x is final after the last barrier
+  for (int vb = blockIdx.x; vb < nv; vb += gridDim.x) {
+    const int f = vb / a.nblk, blk = vb - f * a.nblk;
+    const size_t fo = (size_t)f * a.MN;
+    const bool empty = pcount[f] <= 0;
+    const T nvf = nvar ? nvar[f] : a.lam[f];
+    const T scale = nvf > T(0) ? T(1) / nvf : T(1);
+    int errs = 0;
+    for (int e = 0; e < kGPerThread; ++e) {
+      const int q = blk * kGBlock + e * kGThreads + threadIdx.x;
+      if (q >= a.MN) break;
+      if (empty) {
+        a.x[fo + q] = czero<V>();
+        if (labels) labels[fo + q] = 0;
+        if (llr) for (int b = 0; b < 2 * BA; ++b) llr[(fo + q) * (2 * BA) + b] = 0.f;
+        continue;
+      }
+      if (!labels && !llr && !txl) continue;
+      const V xv = a.x[fo + q];
+      float l[2 * BA];
+      const int lab = qam_symbol<T, BA>(xv.x, xv.y, scale, llr ? l : nullptr);
+      if (llr)
+        for (int b = 0; b < 2 * BA; ++b) llr[(fo + q) * (2 * BA) + b] = l[b];
+      if (labels) labels[fo + q] = (uint8_t)lab;
+      if (txl) errs += __popc((unsigned)lab ^ tx_label_at(txl, fo + q, 2 * BA, txpk));
+    }
+    if (berr) {
+      if (empty) {
+        if (blk == 0 && threadIdx.x == 0) berr[f] = a.MN * BA;  // bps * MN / 2
+      } else {
+        errs = warp_sum(errs);
+        if ((threadIdx.x & 31) == 0 && errs) atomicAdd(berr + f, errs);
+      }
+    }
+  }
+}
+
 template <typename T>
 __global__ void g_zero_int(int* p, int n) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -405,6 +622,27 @@ cudaError_t launch_sscga_global(const SolveArgs& s, void* ws, cudaStream_t st) {
   if (s.B == 0) return cudaSuccess;
   const size_t smem = (size_t)(a.TL + a.TH + a.N) * sizeof(V) + kGTaps * sizeof(GTap<T>);
   cudaError_t e;
+  if (s.B <= kPersistB && !getenv("DDB_NO_PERSIST")) {
+    // one cooperative launch: grid = co-resident blocks, capped at the work
+    const size_t psmem = (size_t)(a.TL + a.TH + a.N) * sizeof(V) + (size_t)s.B * kGTaps * sizeof(GTap<T>);
+    const T* nvar = reinterpret_cast<const T*>(s.nvar);
+    void* kfn = s.bps == 2 ? (void*)g_persist<T, 1> : (s.bps == 6 ? (void*)g_persist<T, 3> : (void*)g_persist<T, 2>);
+    if ((e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psmem))) return e;
+    int dev = 0, sms = 0, per_sm = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, kGThreads, psmem))) return e;
+    const int blocks = std::min(per_sm * sms, a.nblk * s.B);
+    if (blocks >= 1) {
+      uint8_t* labels = s.bps ? s.labels : nullptr;
+      float* llr = s.bps ? s.llr : nullptr;
+      const uint8_t* txl = s.bps ? s.txl : nullptr;
+      int* berr = s.bps ? s.berr : nullptr;
+      int txpk = s.txpk;
+      void* args[] = {&a, &labels, &llr, (void*)&nvar, (void*)&txl, &txpk, &berr};
+      return cudaLaunchCooperativeKernel(kfn, dim3(blocks), dim3(kGThreads), args, psmem, st);
+    }
+  }
   if ((e = cudaFuncSetAttribute(g_init<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem))) return e;
   if ((e = cudaFuncSetAttribute(g_fwd<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem))) return e;
   if ((e = cudaFuncSetAttribute(g_herm<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem))) return e;
