@@ -479,6 +479,30 @@ def main():
     # ---- single-frame latency: CUDA graph of a batch-1 solve, replayed
     latency = None
     if not args.no_latency and rank == 0:
+        # the whole receiver for one packet from time-domain pilot and data frames
+        # (SsCgaSolver.receive: pilot DZT + detect_paths + CSR, data DZT, solve), as
+        # the paper's full-receiver p99.9 (PAPER.md:1479); not graph-captured (the
+        # tap CSR is sized on the host), so host round trips are inside the time
+        from paper_2604_02266_b200.synth import synthesize_packets
+        pk1 = synthesize_packets(s, 1, snr_db=args.snr, nu_max_hz=cfg["nu"], modulation=cfg["mod"], seed=7,
+                                 cdtype=s.cdtype)
+        for _ in range(10):
+            s.receive(pk1.pilot_rx, pk1.data_rx, pk1.lam, 0.08, tx_labels=pk1.tx_labels, trace=False)
+        torch.cuda.synchronize()
+        import gc
+        gc.collect()
+        gc.disable()  # a collector pass inside the loop is host jitter, not receiver time
+        rlat = []
+        for _ in range(args.lat_runs):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            s.receive(pk1.pilot_rx, pk1.data_rx, pk1.lam, 0.08, tx_labels=pk1.tx_labels, trace=False)
+            b.record()
+            b.synchronize()
+            rlat.append(a.elapsed_time(b))
+        gc.enable()
+        rlat.sort()
+        del pk1
         y1 = fb.y[:1].clone()
         lam1 = fb.lam[:1].clone()
         tx1 = fb.tx_labels[:1].clone()
@@ -502,30 +526,6 @@ def main():
         torch.cuda.synchronize()
         lat = sorted(a.elapsed_time(b) for a, b in ev)
         n_clu = max(1, sms // max(1, s.plan()["cluster"]))  # persistent clusters (1 CTA per SM)
-        # the whole receiver for one packet from time-domain pilot and data frames
-        # (SsCgaSolver.receive: pilot DZT + detect_paths + CSR, data DZT, solve), as
-        # the paper's full-receiver p99.9 (PAPER.md:1479); not graph-captured (the
-        # tap CSR is sized on the host), so host round trips are inside the time
-        from paper_2604_02266_b200.synth import synthesize_packets
-        pk1 = synthesize_packets(s, 1, snr_db=args.snr, nu_max_hz=cfg["nu"], modulation=cfg["mod"], seed=7,
-                                 cdtype=s.cdtype)
-        for _ in range(5):
-            s.receive(pk1.pilot_rx, pk1.data_rx, pk1.lam, 0.08, tx_labels=pk1.tx_labels, trace=False)
-        torch.cuda.synchronize()
-        import gc
-        gc.collect()
-        gc.disable()  # a collector pass inside the loop is host jitter, not receiver time
-        rlat = []
-        for _ in range(args.lat_runs):
-            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            a.record()
-            s.receive(pk1.pilot_rx, pk1.data_rx, pk1.lam, 0.08, tx_labels=pk1.tx_labels, trace=False)
-            b.record()
-            b.synchronize()
-            rlat.append(a.elapsed_time(b))
-        gc.enable()
-        rlat.sort()
-        del pk1
         latency = {"p50_ms": lat[len(lat) // 2], "p99_ms": lat[int(len(lat) * 0.99)],
                    "p999_ms": lat[int(len(lat) * 0.999)],
                    "max_ms": lat[-1], "runs": len(lat), "frame_duration_ms": 1e3 * N / 30e3,
@@ -563,8 +563,23 @@ def main():
         h2d = hy.numel() * hy.element_size() + hl.numel() * hl.element_size() + ht.numel() + \
             sum(t.numel() * t.element_size() for t in hp)
         d2h = lab_h.numel() + err_h.numel() * 4
+        # the bound: this box's pinned H2D copy bandwidth (one 512 MB copy, device events)
+        probe_h = torch.empty(1 << 29, dtype=torch.uint8).pin_memory()
+        probe_d = torch.empty(1 << 29, dtype=torch.uint8, device="cuda")
+        probe_d.copy_(probe_h, non_blocking=True)
+        a2, b2 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        a2.record()
+        probe_d.copy_(probe_h, non_blocking=True)
+        b2.record()
+        b2.synchronize()
+        h2d_peak = (1 << 29) / (a2.elapsed_time(b2) * 1e-3) / 1e9
+        del probe_h, probe_d
+        h2d_gbs = h2d / (ems / k2 * 1e-3) / 1e9
         e2e = {"value": world * B * MN * k2 / (ems * 1e-3), "unit": "symbols/s", "h2d_bytes_per_step": h2d,
                "d2h_bytes_per_step": d2h, "steps": k2, "ms_per_step": ems / k2,
+               "pcie": {"h2d_gbs": h2d_gbs, "h2d_peak_gbs": h2d_peak, "frac": h2d_gbs / h2d_peak,
+                        "peak_source": "one 512 MB pinned H2D copy on this box"},
                "what": "HostPipeline: pinned H2D of y/taps/lam/tx labels (bps bits per symbol), fused solve, "
                        "D2H labels + bit errors"}
         assert torch.equal(err_h, out.bit_errors.cpu())

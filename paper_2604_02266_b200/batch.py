@@ -257,7 +257,7 @@ class SsCgaSolver:
 
     # -- receiver front end ---------------------------
     def detect(self, pilot_rx: torch.Tensor, theta: float = 0.08, *, max_paths: int = 64,
-               amplitude: Optional[float] = None, stream=None) -> PathBatch:
+               amplitude: Optional[float] = None, stream=None, _deferred: Optional[list] = None) -> PathBatch:
         """Taps of every frame from its received pilot frame, on the device.
 
         pilot_rx: complex [B, M*N] time-domain samples of the point-pilot frame.
@@ -291,6 +291,9 @@ class SsCgaSolver:
         nat.check(self.lib.ddb_paths_csr(B, max_paths, _ptr(cnt), _ptr(kk), _ptr(ll), _ptr(gg), self.dtype_code,
                                          _ptr(off), _ptr(k), _ptr(l), _ptr(g), _ptr(stats), _stream_handle(stream)),
                   "ddb_paths_csr")
+        if _deferred is not None:  # receive(): checked after the solve is queued (no mid-pipeline sync)
+            _deferred.append((stats, max_paths))
+            return PathBatch(off, k, l, g)
         if stream is not None:
             stream.synchronize()
         cmin, cmax, total = (int(v) for v in stats.tolist())
@@ -310,10 +313,22 @@ class SsCgaSolver:
         solve with hard decisions (and LLRs / bit errors).  data_rx: complex
         [B, M*N] time-domain samples of the data frame."""
         from .zak import dzt_device
-        paths = self.detect(pilot_rx, theta, max_paths=max_paths, stream=stream)
+        pending: list = []
+        paths = self.detect(pilot_rx, theta, max_paths=max_paths, stream=stream, _deferred=pending)
         y = dzt_device(data_rx.to(device=self.device, dtype=self.cdtype), self.M, self.N, colmajor=True,
                        stream=stream)
-        return self.solve(y, paths, lam, tx_labels=tx_labels, llr=llr, trace=trace, stream=stream)
+        res = self.solve(y, paths, lam, tx_labels=tx_labels, llr=llr, trace=trace, stream=stream)
+        # the tap batch's checks, after everything is queued: one small read
+        stats, mp = pending[0]
+        if stream is not None:
+            stream.synchronize()
+        cmin, cmax, _ = (int(v) for v in stats.tolist())
+        if cmin < 0:
+            raise nat.DdbError(nat.DDB_ERR_UNSUPPORTED, "ddb_detect_paths",
+                               "candidate list exceeds the per-frame shared-memory capacity")
+        if cmax > mp:
+            raise ValueError(f"a frame has {cmax} taps above threshold > max_paths={mp}")
+        return res
 
     # -- matrix-free operator -------------------------------------------------
     def apply(self, v: torch.Tensor, paths: PathBatch, hermitian: bool = False,

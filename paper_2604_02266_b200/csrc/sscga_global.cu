@@ -112,6 +112,67 @@ __device__ __forceinline__ void g_apply4(const GArgs<T>& a, const Vec<T>* v, int
   using V = Vec<T>;
   const int M = a.M, N = a.N, MN = a.MN;
   const int tlb = __ffs(a.TL) - 1;
+  if (M % kGBlock == 0) {
+    // The block's kGBlock elements lie in one Doppler column l (rows kb ..):
+    // a tap whose delay shift keeps the block's source rows inside the column
+    // reads one contiguous run at a block-uniform offset (no per-element
+    // index or wrap arithmetic), and a Doppler tap's row-dependent
+    // coefficient advances by the constant W^{sg kGThreads} between this
+    // thread's elements.  Taps that would wrap take the general path below.
+    const int qb = q0 - (int)threadIdx.x;
+    const int l = qb / M, kb = qb - l * M;
+    const int k = kb + (int)threadIdx.x;
+#pragma unroll
+    for (int e = 0; e < kGPerThread; ++e) acc[e] = czero<V>();
+    for (int p = 0; p < P; ++p) {
+      GTap<T> t;
+      if (p < kGTaps) {
+        t = taps[p];
+      } else {
+        t.dk = a.K0 - a.pk[P0 + p];
+        t.dl = a.L0 - a.pl[P0 + p];
+        const V h = a.ph[P0 + p];
+        t.hf = t.dl ? cmul(h, gtwid<T>(tlo, thi, tlb, wrap1(-t.dl * t.dk, MN))) : h;
+        t.hh = cconj(h);
+      }
+      const int sft = HERM ? -t.dk : t.dk;
+      int l2 = l + (HERM ? -t.dl : t.dl);
+      const int ls = l2 < 0 ? l2 + N : (l2 >= N ? l2 - N : l2);
+      if (kb + sft >= 0 && kb + sft + kGBlock <= M) {
+        const V* src = v + (size_t)ls * M + k + sft;
+        V sv[kGPerThread];
+#pragma unroll
+        for (int e = 0; e < kGPerThread; ++e) sv[e] = __ldg(src + e * kGThreads);
+        V coef = HERM ? t.hh : t.hf;
+        if (t.dl) {
+          const int sg = HERM ? t.dl : -t.dl;
+          coef = cmul(coef, gtwid<T>(tlo, thi, tlb, wrap1((int)(((long long)sg * k) % MN), MN)));
+          const V step = gtwid<T>(tlo, thi, tlb, wrap1(sg * kGThreads, MN));
+#pragma unroll
+          for (int e = 0; e < kGPerThread; ++e) {
+            cfma(acc[e], coef, sv[e]);
+            coef = cmul(coef, step);
+          }
+        } else {
+#pragma unroll
+          for (int e = 0; e < kGPerThread; ++e) cfma(acc[e], coef, sv[e]);
+        }
+        continue;
+      }
+#pragma unroll
+      for (int e = 0; e < kGPerThread; ++e) {
+        const int ke = k + e * kGThreads;
+        const int ar = ke + sft;
+        const int nw = ar < 0 ? -1 : (ar >= M ? 1 : 0);
+        V x = __ldg(v + (size_t)ls * M + (ar - nw * M));
+        if (nw != 0) x = cmul(x, nw < 0 ? cconj(tw[ls]) : tw[ls]);
+        V coef = HERM ? t.hh : t.hf;
+        if (t.dl) coef = cmul(coef, gtwid<T>(tlo, thi, tlb, wrap1(HERM ? t.dl * ke : -t.dl * ke, MN)));
+        cfma(acc[e], coef, x);
+      }
+    }
+    return;
+  }
   int kk[kGPerThread], ll[kGPerThread];
 #pragma unroll
   for (int e = 0; e < kGPerThread; ++e) {
@@ -627,11 +688,19 @@ cudaError_t launch_sscga_global(const SolveArgs& s, void* ws, cudaStream_t st) {
     const size_t psmem = (size_t)(a.TL + a.TH + a.N) * sizeof(V) + (size_t)s.B * kGTaps * sizeof(GTap<T>);
     const T* nvar = reinterpret_cast<const T*>(s.nvar);
     void* kfn = s.bps == 2 ? (void*)g_persist<T, 1> : (s.bps == 6 ? (void*)g_persist<T, 3> : (void*)g_persist<T, 2>);
-    if ((e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psmem))) return e;
-    int dev = 0, sms = 0, per_sm = 0;
+    // attribute + occupancy query once per (kernel, shared memory, device): host time is latency here
+    struct Occ { void* fn; size_t smem; int dev, sms, per_sm; };
+    static thread_local Occ occ = {nullptr, 0, -1, 0, 0};
+    int dev = 0;
     cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, kGThreads, psmem))) return e;
+    if (occ.fn != kfn || occ.smem != psmem || occ.dev != dev) {
+      if ((e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psmem))) return e;
+      int sms = 0, per_sm = 0;
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+      if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, kGThreads, psmem))) return e;
+      occ = Occ{kfn, psmem, dev, sms, per_sm};
+    }
+    const int sms = occ.sms, per_sm = occ.per_sm;
     const int blocks = std::min(per_sm * sms, a.nblk * s.B);
     if (blocks >= 1) {
       uint8_t* labels = s.bps ? s.labels : nullptr;
