@@ -859,3 +859,59 @@ def test_detect_paths_tiled_large_frames(pkg, case):
             np.testing.assert_array_equal(k.cpu().numpy()[a:e], kk[f, :e - a])
             np.testing.assert_array_equal(g.cpu().numpy()[a:e], gg[f, :e - a])
         del s
+
+
+@pytest.mark.parametrize("M,N,P", [(8192, 32, 6), (2048, 16, 5), (96, 12, 4)])
+@pytest.mark.parametrize("precision", ["fp32", "fp64"])
+def test_workspace_persistent_equals_multikernel(pkg, M, N, P, precision, monkeypatch):
+    """Batches of <= 8 frames on the workspace path run as one cooperative
+    launch (g_persist) with the per-phase kernels' gathers and fixed-order
+    folds; results agree to rounding (the compiler may contract the update
+    expressions differently in the two kernels), with equal iteration counts
+    and status.  Includes an empty frame (EmptyChannel) and grids with and
+    without the block-uniform gather fast path (M % 1024)."""
+    monkeypatch.setenv("DDB_KERNEL", "global")
+    rng = np.random.default_rng(M + N + P)
+    B = 4
+    off, k, l, g, y = _random_problem(M, N, B, P, rng)
+    off = np.asarray(off).copy()
+    k, l, g = (np.asarray(v) for v in (k, l, g))
+    # frame 2 empty: drop its taps
+    a, e = int(off[2]), int(off[3])
+    k, l, g = (np.concatenate([v[:a], v[e:]]) for v in (k, l, g))
+    off[3:] -= e - a
+    s = solver_for(pkg, M, N, 10, precision, 4)
+    assert s.plan()["kernel"] == "workspace"
+    paths = pkg.PathBatch.from_arrays(off, k, l, g, cdtype=s.cdtype)
+    yt = torch.as_tensor(y, device="cuda").to(s.cdtype).contiguous()
+    lam = np.array([1e-2, 0.0, 0.1, 3e-3])
+    tx = torch.randint(0, 16, (B, M * N), dtype=torch.uint8, device="cuda")
+    r1 = s.solve(yt, paths, lam, tx_labels=tx, llr=True)
+    monkeypatch.setenv("DDB_NO_PERSIST", "1")
+    r2 = s.solve(yt, paths, lam, tx_labels=tx, llr=True)
+    torch.cuda.synchronize()
+    tol = 1e-12 if precision == "fp64" else 1e-5
+    x1, x2 = r1.x.cpu().numpy(), r2.x.cpu().numpy()
+    for f in range(B):
+        if f == 2:
+            assert not x1[f].any() and not x2[f].any()
+            continue
+        assert rel_l2(x1[f], x2[f]) < tol, (f, rel_l2(x1[f], x2[f]))
+    np.testing.assert_allclose(r1.c_norm.cpu().numpy(), r2.c_norm.cpu().numpy(), rtol=tol * 10, atol=0)
+    assert torch.equal(r1.iterations_done, r2.iterations_done) and torch.equal(r1.status, r2.status)
+    assert (r1.labels != r2.labels).float().mean().item() < 1e-4
+    assert int(r1.status[2]) & 1 and int(r1.bit_errors[2]) == int(r2.bit_errors[2]) == 4 * M * N // 2
+
+
+def test_receive_reports_truncated_tap_batch(pkg):
+    """receive() checks the detected tap batch after queueing the solve: a frame
+    with more taps than max_paths still raises (the operator would be truncated)."""
+    d = load_golden("frontend")
+    M, N, iters, b = (int(v) for v in d["c1_meta"])
+    s = solver_for(pkg, M, N, iters, "fp32", b)
+    pil = torch.as_tensor(d["c1_pilot_rx"], device="cuda")
+    dat = torch.as_tensor(d["c1_data_rx"], device="cuda")
+    with pytest.raises(ValueError):
+        s.receive(pil, dat, torch.as_tensor(d["c1_lam"]), float(d["c1_theta"]), max_paths=2)
+    res = s.receive(pil, dat, torch.as_tensor(d["c1_lam"]), float(d["c1_theta"]))
+    assert res.x.shape == (pil.shape[0], M * N)
