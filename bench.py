@@ -314,8 +314,10 @@ def main():
 
     from paper_2604_02266_b200 import dist as ddist
     rank, local, world = ddist.world()
-    torch.cuda.set_device(local)
-    ddist.init("nccl")
+    # one process per GPU (local rank = device); the modulo and DDB_DIST_BACKEND=gloo
+    # only serve to exercise the multi-rank path with several ranks on one device
+    torch.cuda.set_device(local % torch.cuda.device_count())
+    ddist.init(os.environ.get("DDB_DIST_BACKEND", "nccl"))
 
     import ctypes as C
     import paper_2604_02266_b200 as pkg
@@ -612,7 +614,10 @@ def main():
             "cpu_baseline": cpu,
             "e2e": e2e,
             "frontend": frontend,
-            "gpu_launches": args.steps,
+            # our kernels per step: one fused launch, one cooperative launch (workspace
+            # path, <= 8 frames), else the workspace phase sequence of launch_sscga_global
+            "gpu_launches": args.steps * (1 if s.plan()["kernel"] != "workspace" or B <= 8
+                                          else 4 * args.iters + 5),
             "clocks": clocks,
             "plan": s.plan(),
             "ber": ber,

@@ -76,6 +76,9 @@ def init(backend: Optional[str] = None) -> tuple[int, int, int]:
         if backend == "nccl":
             torch.cuda.set_device(local)
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        elif backend == "gloo" and torch.cuda.is_available():
+            torch.cuda.set_device(local % torch.cuda.device_count())
+            dist.init_process_group("gloo")
         else:
             dist.init_process_group(backend)
     return rank, local, ws
