@@ -227,7 +227,11 @@ __device__ __forceinline__ void tmem_taps(int jr, const TmSm& sm, uint32_t tv, u
   constexpr int H2 = R / 2;  // complex values per half run
   constexpr int W = R;       // 32-bit TMEM columns per half run
   if (!m) return;
-  auto addr = [&](const PathEnt<float>& e) { return tv + (uint32_t)(2 * (jr + (HERM ? -e.dk : e.dk))); };
+  // the run's TMEM base, made opaque so ptxas keeps it in a register instead
+  // of rematerialising the lane base from the thread index on every tap
+  uint32_t tvj;
+  asm volatile("mov.b32 %0, %1;" : "=r"(tvj) : "r"(tv + (uint32_t)(2 * jr)));
+  auto addr = [&](const PathEnt<float>& e) { return tvj + (uint32_t)(2 * (HERM ? -e.dk : e.dk)); };
   const PathEnt<float>* ent = &sm.ptab[__ffs(m) - 1];
   m &= m - 1;
   uint32_t ad = addr(*ent);

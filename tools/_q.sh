@@ -1,5 +1,6 @@
-export DDB_DIST_BACKEND=gloo
-timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29533 bench.py --gpus 2 --steps 3 --warmup 3 --no-cpu --no-latency --no-frontend > gpurun_out/mr_bench.log 2>&1; echo "torchrun rc=$?"
-grep -c '^{' gpurun_out/mr_bench.log; grep '^{' gpurun_out/mr_bench.log | python -c "import json,sys; d=json.loads(sys.stdin.readline()); print(d['n_gpus'], d['value']/1e9, d['e2e']['value']/1e9 if d['e2e'] else None, d['scaling'], d['gpu_launches'])"
-timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29534 bench.py --impl reference --gpus 2 --steps 1 --warmup 0 --cpu-seconds 2 > gpurun_out/mr_ref.log 2>&1; echo "ref rc=$?"; grep -c '^{' gpurun_out/mr_ref.log
-tail -3 gpurun_out/mr_bench.log
+timeout 900 python -m pytest tests -m gpu -q -x > gpurun_out/op2_pytest.log 2>&1; echo "pytest rc=$?"; tail -1 gpurun_out/op2_pytest.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/op2_smoke.log 2>&1; echo "smoke rc=$?"
+timeout 600 python bench.py > gpurun_out/op2_bench.log 2>&1; echo "bench rc=$?"
+grep '^{' gpurun_out/op2_bench.log | python -c "import json,sys; d=json.loads(sys.stdin.readline()); print(round(d['value']/1e9,3), round(d['roofline']['frac'],4), round(d['e2e']['value']/1e9,3), d['e2e']['pcie']['frac'], d['cpu_baseline']['value']/1e6, d['latency']['p50_ms'], d['latency']['receiver_p999_ms'], d['clocks'])"
+timeout 300 python tools/phase_profile.py > gpurun_out/op2_phase.log 2>&1
+for c in cfg3det paper128 cfg2; do timeout 600 python bench.py --config $c --no-cpu > gpurun_out/op2_$c.log 2>&1; grep '^{' gpurun_out/op2_$c.log | python -c "import json,sys; d=json.loads(sys.stdin.readline()); print('$c', round(d['value']/1e9,3))"; done
