@@ -915,3 +915,45 @@ def test_receive_reports_truncated_tap_batch(pkg):
         s.receive(pil, dat, torch.as_tensor(d["c1_lam"]), float(d["c1_theta"]), max_paths=2)
     res = s.receive(pil, dat, torch.as_tensor(d["c1_lam"]), float(d["c1_theta"]))
     assert res.x.shape == (pil.shape[0], M * N)
+
+
+@pytest.mark.parametrize("P", [31, 32, 33, 64])
+@pytest.mark.parametrize("fp32_kernel_name", ["tmem", "row"])
+def test_tap_count_mask_boundary(pkg, P, fp32_kernel_name, monkeypatch):
+    """Per-warp tap masks hold up to 32 taps; frames with more take the per-tap
+    classification path.  Both sides of the boundary (and the in-shared-memory
+    tap-table capacity) against the oracle, at the headline grid, with taps
+    near the pilot (local routes) and a few Doppler-shifted ones (DSMEM)."""
+    if fp32_kernel_name == "row":
+        monkeypatch.setenv("DDB_KERNEL", "row")
+    M, N, B = 512, 32, 2
+    rng = np.random.default_rng(P)
+    off, k, l, g, y = _random_problem(M, N, B, P, rng, anywhere=False)
+    s = solver_for(pkg, M, N, 10, "fp32")
+    paths = pkg.PathBatch.from_arrays(off, k, l, g, cdtype=s.cdtype)
+    yt = torch.as_tensor(y, device="cuda").to(s.cdtype).contiguous()
+    res = s.solve(yt, paths, np.array([1e-2, 3e-2]))
+    x = res.x.cpu().numpy()
+    for f in range(B):
+        taps = [orc.Tap(int(a), int(b), complex(c)) for a, b, c in zip(k[off[f]:off[f + 1]], l[off[f]:off[f + 1]],
+                                                                       g[off[f]:off[f + 1]])]
+        xr, _ = orc.cga(orc.build_tables(taps, M, N), yt[f].cpu().numpy().astype(np.complex128), 10,
+                        [1e-2, 3e-2][f])
+        assert rel_l2(x[f], xr) < REL_L2_FP32, (P, f, rel_l2(x[f], xr))
+
+
+def test_duplicate_taps_equal_merged_tap(pkg):
+    """Two CSR entries at the same (k, l) act as one tap with the summed gain
+    (the operator is linear in the taps; the reference accumulates coincident
+    paths the same way, channel.py:139-149)."""
+    M, N = 512, 32
+    s = solver_for(pkg, M, N, 10, "fp64")
+    rng = np.random.default_rng(9)
+    y = torch.as_tensor(rng.normal(size=(2, M * N)) + 1j * rng.normal(size=(2, M * N)), device="cuda")
+    k = np.array([256, 260, 260, 256, 260])
+    l = np.array([16, 16, 16, 16, 16])
+    g = np.array([1.0, 0.1 + 0.05j, 0.07 - 0.02j, 1.0, 0.17 + 0.03j])
+    paths = pkg.PathBatch.from_arrays(np.array([0, 3, 5]), k, l, g, cdtype=s.cdtype)
+    res = s.solve(y[[0, 0]].contiguous(), paths, 1e-2)
+    x = res.x.cpu().numpy()
+    assert rel_l2(x[0], x[1]) < 1e-12
