@@ -306,6 +306,14 @@ __device__ __forceinline__ void mvm_remote(const SolveArgs& a, const TmThr& th, 
   }
 }
 
+// A value ptxas must keep in a register (it cannot see through the move, so it
+// does not rebuild it from %tid at every use).
+__device__ __forceinline__ uint32_t opaque_u32(uint32_t v) {
+  uint32_t r;
+  asm volatile("mov.b32 %0, %1;" : "=r"(r) : "r"(v));
+  return r;
+}
+
 // ---- TMEM runs of E complex values (2E words) ----------------------------
 template <int E>
 __device__ __forceinline__ void tm_ld(uint32_t ta, uint32_t (&r)[2 * E]) {
@@ -687,13 +695,14 @@ __global__ void __launch_bounds__(MAXT, 1) sscga_tm_kernel(const SolveArgs a) {
         V nu = make_float2(0.f, 0.f), np = make_float2(0.f, 0.f);
         const int lo_u = fs.lo_u, hi_u = fs.hi_u;
         const V twl = tw[th.colg];
+        const uint32_t rb = opaque_u32(tC(0));  // this thread's run in region c; u, p at + 2G, + 4G
 #pragma unroll
         for (int c0 = 0; c0 < R; c0 += E) {
           uint32_t ru[2 * E], rc[2 * E], rp[2 * E];
-          tm_ld<E>(tC(c0), rc);
+          tm_ld<E>(rb + 2 * c0, rc);
           if (it > 0) {
-            tm_ld<E>(tU(c0), ru);
-            tm_ld<E>(tP(c0), rp);
+            tm_ld<E>(rb + 2 * (a.G + c0), ru);
+            tm_ld<E>(rb + 2 * (2 * a.G + c0), rp);
             tmem_wait_ld_tie<2 * E>(ru);
             tmem_wait_ld_tie<2 * E>(rp);
           }
@@ -708,8 +717,8 @@ __global__ void __launch_bounds__(MAXT, 1) sscga_tm_kernel(const SolveArgs a) {
             nacc(nu, w[i]);
             nacc(np, pv[i]);
           }
-          tm_st<E>(tU(c0), w);
-          tm_st<E>(tP(c0), pv);
+          tm_st<E>(rb + 2 * (a.G + c0), w);
+          tm_st<E>(rb + 2 * (2 * a.G + c0), pv);
           put_col<E>(ucol, th.r0 + c0, M, lo_u, hi_u, twl, w);
         }
         red_stage<float>(make_float2(nu.x + nu.y, np.x + np.y), red + par0 * kPushSlots, warp, lane);
@@ -740,12 +749,13 @@ __global__ void __launch_bounds__(MAXT, 1) sscga_tm_kernel(const SolveArgs a) {
         V nc = make_float2(0.f, 0.f);
         const int lo_c = fs.lo_c, hi_c = fs.hi_c;
         const V twl = tw[th.colg];
+        const uint32_t rb = opaque_u32(tC(0));  // this thread's run in region c; p at + 4G, x at + 6G
 #pragma unroll
         for (int c0 = 0; c0 < R; c0 += E) {
           uint32_t rx[2 * E], rp[2 * E], rc[2 * E];
-          tm_ld<E>(tX(c0), rx);
-          tm_ld<E>(tP(c0), rp);
-          tm_ld<E>(tC(c0), rc);
+          tm_ld<E>(rb + 2 * (3 * a.G + c0), rx);
+          tm_ld<E>(rb + 2 * (2 * a.G + c0), rp);
+          tm_ld<E>(rb + 2 * c0, rc);
           tmem_wait_ld_tie<2 * E>(rx);
           tmem_wait_ld_tie<2 * E>(rp);
           tmem_wait_ld_tie<2 * E>(rc);
@@ -758,8 +768,8 @@ __global__ void __launch_bounds__(MAXT, 1) sscga_tm_kernel(const SolveArgs a) {
             cv[i] = axpy(tm_get_v<E>(rc, i), -alpha, ap);
             nacc(nc, cv[i]);
           }
-          tm_st<E>(tX(c0), xv);
-          tm_st<E>(tC(c0), cv);
+          tm_st<E>(rb + 2 * (3 * a.G + c0), xv);
+          tm_st<E>(rb + 2 * c0, cv);
           put_col<E>(ccol, th.r0 + c0, M, lo_c, hi_c, twl, cv);
           if (a.snaps) {
             V* sp = reinterpret_cast<V*>(a.snaps) + ((size_t)f * a.iters + it) * a.MN + (qown - fo) + c0;
