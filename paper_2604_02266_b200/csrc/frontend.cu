@@ -142,11 +142,19 @@ __global__ void __launch_bounds__(kDztThreads) dzt_fft_kernel(int M, int N, int 
   extern __shared__ __align__(16) unsigned char smem[];
   V* xs = reinterpret_cast<V*>(smem);  // [N][kTk], block index bit-reversed
   V* wn = xs + (size_t)N * kTk;        // [N/2]: W_N^{sgn e} (sgn -1: dzt, +1: idzt)
+  V* twist = wn + N / 2;               // [N] (PILOT): e^{-j2pi K0 (l - L0)/MN} / amplitude, per Doppler column
   const int f = blockIdx.y;
   const int k0 = blockIdx.x * kTk;
   const int MN = M * N;
   const VIN* yf = y + (size_t)f * MN;
   for (int e = threadIdx.x; e < N / 2; e += blockDim.x) wn[e] = twiddle(T(0), mod_pos(sgn * e, N), N);
+  if constexpr (PILOT) {
+    for (int l = threadIdx.x; l < N; l += blockDim.x) {
+      const long long e = (long long)(M / 2) * (l - N / 2);
+      const int er = (int)(((-e) % MN + MN) % MN);
+      twist[l] = cscale(twiddle(T(0), er, MN), inv_amp);
+    }
+  }
   for (int idx = threadIdx.x; idx < N * kTk; idx += blockDim.x) {
     const int i = idx / kTk, kl = idx - i * kTk;
     const int k = k0 + kl;
@@ -179,11 +187,7 @@ __global__ void __launch_bounds__(kDztThreads) dzt_fft_kernel(int M, int N, int 
   if (k >= M) return;
   for (int l = g0; l < N; l += groups) {
     V r = cscale(xs[l * kTk + kl], rs);
-    if constexpr (PILOT) {
-      const long long e = (long long)(M / 2) * (l - N / 2);
-      const int er = (int)(((-e) % MN + MN) % MN);
-      r = cscale(cmul(r, twiddle(T(0), er, MN)), inv_amp);
-    }
+    if constexpr (PILOT) r = cmul(r, twist[l]);  // twist constant along delay (pilot.py:29-37)
     if constexpr (COLMAJOR) out[(size_t)f * MN + (size_t)l * M + k] = r;
     else out[(size_t)f * MN + (size_t)k * N + l] = r;
   }
@@ -205,7 +209,7 @@ cudaError_t launch_dzt_t(int B, int M, int N, const void* y, const void* kern, i
   if (!kern && N >= 2 && (N & (N - 1)) == 0) {  // default kernel, power-of-two N: FFT
     int logn = 0;
     while ((1 << logn) < N) ++logn;
-    const size_t fsmem = ((size_t)N * kTk + N / 2) * sizeof(V);
+    const size_t fsmem = ((size_t)N * kTk + N / 2 + N) * sizeof(V);
     cudaError_t e = cudaFuncSetAttribute(dzt_fft_kernel<T, COLMAJOR, PILOT>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fsmem);
     if (e != cudaSuccess) return e;
@@ -242,7 +246,7 @@ template <bool COLMAJOR, bool PILOT>
 cudaError_t launch_dzt_mixed_t(int B, int M, int N, const void* y, double amp, void* out, cudaStream_t st) {
   int logn = 0;
   while ((1 << logn) < N) ++logn;
-  const size_t fsmem = ((size_t)N * kTk + N / 2) * sizeof(double2);
+  const size_t fsmem = ((size_t)N * kTk + N / 2 + N) * sizeof(double2);
   auto kfn = dzt_fft_kernel<double, COLMAJOR, PILOT, float2>;
   cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fsmem);
   if (e != cudaSuccess) return e;
