@@ -48,7 +48,8 @@ CONFIGS = {
     "cfg1": dict(M=64, N=16, P=4, mod="qpsk", batch=4096, nu=0.0),
     "cfg2": dict(M=256, N=16, P=4, mod="qam16", batch=1024, nu=300.0),
     "cfg3": dict(M=512, N=32, P=6, mod="qam16", batch=4096, nu=100.0),
-    "cfg4": dict(M=1024, N=64, P=6, mod="qam16", batch=1024, nu=1000.0),
+    # BASELINE config 4: high mobility (nu_max 1000 Hz: Doppler taps), 8 paths, 64-QAM (build extension)
+    "cfg4": dict(M=1024, N=64, P=8, mod="qam64", batch=1024, nu=1000.0),
     # cfg3 grid with the taps the reference's detect_paths finds on fractional-Doppler
     # Veh-A channels (tests/golden/frames_sweep.npz: 8-10 taps per frame, 2-4 of them
     # Doppler-leakage taps at l = L0 +- 1), cycled over the batch
