@@ -957,3 +957,31 @@ def test_duplicate_taps_equal_merged_tap(pkg):
     res = s.solve(y[[0, 0]].contiguous(), paths, 1e-2)
     x = res.x.cpu().numpy()
     assert rel_l2(x[0], x[1]) < 1e-12
+
+
+def test_bench_json_contract(pkg):
+    """bench.py (our arm) prints one JSON line with every key the driver reads."""
+    import json
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+    root = Path(__file__).resolve().parent.parent
+    cmd = [sys.executable, str(root / "bench.py"), "--config", "cfg1", "--steps", "3", "--warmup", "3",
+           "--lat-runs", "50", "--cpu-seconds", "1", "--batch", "296"]
+    out = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=root,
+                         env=dict(os.environ, OPENBLAS_NUM_THREADS="1"))
+    assert out.returncode == 0, out.stderr[-3000:]
+    lines = [ln for ln in out.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    for key in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better",
+                "scaling", "vs_baseline", "dtype", "data", "config", "roofline", "cpu_baseline", "e2e",
+                "gpu_launches", "clocks", "latency"):
+        assert key in d, key
+    assert {"bound", "achieved", "peak", "unit", "frac", "traffic"} <= set(d["roofline"])
+    assert {"value", "unit", "cores", "kind", "sample"} <= set(d["cpu_baseline"])
+    assert {"value", "unit", "h2d_bytes_per_step", "d2h_bytes_per_step"} <= set(d["e2e"])
+    assert d["e2e"]["h2d_bytes_per_step"] > 0 and d["e2e"]["d2h_bytes_per_step"] > 0
+    assert d["gpu_launches"] >= d["steps"] and d["value"] > 0 and d["n_gpus"] == 1
+    assert "workload" in d["config"] and 0 < d["roofline"]["frac"] < 1
