@@ -408,6 +408,17 @@ __device__ __forceinline__ int tm_epilogue(const SolveArgs& a, const V (&xv)[E],
   if constexpr (BA == 0) {
     return 0;
   } else {
+    // the transmitted labels first: their load is then in flight during the
+    // slicing (issued after the label / LLR stores it could not be hoisted
+    // above them -- the pointers may alias as far as the compiler knows)
+    static_assert(E == 4, "one TX word per call");
+    uint32_t txw = 0;
+    if (a.txl) {
+      if (!a.txpk) txw = __ldg(reinterpret_cast<const uint32_t*>(a.txl + q0));
+      else if constexpr (BA <= 2)
+        txw = BA == 2 ? (uint32_t)__ldg(reinterpret_cast<const uint16_t*>(a.txl + (q0 >> 1)))
+                      : (uint32_t)__ldg(a.txl + (q0 >> 2));
+    }
     uint8_t lab[E];
 #pragma unroll
     for (int i = 0; i < E; ++i) {
@@ -432,15 +443,12 @@ __device__ __forceinline__ int tm_epilogue(const SolveArgs& a, const V (&xv)[E],
       if (a.labels) reinterpret_cast<uint32_t*>(a.labels + q0)[w] = word;
       if (a.txl) {
         if (!a.txpk) {
-          errs += __popc(word ^ __ldg(reinterpret_cast<const uint32_t*>(a.txl + q0) + w));
+          errs += __popc(word ^ txw);
         } else if constexpr (BA <= 2) {  // four symbols = 2 BA bits each, LSB-first: 8 or 16 bits
           constexpr int SB = 2 * BA;
           const uint32_t mine = (uint32_t)lab[4 * w] | ((uint32_t)lab[4 * w + 1] << SB) |
                                 ((uint32_t)lab[4 * w + 2] << (2 * SB)) | ((uint32_t)lab[4 * w + 3] << (3 * SB));
-          const size_t q = q0 + 4 * w;
-          const uint32_t tx = SB == 4 ? (uint32_t)__ldg(reinterpret_cast<const uint16_t*>(a.txl + (q >> 1)))
-                                      : (uint32_t)__ldg(a.txl + (q >> 2));
-          errs += __popc(mine ^ tx);
+          errs += __popc(mine ^ txw);
         }  // (64-QAM labels are never packed: the ABI rejects it)
       }
     }
