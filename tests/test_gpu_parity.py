@@ -985,3 +985,29 @@ def test_bench_json_contract(pkg):
     assert d["e2e"]["h2d_bytes_per_step"] > 0 and d["e2e"]["d2h_bytes_per_step"] > 0
     assert d["gpu_launches"] >= d["steps"] and d["value"] > 0 and d["n_gpus"] == 1
     assert "workload" in d["config"] and 0 < d["roofline"]["frac"] < 1
+
+
+def test_veha_batch_draws_and_noiseless_loopback(pkg):
+    """draw_veha_batch follows channel.py:62-92 (ITU Veh-A delays and powers,
+    unit total power, |nu| <= nu_max); a noiseless, Doppler-free synthesised
+    batch comes back through the device receiver with exactly the six taps and
+    no bit errors (criterion 5 style loopback, tests/test_acceptance.py)."""
+    from paper_2604_02266_b200.channel import VEHA_DELAYS_US, draw_veha_batch
+    from paper_2604_02266_b200.synth import synthesize_packets
+    g = pkg.GridConfig(512, 32)
+    gen = torch.Generator(device="cuda")
+    gen.manual_seed(4)
+    ch = draw_veha_batch(1000, g, 300.0, gen)
+    P = len(VEHA_DELAYS_US)
+    assert ch.offsets.cpu().tolist() == list(range(0, 1001 * P, P))
+    bins = ch.delay_bin.view(1000, P).cpu().numpy()
+    assert (bins == np.round(np.array(VEHA_DELAYS_US) * 1e-6 * g.B)).all()
+    pw = (ch.gain.view(1000, P).abs() ** 2).sum(dim=1).cpu().numpy()
+    np.testing.assert_allclose(pw, 1.0, rtol=1e-12)
+    assert float(ch.doppler_hz.abs().max()) <= 300.0 + 1e-9
+    s = pkg.SsCgaSolver(512, 32, 10, precision="fp32", modulation="qpsk")
+    pb = synthesize_packets(s, 64, snr_db=float("inf"), nu_max_hz=0.0, modulation="qpsk", seed=5)
+    paths = s.detect(pb.pilot_rx, 0.08)
+    assert (torch.diff(paths.offsets.cpu()) == P).all()
+    res = s.receive(pb.pilot_rx, pb.data_rx, pb.lam, 0.08, tx_labels=pb.tx_labels)
+    assert int(res.bit_errors.sum()) == 0
