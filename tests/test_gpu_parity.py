@@ -1011,3 +1011,23 @@ def test_veha_batch_draws_and_noiseless_loopback(pkg):
     assert (torch.diff(paths.offsets.cpu()) == P).all()
     res = s.receive(pb.pilot_rx, pb.data_rx, pb.lam, 0.08, tx_labels=pb.tx_labels)
     assert int(res.bit_errors.sum()) == 0
+
+
+def test_dense_receiver_empty_channel_and_zero_frame(pkg):
+    """Dense branch edge cases: a pilot with no energy has no taps, so the packet
+    is scored as run_packet scores EmptyChannel (bits / 2 errors,
+    harness.py:170-178); threshold_frame of an all-zero frame is a copy
+    (sparse.py:165-168)."""
+    from paper_2604_02266_b200 import dense as dn
+    h = load_golden("harness_c6")
+    M, N, iters, b, P = (int(v) for v in h["meta"])
+    s = pkg.SsCgaSolver(M, N, iters, precision="fp64", modulation="qpsk")
+    pil = torch.as_tensor(h["pilot_rx"][:3], device="cuda").clone()
+    pil[1] = 0
+    dat = torch.as_tensor(h["data_rx"][:3], device="cuda")
+    tx = torch.as_tensor(h["tx_labels"][:3], device="cuda")
+    r = dn.receive_lmmse(s, pil, dat, float(h["snr_db"]), float(h["theta"]), tx_labels=tx)
+    assert r["failed"].cpu().tolist() == [False, True, False]
+    assert int(r["bit_errors"][1]) == b * M * N // 2
+    z = np.zeros((M, N), complex)
+    np.testing.assert_array_equal(dn.threshold_frame(z, 0.08, pkg.GridConfig(M, N)), z)
