@@ -1031,3 +1031,41 @@ def test_dense_receiver_empty_channel_and_zero_frame(pkg):
     assert int(r["bit_errors"][1]) == b * M * N // 2
     z = np.zeros((M, N), complex)
     np.testing.assert_array_equal(dn.threshold_frame(z, 0.08, pkg.GridConfig(M, N)), z)
+
+
+@pytest.mark.parametrize("precision", ["fp64", "fp32"])
+def test_criterion8a_residual_trace_non_increasing(pkg, precision):
+    """Acceptance criterion 8(a) (tests/test_acceptance.py:220-235): over 30
+    random channels (a dominant unit tap plus four weaker ones at distinct
+    random bins, detect_paths at theta 0.01) on (16, 8) and (16, 32), 25 CG
+    iterations at lam 1e-3, the residual trace c_norm never increases.  fp64
+    with the reference's 1e-12 slack; fp32 with its rounding level (1e-5)."""
+    rng = np.random.default_rng(88)
+    slack = 1e-12 if precision == "fp64" else 1e-5
+    for m, n in [(16, 8), (16, 32)]:
+        s = solver_for(pkg, m, n, 25, precision)
+        frames, ys = [], []
+        for _ in range(15):
+            fr = np.zeros((m, n), complex)
+            fr[int(rng.integers(m)), int(rng.integers(n))] = 1.0
+            placed = 0
+            while placed < 4:
+                k, l = int(rng.integers(m)), int(rng.integers(n))
+                if fr[k, l] == 0:
+                    fr[k, l] = rng.uniform(0.05, 0.2) * np.exp(2j * np.pi * rng.random())
+                    placed += 1
+            frames.append(fr)
+            ys.append(rng.normal(size=m * n) + 1j * rng.normal(size=m * n))
+        taps = [orc.detect_paths(fr, 0.01) for fr in frames]
+        off = np.concatenate([[0], np.cumsum([len(t) for t in taps])])
+        k = np.array([t.k for ts in taps for t in ts])
+        l = np.array([t.l for ts in taps for t in ts])
+        g = np.array([t.gain for ts in taps for t in ts])
+        paths = pkg.PathBatch.from_arrays(off, k, l, g, cdtype=s.cdtype)
+        y = torch.as_tensor(np.array(ys), device="cuda").to(s.cdtype).contiguous()
+        res = s.solve(y, paths, 1e-3)
+        cn = res.c_norm.cpu().numpy().astype(np.float64)
+        done = res.iterations_done.cpu().numpy()
+        for f in range(len(frames)):
+            t = cn[f, :done[f] + 1]
+            assert np.all(t[1:] <= t[:-1] * (1 + slack)), (m, n, f, t)
