@@ -1069,3 +1069,34 @@ def test_criterion8a_residual_trace_non_increasing(pkg, precision):
         for f in range(len(frames)):
             t = cn[f, :done[f] + 1]
             assert np.all(t[1:] <= t[:-1] * (1 + slack)), (m, n, f, t)
+
+
+def test_criterion7_full_iteration_solve_matches_dense(pkg):
+    """Acceptance criterion 7 (tests/test_acceptance.py:195-217): MN CG
+    iterations reproduce the dense regularised solution (H^H H + lam I)^{-1}
+    H^H y within 1e-6 relative, on (8,4), (16,8), (16,32) at lam 1e-3 and
+    10^-2.5 (fp64 fused kernel; the dense reference from the oracle's
+    restatement of build_dense_hdd, sparse.py:172-206)."""
+    rng = np.random.default_rng(77)
+    worst = 0.0
+    for m, n in [(8, 4), (16, 8), (16, 32)]:
+        for lam in (1e-3, 10 ** -2.5):
+            fr = np.zeros((m, n), complex)
+            fr[int(rng.integers(m)), int(rng.integers(n))] = 1.0
+            placed = 0
+            while placed < 4:
+                k, l = int(rng.integers(m)), int(rng.integers(n))
+                if fr[k, l] == 0:
+                    fr[k, l] = rng.uniform(0.05, 0.2) * np.exp(2j * np.pi * rng.random())
+                    placed += 1
+            taps = orc.detect_paths(fr, 0.01)
+            H = orc.dense_channel(fr, m, n)
+            y = rng.normal(size=m * n) + 1j * rng.normal(size=m * n)
+            s = solver_for(pkg, m, n, m * n, "fp64")
+            paths = pkg.PathBatch.from_arrays(np.array([0, len(taps)]), np.array([t.k for t in taps]),
+                                              np.array([t.l for t in taps]), np.array([t.gain for t in taps]),
+                                              cdtype=s.cdtype)
+            x = s.solve(torch.as_tensor(y[None], device="cuda"), paths, lam).x[0].cpu().numpy()
+            want = np.linalg.solve(H.conj().T @ H + lam * np.eye(m * n), H.conj().T @ y)
+            worst = max(worst, float(np.linalg.norm(x - want) / np.linalg.norm(want)))
+    assert worst < 1e-6, worst
