@@ -1100,3 +1100,42 @@ def test_criterion7_full_iteration_solve_matches_dense(pkg):
             want = np.linalg.solve(H.conj().T @ H + lam * np.eye(m * n), H.conj().T @ y)
             worst = max(worst, float(np.linalg.norm(x - want) / np.linalg.norm(want)))
     assert worst < 1e-6, worst
+
+
+def test_criterion3_sparse_equals_dense_on_device(pkg):
+    """Acceptance criterion 3 (tests/test_acceptance.py:96-130) with both sides
+    on the device: 50 random integer-shift channels up to (128, 32); the
+    matrix-free operator (ddb_ss_apply, both directions) equals the dense
+    matrix of ddb_build_dense_hdd, and every table coefficient of
+    ddb_build_tables equals its dense entry, within 1e-9 max-abs."""
+    from paper_2604_02266_b200 import dense as dn
+    plan = [(8, 4, 12), (16, 8, 12), (32, 16, 12), (64, 32, 9), (128, 32, 5)]
+    rng = np.random.default_rng(2024)
+    worst = 0.0
+    for m, n, count in plan:
+        g = pkg.GridConfig(m, n)
+        s = solver_for(pkg, m, n, 10, "fp64")
+        for _ in range(count):
+            fr = np.zeros((m, n), complex)
+            fr[int(rng.integers(m)), int(rng.integers(n))] = 1.0
+            placed = 0
+            while placed < 4:
+                k, l = int(rng.integers(m)), int(rng.integers(n))
+                if fr[k, l] == 0:
+                    fr[k, l] = rng.uniform(0.05, 0.2) * np.exp(2j * np.pi * rng.random())
+                    placed += 1
+            taps = pkg.detect_paths(fr, 0.01, g)
+            H = dn.build_dense_hdd(fr, g)
+            v = rng.normal(size=m * n) + 1j * rng.normal(size=m * n)
+            paths = pkg.PathBatch.from_arrays(np.array([0, len(taps)]), np.array([t.k_p for t in taps]),
+                                              np.array([t.l_p for t in taps]), np.array([t.gain for t in taps]),
+                                              cdtype=s.cdtype)
+            vt = torch.as_tensor(v[None], device="cuda").contiguous()
+            fwd = s.apply(vt, paths)[0].cpu().numpy()
+            her = s.apply(vt, paths, hermitian=True)[0].cpu().numpy()
+            worst = max(worst, float(np.abs(fwd - H @ v).max()), float(np.abs(her - H.conj().T @ v).max()))
+            ch = pkg.build_ss_channel(taps, g)
+            q = np.arange(m * n)
+            for p in range(ch.P):
+                worst = max(worst, float(np.abs(ch.fwd_coef[p] - H[q, ch.fwd_col[p]]).max()))
+    assert worst < 1e-9, worst
