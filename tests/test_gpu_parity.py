@@ -1139,3 +1139,50 @@ def test_criterion3_sparse_equals_dense_on_device(pkg):
             for p in range(ch.P):
                 worst = max(worst, float(np.abs(ch.fwd_coef[p] - H[q, ch.fwd_col[p]]).max()))
     assert worst < 1e-9, worst
+
+
+def _device_run_packets(pkg, M, N, snr_db, nu_max, theta, packets, seed):
+    """run_packets (harness.py:131-232) with the packet synthesis of run_packet
+    (harness.py:141-149) done by this package's drop-ins in the same draw order
+    on the same numpy generators -- draw_veha, bits, modulate, idzt (device),
+    apply_channel (device, fp64), add_awgn (host, the caller's generator) -- and
+    the receiver (harness.py:155-198) as one device batch.  Returns the mean BER."""
+    from paper_2604_02266_b200 import channel as pch
+    g = pkg.GridConfig(M, N)
+    const = pkg.make_constellation("qpsk")
+    b = const.bits_per_symbol
+    pilot_tx = pch.idzt(pkg.make_pilot_frame(g), g)
+    pil, dat, tx = [], [], []
+    for idx in range(packets):
+        rng = np.random.default_rng([seed, idx])
+        ps = pch.draw_veha(nu_max, g, rng)
+        bits = rng.integers(0, 2, size=b * g.size)
+        data_tx = pch.idzt(pkg.modulate(bits, const, g), g)
+        pil.append(pch.add_awgn(pch.apply_channel(pilot_tx, ps, g), snr_db, rng))
+        dat.append(pch.add_awgn(pch.apply_channel(data_tx, ps, g), snr_db, rng))
+        tx.append(bits.reshape(-1, b) @ (1 << np.arange(b - 1, -1, -1)))
+    s = pkg.SsCgaSolver(M, N, 10, precision="fp64", modulation="qpsk")
+    lam = 0.0 if np.isinf(snr_db) else 10 ** (-snr_db / 10)
+    res = s.receive(torch.as_tensor(np.array(pil), device="cuda"), torch.as_tensor(np.array(dat), device="cuda"),
+                    torch.full((packets,), lam, dtype=torch.float64), theta, max_paths=512,
+                    tx_labels=torch.as_tensor(np.array(tx, np.uint8), device="cuda"))
+    return int(res.bit_errors.sum()) / (packets * b * g.size)
+
+
+@pytest.mark.parametrize("snr,want", [(0.0, 2.0e-1), (10.0, 2.7e-2), (20.0, 9.7e-4), (30.0, 3.1e-4)])
+def test_criterion8b_ber_vs_snr_known_answers(pkg, snr, want):
+    """Acceptance criterion 8(b) (tests/test_acceptance.py:236-249): QPSK at
+    (128, 32), 40 packets, seed 5 -- the reference's per-SNR mean BER
+    [2.0e-1, 2.7e-2, 9.7e-4, 3.1e-4] (test_output.txt:236), reproduced with
+    the packets regenerated from the same seeds and received on the device."""
+    ber = _device_run_packets(pkg, 128, 32, snr, 100.0, 0.08, 40, 5)
+    assert f"{ber:.1e}" == f"{want:.1e}", ber
+
+
+@pytest.mark.parametrize("nu,want", [(0.0, 2.0e-5), (500.0, 1.4e-3), (1000.0, 3.2e-4)])
+def test_criterion8c_ber_vs_doppler_known_answers(pkg, nu, want):
+    """Acceptance criterion 8(c) (tests/test_acceptance.py:251-263): 25 dB,
+    theta 0.03, 60 packets, seed 21 -- BER [2.0e-5, 1.4e-3, 3.2e-4] over
+    nu_max {0, 500, 1000} Hz (test_output.txt:236)."""
+    ber = _device_run_packets(pkg, 128, 32, 25.0, nu, 0.03, 60, 21)
+    assert f"{ber:.1e}" == f"{want:.1e}", ber
