@@ -1141,7 +1141,7 @@ def test_criterion3_sparse_equals_dense_on_device(pkg):
     assert worst < 1e-9, worst
 
 
-def _device_run_packets(pkg, M, N, snr_db, nu_max, theta, packets, seed):
+def _device_run_packets(pkg, M, N, snr_db, nu_max, theta, packets, seed, mod="qpsk", pset=None, per_packet=False):
     """run_packets (harness.py:131-232) with the packet synthesis of run_packet
     (harness.py:141-149) done by this package's drop-ins in the same draw order
     on the same numpy generators -- draw_veha, bits, modulate, idzt (device),
@@ -1149,23 +1149,25 @@ def _device_run_packets(pkg, M, N, snr_db, nu_max, theta, packets, seed):
     the receiver (harness.py:155-198) as one device batch.  Returns the mean BER."""
     from paper_2604_02266_b200 import channel as pch
     g = pkg.GridConfig(M, N)
-    const = pkg.make_constellation("qpsk")
+    const = pkg.make_constellation(mod)
     b = const.bits_per_symbol
     pilot_tx = pch.idzt(pkg.make_pilot_frame(g), g)
     pil, dat, tx = [], [], []
     for idx in range(packets):
         rng = np.random.default_rng([seed, idx])
-        ps = pch.draw_veha(nu_max, g, rng)
+        ps = pset if pset is not None else pch.draw_veha(nu_max, g, rng)
         bits = rng.integers(0, 2, size=b * g.size)
         data_tx = pch.idzt(pkg.modulate(bits, const, g), g)
         pil.append(pch.add_awgn(pch.apply_channel(pilot_tx, ps, g), snr_db, rng))
         dat.append(pch.add_awgn(pch.apply_channel(data_tx, ps, g), snr_db, rng))
         tx.append(bits.reshape(-1, b) @ (1 << np.arange(b - 1, -1, -1)))
-    s = pkg.SsCgaSolver(M, N, 10, precision="fp64", modulation="qpsk")
+    s = pkg.SsCgaSolver(M, N, 10, precision="fp64", modulation=mod)
     lam = 0.0 if np.isinf(snr_db) else 10 ** (-snr_db / 10)
     res = s.receive(torch.as_tensor(np.array(pil), device="cuda"), torch.as_tensor(np.array(dat), device="cuda"),
                     torch.full((packets,), lam, dtype=torch.float64), theta, max_paths=512,
                     tx_labels=torch.as_tensor(np.array(tx, np.uint8), device="cuda"))
+    if per_packet:
+        return res.bit_errors.cpu().numpy(), res.status.cpu().numpy()
     return int(res.bit_errors.sum()) / (packets * b * g.size)
 
 
@@ -1186,3 +1188,17 @@ def test_criterion8c_ber_vs_doppler_known_answers(pkg, nu, want):
     nu_max {0, 500, 1000} Hz (test_output.txt:236)."""
     ber = _device_run_packets(pkg, 128, 32, 25.0, nu, 0.03, 60, 21)
     assert f"{ber:.1e}" == f"{want:.1e}", ber
+
+
+@pytest.mark.parametrize("M,N", [(32, 32), (128, 32)])
+@pytest.mark.parametrize("mod", ["qpsk", "qam16"])
+def test_criterion5_noiseless_identity_loopback(pkg, M, N, mod):
+    """Acceptance criterion 5 (tests/test_acceptance.py:154-176): identity
+    channel, no noise, 10 packets per grid and constellation: zero bit errors
+    and no failed packet."""
+    from paper_2604_02266_b200 import channel as pch
+    g = pkg.GridConfig(M, N)
+    ident = pch.PathSet((pch.make_path(1.0, 0.0, 0.0, g),))
+    errs, status = _device_run_packets(pkg, M, N, float("inf"), 0.0, 0.08, 10, 0, mod=mod, pset=ident,
+                                       per_packet=True)
+    assert int(errs.sum()) == 0 and not (status & 1).any()
