@@ -240,19 +240,27 @@ class SsCgaSolver:
                                                         _stream_handle(stream)), "ddb_sscga_profile_phases")
         else:
             ws_bytes = int(self.lib.ddb_sscga_workspace_bytes(C.byref(prob)))
-            ws = self._workspace(ws_bytes)
+            ws = self._workspace(ws_bytes, stream)
             nat.check(self.lib.ddb_sscga_solve(C.byref(prob), C.byref(outs), _ptr(ws), ws_bytes,
                                                _stream_handle(stream)), "ddb_sscga_solve")
         return out
 
-    def _workspace(self, nbytes: int) -> Optional[torch.Tensor]:
-        """Device workspace of the workspace-backed path (grown, never shrunk)."""
+    def _workspace(self, nbytes: int, stream: Optional[torch.cuda.Stream] = None) -> Optional[torch.Tensor]:
+        """Device workspace of the workspace-backed path (grown, never shrunk).
+
+        One buffer per launch stream: two solves on different streams never
+        share c / u / p.  The buffer is allocated with that stream current, so
+        the caching allocator orders its reuse after the stream's pending
+        kernels when it is regrown (the old block is freed on the same stream)."""
         if nbytes == 0:
             return None
-        ws = getattr(self, "_ws", None)
+        s = stream if stream is not None else torch.cuda.current_stream(self.device)
+        pool = self.__dict__.setdefault("_ws", {})
+        ws = pool.get(s.cuda_stream)
         if ws is None or ws.numel() < nbytes:
-            ws = torch.empty(nbytes, dtype=torch.uint8, device=self.device)
-            self._ws = ws
+            with torch.cuda.stream(s):
+                ws = torch.empty(nbytes, dtype=torch.uint8, device=self.device)
+            pool[s.cuda_stream] = ws
         return ws
 
     # -- receiver front end (SURVEY.md §8f row f1) ---------------------------

@@ -226,6 +226,9 @@ __device__ __forceinline__ void block_pair_sum(Vec<T> v, Vec<T>* dst) {
     for (int w = 1; w < kGThreads / 32; ++w) s = cadd(s, red[w]);
     *dst = s;
   }
+  // red[] is reused by the block's next call (g_persist runs several frames'
+  // blocks back to back): no warp may overwrite it before thread 0 has read it
+  __syncthreads();
 }
 
 #define G_SMEM_DECL                                        \
@@ -428,10 +431,20 @@ template <typename T> struct PScal {
   int state, done;
 };
 
+// Block partials of the persistent kernel alternate between two buffers by
+// phase parity: after a grid barrier every block folds phase k's partials
+// while a faster block may already write phase k+1's, and phase k+2 (the next
+// writer of this buffer) starts only after another grid barrier, which every
+// block reaches after its fold of phase k.
 template <typename T>
-__device__ __forceinline__ Vec<T> p_fold(const GArgs<T>& a, int f) {
+__device__ __forceinline__ Vec<T>* p_part(const GArgs<T>& a, int ph) {
+  return a.part + (size_t)(ph & 1) * a.B * a.nblk;
+}
+
+template <typename T>
+__device__ __forceinline__ Vec<T> p_fold(const GArgs<T>& a, int f, int ph) {
   using V = Vec<T>;
-  const V* pp = a.part + (size_t)f * a.nblk;
+  const V* pp = p_part(a, ph) + (size_t)f * a.nblk;
   V v = czero<V>();
   for (int i = threadIdx.x; i < a.nblk; i += blockDim.x) v = cadd(v, pp[i]);
   __shared__ V tot;
@@ -480,6 +493,7 @@ __global__ void __launch_bounds__(kGThreads) g_persist(const GArgs<T> a, uint8_t
   const int nv = a.nblk * a.B;
   const int stride = a.iters + 1;
   const bool lead = blockIdx.x == 0 && threadIdx.x == 0;
+  int ph = 0;  // phase counter: selects the partials buffer (p_part)
 
   // b = H^H y -> c, x = 0
   for (int vb = blockIdx.x; vb < nv; vb += gridDim.x) {
@@ -496,12 +510,12 @@ __global__ void __launch_bounds__(kGThreads) g_persist(const GArgs<T> a, uint8_t
       a.x[fo + q] = czero<V>();
       nrm.x += bb[e].x * bb[e].x + bb[e].y * bb[e].y;
     }
-    block_pair_sum<T>(nrm, a.part + (size_t)f * a.nblk + blk);
+    block_pair_sum<T>(nrm, p_part(a, ph) + (size_t)f * a.nblk + blk);
   }
   grid.sync();
   for (int f = 0; f < a.B; ++f) {
     if (pcount[f] <= 0) continue;
-    const V t = p_fold<T>(a, f);
+    const V t = p_fold<T>(a, f, ph);
     if (threadIdx.x == 0) sc[f] = PScal<T>{t.x, T(0), T(0), 0, 0};
     if (lead && a.cnorm) a.cnorm[(size_t)f * stride] = t.x;
   }
@@ -527,12 +541,13 @@ __global__ void __launch_bounds__(kGThreads) g_persist(const GArgs<T> a, uint8_t
         nu.x += uq.x * uq.x + uq.y * uq.y;
         nu.y += pq.x * pq.x + pq.y * pq.y;
       }
-      block_pair_sum<T>(nu, a.part + (size_t)f * a.nblk + blk);
+      block_pair_sum<T>(nu, p_part(a, ph + 1) + (size_t)f * a.nblk + blk);
     }
     grid.sync();
+    ++ph;
     for (int f = 0; f < a.B; ++f) {
       if (pcount[f] <= 0 || sc[f].state) continue;
-      const V t = p_fold<T>(a, f);
+      const V t = p_fold<T>(a, f, ph);
       if (threadIdx.x == 0) {
         const T denom = t.x + a.lam[f] * t.y;  // equalize.py:60-67
         if (denom == T(0)) sc[f].state = 1;
@@ -561,12 +576,13 @@ __global__ void __launch_bounds__(kGThreads) g_persist(const GArgs<T> a, uint8_t
         if (a.snaps) a.snaps[((size_t)f * a.iters + it) * a.MN + q] = xq;
         nc.x += cq.x * cq.x + cq.y * cq.y;
       }
-      block_pair_sum<T>(nc, a.part + (size_t)f * a.nblk + blk);
+      block_pair_sum<T>(nc, p_part(a, ph + 1) + (size_t)f * a.nblk + blk);
     }
     grid.sync();
+    ++ph;
     for (int f = 0; f < a.B; ++f) {
       if (pcount[f] <= 0 || sc[f].state) continue;
-      const V t = p_fold<T>(a, f);
+      const V t = p_fold<T>(a, f, ph);
       if (threadIdx.x == 0) {
         sc[f].beta = t.x / sc[f].cn;
         sc[f].cn = t.x;
@@ -636,7 +652,8 @@ __global__ void g_zero_int(int* p, int n) {
 template <typename T>
 size_t g_workspace(int B, int MN) {
   const int nblk = (MN + kGBlock - 1) / kGBlock;
-  return align_up(3 * (size_t)B * MN * sizeof(Vec<T>), 256) + align_up((size_t)B * nblk * sizeof(Vec<T>), 256) +
+  // partials: two buffers (g_persist alternates them by phase parity, p_part)
+  return align_up(3 * (size_t)B * MN * sizeof(Vec<T>), 256) + align_up(2 * (size_t)B * nblk * sizeof(Vec<T>), 256) +
          align_up((size_t)B * sizeof(FrameScal<T>), 256);
 }
 
@@ -674,7 +691,7 @@ cudaError_t launch_sscga_global(const SolveArgs& s, void* ws, cudaStream_t st) {
   a.p = reinterpret_cast<V*>(w + 2 * vb);
   w += align_up(3 * vb, 256);
   a.part = reinterpret_cast<V*>(w);
-  w += align_up((size_t)s.B * a.nblk * sizeof(V), 256);
+  w += align_up(2 * (size_t)s.B * a.nblk * sizeof(V), 256);
   a.sc = reinterpret_cast<FrameScal<T>*>(w);
   a.cnorm = reinterpret_cast<T*>(s.cnorm);
   a.itdone = s.itdone;

@@ -4,7 +4,13 @@
 ((x_hat complex128 [MN], CgaTrace)) of equalize.py:43-77 and its config
 errors (equalize.py:14-30), but runs the fused matrix-free sm_100a kernel:
 only `ch.M`, `ch.N` and `ch.paths` are read — the operator is regenerated on
-the fly, never read from the tables.
+the fly, never read from the tables.  That is exact only when the tables are
+the closed form of the paths: channels from this package's build_ss_channel
+carry that guarantee; any other channel (built by the reference itself, or a
+dataclasses.replace copy such as oracle_check's perturbed fwd_coef,
+harness.py:368-369) has its tables compared with the closed form on the
+device first, and a channel whose tables differ is solved with the
+table-driven operator (ddb_ss_mvm_tables), exactly as the reference would.
 
 Precision: the drop-in defaults to the kernel's fp64 instantiation so the
 reference's own float64 tolerances hold; `set_precision("fp32")` switches it
@@ -70,6 +76,80 @@ def _solver(M: int, N: int, iterations: int, precision: str) -> SsCgaSolver:
     return s
 
 
+def _tables_canonical(ch) -> bool:
+    """True when ch's tables equal the closed form of ch.paths (indices exactly,
+    coefficients to 1e-9 relative): checked on the device (ddb_build_tables)."""
+    if getattr(ch, "canonical", False):
+        return True
+    from .sparse import _device_tables
+    if len(ch.paths) == 0:
+        return False
+    tabs = (ch.fwd_coef, ch.fwd_col, ch.herm_coef, ch.herm_row)
+    if any(np.shape(t) != (len(ch.paths), ch.M * ch.N) for t in tabs):
+        return False
+    fc, fi, hc, hi = _device_tables(ch.paths, int(ch.M), int(ch.N))
+    dev = fc.device
+    for ours, theirs in ((fi, ch.fwd_col), (hi, ch.herm_row)):
+        if not torch.equal(ours, torch.as_tensor(np.asarray(theirs, np.int32), device=dev)):
+            return False
+    for ours, theirs in ((fc, ch.fwd_coef), (hc, ch.herm_coef)):
+        t = torch.as_tensor(np.asarray(theirs, np.complex128), device=dev)
+        scale = max(float(torch.abs(ours).max()), 1e-300)
+        if float(torch.abs(ours - t).max()) > 1e-9 * scale:
+            return False
+    return True
+
+
+def _cga_tables(ch, y: np.ndarray, cfg):
+    """equalize.py:43-77 step for step on the device with the table-driven
+    products (ddb_ss_mvm_tables, sparse.py:147-160): the path for channels
+    whose tables are not the closed form of their paths."""
+    from .sparse import _checked_tables, _dev, _p, _stream
+    dev = _dev()
+    size = int(ch.M) * int(ch.N)
+    lib = nat.load()
+    fc, fi = (torch.as_tensor(np.ascontiguousarray(t), device=dev)
+              for t in _checked_tables(ch.fwd_coef, ch.fwd_col, size))
+    hc, hi = (torch.as_tensor(np.ascontiguousarray(t), device=dev)
+              for t in _checked_tables(ch.herm_coef, ch.herm_row, size))
+    fc, hc = fc.to(torch.complex128), hc.to(torch.complex128)
+    fi, hi = fi.to(torch.int32), hi.to(torch.int32)
+
+    def mvm(coef, idx, v):
+        out = torch.empty(size, dtype=torch.complex128, device=dev)
+        nat.check(lib.ddb_ss_mvm_tables(size, int(coef.shape[0]), _p(coef), _p(idx), _p(v), _p(out), _stream()),
+                  "ddb_ss_mvm_tables")
+        return out
+
+    trace = CgaTrace()
+    b = mvm(hc, hi, torch.as_tensor(np.ascontiguousarray(y, np.complex128), device=dev))
+    trace.mvm_count = 1
+    x = torch.zeros(size, dtype=torch.complex128, device=dev)
+    c = b.clone()
+    p = b.clone()
+    c_norm = float(torch.vdot(c, c).real)
+    trace.c_norm.append(c_norm)
+    for _ in range(cfg.iterations):
+        ap = mvm(hc, hi, mvm(fc, fi, p))
+        trace.mvm_count += 2
+        if cfg.lam:
+            ap = ap + cfg.lam * p
+        denom = float(torch.vdot(p, ap).real)
+        if denom == 0.0:
+            trace.exact_converged = True
+            break
+        alpha = c_norm / denom
+        x = x + alpha * p
+        c = c - alpha * ap
+        new_norm = float(torch.vdot(c, c).real)
+        p = c + (new_norm / c_norm) * p
+        c_norm = new_norm
+        trace.c_norm.append(c_norm)
+        if cfg.profile:
+            trace.snapshots.append(x.cpu().numpy().copy())
+    return x.cpu().numpy(), trace
+
+
 def cga_equalize(ch, y_dd, cfg):
     """Run cfg.iterations CG steps on (H^H H + lam I) x = H^H y (equalize.py:43-77)."""
     if cfg.iterations < 1:
@@ -80,6 +160,8 @@ def cga_equalize(ch, y_dd, cfg):
     y = np.asarray(y_dd)
     if y.shape != (M * N,):
         raise ValueError(f"vector length {y.shape} != {M * N}")
+    if not _tables_canonical(ch):
+        return _cga_tables(ch, y, cfg)
     s = _solver(M, N, int(cfg.iterations), _PRECISION)
     dev = s.device
     yt = torch.as_tensor(np.ascontiguousarray(y, dtype=np.complex128), device=dev).to(s.cdtype).reshape(1, -1)

@@ -16,7 +16,7 @@ numeric step runs in the ddb CUDA library:
 from __future__ import annotations
 
 import ctypes as C
-from dataclasses import dataclass
+from dataclasses import dataclass, field
 
 import numpy as np
 import torch
@@ -54,6 +54,10 @@ class StructuredSparseChannel:
     fwd_col: np.ndarray
     herm_coef: np.ndarray
     herm_row: np.ndarray
+    # set by build_ss_channel only: the tables are the closed form of `paths`,
+    # so the fused solve may regenerate them on the fly.  dataclasses.replace
+    # (e.g. oracle_check's perturbed fwd_coef, harness.py:368-369) resets it.
+    canonical: bool = field(default=False, init=False, repr=False, compare=False)
 
     @property
     def P(self):
@@ -135,11 +139,31 @@ def build_ss_channel(paths, cfg):
     if len(paths) == 0:
         raise EmptyChannel("no taps above threshold")
     fc, fi, hc, hi = _device_tables(paths, cfg.M, cfg.N)
-    return StructuredSparseChannel(
+    ch = StructuredSparseChannel(
         M=cfg.M, N=cfg.N, paths=tuple(paths),
         fwd_coef=fc.cpu().numpy(), fwd_col=fi.cpu().numpy(),
         herm_coef=hc.cpu().numpy(), herm_row=hi.cpu().numpy(),
     )
+    object.__setattr__(ch, "canonical", True)
+    return ch
+
+
+def _checked_tables(coef, index, size):
+    """The reference's einsum("pq,pq->q", coef, v[index]) semantics on the host
+    side of the boundary: matching (P, size) shapes (ValueError otherwise),
+    numpy's negative-index wrap and IndexError outside [-size, size)."""
+    c = np.asarray(coef)
+    i = np.asarray(index)
+    if c.ndim != 2 or i.shape != c.shape or c.shape[1] != size:
+        raise ValueError(f"table shapes {c.shape} / {i.shape} do not match (P, {size})")
+    if not np.issubdtype(i.dtype, np.integer):
+        raise IndexError("arrays used as indices must be of integer type")
+    if i.size and (i.min() < -size or i.max() >= size):
+        bad = int(i.max()) if i.max() >= size else int(i.min())
+        raise IndexError(f"index {bad} is out of bounds for axis 0 with size {size}")
+    if i.size and i.min() < 0:
+        i = np.where(i < 0, i + size, i)
+    return c, i
 
 
 def _mvm_tables(coef, index, v, size):
@@ -147,6 +171,7 @@ def _mvm_tables(coef, index, v, size):
     v = np.asarray(v)
     if v.shape != (size,):
         raise ValueError(f"vector length {v.shape} != {size}")
+    coef, index = _checked_tables(coef, index, size)
     c = torch.as_tensor(np.ascontiguousarray(coef, dtype=np.complex128), device=dev)
     i = torch.as_tensor(np.ascontiguousarray(index, dtype=np.int32), device=dev)
     vv = torch.as_tensor(np.ascontiguousarray(v, dtype=np.complex128), device=dev)
