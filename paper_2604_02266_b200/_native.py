@@ -144,7 +144,13 @@ def load(build_if_missing: bool = False):
         return lib
 
 
+# per-entry-point call counts (status checks), so a run through the patcher can
+# show which kernels the reference's code actually reached (pytest_plugin)
+CALLS: dict = {}
+
+
 def check(status: int, where: str) -> None:
+    CALLS[where] = CALLS.get(where, 0) + 1
     if status != DDB_OK:
         msg = load().ddb_last_error().decode(errors="replace")
         raise DdbError(status, where, msg)

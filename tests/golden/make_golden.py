@@ -435,6 +435,34 @@ def dense_fixture(d):
     np.savez_compressed(OUT / "dense.npz", **out)
 
 
+def sweep_fixture(d):
+    """Config 5 (BASELINE.json configs[4]): SNR 0..30 dB in 5 dB steps, 64
+    run_packet packets per SNR at (512, 32), 16-QAM (tests/golden/ref_sweep.py).
+    Stores the reference's compact per-packet results -- taps, bit errors on
+    the fp64 frame and on its complex64 rounding, residual traces -- so the GPU
+    box's own reference run is checked against this container's."""
+    sys.path.insert(0, str(OUT))
+    import ref_sweep as rs
+    res = rs.run_all([str(REF)], keep_frames=False)
+    keys = sorted(res)
+    taps = [res[k] for k in keys]
+    off = np.concatenate([[0], np.cumsum([t["P"] for t in taps])]).astype(np.int32)
+    np.savez_compressed(
+        OUT / "sweep_cfg5.npz",
+        meta=np.array([rs.M, rs.N, rs.ITERS, rs.SEED, rs.PACKETS], np.int64),
+        snr=np.array([k[0] for k in keys]), idx=np.array([k[1] for k in keys], np.int32),
+        path_off=off,
+        path_k=np.concatenate([t["tap_k"] for t in taps]).astype(np.int32),
+        path_l=np.concatenate([t["tap_l"] for t in taps]).astype(np.int32),
+        path_g=np.concatenate([t["tap_g"] for t in taps]),
+        errors=np.array([t["errors"] for t in taps], np.int64),
+        errors32=np.array([t["errors32"] for t in taps], np.int64),
+        failed=np.array([t["failed"] for t in taps], bool),
+        c_norm=np.stack([t["c_norm"] for t in taps]),
+        c_norm32=np.stack([t["c_norm32"] for t in taps]),
+    )
+
+
 def main():
     d = _ref()
     if len(sys.argv) > 1:  # regenerate selected fixtures only, e.g. `make_golden.py frontend`
@@ -450,6 +478,7 @@ def main():
     harness_fixture(d)
     channel_fixture(d)
     dense_fixture(d)
+    sweep_fixture(d)
     for p in sorted(OUT.glob("*.npz")):
         print(f"{p.name:24s} {p.stat().st_size / 1024:8.1f} KiB")
 
