@@ -1202,3 +1202,56 @@ def test_criterion5_noiseless_identity_loopback(pkg, M, N, mod):
     errs, status = _device_run_packets(pkg, M, N, float("inf"), 0.0, 0.08, 10, 0, mod=mod, pset=ident,
                                        per_packet=True)
     assert int(errs.sum()) == 0 and not (status & 1).any()
+
+
+# ---------------------------------------------------------------- fused demod epilogue vs the oracle
+@pytest.mark.parametrize("case", ["cfg4_qam64", "cfg3_qam64", "cfg1_qpsk", "cfg3_qam16"])
+def test_fused_epilogue_labels_and_llr_magnitudes(pkg, case, fp32_kernel):
+    """The fused epilogue's hard labels and max-log LLR *values* (not only their
+    signs) against the oracle's demod (orc.hard_demod / orc.llr_maxlog with
+    noise_var = lam) of (a) the device's own x_hat -- a pure demod check at
+    1e-4 -- and (b) the oracle's x_hat, labels outside the tie band.  64-QAM
+    frames are transmitted with 64-QAM symbols through the fixture's channel
+    (oracle forward operator + AWGN), so the epi_pass<3> branch
+    (csrc/sscga_tm.cu) runs on equalized 64-QAM data."""
+    name, mod = {"cfg4_qam64": ("frames_cfg4", "qam64"), "cfg3_qam64": ("frames_cfg3", "qam64"),
+                 "cfg1_qpsk": ("frames_cfg1", "qpsk"), "cfg3_qam16": ("frames_cfg3", "qam16")}[case]
+    d = load_golden(name)
+    M, N, iters, _ = (int(v) for v in d["meta"])
+    const = orc.qam(mod)
+    b = int(np.log2(len(const.points)))
+    rng = np.random.default_rng(64 + M)
+    B = d["y"].shape[0]
+    ys, txs = [], []
+    for f in range(B):
+        lab = rng.integers(0, len(const.points), size=M * N)
+        t = orc.build_tables(frame_taps(d, f), M, N)
+        yv = orc.forward(t, const.points[lab])
+        sig = float(np.mean(np.abs(yv) ** 2))
+        yv = yv + np.sqrt(sig * float(d["lam"][f]) / 2) * (rng.normal(size=M * N) + 1j * rng.normal(size=M * N))
+        ys.append(yv.astype(np.complex64))
+        txs.append(lab.astype(np.uint8))
+    s = solver_for(pkg, M, N, iters, "fp32", b)
+    paths = paths_from_fixture(pkg, d, s.cdtype)
+    res = s.solve(torch.as_tensor(np.stack(ys), device="cuda"), paths, torch.as_tensor(d["lam"]),
+                  tx_labels=torch.as_tensor(np.stack(txs), device="cuda"), llr=True)
+    torch.cuda.synchronize()
+    x = res.x.cpu().numpy()
+    labels = res.labels.cpu().numpy()
+    llr = res.llr.cpu().numpy()
+    for f in range(B):
+        lam = float(d["lam"][f])
+        xd = x[f].astype(np.complex128)
+        want_lab, _ = orc.hard_demod(xd, const)
+        mism = labels[f] != want_lab
+        assert np.all(orc.decision_margin(xd, const)[mism] < TIE_BAND)
+        want = orc.llr_maxlog(xd, const, lam)
+        np.testing.assert_allclose(llr[f], want, rtol=1e-4, atol=1e-4 * float(np.abs(want).max()))
+        xo, _, lab_o, _ = orc.receive(frame_taps(d, f), ys[f].astype(np.complex128), M, N, iters, lam, const)
+        assert rel_l2(xd, xo) < REL_L2_FP32
+        mism = labels[f] != lab_o
+        assert np.all(orc.decision_margin(xo, const)[mism] < TIE_BAND)
+        lo = orc.llr_maxlog(xo, const, lam)
+        assert float(np.abs(llr[f] - lo).max()) <= 1e-3 * float(np.abs(lo).max())
+        errs = int(np.unpackbits((labels[f] ^ txs[f])[:, None], axis=1).sum())
+        assert int(res.bit_errors[f]) == errs
