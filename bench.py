@@ -528,7 +528,8 @@ def main():
             b.record()
         torch.cuda.synchronize()
         lat = sorted(a.elapsed_time(b) for a, b in ev)
-        n_clu = max(1, sms // max(1, s.plan()["cluster"]))  # persistent clusters (1 CTA per SM)
+        pl = s.plan()  # persistent clusters: ctas_per_sm frames-slices per SM (measured TMEM residency)
+        n_clu = max(1, sms * max(1, pl["ctas_per_sm"]) // max(1, pl["cluster"]))
         latency = {"p50_ms": lat[len(lat) // 2], "p99_ms": lat[int(len(lat) * 0.99)],
                    "p999_ms": lat[int(len(lat) * 0.999)],
                    "max_ms": lat[-1], "runs": len(lat), "frame_duration_ms": 1e3 * N / 30e3,

@@ -54,8 +54,14 @@ int smem_optin() {
 // TMEM-operand kernel (sscga_tm.cu, fp32): 128 TMEM lanes = Lcta columns x
 // S segments of G = M / S delay rows, G <= 64 so that c | u | p | x fit the
 // 512 lane columns; WQ warps per lane quarter, R = G / WQ rows per thread.
-// Smallest cluster that fits, most warps first; the extended column-major
-// slices of c and u take the rest of shared memory as halo (up to M rows).
+// The smallest cluster that fits (largest segment G: most d_l = 0 taps read
+// TMEM); then the WQ that puts the most frames on an SM.  tcgen05 CTAs do
+// co-reside (tools/ubench/resident.cu: 2 x 256 or 4 x 128 TMEM columns per
+// SM) although the occupancy API reports 1, so a CTA of 128 or 256 threads
+// whose shared memory is capped to its share of the SM runs 2-4 frames per SM
+// (cfg1 5.4 -> 12.9, cfg2 13.0 -> 15.8 G symbols/s, profiles/r2_residency.md).
+// Ties keep the larger CTA.  The halo then takes the rest of the CTA's share
+// (at least min(M, 64) rows: the Veh-A delay spread is <= 39 bins at M = 512).
 bool make_plan_tm(int32_t M, int32_t N, ddb::LaunchShape* s) {
   const char* env_k = getenv("DDB_KERNEL");
   if (env_k && env_k[0] == 'r') return false;  // DDB_KERNEL=row: force the row-slice kernel
@@ -65,6 +71,8 @@ bool make_plan_tm(int32_t M, int32_t N, ddb::LaunchShape* s) {
   ddb::twiddle_split(M * N, &TL, &TH);
   const int hmin = M < 64 ? M : 64;
   const char* env_c = getenv("DDB_PLAN_C");
+  const char* env_wq = getenv("DDB_PLAN_WQ");
+  const char* env_cap = getenv("DDB_PLAN_SMEM_CAP");
   const int cmin = env_c ? atoi(env_c) : 1;
   for (int C = 1; C <= 16; C *= 2) {
     if (N % C || C < cmin) continue;
@@ -74,19 +82,34 @@ bool make_plan_tm(int32_t M, int32_t N, ddb::LaunchShape* s) {
     if (M % S) continue;
     const int G = M / S;
     if (G > 64 || G % 2) continue;
-    int wq = 0, R = 0;
-    const char* env_wq = getenv("DDB_PLAN_WQ");
-    for (int w = 4; w >= 1; w /= 2) {
-      if (G % w || (env_wq && atoi(env_wq) != w)) continue;
-      const int r = G / w;
-      if (r == 4 || r == 8 || r == 16) { wq = w; R = r; break; }
-    }
-    if (!wq) continue;
     auto cs_of = [&](int h) { int cs = M + 2 * h + 2; return cs % 4 == 2 ? cs : cs + 2; };
     auto smem_of = [&](int h) { return ddb::sscga_tm_layout(M, lcta, N, cs_of(h), TL, TH, pcap).total; };
     if (smem_of(hmin) > (size_t)cap) continue;
-    int h = M;
-    while (h > hmin && smem_of(h) > (size_t)cap) h -= 2;
+    int tc = 32;
+    while (tc < 8 * G) tc *= 2;
+    int best_wq = 0, best_n = 0, best_h = 0;
+    for (int w = 4; w >= 1; w /= 2) {
+      if (G % w || (env_wq && atoi(env_wq) != w)) continue;
+      const int r = G / w;
+      if (r != 4 && r != 8 && r != 16) continue;
+      const int threads = 128 * w;
+      // frames per SM: TMEM columns, threads (<= 128 registers each), shared memory
+      int n = 512 / tc;
+      if (65536 / (threads * 128) < n) n = 65536 / (threads * 128);
+      int share = 0, h = 0;
+      for (; n >= 1; --n) {
+        share = 233472 / n - 1024;  // 228 KiB per SM, 1 KiB reserved per CTA
+        if (share > cap) share = cap;
+        if (env_cap && atoi(env_cap) < share) share = atoi(env_cap);
+        if (smem_of(hmin) <= (size_t)share) break;
+      }
+      if (n < 1) continue;
+      h = M;
+      while (h > hmin && smem_of(h) > (size_t)share) h -= 2;
+      if (n > best_n) { best_n = n; best_wq = w; best_h = h; }
+    }
+    if (!best_wq) continue;
+    int h = best_h;
     if (const char* env_h = getenv("DDB_PLAN_H")) h = h < atoi(env_h) ? h : atoi(env_h);
     h &= ~1;
     s->kind = 1;
@@ -94,29 +117,21 @@ bool make_plan_tm(int32_t M, int32_t N, ddb::LaunchShape* s) {
     s->lcta = lcta;
     s->lc = 1;
     s->g = G;
-    s->wq = wq;
-    s->rows = R;
-    s->threads = 128 * wq;
+    s->wq = best_wq;
+    s->rows = G / best_wq;
+    s->threads = 128 * best_wq;
     s->halo = h;
     s->cs = cs_of(h);
     s->tl = TL;
     s->th = TH;
     s->pcap = pcap;
-    int tc = 32;
-    while (tc < 8 * G) tc *= 2;
     s->tcols = tc;
+    s->smem = (int)smem_of(h);
     // keep (CTAs per SM) x (TMEM columns per CTA) <= 512 so tcgen05.alloc never
-    // waits on a co-resident CTA (228 KiB per SM, 1 KiB reserved per CTA)
+    // waits on a co-resident CTA: pad the shared memory of small CTAs
     const int max_ctas = 512 / tc;
     int floor_smem = 233472 / (max_ctas + 1) - 1024 + 16;
     if (floor_smem > cap) floor_smem = cap;
-    s->smem = (int)smem_of(h);
-    if (const char* env_h = getenv("DDB_PLAN_SMEM_CAP")) {  // tuning: cap the halo so more CTAs fit
-      while (h > hmin && smem_of(h) > (size_t)atoi(env_h)) h -= 2;
-      s->halo = h;
-      s->cs = cs_of(h);
-      s->smem = (int)smem_of(h);
-    }
     if (s->smem < floor_smem) s->smem = floor_smem;
     return true;
   }

@@ -31,6 +31,7 @@
 // CG step (u-recurrence, two cluster barriers per iteration) and the
 // deterministic reductions are those of sscga.cu.
 #include <climits>
+#include <cstdlib>
 
 #include "cg.cuh"
 #include "common.cuh"
@@ -862,17 +863,35 @@ __global__ void __launch_bounds__(MAXT, 1) sscga_tm_kernel(const SolveArgs a) {
   if (warp == 0) tmem_dealloc(tbase, (uint32_t)a.tcols);
 }
 
+// CTAs of this kernel one SM really holds.  The occupancy API reports 1 for any
+// kernel that issues tcgen05.alloc, but the hardware co-schedules such CTAs as
+// long as shared memory, registers, threads and TMEM columns allow
+// (tools/ubench/resident.cu, profiles/r2_resident.txt: two 256-column CTAs per
+// SM, three 128-column ones).  DDB_TM_CTAS_PER_SM overrides (A/B runs).
+inline int tm_hw_ctas_per_sm(const LaunchShape& s, int regs) {
+  if (const char* env = getenv("DDB_TM_CTAS_PER_SM")) return atoi(env) > 0 ? atoi(env) : 1;
+  int n = 512 / (s.tcols > 32 ? s.tcols : 32);                     // TMEM columns
+  const int by_smem = 233472 / (s.smem + 1024);                     // 228 KiB, 1 KiB reserved per CTA
+  const int warp_regs = ((regs > 0 ? regs : 128) * 32 + 255) / 256 * 256;
+  const int by_regs = 65536 / (warp_regs * (s.threads / 32));
+  const int by_thr = 2048 / s.threads;
+  n = n < by_smem ? n : by_smem;
+  n = n < by_regs ? n : by_regs;
+  n = n < by_thr ? n : by_thr;
+  return n > 0 ? n : 1;
+}
+
+// Attribute setting, the cluster-occupancy query and the residency computation
+// run once per (kernel, shared memory, threads, cluster, device): the host time
+// of a launch is part of the batch-1 latency.
+struct TmOcc {
+  const void* fn;
+  int smem, threads, cluster, dev, clusters;
+};
+
 template <int R, int MAXT, bool PROF = false>
 cudaError_t launch_r(SolveArgs a, const LaunchShape& s, cudaStream_t st) {
   auto kern = sscga_tm_kernel<R, MAXT, PROF>;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, s.smem);
-  if (e != cudaSuccess) return e;
-  e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-  if (e != cudaSuccess) return e;
-  if (s.cluster > 8) {
-    e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-    if (e != cudaSuccess) return e;
-  }
   cudaLaunchConfig_t cfg = {};
   cfg.blockDim = dim3(s.threads);
   cfg.dynamicSmemBytes = s.smem;
@@ -884,11 +903,41 @@ cudaError_t launch_r(SolveArgs a, const LaunchShape& s, cudaStream_t st) {
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  cfg.gridDim = dim3(s.cluster);
-  int max_clusters = 0;
-  e = cudaOccupancyMaxActiveClusters(&max_clusters, kern, &cfg);
+  static thread_local TmOcc cache[4] = {};
+  static thread_local int next = 0;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
   if (e != cudaSuccess) return e;
-  if (max_clusters < 1) return cudaErrorInvalidConfiguration;
+  int max_clusters = 0;
+  for (const TmOcc& c : cache)
+    if (c.fn == (const void*)kern && c.smem == s.smem && c.threads == s.threads && c.cluster == s.cluster && c.dev == dev)
+      max_clusters = c.clusters;
+  if (max_clusters == 0) {
+    e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, s.smem);
+    if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    if (e != cudaSuccess) return e;
+    if (s.cluster > 8) {
+      e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+      if (e != cudaSuccess) return e;
+    }
+    cfg.gridDim = dim3(s.cluster);
+    int api = 0, api_per_sm = 0;
+    e = cudaOccupancyMaxActiveClusters(&api, kern, &cfg);
+    if (e != cudaSuccess) return e;
+    if (api < 1) return cudaErrorInvalidConfiguration;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&api_per_sm, kern, s.threads, s.smem);
+    if (e != cudaSuccess) return e;
+    cudaFuncAttributes fa;
+    e = cudaFuncGetAttributes(&fa, kern);
+    if (e != cudaSuccess) return e;
+    const int hw = tm_hw_ctas_per_sm(s, fa.numRegs);
+    // the API's cluster count assumes its own per-SM figure; scale it to the
+    // measured residency (persistent grid: every cluster is resident at once)
+    max_clusters = hw > api_per_sm && api_per_sm > 0 ? api * hw / api_per_sm : api;
+    cache[next] = TmOcc{(const void*)kern, s.smem, s.threads, s.cluster, dev, max_clusters};
+    next = (next + 1) % 4;
+  }
   const int nclu = a.B < max_clusters ? a.B : max_clusters;
   a.n_clusters = nclu;
   cfg.gridDim = dim3(nclu * s.cluster);
@@ -900,9 +949,11 @@ cudaError_t occ_r(const LaunchShape& s, int* n) {
   auto kern = sscga_tm_kernel<R, MAXT, false>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, s.smem);
   if (e != cudaSuccess) return e;
-  e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+  cudaFuncAttributes fa;
+  e = cudaFuncGetAttributes(&fa, kern);
   if (e != cudaSuccess) return e;
-  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(n, kern, s.threads, s.smem);
+  *n = tm_hw_ctas_per_sm(s, fa.numRegs);  // measured residency, not the API's 1
+  return cudaSuccess;
 }
 
 }  // namespace

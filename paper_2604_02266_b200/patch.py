@@ -24,11 +24,18 @@ device too: ddlink.zak.idzt / ddlink.harness.idzt (bound
 by name, harness.py:24) and ddlink.channel.apply_channel (called through the
 module, harness.py:146-148), fp64 to rounding.  add_awgn keeps the caller's
 numpy generator, so seeded runs draw the reference's noise.
+
+run_packets with workers > 1 (harness.py:217-232) uses a process pool.  A
+forked child cannot use the parent's CUDA context, so the pool is rebound to a
+spawn-context pool whose workers install this same patch before their first
+packet: every worker runs on the device too.
 """
 
 from __future__ import annotations
 
+import concurrent.futures as _cf
 import importlib
+import multiprocessing as _mp
 
 from . import channel as _ch
 from . import dense as _dn
@@ -40,6 +47,23 @@ from . import zak as _zk
 
 _SPARSE = ("detect_paths", "build_ss_channel", "ss_mvm", "ss_mvm_hermitian",
            "forward_index", "inverse_index", "coefficient")
+
+
+def _worker_init(modname: str, precision: str, synthesis: bool) -> None:
+    install(importlib.import_module(modname), precision=precision, synthesis=synthesis)
+
+
+def _spawn_pool(modname: str, precision: str, synthesis: bool):
+    """ProcessPoolExecutor factory for harness.run_packets: spawned workers
+    (CUDA cannot be re-initialised in a forked child), each patched on start."""
+
+    def make(max_workers=None, **kw):
+        kw.setdefault("mp_context", _mp.get_context("spawn"))
+        kw.setdefault("initializer", _worker_init)
+        kw.setdefault("initargs", (modname, precision, synthesis))
+        return _cf.ProcessPoolExecutor(max_workers=max_workers, **kw)
+
+    return make
 
 
 def install(ddlink_module=None, precision: str = "fp64", synthesis: bool = False) -> dict:
@@ -79,6 +103,8 @@ def install(ddlink_module=None, precision: str = "fp64", synthesis: bool = False
     for mod in (equalize, harness, d):
         if hasattr(mod, "lmmse_equalize"):
             bind(mod, "lmmse_equalize", _dn.lmmse_equalize)
+    if hasattr(harness, "ProcessPoolExecutor"):
+        bind(harness, "ProcessPoolExecutor", _spawn_pool(d.__name__, precision, synthesis))
     if synthesis:
         channel = importlib.import_module(d.__name__ + ".channel")
         for mod in (zak, harness, d):
