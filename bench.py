@@ -83,6 +83,12 @@ def parse():
     ap.add_argument("--e2e-depth", type=int, default=2)
     ap.add_argument("--lat-runs", type=int, default=2000)
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--scaling", choices=("weak", "strong"), default="weak",
+                    help="weak: every rank solves the config's batch; strong: the batch is split over the ranks "
+                         "(dist.shard)")
+    ap.add_argument("--precision", choices=("fp32", "fp64"), default="fp32",
+                    help="fp64 = the drop-in cga_equalize default (complex128, bit-identical decisions)")
+    ap.add_argument("--no-dropin", action="store_true", help="skip the drop-in cga_equalize per-call latency")
     return ap.parse_args()
 
 
@@ -206,50 +212,102 @@ def _solve_chunk(idx):
     import ddlink_oracle as orc
     frames, cfg, iters = _WORK
     const = orc.qam(cfg["mod"])
+    times = []
     for i in idx:
         taps, y, lam = frames[i % len(frames)]
+        t0 = time.perf_counter()
         orc.receive(taps, y, cfg["M"], cfg["N"], iters, lam, const)
-    return len(idx)
+        times.append(time.perf_counter() - t0)
+    return times
+
+
+def _solve_chunk_ref(idx):
+    """The unmodified reference (baseline/_ref ddlink): build_ss_channel ->
+    cga_equalize -> hard_demod per frame (harness.py:163, 189-194)."""
+    import numpy as np
+    from ddlink import grid as G, sparse as SP
+    from ddlink.equalize import CgaConfig, cga_equalize
+    frames, cfg, iters = _WORK
+    g = G.GridConfig(cfg["M"], cfg["N"], 30e3)
+    const = G.make_constellation(cfg["mod"])
+    times = []
+    for i in idx:
+        taps, y, lam = frames[i % len(frames)]
+        paths = [SP.DominantPath(t.k, t.l, t.gain) for t in taps]
+        t0 = time.perf_counter()
+        ch = SP.build_ss_channel(paths, g)
+        x, _ = cga_equalize(ch, np.asarray(y), CgaConfig(iterations=iters, lam=lam))
+        G.hard_demod(G.unflatten(x, g), const, g)
+        times.append(time.perf_counter() - t0)
+    return times
+
+
+def cpu_model() -> str:
+    try:
+        for line in Path("/proc/cpuinfo").read_text().splitlines():
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def have_reference() -> bool:
+    return (ROOT / "baseline" / "_ref" / "ddlink" / "__init__.py").exists()
 
 
 class CpuArm:
     """The reference hot path (build_ss_channel -> cga_equalize -> hard_demod)
-    in its numpy restatement, one process per host core like run_packets
-    (harness.py:217-232)."""
+    on the host cores, one process per core like run_packets (harness.py:217-232):
+    the unmodified reference from baseline/_ref when it is installed
+    (kind "reference"), else its numpy restatement (kind "port")."""
 
-    def __init__(self, cfg, snr_db, iters, seed=123):
+    def __init__(self, cfg, snr_db, iters, seed=123, prefer_reference=True):
         import multiprocessing as mp
         os.environ["OPENBLAS_NUM_THREADS"] = "1"
         os.environ["OMP_NUM_THREADS"] = "1"
         self.cores = len(os.sched_getaffinity(0))
         self.cfg, self.iters = cfg, iters
+        self.kind = "port"
+        self.fn = _solve_chunk
+        # the reference demodulates QPSK / 16-QAM only (grid.py:126-154); 64-QAM runs the port
+        if prefer_reference and have_reference() and cfg["mod"] in ("qpsk", "qam16"):
+            ref = str(ROOT / "baseline" / "_ref")
+            if ref not in sys.path:
+                sys.path.insert(0, ref)
+            try:
+                import ddlink  # noqa: F401
+                self.kind, self.fn = "reference", _solve_chunk_ref
+            except ImportError:
+                pass
         frames, _ = _cpu_frames(cfg, 8, snr_db, iters, seed)
         self.pool = mp.get_context("fork").Pool(self.cores, initializer=_init_worker,
                                                 initargs=(frames, cfg, iters))
-        self.pool.map(_solve_chunk, [[0]] * self.cores)  # warm every worker
-        t0 = time.perf_counter()
-        _single_thread_blas()
-        _solve_chunk_local(frames, cfg, iters, 2)
-        self.frame_s = (time.perf_counter() - t0) / 2
+        self.pool.map(self.fn, [[0]] * self.cores)  # warm every worker
+        _init_worker(frames, cfg, iters)
+        t = self.fn([0, 1])
+        self.frame_s = sum(t) / len(t)
+        self.frame_times = []
 
     def run(self, frames_total):
         per = max(1, frames_total // self.cores)
         chunks = [list(range(i * per, (i + 1) * per)) for i in range(self.cores)]
         t0 = time.perf_counter()
-        done = sum(self.pool.map(_solve_chunk, chunks))
+        parts = self.pool.map(self.fn, chunks)
         dt = time.perf_counter() - t0
-        return done, dt
+        times = [x for p in parts for x in p]
+        self.frame_times.extend(times)
+        return len(times), dt
+
+    def frame_stats(self) -> dict:
+        t = sorted(self.frame_times)
+        if not t:
+            return {}
+        return {"p50_frame_ms": 1e3 * t[len(t) // 2], "p99_frame_ms": 1e3 * t[min(len(t) - 1, int(len(t) * 0.99))],
+                "frames_timed": len(t)}
 
     def close(self):
         self.pool.terminate()
-
-
-def _solve_chunk_local(frames, cfg, iters, n):
-    import ddlink_oracle as orc
-    const = orc.qam(cfg["mod"])
-    for i in range(n):
-        taps, y, lam = frames[i % len(frames)]
-        orc.receive(taps, y, cfg["M"], cfg["N"], iters, lam, const)
 
 
 def sample_frames(arm, seconds):
@@ -267,25 +325,31 @@ def run_reference(args, cfg):
     per_step = max(arm.cores, int(min(args.cpu_seconds, 8.0) / arm.frame_s))
     for _ in range(args.warmup):
         arm.run(arm.cores)
+    arm.frame_times = []
     total_frames, total_t = 0, 0.0
     for _ in range(args.steps):
         n, dt = arm.run(per_step)
         total_frames += n
         total_t += dt
+    stats = arm.frame_stats()
     arm.close()
+    arm.frame_stats = lambda: stats  # noqa: E731 (pool closed; keep the sample's statistics)
     value = total_frames * MN / total_t
-    sample = (f"{per_step} frames per step (~{per_step * arm.frame_s:.1f} s CPU work), "
+    what = ("ddlink (baseline/_ref, unmodified) build_ss_channel -> cga_equalize -> hard_demod"
+            if arm.kind == "reference" else "numpy port of build_ss_channel -> cga_equalize -> hard_demod")
+    sample = (f"{per_step} frames per step (~{per_step * arm.frame_s:.1f} s CPU work) of {what}, "
               f"{arm.cores} processes, OPENBLAS_NUM_THREADS=1")
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "symbols/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": 1e3 * total_t / args.steps, "higher_is_better": True, "scaling": "weak",
+        "ms_per_step": 1e3 * total_t / args.steps, "higher_is_better": True, "scaling": args.scaling,
         "vs_baseline": None, "dtype": "fp64 (complex128)", "data": "synthetic (host numpy, Veh-A taps)",
         "config": _config_json(args, cfg),
-        "cpu_baseline": {"value": value, "unit": "symbols/s", "cores": arm.cores, "kind": "port",
-                         "sample": sample},
+        "cpu_baseline": {"value": value, "unit": "symbols/s", "cores": arm.cores, "kind": arm.kind,
+                         "sample": sample, "cpu_model": cpu_model(), **arm.frame_stats()},
         "e2e": {"value": value, "unit": "symbols/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-        "latency": {"p50_ms": 1e3 * arm.frame_s, "what": "single-core per-frame time of the port"},
+        "latency": {"p50_ms": arm.frame_stats().get("p50_frame_ms"), "p99_ms": arm.frame_stats().get("p99_frame_ms"),
+                    "what": "single-core per-frame time of the reference path"},
     }
     print(json.dumps(line), flush=True)
 
@@ -293,9 +357,11 @@ def run_reference(args, cfg):
 def _config_json(args, cfg):
     B = args.batch or cfg["batch"]
     ptxt = f"P={cfg['P']}" if cfg["P"] else f"P=detect_paths taps of {cfg['taps']}"
+    per = "frames/GPU" if args.scaling == "weak" else f"frames in all over {args.gpus} GPU(s)"
     return {"workload": f"{args.config}: OTFS M={cfg['M']} N={cfg['N']} {ptxt} {cfg['mod']} "
-                        f"batch {B} frames/GPU, Xi={args.iters}, {args.snr:g} dB",
-            "M": cfg["M"], "N": cfg["N"], "P": cfg["P"], "modulation": cfg["mod"], "batch_per_gpu": B,
+                        f"batch {B} {per}, Xi={args.iters}, {args.snr:g} dB, {args.precision}",
+            "M": cfg["M"], "N": cfg["N"], "P": cfg["P"], "modulation": cfg["mod"],
+            "batch_per_gpu": B if args.scaling == "weak" else -(-B // max(1, args.gpus)), "scaling": args.scaling,
             "iterations": args.iters, "snr_db": args.snr, "nu_max_hz": cfg["nu"],
             "parallelism": f"frame-sharded x{args.gpus}, no collective on the solve path",
             "l2": "inputs exceed L2 (y alone is batch*MN*8 B per GPU)"}
@@ -327,9 +393,14 @@ def main():
 
     M, N, P = cfg["M"], cfg["N"], (args.paths or cfg["P"])
     MN = M * N
-    B = args.batch or cfg["batch"]
+    B_job = args.batch or cfg["batch"]
+    if args.scaling == "strong":  # the job's batch split over the ranks, no collective
+        lo, hi = ddist.shard(B_job, rank, world)
+        B = hi - lo
+    else:
+        B = B_job
     bps = BPS[cfg["mod"]]
-    s = pkg.SsCgaSolver(M, N, args.iters, precision="fp32", modulation=cfg["mod"])
+    s = pkg.SsCgaSolver(M, N, args.iters, precision=args.precision, modulation=cfg["mod"])
     given = None
     if cfg.get("taps"):
         import numpy as np
@@ -362,9 +433,10 @@ def main():
     clocks = sampler.stop()
     ms = ddist.max_over_ranks(e0.elapsed_time(e1))
     ms_step = ms / args.steps
-    value = world * B * MN * args.steps / (ms * 1e-3)
+    frames_job = world * B if args.scaling == "weak" else B_job
+    value = frames_job * MN * args.steps / (ms * 1e-3)
     bit_errors = ddist.sum_over_ranks(int(out.bit_errors.sum().item()))
-    ber = bit_errors / (world * B * MN * bps)
+    ber = bit_errors / (frames_job * MN * bps)
 
     # ---- FP32 peak of this box (FFMA / FFMA2 probe), HBM peak from MEASURED_PEAKS
     scratch = torch.empty(148 * 8, dtype=torch.float32, device="cuda")
@@ -372,8 +444,8 @@ def main():
     lib = nat.load()
     peak_tflops = 0.0
     probe = {}
-    for mode in (0, 1):
-        blocks, iters = sms * 8, 2000
+    for mode in ((0, 1) if args.precision == "fp32" else (2,)):
+        blocks, iters = sms * 8, 2000 if mode < 2 else 200
         for _ in range(2):
             nat.check(lib.ddb_probe_fp32(mode, blocks, iters, C.c_void_p(scratch.data_ptr()),
                                          C.c_void_p(stream.cuda_stream)), "probe")
@@ -384,15 +456,21 @@ def main():
         b.record(stream)
         b.synchronize()
         tf = blocks * 256 * iters * 256 * 2 / (a.elapsed_time(b) * 1e-3) / 1e12
-        probe["ffma" if mode == 0 else "ffma2"] = tf
+        probe[("ffma", "ffma2", "dfma")[mode]] = tf
         peak_tflops = max(peak_tflops, tf)
     peaks_path = ROOT / "MEASURED_PEAKS.json"
     hbm_peak = json.loads(peaks_path.read_text())["hbm_gbs"] if peaks_path.exists() else 6650.0
     P_avg = float((fb.paths.offsets[-1] - fb.paths.offsets[0]).item()) / B
     fl = flops_per_frame(P_avg, MN, args.iters)
     achieved = B * fl / (ms_step * 1e-3) / 1e12
-    io_bytes = B * (8 * MN + 8 * MN + 4 * bps * MN + MN + MN + 16 * P_avg)  # y, x, llr, labels, tx, taps
-    hbm_gbs = io_bytes / (ms_step * 1e-3) / 1e9
+    eb = 8 if args.precision == "fp32" else 16  # complex element bytes
+    io_bytes = B * (eb * MN + eb * MN + 4 * bps * MN + MN + MN + 16 * P_avg)  # y, x, llr, labels, tx, taps
+    workspace = s.plan()["kernel"] == "workspace"
+    # workspace path: c, u, p stream through HBM every phase -- per iteration
+    # g_fwd reads c (gather), u, p and writes u, p; g_herm reads u (gather), p,
+    # x, c and writes x, c (11 vector passes); g_init reads y, writes c and x
+    ws_bytes = B * (11 * args.iters + 3) * eb * MN if workspace else 0
+    hbm_gbs = (io_bytes + ws_bytes) / (ms_step * 1e-3) / 1e9
     traffic = None
     ncu_sum = ROOT / "profiles" / f"ncu_{args.config}.json"
     if ncu_sum.exists():  # per-frame DRAM bytes of the committed ncu --set full capture, scaled to this launch
@@ -580,7 +658,7 @@ def main():
         h2d_peak = (1 << 29) / (a2.elapsed_time(b2) * 1e-3) / 1e9
         del probe_h, probe_d
         h2d_gbs = h2d / (ems / k2 * 1e-3) / 1e9
-        e2e = {"value": world * B * MN * k2 / (ems * 1e-3), "unit": "symbols/s", "h2d_bytes_per_step": h2d,
+        e2e = {"value": frames_job * MN * k2 / (ems * 1e-3), "unit": "symbols/s", "h2d_bytes_per_step": h2d,
                "d2h_bytes_per_step": d2h, "steps": k2, "ms_per_step": ems / k2,
                "pcie": {"h2d_gbs": h2d_gbs, "h2d_peak_gbs": h2d_peak, "frac": h2d_gbs / h2d_peak,
                         "peak_source": "one 512 MB pinned H2D copy on this box"},
@@ -594,25 +672,63 @@ def main():
         arm = CpuArm(cfg, args.snr, args.iters)
         n = sample_frames(arm, args.cpu_seconds)
         done, dt = arm.run(n)
+        stats = arm.frame_stats
         arm.close()
-        cpu = {"value": done * MN / dt, "unit": "symbols/s", "cores": arm.cores, "kind": "port",
-               "sample": f"{done} cfg frames (numpy oracle port of build_ss_channel->cga_equalize->"
-                         f"hard_demod), {arm.cores} processes, {dt:.1f} s wall",
-               "p50_frame_ms_1core": 1e3 * arm.frame_s}
+        cpu = {"value": done * MN / dt, "unit": "symbols/s", "cores": arm.cores, "kind": arm.kind,
+               "sample": f"{done} cfg frames ({'ddlink from baseline/_ref' if arm.kind == 'reference' else 'numpy port'}"
+                         f": build_ss_channel->cga_equalize->hard_demod), {arm.cores} processes, {dt:.1f} s wall",
+               "cpu_model": cpu_model(), **stats()}
+
+    roof_fp = {"bound": args.precision, "achieved": achieved, "peak": peak_tflops, "unit": "TFLOP/s",
+               "frac": achieved / peak_tflops, "traffic": None if workspace else traffic,
+               "flops_per_frame": fl, "peak_source": f"FMA probe on this GPU {probe}"}
+    roof_hbm = {"bound": "hbm", "achieved": hbm_gbs, "peak": hbm_peak, "unit": "GB/s",
+                "frac": hbm_gbs / hbm_peak, "traffic": traffic if workspace else None,
+                "bytes_per_frame": (io_bytes + ws_bytes) / B, "workspace_bytes_per_frame": ws_bytes / B,
+                "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks_path.exists() else "fallback"}
+
+    # ---- the drop-in a ddlink user calls: cga_equalize(ch, y, cfg) on numpy
+    #      arrays, one frame per call (host wall clock around the call)
+    dropin = None
+    if not args.no_dropin and rank == 0:
+        from paper_2604_02266_b200 import equalize as eqz
+        o0, o1 = int(fb.paths.offsets[0]), int(fb.paths.offsets[1])
+        taps = [pkg.DominantPath(int(k), int(l), complex(g)) for k, l, g in
+                zip(fb.paths.k[o0:o1].tolist(), fb.paths.l[o0:o1].tolist(), fb.paths.gain[o0:o1].cpu().numpy())]
+        ch = pkg.build_ss_channel(taps, pkg.GridConfig(M, N))
+        y0 = fb.y[0].cpu().numpy().astype(np.complex128)
+        ccfg = pkg.CgaConfig(iterations=args.iters, lam=float(fb.lam[0]))
+        dropin = {"what": "drop-in cga_equalize (numpy complex128 in/out, one frame per call, H2D + solve + "
+                          "D2H), host wall clock, median of 50 calls"}
+        prev = eqz.get_precision()
+        for prec in ("fp64", "fp32"):
+            eqz.set_precision(prec)
+            for _ in range(5):
+                eqz.cga_equalize(ch, y0, ccfg)
+            t = []
+            for _ in range(50):
+                t0 = time.perf_counter()
+                eqz.cga_equalize(ch, y0, ccfg)
+                t.append(time.perf_counter() - t0)
+            t.sort()
+            dropin[f"{prec}_p50_ms"] = 1e3 * t[len(t) // 2]
+            dropin[f"{prec}_p99_ms"] = 1e3 * t[-1]
+        eqz.set_precision(prev)
+        dropin["default_precision"] = prev
 
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "symbols/s", "n_gpus": world, "steps": args.steps,
             "warmup": max(3, args.warmup), "ms_per_step": ms_step, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "fp32",
+            "scaling": args.scaling, "vs_baseline": None, "dtype": args.precision,
             "data": "synthetic (device-generated Veh-A taps, uniform labels, y = Hx + AWGN)",
             "config": _config_json(args, cfg),
             "latency": latency,
-            "roofline": {"bound": "fp32", "achieved": achieved, "peak": peak_tflops, "unit": "TFLOP/s",
-                         "frac": achieved / peak_tflops, "traffic": traffic,
-                         "flops_per_frame": fl, "peak_source": f"FFMA probe on this GPU {probe}"},
-            "roofline_hbm": {"bound": "hbm", "achieved": hbm_gbs, "peak": hbm_peak, "unit": "GB/s",
-                             "frac": hbm_gbs / hbm_peak, "bytes_per_frame": io_bytes / B},
+            # the bound of the dominant kernel: the fused kernels keep the CG state on chip
+            # (FP32 / FP64 FMA bound); the workspace path streams it through HBM
+            "roofline": (roof_hbm if workspace else roof_fp),
+            ("roofline_fp" if workspace else "roofline_hbm"): (roof_fp if workspace else roof_hbm),
+            "dropin": dropin,
             "cpu_baseline": cpu,
             "e2e": e2e,
             "frontend": frontend,

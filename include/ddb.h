@@ -206,6 +206,23 @@ int32_t ddb_dzt(int32_t batch, int32_t M, int32_t N, int32_t dtype, const void* 
 int32_t ddb_estimate_heff(int64_t count, int32_t dtype, const void* y_dd, const void* twist, double amplitude,
                           void* heff, void* stream);
 
+/* ---- host-buffer round trips for one frame (the numpy drop-ins the
+ *      reference calls once per packet, harness.py:156-159): every pointer is
+ *      HOST memory (complex128 = interleaved double pairs); one call copies the
+ *      inputs into a per-thread device scratch, runs the kernel above and
+ *      copies the result back, with one stream synchronisation.  The
+ *      reference's receive path pays one such round trip per function.
+ *      ddb_host_dzt            zak.py:50-55   y [M*N] -> out (M, N) row-major;
+ *                                             kernel [N, N] or NULL (default)
+ *      ddb_host_estimate_heff  pilot.py:40-49 y_dd, twist [count] -> heff
+ *      ddb_host_detect_paths   sparse.py:69-88 heff (M, N) -> *count taps
+ *                                             (k, l, gain) ranked; capacity
+ *                                             max_paths (M*N returns all) */
+int32_t ddb_host_dzt(int32_t M, int32_t N, const void* y_time, const void* kernel, void* out);
+int32_t ddb_host_estimate_heff(int64_t count, const void* y_dd, const void* twist, double amplitude, void* heff);
+int32_t ddb_host_detect_paths(int32_t M, int32_t N, const void* heff, double theta, int32_t max_paths,
+                              int32_t* count, int32_t* path_k, int32_t* path_l, void* path_gain);
+
 /* ---- frame synthesis on the device: the transmit
  *      side and channel of one packet (harness.py:141-149) for a batch.
  *      ddb_modulate        grid.py:157-169  labels [count] (bits MSB first,
@@ -248,7 +265,8 @@ int32_t ddb_build_dense_hdd(int32_t batch, int32_t M, int32_t N, int32_t dtype, 
 /* ---- measurement helper (not a reference interface): FP32 FMA throughput
  *      probe used by bench.py to state the measured FP32 roofline.  Launches
  *      blocks x 256 threads, each doing iters x 256 FMAs (mode 0: FFMA,
- *      mode 1: packed FFMA2).  scratch: device float[blocks]. */
+ *      mode 1: packed FFMA2, mode 2: DFMA, the fp64 rate).  scratch: device
+ *      float[blocks]. */
 int32_t ddb_probe_fp32(int32_t mode, int32_t blocks, int32_t iters, float* scratch, void* stream);
 
 /* ---- measurement helper (not a reference interface): ddb_sscga_solve with

@@ -92,6 +92,10 @@ _SIGNATURES = {
                             C.c_double, C.c_void_p, C.c_void_p]),
     "ddb_estimate_heff": (C.c_int32, [C.c_int64, C.c_int32, C.c_void_p, C.c_void_p, C.c_double, C.c_void_p,
                                       C.c_void_p]),
+    "ddb_host_dzt": (C.c_int32, [C.c_int32, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p]),
+    "ddb_host_estimate_heff": (C.c_int32, [C.c_int64, C.c_void_p, C.c_void_p, C.c_double, C.c_void_p]),
+    "ddb_host_detect_paths": (C.c_int32, [C.c_int32, C.c_int32, C.c_void_p, C.c_double, C.c_int32, C.c_void_p,
+                                          C.c_void_p, C.c_void_p, C.c_void_p]),
     "ddb_paths_csr": (C.c_int32, [C.c_int32, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32,
                                   C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
     "ddb_modulate": (C.c_int32, [C.c_int64, C.c_int32, C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p]),

@@ -169,6 +169,129 @@ __device__ __forceinline__ double block_max(double v, double* scratch) {
   return v;
 }
 
+__device__ __forceinline__ int block_sum_int(int v, int* scratch) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (lane == 0) scratch[warp] = v;
+  __syncthreads();
+  int t = 0;
+  for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += scratch[w];
+  __syncthreads();
+  return t;
+}
+
+// Candidates beyond the shared-memory list (e.g. theta = 0 on a 131 K-bin
+// frame): the reference has no such limit (sparse.py:79-88), so the frame's
+// own output rows [f * max_paths, + k) serve as the list, k = min(total,
+// max_paths).  With truncation (total > max_paths) the k-th largest magnitude
+// T is found by bisection over the bit patterns of the non-negative doubles
+// (64 counting passes), and the list takes every bin above T plus the first
+// ties at T in row-major order -- exactly the first k of the stable descending
+// argsort.  The list (bin index in pk, |h| in ph.x) is then sorted in place by
+// (|h| descending, bin ascending), a total order, with a bitonic network whose
+// virtual padding beyond k never moves, and finally expanded to (k_p, l_p, h).
+__device__ __noinline__ void detect_overflow(int f, int M, int N, const double2* __restrict__ h, double thr,
+                                             double peak, int total, int max_paths, const double* mag, int* wcount,
+                                             int* count, int* pk, int* pl, double2* ph) {
+  const int n = M * N;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  __shared__ int iscratch[32];
+  auto magnitude = [&](int i) { return mag ? mag[i] : np_cabs(h[i].x, h[i].y); };
+  const int k = total < max_paths ? total : max_paths;
+  double tstar = thr;  // keep everything above thr (no truncation)
+  int ties = 0;        // bins equal to tstar taken, in row-major order
+  if (total > max_paths) {
+    unsigned long long lo = (unsigned long long)__double_as_longlong(thr) + 1ull;
+    unsigned long long hi = (unsigned long long)__double_as_longlong(peak);
+    while (lo < hi) {  // largest v with #{m >= v} >= k
+      const unsigned long long mid = lo + (hi - lo + 1ull) / 2ull;
+      const double v = __longlong_as_double((long long)mid);
+      int c = 0;
+      for (int i = threadIdx.x; i < n; i += blockDim.x) c += magnitude(i) >= v;
+      if (block_sum_int(c, iscratch) >= k) lo = mid;
+      else hi = mid - 1ull;
+    }
+    tstar = __longlong_as_double((long long)lo);
+    int c = 0;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) c += magnitude(i) > tstar;
+    ties = k - block_sum_int(c, iscratch);
+  }
+  // ordered emission (warp w walks bins [w S, (w + 1) S)): counts of bins above
+  // tstar and of ties per warp, then the emitting pass at the warp's prefixes
+  const int S = (n + nw - 1) / nw;
+  const int b0 = min(n, warp * S), b1 = min(n, b0 + S);
+  int cg = 0, ce = 0;
+  for (int base = b0; base < b1; base += 32) {
+    const int i = base + lane;
+    const double m = i < b1 ? magnitude(i) : -1.0;
+    cg += __popc(__ballot_sync(0xffffffffu, m > tstar));
+    ce += __popc(__ballot_sync(0xffffffffu, i < b1 && m == tstar && tstar > thr));
+  }
+  __shared__ int wc_eq[32];
+  if (lane == 0) { wcount[warp] = cg; wc_eq[warp] = ce; }
+  __syncthreads();
+  int pos_g = 0, pos_e = 0;
+  for (int w = 0; w < warp; ++w) { pos_g += wcount[w]; pos_e += wc_eq[w]; }
+  const size_t fo = (size_t)f * max_paths;
+  for (int base = b0; base < b1; base += 32) {
+    const int i = base + lane;
+    const double m = i < b1 ? magnitude(i) : -1.0;
+    const bool gt = m > tstar, eq = i < b1 && m == tstar && tstar > thr;
+    const unsigned bg = __ballot_sync(0xffffffffu, gt), be = __ballot_sync(0xffffffffu, eq);
+    const unsigned below = (1u << lane) - 1u;
+    const int er = pos_e + __popc(be & below);  // ties before bin i (row-major) = its tie rank
+    // position = bins above tstar before i + ties taken before i
+    const int p = pos_g + __popc(bg & below) + min(er, ties);
+    if ((gt || (eq && er < ties)) && p < k) {
+      pk[fo + p] = i;
+      ph[fo + p].x = m;
+    }
+    pos_g += __popc(bg);
+    pos_e += __popc(be);
+  }
+  __syncthreads();
+  // bitonic sort of [0, k): "before" = larger |h|, then smaller bin index
+  int p2 = 1;
+  while (p2 < k) p2 <<= 1;
+  auto before = [&](int a, int b) {
+    const double ma = ph[fo + a].x, mb = ph[fo + b].x;
+    return ma > mb || (ma == mb && pk[fo + a] < pk[fo + b]);
+  };
+  for (int size = 2; size <= p2; size <<= 1) {
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      for (int t = threadIdx.x; t < p2 / 2; t += blockDim.x) {
+        int i, j;
+        if (stride == size >> 1) {  // flip: i pairs with its mirror in the size-block
+          const int blk = t / stride, off = t - blk * stride;
+          i = blk * size + off;
+          j = blk * size + size - 1 - off;
+        } else {                    // half-cleaner
+          const int blk = t / stride, off = t - blk * stride;
+          i = blk * 2 * stride + off;
+          j = i + stride;
+        }
+        if (j < k && before(j, i)) {
+          const int ti = pk[fo + i];
+          pk[fo + i] = pk[fo + j];
+          pk[fo + j] = ti;
+          const double tm = ph[fo + i].x;
+          ph[fo + i].x = ph[fo + j].x;
+          ph[fo + j].x = tm;
+        }
+      }
+      __syncthreads();
+    }
+  }
+  for (int j = threadIdx.x; j < k; j += blockDim.x) {
+    const int ic = pk[fo + j];
+    pk[fo + j] = ic / N;
+    pl[fo + j] = ic - (ic / N) * N;
+    ph[fo + j] = h[ic];
+  }
+  if (threadIdx.x == 0) count[f] = total;
+}
+
 // |h| is evaluated once per bin into shared memory when the frame fits (else
 // re-read), candidates are compacted in row-major order with warp ballots over
 // coalesced bin ranges, then ranked.  One CTA handles frame f.
@@ -236,8 +359,11 @@ __device__ __forceinline__ void detect_frame(int f, int M, int N, const double2*
     pos += __popc(bal);
   }
   __syncthreads();
-  if (threadIdx.x == 0) count[f] = total > cap ? -1 : total;
-  if (total > cap) return;  // -1: candidate list exceeds shared memory; host reports it
+  if (total > cap) {  // more candidates than shared memory holds: rank them in the output rows
+    detect_overflow(f, M, N, h, thr, peak, total, max_paths, mag_smem ? mag : nullptr, wcount, count, pk, pl, ph);
+    return;
+  }
+  if (threadIdx.x == 0) count[f] = total;
   // descending |h|, ties in row-major order (argsort kind="stable")
   for (int c = threadIdx.x; c < total; c += blockDim.x) {
     const int ic = cidx[c];
@@ -583,8 +709,27 @@ __global__ void __launch_bounds__(256) fp32_probe_kernel(float* out, int iters, 
   if (s == 1234.5f) out[blockIdx.x] = s;  // keep the chains alive
 }
 
+// mode 2: the FP64 rate (DFMA chains), the roofline of the drop-in's default
+// complex128 solve.  Same work per thread: iters x 256 FMAs.
+__global__ void __launch_bounds__(256) fp64_probe_kernel(float* out, int iters, double m, double c) {
+  double a[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) a[i] = threadIdx.x * 1e-3 + i;
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int u = 0; u < 32; ++u)
+#pragma unroll
+      for (int i = 0; i < 8; ++i) a[i] = fma(a[i], m, c);
+  }
+  double s = 0.0;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) s += a[i];
+  if (s == 1234.5) out[blockIdx.x] = (float)s;
+}
+
 cudaError_t launch_fp32_probe(int mode, int blocks, int iters, float* out, cudaStream_t st) {
-  if (mode == 0) fp32_probe_kernel<0><<<blocks, 256, 0, st>>>(out, iters, 0.999f, 1e-3f);
+  if (mode == 2) fp64_probe_kernel<<<blocks, 256, 0, st>>>(out, iters, 0.999, 1e-3);
+  else if (mode == 0) fp32_probe_kernel<0><<<blocks, 256, 0, st>>>(out, iters, 0.999f, 1e-3f);
   else fp32_probe_kernel<1><<<blocks, 256, 0, st>>>(out, iters, 0.999f, 1e-3f);
   return cudaGetLastError();
 }

@@ -499,6 +499,112 @@ int32_t ddb_dzt(int32_t batch, int32_t M, int32_t N, int32_t dtype, const void* 
   return ok();
 }
 
+// ---- host round trips: a per-thread, per-device scratch and stream
+namespace {
+struct HostScratch {
+  int dev = -1;
+  cudaStream_t st = nullptr;
+  void* buf = nullptr;
+  size_t cap = 0;
+};
+thread_local HostScratch g_hs;
+
+// Device scratch of at least `bytes` on the current device (grown, never shrunk).
+cudaError_t host_scratch(size_t bytes, unsigned char** out, cudaStream_t* st) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  if (g_hs.dev != dev) {  // a new device for this thread: the old scratch stays with its device
+    g_hs = HostScratch{};
+    g_hs.dev = dev;
+    if ((e = cudaStreamCreateWithFlags(&g_hs.st, cudaStreamNonBlocking)) != cudaSuccess) return e;
+  }
+  if (g_hs.cap < bytes) {
+    if (g_hs.buf) cudaFree(g_hs.buf);
+    g_hs.buf = nullptr;
+    g_hs.cap = 0;
+    size_t cap = 1 << 16;
+    while (cap < bytes) cap <<= 1;
+    if ((e = cudaMalloc(&g_hs.buf, cap)) != cudaSuccess) return e;
+    g_hs.cap = cap;
+  }
+  *out = static_cast<unsigned char*>(g_hs.buf);
+  *st = g_hs.st;
+  return cudaSuccess;
+}
+inline size_t al256(size_t v) { return (v + 255) & ~size_t(255); }
+}  // namespace
+
+int32_t ddb_host_dzt(int32_t M, int32_t N, const void* y_time, const void* kernel, void* out) {
+  if (M < 1 || N < 1 || !y_time || !out) return fail(DDB_ERR_INVALID, "bad host dzt arguments");
+  const size_t n = (size_t)M * N * 16, nk = kernel ? (size_t)N * N * 16 : 0;
+  unsigned char* d;
+  cudaStream_t st;
+  cudaError_t e = host_scratch(2 * al256(n) + al256(nk), &d, &st);
+  if (e != cudaSuccess) return cuda_fail(e, "host scratch");
+  unsigned char *dy = d, *dout = d + al256(n), *dk = kernel ? d + 2 * al256(n) : nullptr;
+  if ((e = cudaMemcpyAsync(dy, y_time, n, cudaMemcpyHostToDevice, st)) != cudaSuccess) return cuda_fail(e, "H2D");
+  if (kernel && (e = cudaMemcpyAsync(dk, kernel, nk, cudaMemcpyHostToDevice, st)) != cudaSuccess)
+    return cuda_fail(e, "H2D");
+  int32_t r = ddb_dzt(1, M, N, DDB_F64, dy, dk, 0, 1.0, dout, st);
+  if (r) return r;
+  if ((e = cudaMemcpyAsync(out, dout, n, cudaMemcpyDeviceToHost, st)) != cudaSuccess) return cuda_fail(e, "D2H");
+  if ((e = cudaStreamSynchronize(st)) != cudaSuccess) return cuda_fail(e, "host dzt");
+  return ok();
+}
+
+int32_t ddb_host_estimate_heff(int64_t count, const void* y_dd, const void* twist, double amplitude, void* heff) {
+  if (count < 0 || (count && (!y_dd || !twist || !heff))) return fail(DDB_ERR_INVALID, "bad host estimate arguments");
+  if (!(amplitude > 0)) return fail(DDB_ERR_INVALID, "pilot amplitude must be positive");  // pilot.py:45-46
+  if (count == 0) return ok();
+  const size_t n = (size_t)count * 16;
+  unsigned char* d;
+  cudaStream_t st;
+  cudaError_t e = host_scratch(3 * al256(n), &d, &st);
+  if (e != cudaSuccess) return cuda_fail(e, "host scratch");
+  unsigned char *dy = d, *dt = d + al256(n), *dh = d + 2 * al256(n);
+  if ((e = cudaMemcpyAsync(dy, y_dd, n, cudaMemcpyHostToDevice, st)) != cudaSuccess) return cuda_fail(e, "H2D");
+  if ((e = cudaMemcpyAsync(dt, twist, n, cudaMemcpyHostToDevice, st)) != cudaSuccess) return cuda_fail(e, "H2D");
+  int32_t r = ddb_estimate_heff(count, DDB_F64, dy, dt, amplitude, dh, st);
+  if (r) return r;
+  if ((e = cudaMemcpyAsync(heff, dh, n, cudaMemcpyDeviceToHost, st)) != cudaSuccess) return cuda_fail(e, "D2H");
+  if ((e = cudaStreamSynchronize(st)) != cudaSuccess) return cuda_fail(e, "host estimate_heff");
+  return ok();
+}
+
+int32_t ddb_host_detect_paths(int32_t M, int32_t N, const void* heff, double theta, int32_t max_paths,
+                              int32_t* count, int32_t* path_k, int32_t* path_l, void* path_gain) {
+  if (max_paths < 0 || !heff || !count || (max_paths > 0 && (!path_k || !path_l || !path_gain)))
+    return fail(DDB_ERR_INVALID, "bad host detect arguments");
+  int32_t r = check_grid(M, N);
+  if (r) return r;
+  const size_t n = (size_t)M * N * 16, cap = (size_t)(max_paths > 0 ? max_paths : 1);
+  // device layout [heff | gains 16 cap | k 4 cap | l 4 cap | count]: one D2H of the results
+  const size_t og = al256(n), ok_ = og + 16 * cap, ol = ok_ + 4 * cap, oc = ol + 4 * cap;
+  unsigned char* d;
+  cudaStream_t st;
+  cudaError_t e = host_scratch(oc + 16, &d, &st);
+  if (e != cudaSuccess) return cuda_fail(e, "host scratch");
+  if ((e = cudaMemcpyAsync(d, heff, n, cudaMemcpyHostToDevice, st)) != cudaSuccess) return cuda_fail(e, "H2D");
+  r = ddb_detect_paths(1, M, N, d, theta, max_paths, reinterpret_cast<int32_t*>(d + oc),
+                       reinterpret_cast<int32_t*>(d + ok_), reinterpret_cast<int32_t*>(d + ol), d + og, st);
+  if (r) return r;
+  // count first (4 bytes), then only the rows that hold taps
+  int32_t c = 0;
+  if ((e = cudaMemcpyAsync(&c, d + oc, 4, cudaMemcpyDeviceToHost, st)) != cudaSuccess) return cuda_fail(e, "D2H");
+  if ((e = cudaStreamSynchronize(st)) != cudaSuccess) return cuda_fail(e, "host detect_paths");
+  *count = c;
+  const size_t rows = (size_t)(c < max_paths ? c : max_paths);
+  if (rows > 0) {
+    if ((e = cudaMemcpyAsync(path_gain, d + og, 16 * rows, cudaMemcpyDeviceToHost, st)) != cudaSuccess ||
+        (e = cudaMemcpyAsync(path_k, d + ok_, 4 * rows, cudaMemcpyDeviceToHost, st)) != cudaSuccess ||
+        (e = cudaMemcpyAsync(path_l, d + ol, 4 * rows, cudaMemcpyDeviceToHost, st)) != cudaSuccess)
+      return cuda_fail(e, "D2H");
+    if ((e = cudaStreamSynchronize(st)) != cudaSuccess) return cuda_fail(e, "host detect_paths");
+  }
+  return ok();
+}
+
 int32_t ddb_estimate_heff(int64_t count, int32_t dtype, const void* y_dd, const void* twist, double amplitude,
                           void* heff, void* stream) {
   if (count < 0) return fail(DDB_ERR_INVALID, "negative count");
@@ -594,7 +700,7 @@ int32_t ddb_build_dense_hdd(int32_t batch, int32_t M, int32_t N, int32_t dtype, 
 }
 
 int32_t ddb_probe_fp32(int32_t mode, int32_t blocks, int32_t iters, float* scratch, void* stream) {
-  if ((mode != 0 && mode != 1) || blocks < 1 || iters < 1 || !scratch)
+  if (mode < 0 || mode > 2 || blocks < 1 || iters < 1 || !scratch)
     return fail(DDB_ERR_INVALID, "bad probe arguments");
   cudaError_t e = ddb::launch_fp32_probe(mode, blocks, iters, scratch, static_cast<cudaStream_t>(stream));
   if (e != cudaSuccess) return cuda_fail(e, "fp32 probe launch");

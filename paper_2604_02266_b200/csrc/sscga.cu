@@ -39,6 +39,7 @@
 //   beta = ||c'||^2 / ||c||^2                                  (equalize.py:71-73)
 // Reductions are deterministic: every warp of every CTA sums the same per-warp
 // partials in the same order, so all CTAs take identical branches.
+#include <cstdlib>
 #include <climits>
 
 #include "cg.cuh"
@@ -820,6 +821,9 @@ static cudaError_t launch_lc(SolveArgs a, const LaunchShape& s, cudaStream_t st)
   const int nclu = a.B < max_clusters ? a.B : max_clusters;
   a.n_clusters = nclu;
   cfg.gridDim = dim3(nclu * s.cluster);
+  // single-CTA frames need no cluster attribute; DDB_NO_CLUSTER_ATTR drops it
+  // (compute-sanitizer runs: synccheck misreports cluster launches, profiles/r2_sanitizer.md)
+  if (s.cluster == 1 && getenv("DDB_NO_CLUSTER_ATTR")) cfg.numAttrs = 0;
   return cudaLaunchKernelEx(&cfg, kern, a);
 }
 

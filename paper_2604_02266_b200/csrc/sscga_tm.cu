@@ -941,6 +941,9 @@ cudaError_t launch_r(SolveArgs a, const LaunchShape& s, cudaStream_t st) {
   const int nclu = a.B < max_clusters ? a.B : max_clusters;
   a.n_clusters = nclu;
   cfg.gridDim = dim3(nclu * s.cluster);
+  // single-CTA frames need no cluster attribute; DDB_NO_CLUSTER_ATTR drops it
+  // (compute-sanitizer runs: synccheck misreports cluster launches, profiles/r2_sanitizer.md)
+  if (s.cluster == 1 && getenv("DDB_NO_CLUSTER_ATTR")) cfg.numAttrs = 0;
   return cudaLaunchKernelEx(&cfg, kern, a);
 }
 

@@ -1,7 +1,9 @@
 """Multi-GPU host logic: frames are independent (harness.py:212 seeds every
 packet separately), so the path shards by frame batch with no collective on
 the data path.  torch.distributed carries only the timing
-barrier, the max-over-ranks step time and the host-side BER totals.
+barrier, the max-over-ranks step time and the BER totals; the scalars travel
+as host tensors over a gloo group (a host-side gather, as run_packets sums its
+workers' results, harness.py:228-231), never through NCCL.
 """
 
 from __future__ import annotations
@@ -33,18 +35,22 @@ def rank_seed(seed: int, rank: int) -> int:
     return seed + 1000 * rank
 
 
-def _device() -> torch.device:
-    if dist.is_initialized() and dist.get_backend() == "nccl":
-        return torch.device("cuda", torch.cuda.current_device())
-    return torch.device("cpu")
+_HOST_GROUP = None
+
+
+def _host_group():
+    """gloo process group for host scalars (created in init(), every rank in the same order)."""
+    if _HOST_GROUP is not None:
+        return _HOST_GROUP
+    return dist.group.WORLD
 
 
 def max_over_ranks(value: float) -> float:
     """The slowest rank's time: the job's step time is the max over ranks."""
     if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size() == 1:
         return float(value)
-    t = torch.tensor([float(value)], dtype=torch.float64, device=_device())
-    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    t = torch.tensor([float(value)], dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX, group=_host_group())
     return float(t.item())
 
 
@@ -52,8 +58,8 @@ def sum_over_ranks(value: int) -> int:
     """Host-side totals (bit errors, bits): an int64 sum, as run_packets sums packets."""
     if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size() == 1:
         return int(value)
-    t = torch.tensor([int(value)], dtype=torch.int64, device=_device())
-    dist.all_reduce(t, op=dist.ReduceOp.SUM)
+    t = torch.tensor([int(value)], dtype=torch.int64)
+    dist.all_reduce(t, op=dist.ReduceOp.SUM, group=_host_group())
     return int(t.item())
 
 
@@ -81,4 +87,6 @@ def init(backend: Optional[str] = None) -> tuple[int, int, int]:
             dist.init_process_group("gloo")
         else:
             dist.init_process_group(backend)
+        global _HOST_GROUP
+        _HOST_GROUP = dist.new_group(backend="gloo") if dist.get_backend() != "gloo" else dist.group.WORLD
     return rank, local, ws

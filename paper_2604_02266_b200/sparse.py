@@ -134,16 +134,34 @@ def coefficient(path, q, cfg):
     return complex(out) if qa.ndim == 0 else out
 
 
+_TABLES = ("fwd_coef", "fwd_col", "herm_coef", "herm_row")
+
+
+class _LazyTablesChannel(StructuredSparseChannel):
+    """A StructuredSparseChannel whose four (P, MN) tables are generated on
+    the device (ddb_build_tables) the first time one is read.  The fused solve
+    needs only M, N and the paths (it regenerates the coefficients on the
+    fly), so a receiver that never looks at the tables (run_packet,
+    harness.py:163-190) pays nothing for them; any reader (ss_mvm, the
+    reference's table tests, dataclasses.replace) sees the same arrays
+    build_ss_channel used to return eagerly."""
+
+    def __getattribute__(self, name):
+        if name in _TABLES and object.__getattribute__(self, name) is None:
+            fc, fi, hc, hi = _device_tables(object.__getattribute__(self, "paths"),
+                                            object.__getattribute__(self, "M"), object.__getattribute__(self, "N"))
+            for key, t in zip(_TABLES, (fc, fi, hc, hi)):
+                object.__setattr__(self, key, t.cpu().numpy())
+        return object.__getattribute__(self, name)
+
+
 def build_ss_channel(paths, cfg):
-    """Forward and Hermitian tables for the detected taps (sparse.py:124-144)."""
+    """Forward and Hermitian tables for the detected taps (sparse.py:124-144);
+    the tables are materialised on first access."""
     if len(paths) == 0:
         raise EmptyChannel("no taps above threshold")
-    fc, fi, hc, hi = _device_tables(paths, cfg.M, cfg.N)
-    ch = StructuredSparseChannel(
-        M=cfg.M, N=cfg.N, paths=tuple(paths),
-        fwd_coef=fc.cpu().numpy(), fwd_col=fi.cpu().numpy(),
-        herm_coef=hc.cpu().numpy(), herm_row=hi.cpu().numpy(),
-    )
+    ch = _LazyTablesChannel(M=cfg.M, N=cfg.N, paths=tuple(paths),
+                            fwd_coef=None, fwd_col=None, herm_coef=None, herm_row=None)
     object.__setattr__(ch, "canonical", True)
     return ch
 
@@ -197,19 +215,16 @@ def detect_paths(heff, theta, cfg):
     heff = check_frame(heff, cfg)
     if theta < 0:
         raise ValueError("theta must be nonnegative")
-    dev = _dev()
+    _dev()
     M, N = cfg.M, cfg.N
-    h = torch.as_tensor(np.ascontiguousarray(heff, dtype=np.complex128), device=dev)
+    # one host round trip (ddb_host_detect_paths): every candidate, ranked
+    h = np.ascontiguousarray(heff, dtype=np.complex128)
     cap = M * N
-    cnt = torch.empty(1, dtype=torch.int32, device=dev)
-    k = torch.empty(cap, dtype=torch.int32, device=dev)
-    l = torch.empty(cap, dtype=torch.int32, device=dev)
-    g = torch.empty(cap, dtype=torch.complex128, device=dev)
-    nat.check(nat.load().ddb_detect_paths(1, M, N, _p(h), float(theta), cap, _p(cnt), _p(k), _p(l), _p(g),
-                                          _stream()), "ddb_detect_paths")
-    n = int(cnt.item())
-    if n < 0:
-        raise nat.DdbError(nat.DDB_ERR_UNSUPPORTED, "ddb_detect_paths",
-                           "candidate list exceeds the per-frame shared-memory capacity")
-    kk, ll, gg = k[:n].cpu().numpy(), l[:n].cpu().numpy(), g[:n].cpu().numpy()
-    return [DominantPath(int(a), int(b), complex(c)) for a, b, c in zip(kk, ll, gg)]
+    cnt = np.zeros(1, dtype=np.int32)
+    kk = np.empty(cap, dtype=np.int32)
+    ll = np.empty(cap, dtype=np.int32)
+    gg = np.empty(cap, dtype=np.complex128)
+    nat.check(nat.load().ddb_host_detect_paths(M, N, h.ctypes.data, float(theta), cap, cnt.ctypes.data,
+                                               kk.ctypes.data, ll.ctypes.data, gg.ctypes.data), "ddb_host_detect_paths")
+    n = int(cnt[0])
+    return [DominantPath(int(a), int(b), complex(c)) for a, b, c in zip(kk[:n], ll[:n], gg[:n])]

@@ -794,7 +794,7 @@ class TestDense:
 
 
 # ---------------------------------------------------------------- tiled detect_paths (frames >= 65536 bins)
-@pytest.mark.parametrize("case", ["sparse", "ties", "overflow", "zero", "all_kept"])
+@pytest.mark.parametrize("case", ["sparse", "ties", "overflow", "zero", "all_kept", "kept_ties"])
 def test_detect_paths_tiled_large_frames(pkg, case):
     """Frames of the paper's size class take the tiled multi-CTA detect path;
     the result is the oracle's detect_paths (sparse.py:69-88) tap for tap:
@@ -819,8 +819,11 @@ def test_detect_paths_tiled_large_frames(pkg, case):
             h[f].reshape(-1)[pos[10:20]] = h[f].reshape(-1)[pos[10]]
     if case == "zero":
         h[1] = 0
-    if case == "all_kept":
-        theta = 0.0  # every nonzero bin: more candidates than shared memory holds
+    if case in ("all_kept", "kept_ties"):
+        theta = 0.0  # every nonzero bin: more candidates than shared memory holds (ranked in the output rows)
+    if case == "kept_ties":  # the truncation boundary (max_paths = 64) falls inside a run of 100 equal peaks
+        for f in range(B):
+            h[f].reshape(-1)[rng.choice(M * N, 100, replace=False)] = 2.0 + 1.0j
     hd = torch.as_tensor(h, device="cuda")
     cnt = torch.empty(B, dtype=torch.int32, device="cuda")
     kk = torch.empty(B, mp, dtype=torch.int32, device="cuda")
@@ -832,9 +835,6 @@ def test_detect_paths_tiled_large_frames(pkg, case):
     cnt, kk, ll, gg = cnt.cpu().numpy(), kk.cpu().numpy(), ll.cpu().numpy(), gg.cpu().numpy()
     for f in range(B):
         want = orc.detect_paths(h[f], theta)
-        if case == "all_kept":
-            assert cnt[f] == -1  # candidate list exceeds shared memory (host reports it)
-            continue
         assert cnt[f] == len(want), (f, cnt[f], len(want))
         n = min(len(want), mp)
         assert list(zip(kk[f, :n], ll[f, :n])) == [(t.k, t.l) for t in want[:n]]
@@ -859,6 +859,26 @@ def test_detect_paths_tiled_large_frames(pkg, case):
             np.testing.assert_array_equal(k.cpu().numpy()[a:e], kk[f, :e - a])
             np.testing.assert_array_equal(g.cpu().numpy()[a:e], gg[f, :e - a])
         del s
+
+
+@pytest.mark.parametrize("theta,ties", [(0.0, False), (0.0, True), (1e-4, True)])
+def test_detect_paths_beyond_shared_memory_drop_in(pkg, theta, ties):
+    """detect_paths (sparse.py:69-88) has no capacity limit: a 131 K-bin frame
+    where (nearly) every bin is a candidate returns every tap, ranked exactly as
+    the reference's stable argsort (ties in row-major order) -- the list then
+    lives in the output rows and is sorted there (csrc/aux.cu detect_overflow)."""
+    M, N = 4096, 32
+    rng = np.random.default_rng(7)
+    h = rng.normal(size=(M, N)) + 1j * rng.normal(size=(M, N))
+    if ties:  # many exactly equal magnitudes
+        h.reshape(-1)[rng.choice(M * N, 5000, replace=False)] = 0.75 + 0.25j
+        h.reshape(-1)[rng.choice(M * N, 3000, replace=False)] = 0.25 - 0.75j
+    cfg = pkg.GridConfig(M, N, 30e3)
+    got = pkg.detect_paths(h, theta, cfg)
+    want = orc.detect_paths(h, theta)
+    assert len(got) == len(want)
+    assert [(t.k_p, t.l_p) for t in got] == [(t.k, t.l) for t in want]
+    np.testing.assert_array_equal([t.gain for t in got], [t.gain for t in want])
 
 
 @pytest.mark.parametrize("M,N,P", [(8192, 32, 6), (2048, 16, 5), (96, 12, 4)])

@@ -65,7 +65,8 @@ def test_reference_suite_fp64_through_patcher(tmp_path):
     (ROOT / "gpurun_out").mkdir(exist_ok=True)
     (ROOT / "gpurun_out" / "reference_suite_fp64.log").write_text(proc.stdout + proc.stderr)
     assert report["libddb_mapped"], "libddb.so was not loaded by the patched suite"
-    for name in ("ddb_sscga_solve", "ddb_build_tables", "ddb_ss_mvm_tables", "ddb_detect_paths", "ddb_dzt"):
+    for name in ("ddb_sscga_solve", "ddb_build_tables", "ddb_ss_mvm_tables", "ddb_host_detect_paths", "ddb_host_dzt",
+                 "ddb_host_estimate_heff"):
         assert report["calls"].get(name, 0) > 0, f"{name} never called through the patcher: {report['calls']}"
     assert len(passed) + len(failed) >= 170, tail
     assert failed == DESIGNED_FAIL, f"unexpected failures {sorted(failed - DESIGNED_FAIL)}\n{tail}"
