@@ -89,6 +89,7 @@ def parse():
     ap.add_argument("--precision", choices=("fp32", "fp64"), default="fp32",
                     help="fp64 = the drop-in cga_equalize default (complex128, bit-identical decisions)")
     ap.add_argument("--no-dropin", action="store_true", help="skip the drop-in cga_equalize per-call latency")
+    ap.add_argument("--delay-scale", type=float, default=1.0, help="scale the Veh-A delays (kernel analysis only)")
     return ap.parse_args()
 
 
@@ -408,7 +409,7 @@ def main():
         with np.load(ROOT / "tests" / "golden" / f"{cfg['taps']}.npz") as z:
             given = cycle_paths(B, z["path_off"], z["path_k"], z["path_l"], z["path_g"], "cuda", s.cdtype)
     fb = make_frames(s, B, snr_db=args.snr, nu_max_hz=cfg["nu"], modulation=cfg["mod"],
-                     seed=ddist.rank_seed(1000, rank), n_paths=P or 6, paths=given)
+                     seed=ddist.rank_seed(1000, rank), n_paths=P or 6, paths=given, delay_scale=args.delay_scale)
     out = s.alloc(B, llr=True, trace=True, bit_errors=True)
     stream = torch.cuda.current_stream()
 

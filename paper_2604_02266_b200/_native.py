@@ -8,11 +8,14 @@ entry point raises, so a silent CPU path can never stand in for the kernels.
 from __future__ import annotations
 
 import ctypes as C
+import os
 import re
 import threading
 from pathlib import Path
 
-LIB_PATH = Path(__file__).resolve().parent / "libddb.so"
+# DDB_LIB: an alternative build of the same library (A/B measurement builds of build.py --variant)
+LIB_PATH = Path(os.environ["DDB_LIB"]).resolve() if os.environ.get("DDB_LIB") else \
+    Path(__file__).resolve().parent / "libddb.so"
 HEADER_PATH = Path(__file__).resolve().parent.parent / "include" / "ddb.h"
 
 DDB_OK = 0

@@ -48,12 +48,15 @@ def is_stale() -> bool:
     return any(p.stat().st_mtime > mtime for p in _inputs())
 
 
-def build(force: bool = False, verbose: bool = False) -> Path:
-    """Compile every CUDA source into libddb.so (no-op when up to date)."""
-    if not force and not is_stale():
+def build(force: bool = False, verbose: bool = False, variant: str = "", defines=()) -> Path:
+    """Compile every CUDA source into libddb.so (no-op when up to date).  A
+    variant (measurement A/B builds) goes to libddb_<variant>.so with extra
+    -D defines; select it at run time with DDB_LIB."""
+    lib_path = LIB_PATH if not variant else PKG_DIR / f"libddb_{variant}.so"
+    if not variant and not force and not is_stale():
         return LIB_PATH
     nvcc = nvcc_path()
-    objdir = PKG_DIR / "build"
+    objdir = PKG_DIR / ("build" if not variant else f"build_{variant}")
     objdir.mkdir(exist_ok=True)
     hdr_mtime = max(p.stat().st_mtime for p in [REPO_DIR / "include" / "ddb.h", *(CSRC / h for h in HEADERS)])
     objs, cmds = [], []
@@ -62,7 +65,7 @@ def build(force: bool = False, verbose: bool = False) -> Path:
         objs.append(str(obj))
         if not force and obj.exists() and obj.stat().st_mtime > max(hdr_mtime, (CSRC / src).stat().st_mtime):
             continue  # object up to date
-        cmd = [nvcc, *NVCC_FLAGS, "-c", str(CSRC / src), "-o", str(obj)]
+        cmd = [nvcc, *NVCC_FLAGS, *(f"-D{d}" for d in defines), "-c", str(CSRC / src), "-o", str(obj)]
         if verbose:
             cmd += ["-Xptxas", "-v"]
         cmds.append(cmd)
@@ -70,11 +73,11 @@ def build(force: bool = False, verbose: bool = False) -> Path:
     with ThreadPoolExecutor(max_workers=max(1, min(len(cmds), os.cpu_count() or 1))) as pool:
         for fut in [pool.submit(_run, c, verbose) for c in cmds]:
             fut.result()
-    tmp = LIB_PATH.with_suffix(".so.tmp")
+    tmp = lib_path.with_suffix(".so.tmp")
     _run([nvcc, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-Xcompiler", "-fPIC",
           *objs, "-o", str(tmp)], verbose)
-    os.replace(tmp, LIB_PATH)
-    return LIB_PATH
+    os.replace(tmp, lib_path)
+    return lib_path
 
 
 def _run(cmd, verbose):
@@ -87,5 +90,11 @@ def _run(cmd, verbose):
 
 
 if __name__ == "__main__":
-    build(force="--force" in sys.argv, verbose="-v" in sys.argv)
-    print(LIB_PATH)
+    import argparse
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--force", action="store_true")
+    ap.add_argument("-v", action="store_true")
+    ap.add_argument("--variant", default="")
+    ap.add_argument("-D", action="append", default=[])
+    args = ap.parse_args()
+    print(build(force=args.force, verbose=args.v, variant=args.variant, defines=args.D))

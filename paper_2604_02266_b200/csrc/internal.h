@@ -24,6 +24,7 @@ struct SolveArgs {
   int G;              // delay rows per TMEM lane segment (M / segments per column)
   int WQ;             // warps per TMEM lane quarter (threads = 128 WQ)
   int CS;             // column stride (complex elements) of the column-major extended slices
+  int stream_y;       // 1: a frame's y arrives by cp.async.bulk into the u slice during the previous frame
   const int* off;
   const int* pk;
   const int* pl;

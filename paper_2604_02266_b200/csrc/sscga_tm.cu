@@ -70,7 +70,7 @@ __host__ __device__ inline SmemLayout tm_layout_impl(int Lcta, int N, int CS, in
   o += 16;
   L.p = o; o = a16(o + (size_t)Lcta * CS * sizeof(V)) + 16;
   L.u = o; o = a16(o + (size_t)Lcta * CS * sizeof(V));
-  L.x = o; o = a16(o + 16);                             // TMEM base-address slot
+  L.x = o; o = a16(o + 16);                             // TMEM base-address slot (+0), y mbarrier (+8)
   L.tlo = o; o = a16(o + (size_t)TL * sizeof(V));
   L.thi = o; o = a16(o + (size_t)TH * sizeof(V));
   L.tw = o; o = a16(o + (size_t)N * sizeof(V));
@@ -262,6 +262,7 @@ __device__ __forceinline__ void tmem_taps(int jr, const TmSm& sm, uint32_t tv, u
   }
 }
 
+
 // Local pass (after the CTA barrier): TMEM runs and own-column shared runs.
 template <int R, bool HERM>
 __device__ __forceinline__ void mvm_local(const SolveArgs& a, const TmThr& th, const TmSm& sm, const FrameSm& fs,
@@ -338,11 +339,14 @@ __device__ __forceinline__ V tm_get_v(const uint32_t (&r)[2 * E], int i) {
 // Store E values of rows rr .. rr + E - 1 into the lane's extended column
 // (16-byte stores), plus the quasi-periodic copies a frame's shifts need:
 // ext[r - M] = v W_N^{-l} for r >= M - lo, ext[r + M] = v W_N^{+l} for r < hi.
-template <int E>
+// MAIN false: the rows themselves are already in place (a bulk copy wrote them).
+template <int E, bool MAIN = true>
 __device__ __forceinline__ void put_col(V* colp, int rr, int M, int lo, int hi, V tw, const V (&v)[E]) {
-  float4* q = reinterpret_cast<float4*>(colp + rr);
+  if constexpr (MAIN) {
+    float4* q = reinterpret_cast<float4*>(colp + rr);
 #pragma unroll
-  for (int i = 0; i < E / 2; ++i) q[i] = make_float4(v[2 * i].x, v[2 * i].y, v[2 * i + 1].x, v[2 * i + 1].y);
+    for (int i = 0; i < E / 2; ++i) q[i] = make_float4(v[2 * i].x, v[2 * i].y, v[2 * i + 1].x, v[2 * i + 1].y);
+  }
   if (rr + E > M - lo) {
     const V t = cconj(tw);
 #pragma unroll
@@ -525,10 +529,27 @@ __global__ void __launch_bounds__(MAXT, 1) sscga_tm_kernel(const SolveArgs a) {
   for (int i = tid; i < a.TL; i += blockDim.x) tlo[i] = twiddle(0.f, i, a.MN);
   for (int i = tid; i < a.TH; i += blockDim.x) thi[i] = twiddle(0.f, (int)(((long long)i * a.TL) % a.MN), a.MN);
   for (int l = tid; l < a.N; l += blockDim.x) tw[l] = twiddle(0.f, l, a.N);
+  // y streaming (a.stream_y): the CTA's slice of a frame's y -- Lcta columns of
+  // M contiguous complex values -- is copied by the TMA engine (cp.async.bulk,
+  // one 8M-byte copy per column) straight into the rows of the extended u
+  // columns, where setup needs it.  The copy of frame f + n_clusters is issued
+  // as soon as frame f's last gather of u is behind a barrier, so it lands
+  // during f's final update and epilogue; completion on the mbarrier ymb.
+  void* const ymb = smem + L.x + 8;
+  const V* const yg = reinterpret_cast<const V*>(a.y);
+  auto issue_y = [&](int fy) {  // thread 0 only
+    const V* src = yg + (size_t)fy * a.MN + (size_t)rank * a.Lcta * M;
+    fence_proxy_async();  // this CTA's generic reads / writes of the u slice come first
+    mbar_expect_tx(ymb, (uint32_t)(a.Lcta * M * (int)sizeof(V)));
+    for (int c = 0; c < a.Lcta; ++c) bulk_g2s(sm.u + (size_t)c * a.CS + a.H, src + (size_t)c * M, M * sizeof(V), ymb);
+  };
+  uint32_t yph = 0;
+  if (a.stream_y && tid == 0) mbar_init(ymb, 1);
   if (warp == 0) tmem_alloc(sm.tslot, (uint32_t)a.tcols);
   tmem_fence_before();
   __syncthreads();
   tmem_fence_after();
+  if (a.stream_y && tid == 0 && (int)(blockIdx.x / a.C) < a.B) issue_y(blockIdx.x / a.C);
   const uint32_t tbase = *sm.tslot;
   th.tl = tbase + ((uint32_t)(32 * (warp & 3)) << 16);
   // TMEM regions of this lane: c | u (segment rows 0..G-1) | p | x (own runs)
@@ -552,6 +573,12 @@ __global__ void __launch_bounds__(MAXT, 1) sscga_tm_kernel(const SolveArgs a) {
     const int P = __ldg(a.off + f + 1) - P0;
 
     if (P <= 0) {  // EmptyChannel (sparse.py:126-127): flag it, no NaNs
+      if (a.stream_y) {  // this frame's y is not needed, but its copy must retire before the next one
+        mbar_wait(ymb, yph);
+        yph ^= 1;
+        __syncthreads();
+        if (tid == 0 && f + a.n_clusters < a.B) issue_y(f + a.n_clusters);
+      }
 #pragma unroll 1
       for (int i = 0; i < R; ++i) {
         reinterpret_cast<V*>(a.x)[qown + i] = make_float2(0.f, 0.f);
@@ -572,10 +599,17 @@ __global__ void __launch_bounds__(MAXT, 1) sscga_tm_kernel(const SolveArgs a) {
     // ---- frame setup: tap table, halo extents, per-row-block tap classes
     if constexpr (PROF) prof_mark(a.prof, psm, kSetup);
     // this frame's y first: the 16-byte loads are in flight during the tap-table work
-    const V* y = reinterpret_cast<const V*>(a.y);
+    const V* y = yg;
     float4 yv[R / 2];
+    if (a.stream_y) {  // from the u slice, where the bulk copy put it
+      mbar_wait(ymb, yph);
+      yph ^= 1;
 #pragma unroll
-    for (int i = 0; i < R / 2; ++i) yv[i] = __ldg(reinterpret_cast<const float4*>(y + qown) + i);
+      for (int i = 0; i < R / 2; ++i) yv[i] = reinterpret_cast<const float4*>(ucol + th.r0)[i];
+    } else {
+#pragma unroll
+      for (int i = 0; i < R / 2; ++i) yv[i] = __ldg(reinterpret_cast<const float4*>(y + qown) + i);
+    }
     const bool in_smem = P <= a.pcap;
     if (warp == 0) {  // tap table and shift extents, lanes over taps
       const V* gains = reinterpret_cast<const V*>(a.ph);
@@ -638,7 +672,8 @@ __global__ void __launch_bounds__(MAXT, 1) sscga_tm_kernel(const SolveArgs a) {
           w[2 * i + 1] = make_float2(t.z, t.w);
         }
         tm_st<E>(tU(c0), w);
-        put_col<E>(ucol, th.r0 + c0, M, lo_u, hi_u, twl, w);
+        if (a.stream_y) put_col<E, false>(ucol, th.r0 + c0, M, lo_u, hi_u, twl, w);
+        else put_col<E>(ucol, th.r0 + c0, M, lo_u, hi_u, twl, w);
         V z[E];
 #pragma unroll
         for (int i = 0; i < E; ++i) z[i] = make_float2(0.f, 0.f);
@@ -647,8 +682,9 @@ __global__ void __launch_bounds__(MAXT, 1) sscga_tm_kernel(const SolveArgs a) {
       // warm L2 with this cluster's next frame (y, TX labels) while this one solves
       if (f + a.n_clusters < a.B) {
         const size_t qn = qown + (size_t)a.n_clusters * a.MN;
+        if (!a.stream_y)
 #pragma unroll
-        for (int c0 = 0; c0 < R; c0 += 16) asm volatile("prefetch.global.L2 [%0];" :: "l"(y + qn + c0));
+          for (int c0 = 0; c0 < R; c0 += 16) asm volatile("prefetch.global.L2 [%0];" :: "l"(y + qn + c0));
         if (a.txl) asm volatile("prefetch.global.L2 [%0];" :: "l"(tx_label_ptr(a.txl, qn, a.bps, a.txpk)));
       }
     }
@@ -802,6 +838,8 @@ __global__ void __launch_bounds__(MAXT, 1) sscga_tm_kernel(const SolveArgs a) {
       done = it + 1;
       if (lead && a.cnorm) reinterpret_cast<float*>(a.cnorm)[(size_t)f * stride + done] = cn;
     }
+    // every gather of this frame's u (here and in the peers) is behind the last barrier
+    if (a.stream_y && tid == 0 && f + a.n_clusters < a.B) issue_y(f + a.n_clusters);
     if (lead) {
       float* cnorm = reinterpret_cast<float*>(a.cnorm);
       if (cnorm) for (int i = done + 1; i < stride; ++i) cnorm[(size_t)f * stride + i] = 0.f;

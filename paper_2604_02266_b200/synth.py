@@ -36,12 +36,13 @@ class FrameBatch:
 
 
 def veha_paths(B: int, grid: GridConfig, nu_max_hz: float, gen: torch.Generator, device,
-               cdtype=torch.complex64, n_paths: int = 6) -> PathBatch:
+               cdtype=torch.complex64, n_paths: int = 6, delay_scale: float = 1.0) -> PathBatch:
     # beyond the six Veh-A paths, extra taps model fractional-Doppler leakage:
     # the same delays one Doppler bin away, 25 dB down (analysis / stress only)
     base = np.asarray(VEHA_DELAYS_US)
     idx = np.arange(n_paths) % len(base)
-    delays = np.round(base[idx] * 1e-6 * grid.B).astype(np.int64)
+    # delay_scale != 1 compresses the delay profile (kernel analysis only)
+    delays = np.round(base[idx] * delay_scale * 1e-6 * grid.B).astype(np.int64)
     if delays.max() >= grid.M:
         raise ValueError("Veh-A delay spread exceeds the delay period; increase M")
     pdb = np.where(np.arange(n_paths) < len(base), np.asarray(VEHA_POWERS_DB)[idx], -25.0)
@@ -78,7 +79,7 @@ def cycle_paths(B: int, offsets, k, l, gain, device, cdtype) -> PathBatch:
 
 def make_frames(solver: SsCgaSolver, B: int, snr_db: float = 25.0, nu_max_hz: float = 100.0,
                 modulation: str = "qam16", seed: int = 0, n_paths: int = 6, delta_f: float = 30e3,
-                paths: PathBatch | None = None) -> FrameBatch:
+                paths: PathBatch | None = None, delay_scale: float = 1.0) -> FrameBatch:
     """paths: use these taps instead of drawing Veh-A ones."""
     dev = solver.device
     grid = GridConfig(solver.M, solver.N, delta_f)
@@ -89,7 +90,7 @@ def make_frames(solver: SsCgaSolver, B: int, snr_db: float = 25.0, nu_max_hz: fl
     labels = torch.randint(0, len(const.points), (B, solver.MN), generator=gen, device=dev, dtype=torch.int64)
     x = pts[labels].contiguous()
     if paths is None:
-        paths = veha_paths(B, grid, nu_max_hz, gen, dev, solver.cdtype, n_paths)
+        paths = veha_paths(B, grid, nu_max_hz, gen, dev, solver.cdtype, n_paths, delay_scale)
     hx = solver.apply(x, paths)
     if np.isinf(snr_db):
         y = hx
