@@ -60,6 +60,12 @@ CONFIGS = {
     # the grid the paper times its SS-CGA equalization on (PAPER.md:1529, 1627-1629:
     # (128, 32), QPSK; 0.54-0.78 ms per frame on H200)
     "paper128": dict(M=128, N=32, P=6, mod="qpsk", batch=4096, nu=100.0),
+    # SURVEY.md 8(d)(3)'s fixed-P kernel benchmark: a dominant unit tap plus 5
+    # taps of magnitude 0.05-0.2 at distinct random bins anywhere on the grid
+    # (tests/test_acceptance.py:40-50, random_tap_frame), so most taps shift
+    # Doppler (DSMEM / per-element route); y = Hx + AWGN as for the others (the
+    # survey's y ~ CN(0, 1) changes nothing: the solve's cost is data-independent)
+    "cfg3rand": dict(M=512, N=32, P=6, mod="qam16", batch=4096, nu=0.0, taps="random"),
 }
 BPS = {"qpsk": 2, "qam16": 4, "qam64": 6}
 
@@ -90,6 +96,8 @@ def parse():
                     help="fp64 = the drop-in cga_equalize default (complex128, bit-identical decisions)")
     ap.add_argument("--no-dropin", action="store_true", help="skip the drop-in cga_equalize per-call latency")
     ap.add_argument("--delay-scale", type=float, default=1.0, help="scale the Veh-A delays (kernel analysis only)")
+    ap.add_argument("--no-geometry", action="store_true",
+                    help="skip the cfg3det / cfg3rand tap-geometry lines reported beside the headline")
     return ap.parse_args()
 
 
@@ -263,7 +271,7 @@ class CpuArm:
     the unmodified reference from baseline/_ref when it is installed
     (kind "reference"), else its numpy restatement (kind "port")."""
 
-    def __init__(self, cfg, snr_db, iters, seed=123, prefer_reference=True):
+    def __init__(self, cfg, snr_db, iters, seed=123, prefer_reference=True, frames=None):
         import multiprocessing as mp
         os.environ["OPENBLAS_NUM_THREADS"] = "1"
         os.environ["OMP_NUM_THREADS"] = "1"
@@ -281,7 +289,8 @@ class CpuArm:
                 self.kind, self.fn = "reference", _solve_chunk_ref
             except ImportError:
                 pass
-        frames, _ = _cpu_frames(cfg, 8, snr_db, iters, seed)
+        if frames is None:
+            frames, _ = _cpu_frames(cfg, 8, snr_db, iters, seed)
         self.pool = mp.get_context("fork").Pool(self.cores, initializer=_init_worker,
                                                 initargs=(frames, cfg, iters))
         self.pool.map(self.fn, [[0]] * self.cores)  # warm every worker
@@ -403,7 +412,10 @@ def main():
     bps = BPS[cfg["mod"]]
     s = pkg.SsCgaSolver(M, N, args.iters, precision=args.precision, modulation=cfg["mod"])
     given = None
-    if cfg.get("taps"):
+    if cfg.get("taps") == "random":
+        from paper_2604_02266_b200.synth import random_paths
+        given = random_paths(B, M, N, P, ddist.rank_seed(3000, rank), s.cdtype)
+    elif cfg.get("taps"):
         import numpy as np
         from paper_2604_02266_b200.synth import cycle_paths
         with np.load(ROOT / "tests" / "golden" / f"{cfg['taps']}.npz") as z:
@@ -438,6 +450,30 @@ def main():
     value = frames_job * MN * args.steps / (ms * 1e-3)
     bit_errors = ddist.sum_over_ranks(int(out.bit_errors.sum().item()))
     ber = bit_errors / (frames_job * MN * bps)
+
+    # ---- the same grid with other tap geometries (reported beside the headline):
+    #      the taps detect_paths finds on fractional-Doppler Veh-A channels
+    #      (Doppler-leakage taps) and SURVEY 8(d)(3)'s random P = 6 taps
+    geometry = None
+    if args.config == "cfg3" and not args.no_geometry:
+        from paper_2604_02266_b200.synth import cycle_paths, random_paths
+        with np.load(ROOT / "tests" / "golden" / "frames_sweep.npz") as z:
+            det = cycle_paths(B, z["path_off"], z["path_k"], z["path_l"], z["path_g"], "cuda", s.cdtype)
+        geometry = {}
+        for name, pb in (("cfg3det", det), ("cfg3rand", random_paths(B, M, N, 6, 4321, s.cdtype))):
+            for _ in range(3):
+                s.solve(fb.y, pb, fb.lam, tx_labels=fb.tx_labels, out=out)
+            g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            g0.record(stream)
+            for _ in range(5):
+                s.solve(fb.y, pb, fb.lam, tx_labels=fb.tx_labels, out=out)
+            g1.record(stream)
+            g1.synchronize()
+            gms = g0.elapsed_time(g1) / 5
+            p_avg = float((pb.offsets[-1] - pb.offsets[0]).item()) / B
+            geometry[name] = {"value": B * MN / (gms * 1e-3), "unit": "symbols/s", "ms_per_step": gms,
+                              "taps_per_frame": p_avg, "flops_per_frame": flops_per_frame(p_avg, MN, args.iters)}
+        s.solve(fb.y, fb.paths, fb.lam, tx_labels=fb.tx_labels, out=out)  # restore the headline's outputs
 
     # ---- FP32 peak of this box (FFMA / FFMA2 probe), HBM peak from MEASURED_PEAKS
     scratch = torch.empty(148 * 8, dtype=torch.float32, device="cuda")
@@ -616,7 +652,8 @@ def main():
                    "receiver_p999_ms": rlat[int(len(rlat) * 0.999)], "receiver_runs": len(rlat),
                    # in a full batch every cluster solves B / clusters frames back to back
                    "in_batch_frame_residency_ms": ms_step * n_clu / B if s.plan()["kernel"] != "workspace" else None,
-                   "what": ("batch-1 solve (one fused launch" if s.plan()["kernel"] != "workspace" else
+                   "what": ("batch-1 solve (the lean + general fused launches" if s.plan()["kernel"] == "tmem" else
+                            "batch-1 solve (one fused launch" if s.plan()["kernel"] != "workspace" else
                             "batch-1 solve (workspace-backed kernels, one graph") + ", CUDA graph replay), device events; "
                            "receiver_*: one packet through SsCgaSolver.receive from time-domain pilot + data "
                            "frames (device-synthesised), events around the call"}
@@ -670,16 +707,30 @@ def main():
     # ---- CPU baseline (oracle port on the host cores), rank 0 at N=1 only
     cpu = None
     if not args.no_cpu and rank == 0 and world == 1:
-        arm = CpuArm(cfg, args.snr, args.iters)
+        # the GPU arm's own frames (taps, y, lam), copied to the host
+        import ddlink_oracle as orc
+        offs = fb.paths.offsets.cpu().numpy()
+        kk, ll = fb.paths.k.cpu().numpy(), fb.paths.l.cpu().numpy()
+        gg = fb.paths.gain.cpu().numpy().astype(np.complex128)
+        own = []
+        for f in range(min(B, 16)):
+            a0, a1 = int(offs[f]), int(offs[f + 1])
+            taps = [orc.Tap(int(kk[i]), int(ll[i]), complex(gg[i])) for i in range(a0, a1)]
+            own.append((taps, fb.y[f].cpu().numpy().astype(np.complex128), float(fb.lam[f])))
+        arm = CpuArm(cfg, args.snr, args.iters, frames=own)
         n = sample_frames(arm, args.cpu_seconds)
         done, dt = arm.run(n)
         stats = arm.frame_stats
         arm.close()
         cpu = {"value": done * MN / dt, "unit": "symbols/s", "cores": arm.cores, "kind": arm.kind,
-               "sample": f"{done} cfg frames ({'ddlink from baseline/_ref' if arm.kind == 'reference' else 'numpy port'}"
+               "sample": f"{done} frames cycled from the first {len(own)} frames of the GPU arm's batch "
+                         f"({'ddlink from baseline/_ref' if arm.kind == 'reference' else 'numpy port'}"
                          f": build_ss_channel->cga_equalize->hard_demod), {arm.cores} processes, {dt:.1f} s wall",
                "cpu_model": cpu_model(), **stats()}
 
+    if geometry:
+        for g in geometry.values():
+            g["fp32_frac"] = g["value"] / MN * g["flops_per_frame"] / 1e12 / peak_tflops
     roof_fp = {"bound": args.precision, "achieved": achieved, "peak": peak_tflops, "unit": "TFLOP/s",
                "frac": achieved / peak_tflops, "traffic": None if workspace else traffic,
                "flops_per_frame": fl, "peak_source": f"FMA probe on this GPU {probe}"}
@@ -730,12 +781,15 @@ def main():
             "roofline": (roof_hbm if workspace else roof_fp),
             ("roofline_fp" if workspace else "roofline_hbm"): (roof_fp if workspace else roof_hbm),
             "dropin": dropin,
+            "tap_geometry": geometry,
             "cpu_baseline": cpu,
             "e2e": e2e,
             "frontend": frontend,
-            # our kernels per step: one fused launch, one cooperative launch (workspace
-            # path, <= 8 frames), else the workspace phase sequence of launch_sscga_global
-            "gpu_launches": args.steps * (1 if s.plan()["kernel"] != "workspace" or B <= 8
+            # our kernels per step: the TMEM kernel's lean + general instantiations
+            # (csrc/sscga_tm.cu launch_r), one row-slice launch, one cooperative launch
+            # (workspace path, <= 8 frames), else the workspace phase sequence
+            "gpu_launches": args.steps * (2 if s.plan()["kernel"] == "tmem" else
+                                          1 if s.plan()["kernel"] != "workspace" or B <= 8
                                           else 4 * args.iters + 5),
             "clocks": clocks,
             "plan": s.plan(),

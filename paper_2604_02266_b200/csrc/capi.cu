@@ -321,6 +321,10 @@ static int32_t solve_impl(const ddb_sscga_problem* prob, const ddb_sscga_outputs
   if (s.kind == 1) a.active_threads = s.threads;
   // TMEM kernel: frames' y streamed by cp.async.bulk (16-byte aligned y; DDB_NO_TMA=1 for A/B runs)
   a.stream_y = s.kind == 1 && (reinterpret_cast<uintptr_t>(prob->y) & 15) == 0 && !getenv("DDB_NO_TMA");
+  {
+    const char* env = getenv("DDB_TM_SPLIT");
+    a.split = s.kind == 1 && (env ? atoi(env) != 0 : 1);
+  }
   a.off = prob->path_offsets;
   a.pk = prob->path_k;
   a.pl = prob->path_l;

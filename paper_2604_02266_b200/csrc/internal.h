@@ -25,6 +25,7 @@ struct SolveArgs {
   int WQ;             // warps per TMEM lane quarter (threads = 128 WQ)
   int CS;             // column stride (complex elements) of the column-major extended slices
   int stream_y;       // 1: a frame's y arrives by cp.async.bulk into the u slice during the previous frame
+  int split;          // 1: lean frames go to the lean instantiation, the rest to the general one; 0: general only
   const int* off;
   const int* pk;
   const int* pl;
@@ -81,7 +82,7 @@ __host__ __device__ constexpr int row_stride(int lcta, int elem_bytes) {
 
 // Shared-memory layout of the fused kernel (byte offsets, 16-byte aligned).
 struct SmemLayout {
-  size_t p, u, x, tlo, thi, tw, ptab, red, total;
+  size_t p, u, x, tlo, thi, tw, ptab, red, q, total;  // q: the TMEM kernel's frame list
 };
 SmemLayout sscga_layout(int M, int N, int C, int elem_bytes, int H, int TL, int TH, int pcap);
 void twiddle_split(int MN, int* TL, int* TH);

@@ -54,7 +54,8 @@ struct FrameSm {
   int in_smem, halo, masks;
   int lo_c, hi_c, lo_u, hi_u;  // extension rows written for c (gathered by H) and u (by H^H)
   int remote;                  // some warp gathers per element (DSMEM): publish c / u with release
-  int pad[2];
+  int wrap;                    // some shift exceeds the halo: runs beyond it wrap the delay period
+  int pad;
   uint32_t mk[8][6];           // [j][tmF, smF, gnF, tmH, smH, gnH]: TMEM run / shared run / per element
 };
 
@@ -76,6 +77,7 @@ __host__ __device__ inline SmemLayout tm_layout_impl(int Lcta, int N, int CS, in
   L.tw = o; o = a16(o + (size_t)N * sizeof(V));
   L.ptab = o; o = a16(o + (size_t)pcap * sizeof(PathEnt<float>));
   L.red = o; o = a16(o + 2 * 2 * kPushSlots * sizeof(V) + sizeof(ProfSm) + sizeof(FrameSm));
+  L.q = o; o = a16(o + (128 + 16) * sizeof(int));       // frame list (kListChunk) of this CTA's class + warp counts
   L.total = o;
   return L;
 }
@@ -148,16 +150,37 @@ __device__ __forceinline__ void gather_tmem(uint32_t ta, U64 X, U64 Y, U64 (&acc
   for (int i = 0; i < R; ++i) cmacxy(acc[i], X, Y, __uint_as_float(v[2 * i]), __uint_as_float(v[2 * i + 1]));
 }
 
+// Start row of a thread's R-row source run in an extended column whose halo
+// rows [-lo, 0) and [M, M + hi) are written.  A run beyond them (a frame whose
+// shifts exceed the halo capacity H, e.g. taps anywhere on the grid) lies
+// wholly outside [0, M) (R <= H), so it is read one delay period over, inside
+// the column itself, and the quasi-periodic twist of that period (put_col:
+// ext[r - M] = v W_N^{-l}, ext[r + M] = v W_N^{+l}) moves into the gain: no
+// per-row wrap.  Returns the twist (1 when the run is in place).
+template <int R>
+__device__ __forceinline__ V wrap_run(int& a0, int M, int lo, int hi, V tw_src) {
+  if (a0 < -lo) {
+    a0 += M;
+    return cconj(tw_src);
+  }
+  if (a0 + R > M + hi) {
+    a0 -= M;
+    return tw_src;
+  }
+  return make_float2(1.f, 0.f);
+}
+
 // One tap with a Doppler shift (d_l != 0), or any tap when the frame's shifts
 // exceed the halo, from the (possibly remote) extended column of the source
 // Doppler column.  With the halo the R source rows are one contiguous run:
 // 16-byte DSMEM loads, and the row-dependent coefficient h W^{-+d_l k} of the
 // forward / hermitian closed form (sparse.py:107-121) advanced by one complex
-// multiply per row from an exact table value every 8 rows.  Without the halo
-// rows wrap the delay period individually (twist applied in registers).
+// multiply per row from an exact table value every 8 rows; a run beyond the
+// written halo (wrap) is read one delay period over (wrap_run).  Without the
+// halo rows wrap the delay period individually (twist applied in registers).
 template <int R, bool HERM>
-__device__ __forceinline__ void tap_elem(const SolveArgs& a, const TmThr& th, const TmSm& sm, bool halo,
-                                         const V* buf, const PathEnt<float>& e, U64 (&acc)[R]) {
+__device__ __forceinline__ void tap_elem(const SolveArgs& a, const TmThr& th, const TmSm& sm, const FrameSm& fs,
+                                         bool halo, const V* buf, const PathEnt<float>& e, U64 (&acc)[R]) {
   const int M = a.M, MN = a.MN;
   const int dl = e.dl;
   const int s = HERM ? -e.dk : e.dk;
@@ -171,7 +194,10 @@ __device__ __forceinline__ void tap_elem(const SolveArgs& a, const TmThr& th, co
   if (halo) {
     constexpr int BS = R < 8 ? R : 8;  // rows per exact re-anchor
     const V step = twid_tm(sm, wrap1(sg, MN));
-    const uint32_t run = colad + (uint32_t)((th.r0 + s) * (int)sizeof(V));
+    int a0 = th.r0 + s;
+    V hw = h0;
+    if (fs.wrap) hw = cmul(h0, wrap_run<R>(a0, M, HERM ? fs.lo_u : fs.lo_c, HERM ? fs.hi_u : fs.hi_c, sm.tw[ls]));
+    const uint32_t run = colad + (uint32_t)(a0 * (int)sizeof(V));
     V v[R];
     if ((s & 1) == 0) {
 #pragma unroll
@@ -194,7 +220,7 @@ __device__ __forceinline__ void tap_elem(const SolveArgs& a, const TmThr& th, co
     }
 #pragma unroll
     for (int b = 0; b < R; b += BS) {
-      V c = cmul(h0, twid_tm(sm, wrap1(sg * (th.r0 + b) % MN, MN)));
+      V c = cmul(hw, twid_tm(sm, wrap1(sg * (th.r0 + b) % MN, MN)));
 #pragma unroll
       for (int i = 0; i < BS; ++i) {
         Acc<float>::mac(acc[b + i], c, v[b + i]);
@@ -263,8 +289,19 @@ __device__ __forceinline__ void tmem_taps(int jr, const TmSm& sm, uint32_t tv, u
 }
 
 
-// Local pass (after the CTA barrier): TMEM runs and own-column shared runs.
+// A d_l = 0 tap's run from the thread's own extended column when the frame's
+// shifts exceed the halo (wrap_run): the period twist goes into the gain pairs.
 template <int R, bool HERM>
+__device__ __forceinline__ void wrap_gain(int& a0, int M, const FrameSm& fs, V tw_own, const PathEnt<float>& e,
+                                          ulonglong2& g) {
+  const V t = wrap_run<R>(a0, M, HERM ? fs.lo_u : fs.lo_c, HERM ? fs.hi_u : fs.hi_c, tw_own);
+  const V h = cmul(e.coef(HERM), t);
+  g = make_ulonglong2(pack2(h.x, h.x), pack2(-h.y, h.y));
+}
+
+// Local pass (after the CTA barrier): TMEM runs and own-column shared runs.
+// GEN false (lean frames): masks always apply and no run wraps.
+template <int R, bool HERM, bool GEN = true>
 __device__ __forceinline__ void mvm_local(const SolveArgs& a, const TmThr& th, const TmSm& sm, const FrameSm& fs,
                                           uint32_t tv, const V* vcol, U64 (&acc)[R]) {
 #pragma unroll
@@ -276,18 +313,27 @@ __device__ __forceinline__ void mvm_local(const SolveArgs& a, const TmThr& th, c
     for (uint32_t m = ms; m; m &= m - 1) {
       const PathEnt<float>& e = sm.ptab[__ffs(m) - 1];
       const int s = HERM ? -e.dk : e.dk;
-      const ulonglong2 g = gain_pairs<HERM>(e);
-      gather_run<R>(vcol + th.r0 + s, (s & 1) != 0, g.x, g.y, acc);
+      ulonglong2 g = gain_pairs<HERM>(e);
+      int a0 = th.r0 + s;
+      if constexpr (GEN)
+        if (fs.wrap) wrap_gain<R, HERM>(a0, a.M, fs, sm.tw[th.colg], e, g);
+      gather_run<R>(vcol + a0, (s & 1) != 0, g.x, g.y, acc);
     }
-  } else {
+  } else if constexpr (GEN) {
     const bool halo = fs.halo;
     for (int p = 0; p < fs.P; ++p) {
       const PathEnt<float> e = tm_get(a, sm, fs, p);
       const int cls = tap_class<R, HERM>(a, th.jr, halo, e);
       const int s = HERM ? -e.dk : e.dk;
       const float4 g = HERM ? e.hh : e.hf;
-      if (cls == 0) gather_tmem<R>(tv + (uint32_t)(2 * (th.jr + s)), pack2(g.x, g.y), pack2(g.z, g.w), acc);
-      else if (cls == 1) gather_run<R>(vcol + th.r0 + s, (s & 1) != 0, pack2(g.x, g.y), pack2(g.z, g.w), acc);
+      if (cls == 0) {
+        gather_tmem<R>(tv + (uint32_t)(2 * (th.jr + s)), pack2(g.x, g.y), pack2(g.z, g.w), acc);
+      } else if (cls == 1) {
+        ulonglong2 gp = make_ulonglong2(pack2(g.x, g.y), pack2(g.z, g.w));
+        int a0 = th.r0 + s;
+        if (fs.wrap) wrap_gain<R, HERM>(a0, a.M, fs, sm.tw[th.colg], e, gp);
+        gather_run<R>(vcol + a0, (s & 1) != 0, gp.x, gp.y, acc);
+      }
     }
   }
 }
@@ -299,11 +345,11 @@ __device__ __forceinline__ void mvm_remote(const SolveArgs& a, const TmThr& th, 
   const bool halo = fs.halo;
   if (fs.masks) {
     for (uint32_t m = fs.mk[th.jr / R][HERM ? 5 : 2]; m; m &= m - 1)
-      tap_elem<R, HERM>(a, th, sm, halo, buf, sm.ptab[__ffs(m) - 1], acc);
+      tap_elem<R, HERM>(a, th, sm, fs, halo, buf, sm.ptab[__ffs(m) - 1], acc);
   } else {
     for (int p = 0; p < fs.P; ++p) {
       const PathEnt<float> e = tm_get(a, sm, fs, p);
-      if (tap_class<R, HERM>(a, th.jr, halo, e) == 2) tap_elem<R, HERM>(a, th, sm, halo, buf, e, acc);
+      if (tap_class<R, HERM>(a, th.jr, halo, e) == 2) tap_elem<R, HERM>(a, th, sm, fs, halo, buf, e, acc);
     }
   }
 }
@@ -492,7 +538,61 @@ __device__ __forceinline__ int epi_pass(const SolveArgs& a, const V* stg, int M,
     }                                                  \
   } while (0)
 
-template <int R, int MAXT, bool PROF>
+// Frames are split between two instantiations of the kernel by tap geometry.
+// "Lean" frames -- 1..32 taps, all Doppler-preserving (l_p = L0), delay shifts
+// within the halo (every Veh-A frame with |nu| < dnu / 2, the headline's) --
+// need only the TMEM and own-column routes; the general kernel (GEN) carries
+// the Doppler (DSMEM), wrapped-run and large-P paths whose extra registers
+// would otherwise spill in the lean one.  Both kernels are launched on every
+// solve (lean first) and each takes its own class; EmptyChannel frames (P = 0)
+// go to the lean one.
+__device__ __forceinline__ bool frame_lean(const SolveArgs& a, int f) {
+  const int P0 = __ldg(a.off + f), P = __ldg(a.off + f + 1) - P0;
+  if (P <= 0) return true;
+  if (P > 32 || P > a.pcap) return false;
+  int dmin = INT_MAX, dmax = INT_MIN;
+  bool dl0 = true;
+  // four taps' loads in flight at a time (one round trip for a Veh-A frame)
+  for (int i0 = 0; i0 < P; i0 += 4) {
+    int kk[4], ll[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int i = min(i0 + u, P - 1);
+      kk[u] = __ldg(a.pk + P0 + i);
+      ll[u] = __ldg(a.pl + P0 + i);
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      dl0 &= ll[u] == a.L0;
+      dmin = min(dmin, a.K0 - kk[u]);
+      dmax = max(dmax, a.K0 - kk[u]);
+    }
+  }
+  return dl0 && max(0, -dmin) <= a.H && max(0, dmax) <= a.H;
+}
+
+// This CTA's next chunk of frames of its class: candidates base + t n_clusters
+// (t < kListChunk), compacted in order into flist; returns the count (all threads).
+constexpr int kListChunk = 128;
+template <bool GEN>
+__device__ __forceinline__ int frame_list(const SolveArgs& a, int base, int* flist, int* wcnt) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+  const int fc = base + tid * a.n_clusters;
+  const bool mine = tid < kListChunk && fc < a.B && (GEN && !a.split ? true : frame_lean(a, fc) != GEN);
+  const unsigned bal = __ballot_sync(0xffffffffu, mine);
+  if (lane == 0) wcnt[warp] = __popc(bal);
+  __syncthreads();
+  int pos = 0, tot = 0;
+  for (int w = 0; w < nw; ++w) {
+    pos += w < warp ? wcnt[w] : 0;
+    tot += wcnt[w];
+  }
+  if (mine) flist[pos + __popc(bal & ((1u << lane) - 1u))] = fc;
+  __syncthreads();
+  return tot;
+}
+
+template <int R, int MAXT, bool PROF, bool GEN>
 __global__ void __launch_bounds__(MAXT, 1) sscga_tm_kernel(const SolveArgs a) {
   constexpr int E = 4;  // elements per TMEM chunk of the elementwise steps
   extern __shared__ __align__(16) unsigned char smem[];
@@ -513,6 +613,8 @@ __global__ void __launch_bounds__(MAXT, 1) sscga_tm_kernel(const SolveArgs a) {
   V* red = reinterpret_cast<V*>(smem + L.red);
   ProfSm* const psm = reinterpret_cast<ProfSm*>(red + 2 * 2 * kPushSlots);
   FrameSm& fs = *reinterpret_cast<FrameSm*>(psm + 1);
+  int* const flist = reinterpret_cast<int*>(smem + L.q);
+  int* const wcnt = flist + 128;
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
   const int rank = a.C > 1 ? (int)cluster_rank() : 0;
@@ -545,11 +647,23 @@ __global__ void __launch_bounds__(MAXT, 1) sscga_tm_kernel(const SolveArgs a) {
   };
   uint32_t yph = 0;
   if (a.stream_y && tid == 0) mbar_init(ymb, 1);
+  // the general instantiation is launched as a programmatic dependent of the
+  // lean one (launch_r): it may start as soon as SMs free up, and its frames
+  // do not depend on the lean ones; it waits for the lean grid only before it
+  // completes, so the stream's order holds for whatever follows the solve
+  if constexpr (!GEN) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  // this CTA's first frames of its class: a CTA (cluster: every CTA computes the
+  // same list) without any frame in the whole batch leaves at once
+  const int base0 = blockIdx.x / a.C;
+  int nlist = frame_list<GEN>(a, base0, flist, wcnt);
+  if (nlist == 0 && base0 + a.n_clusters * kListChunk >= a.B) {
+    if constexpr (GEN) asm volatile("griddepcontrol.wait;" ::: "memory");
+    return;
+  }
   if (warp == 0) tmem_alloc(sm.tslot, (uint32_t)a.tcols);
   tmem_fence_before();
   __syncthreads();
   tmem_fence_after();
-  if (a.stream_y && tid == 0 && (int)(blockIdx.x / a.C) < a.B) issue_y(blockIdx.x / a.C);
   const uint32_t tbase = *sm.tslot;
   th.tl = tbase + ((uint32_t)(32 * (warp & 3)) << 16);
   // TMEM regions of this lane: c | u (segment rows 0..G-1) | p | x (own runs)
@@ -566,7 +680,12 @@ __global__ void __launch_bounds__(MAXT, 1) sscga_tm_kernel(const SolveArgs a) {
   if constexpr (PROF) prof_init(a.prof, psm);
   long long wt[kWarpTimers] = {0, 0, 0, 0, 0, 0, 0, 0};
 
-  for (int f = blockIdx.x / a.C; f < a.B; f += a.n_clusters) {
+  for (int base = base0; base < a.B; base += a.n_clusters * kListChunk) {
+  if (base != base0) nlist = frame_list<GEN>(a, base, flist, wcnt);
+  if (a.stream_y && tid == 0 && nlist > 0) issue_y(flist[0]);
+  for (int li = 0; li < nlist; ++li) {
+    const int f = flist[li];
+    const int fnext = li + 1 < nlist ? flist[li + 1] : -1;  // this CTA's next frame of the class (y prefetch)
     const size_t fo = (size_t)f * a.MN;
     const size_t qown = fo + (size_t)th.colg * M + th.r0;  // first owned element of the frame
     const int P0 = __ldg(a.off + f);
@@ -577,7 +696,7 @@ __global__ void __launch_bounds__(MAXT, 1) sscga_tm_kernel(const SolveArgs a) {
         mbar_wait(ymb, yph);
         yph ^= 1;
         __syncthreads();
-        if (tid == 0 && f + a.n_clusters < a.B) issue_y(f + a.n_clusters);
+        if (tid == 0 && fnext >= 0) issue_y(fnext);
       }
 #pragma unroll 1
       for (int i = 0; i < R; ++i) {
@@ -623,15 +742,19 @@ __global__ void __launch_bounds__(MAXT, 1) sscga_tm_kernel(const SolveArgs a) {
       dmin = __reduce_min_sync(0xffffffffu, dmin);
       dmax = __reduce_max_sync(0xffffffffu, dmax);
       if (lane == 0) {
+        // halo rows written per side: what the shifts need, at most H; a run
+        // beyond them is read one delay period over (wrap_run), which needs
+        // H >= R (the planner's halo is at least min(M, 64) rows)
         const int lo = max(0, -dmin), hi = max(0, dmax);
-        const bool halo = lo <= a.H && hi <= a.H;
+        const bool halo = a.H >= R;
         fs.P0 = P0;
         fs.P = P;
         fs.in_smem = in_smem;
         fs.halo = halo;
+        fs.wrap = halo && (lo > a.H || hi > a.H);
         fs.masks = in_smem && P <= 32;
-        fs.lo_c = halo ? lo : 0;
-        fs.hi_c = halo ? hi : 0;
+        fs.lo_c = halo ? min(lo, a.H) : 0;
+        fs.hi_c = halo ? min(hi, a.H) : 0;
         fs.lo_u = fs.hi_c;
         fs.hi_u = fs.lo_c;
         fs.remote = !fs.masks;  // without per-warp masks assume DSMEM taps
@@ -680,8 +803,8 @@ __global__ void __launch_bounds__(MAXT, 1) sscga_tm_kernel(const SolveArgs a) {
         tm_st<E>(tX(c0), z);  // x = 0
       }
       // warm L2 with this cluster's next frame (y, TX labels) while this one solves
-      if (f + a.n_clusters < a.B) {
-        const size_t qn = qown + (size_t)a.n_clusters * a.MN;
+      if (fnext >= 0) {
+        const size_t qn = qown + (size_t)(fnext - f) * a.MN;
         if (!a.stream_y)
 #pragma unroll
           for (int c0 = 0; c0 < R; c0 += 16) asm volatile("prefetch.global.L2 [%0];" :: "l"(y + qn + c0));
@@ -694,11 +817,11 @@ __global__ void __launch_bounds__(MAXT, 1) sscga_tm_kernel(const SolveArgs a) {
     if constexpr (PROF) prof_mark(a.prof, psm, kArrive);
     tm_arrive(a.C);  // y and the tap classes published
     if constexpr (PROF) prof_mark(a.prof, psm, kMvmLocal);
-    TM_WT(1, mvm_local<R, true>(a, th, sm, fs, tU(0) - 2 * th.jr, ucol, acc));  // b = H^H y (equalize.py:52)
+    TM_WT(1, mvm_local<R, true, GEN>(a, th, sm, fs, tU(0) - 2 * th.jr, ucol, acc));  // b = H^H y (equalize.py:52)
     if constexpr (PROF) prof_mark(a.prof, psm, kWait);
     cl_wait(a.C);
     if constexpr (PROF) prof_mark(a.prof, psm, kMvmRemote);
-    mvm_remote<R, true>(a, th, sm, fs, sm.u, acc);
+    if constexpr (GEN) mvm_remote<R, true>(a, th, sm, fs, sm.u, acc);
     if constexpr (PROF) prof_mark(a.prof, psm, kStep1);
     {
       V nrm = make_float2(0.f, 0.f);
@@ -720,7 +843,7 @@ __global__ void __launch_bounds__(MAXT, 1) sscga_tm_kernel(const SolveArgs a) {
     if constexpr (PROF) prof_mark(a.prof, psm, kArrive);
     TM_WT(2, tm_arrive_red<PROF>(a.C, red + (2 + par1) * kPushSlots, nwarps, warp, lane, rank, !fs.remote, wt));  // c = b published
     if constexpr (PROF) prof_mark(a.prof, psm, kMvmLocal);
-    TM_WT(0, mvm_local<R, false>(a, th, sm, fs, tC(0) - 2 * th.jr, ccol, acc));
+    TM_WT(0, mvm_local<R, false, GEN>(a, th, sm, fs, tC(0) - 2 * th.jr, ccol, acc));
     if constexpr (PROF) prof_mark(a.prof, psm, kWait);
     cl_wait(a.C);
     if constexpr (PROF) prof_mark(a.prof, psm, kRead);
@@ -734,7 +857,7 @@ __global__ void __launch_bounds__(MAXT, 1) sscga_tm_kernel(const SolveArgs a) {
     for (int it = 0; it < a.iters; ++it) {
       // u = H c + beta u_old, p = c + beta p_old      (= H p, p of equalize.py:60, 72)
       if constexpr (PROF) prof_mark(a.prof, psm, kMvmRemote);
-      mvm_remote<R, false>(a, th, sm, fs, sm.c, acc);
+      if constexpr (GEN) mvm_remote<R, false>(a, th, sm, fs, sm.c, acc);
       if constexpr (PROF) prof_mark(a.prof, psm, kStep1);
       {
         V nu = make_float2(0.f, 0.f), np = make_float2(0.f, 0.f);
@@ -772,11 +895,11 @@ __global__ void __launch_bounds__(MAXT, 1) sscga_tm_kernel(const SolveArgs a) {
       TM_WT(2, tm_arrive_red<PROF>(a.C, red + par0 * kPushSlots, nwarps, warp, lane, rank, !fs.remote, wt));  // u published
       // ap = H^H u + lam p;  x += alpha p;  c -= alpha ap      (equalize.py:60-70)
       if constexpr (PROF) prof_mark(a.prof, psm, kMvmLocal);
-      TM_WT(1, mvm_local<R, true>(a, th, sm, fs, tU(0) - 2 * th.jr, ucol, acc));
+      TM_WT(1, mvm_local<R, true, GEN>(a, th, sm, fs, tU(0) - 2 * th.jr, ucol, acc));
       if constexpr (PROF) prof_mark(a.prof, psm, kWait);
       TM_WT(3, cl_wait(a.C));
       if constexpr (PROF) prof_mark(a.prof, psm, kMvmRemote);
-      mvm_remote<R, true>(a, th, sm, fs, sm.u, acc);
+      if constexpr (GEN) mvm_remote<R, true>(a, th, sm, fs, sm.u, acc);
       if constexpr (PROF) prof_mark(a.prof, psm, kRead);
       const V up = red_total<float>(a.C, red + par0 * kPushSlots, nwarps);
       par0 ^= 1;
@@ -827,7 +950,7 @@ __global__ void __launch_bounds__(MAXT, 1) sscga_tm_kernel(const SolveArgs a) {
       if constexpr (PROF) prof_mark(a.prof, psm, kArrive);
       TM_WT(2, tm_arrive_red<PROF>(a.C, red + (2 + par1) * kPushSlots, nwarps, warp, lane, rank, !fs.remote, wt));  // c published
       if constexpr (PROF) prof_mark(a.prof, psm, kMvmLocal);
-      if (it + 1 < a.iters) TM_WT(0, mvm_local<R, false>(a, th, sm, fs, tC(0) - 2 * th.jr, ccol, acc));  // next H c
+      if (it + 1 < a.iters) TM_WT(0, mvm_local<R, false, GEN>(a, th, sm, fs, tC(0) - 2 * th.jr, ccol, acc));  // next H c
       if constexpr (PROF) prof_mark(a.prof, psm, kWait);
       TM_WT(3, cl_wait(a.C));
       if constexpr (PROF) prof_mark(a.prof, psm, kRead);
@@ -839,7 +962,7 @@ __global__ void __launch_bounds__(MAXT, 1) sscga_tm_kernel(const SolveArgs a) {
       if (lead && a.cnorm) reinterpret_cast<float*>(a.cnorm)[(size_t)f * stride + done] = cn;
     }
     // every gather of this frame's u (here and in the peers) is behind the last barrier
-    if (a.stream_y && tid == 0 && f + a.n_clusters < a.B) issue_y(f + a.n_clusters);
+    if (a.stream_y && tid == 0 && fnext >= 0) issue_y(fnext);
     if (lead) {
       float* cnorm = reinterpret_cast<float*>(a.cnorm);
       if (cnorm) for (int i = done + 1; i < stride; ++i) cnorm[(size_t)f * stride + i] = 0.f;
@@ -888,6 +1011,8 @@ __global__ void __launch_bounds__(MAXT, 1) sscga_tm_kernel(const SolveArgs a) {
       if (lane == 0 && errs) atomicAdd(a.berr + f, errs);
     }
   }
+  __syncthreads();  // the next chunk's list overwrites flist
+  }
   if constexpr (PROF) prof_mark(a.prof, psm, kTail);
   if constexpr (PROF) prof_store(a.prof, psm);
   if constexpr (PROF) {
@@ -899,6 +1024,7 @@ __global__ void __launch_bounds__(MAXT, 1) sscga_tm_kernel(const SolveArgs a) {
   tmem_fence_before();
   cl_sync<float>(a.C);
   if (warp == 0) tmem_dealloc(tbase, (uint32_t)a.tcols);
+  if constexpr (GEN) asm volatile("griddepcontrol.wait;" ::: "memory");
 }
 
 // CTAs of this kernel one SM really holds.  The occupancy API reports 1 for any
@@ -927,21 +1053,23 @@ struct TmOcc {
   int smem, threads, cluster, dev, clusters;
 };
 
-template <int R, int MAXT, bool PROF = false>
-cudaError_t launch_r(SolveArgs a, const LaunchShape& s, cudaStream_t st) {
-  auto kern = sscga_tm_kernel<R, MAXT, PROF>;
+template <int R, int MAXT, bool PROF, bool GEN>
+cudaError_t launch_one(SolveArgs a, const LaunchShape& s, cudaStream_t st) {
+  auto kern = sscga_tm_kernel<R, MAXT, PROF, GEN>;
   cudaLaunchConfig_t cfg = {};
   cfg.blockDim = dim3(s.threads);
   cfg.dynamicSmemBytes = s.smem;
   cfg.stream = st;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = s.cluster;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  static thread_local TmOcc cache[4] = {};
+  static thread_local TmOcc cache[8] = {};
   static thread_local int next = 0;
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);
@@ -951,7 +1079,12 @@ cudaError_t launch_r(SolveArgs a, const LaunchShape& s, cudaStream_t st) {
     if (c.fn == (const void*)kern && c.smem == s.smem && c.threads == s.threads && c.cluster == s.cluster && c.dev == dev)
       max_clusters = c.clusters;
   if (max_clusters == 0) {
-    e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, s.smem);
+    // the function's dynamic shared-memory ceiling goes to the device maximum,
+    // so a launch of any plan is valid whatever plan set it last
+    int optin = 0;
+    e = cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, optin > s.smem ? optin : s.smem);
     if (e != cudaSuccess) return e;
     e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     if (e != cudaSuccess) return e;
@@ -974,21 +1107,36 @@ cudaError_t launch_r(SolveArgs a, const LaunchShape& s, cudaStream_t st) {
     // measured residency (persistent grid: every cluster is resident at once)
     max_clusters = hw > api_per_sm && api_per_sm > 0 ? api * hw / api_per_sm : api;
     cache[next] = TmOcc{(const void*)kern, s.smem, s.threads, s.cluster, dev, max_clusters};
-    next = (next + 1) % 4;
+    next = (next + 1) % 8;
   }
   const int nclu = a.B < max_clusters ? a.B : max_clusters;
   a.n_clusters = nclu;
   cfg.gridDim = dim3(nclu * s.cluster);
+  if (GEN && a.split && !getenv("DDB_NO_PDL")) cfg.numAttrs = 2;  // programmatic dependent of the lean launch
   // single-CTA frames need no cluster attribute; DDB_NO_CLUSTER_ATTR drops it
   // (compute-sanitizer runs: synccheck misreports cluster launches, profiles/r2_sanitizer.md)
   if (s.cluster == 1 && getenv("DDB_NO_CLUSTER_ATTR")) cfg.numAttrs = 0;
   return cudaLaunchKernelEx(&cfg, kern, a);
 }
 
+// Both instantiations on the stream: the lean frames, then the others.
+template <int R, int MAXT, bool PROF = false>
+cudaError_t launch_r(SolveArgs a, const LaunchShape& s, cudaStream_t st) {
+  if (a.split) {
+    cudaError_t e = launch_one<R, MAXT, PROF, false>(a, s, st);
+    if (e != cudaSuccess) return e;
+  }
+  return launch_one<R, MAXT, PROF, true>(a, s, st);
+}
+
 template <int R, int MAXT>
 cudaError_t occ_r(const LaunchShape& s, int* n) {
-  auto kern = sscga_tm_kernel<R, MAXT, false>;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, s.smem);
+  auto kern = sscga_tm_kernel<R, MAXT, false, false>;
+  int dev = 0, optin = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  // never below what a cached launch of another plan may need (see launch_one)
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, optin > s.smem ? optin : s.smem);
   if (e != cudaSuccess) return e;
   cudaFuncAttributes fa;
   e = cudaFuncGetAttributes(&fa, kern);

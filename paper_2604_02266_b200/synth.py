@@ -61,6 +61,24 @@ def veha_paths(B: int, grid: GridConfig, nu_max_hz: float, gen: torch.Generator,
                      gain.reshape(-1).to(cdtype).contiguous())
 
 
+def random_paths(B: int, M: int, N: int, P: int, seed: int, cdtype=torch.complex64, device="cuda") -> PathBatch:
+    """SURVEY.md 8(d)(3)'s kernel-benchmark taps: per frame a dominant unit tap
+    plus P - 1 taps of magnitude U(0.05, 0.2) and uniform phase, all at
+    distinct uniformly random (k, l) bins (tests/test_acceptance.py:40-50,
+    random_tap_frame).  Benchmark input generation only (host numpy)."""
+    rng = np.random.default_rng(seed)
+    k = np.empty((B, P), np.int32)
+    l = np.empty((B, P), np.int32)
+    g = np.empty((B, P), np.complex128)
+    for f in range(B):
+        bins = rng.choice(M * N, P, replace=False)
+        k[f], l[f] = bins // N, bins % N
+        g[f, 0] = 1.0
+        g[f, 1:] = rng.uniform(0.05, 0.2, P - 1) * np.exp(2j * np.pi * rng.random(P - 1))
+    off = np.arange(0, (B + 1) * P, P, dtype=np.int32)
+    return PathBatch.from_arrays(off, k.reshape(-1), l.reshape(-1), g.reshape(-1), device, cdtype)
+
+
 def cycle_paths(B: int, offsets, k, l, gain, device, cdtype) -> PathBatch:
     """B frames whose tap sets cycle through the given CSR tap sets (e.g. the
     reference's detect_paths output on fractional-Doppler Veh-A channels)."""

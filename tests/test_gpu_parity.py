@@ -1275,3 +1275,28 @@ def test_fused_epilogue_labels_and_llr_magnitudes(pkg, case, fp32_kernel):
         assert float(np.abs(llr[f] - lo).max()) <= 1e-3 * float(np.abs(lo).max())
         errs = int(np.unpackbits((labels[f] ^ txs[f])[:, None], axis=1).sum())
         assert int(res.bit_errors[f]) == errs
+
+
+@pytest.mark.parametrize("fp32_kernel_name", ["tmem", "row"])
+def test_random_geometry_bench_taps_vs_oracle(pkg, fp32_kernel_name, monkeypatch):
+    """bench.py's cfg3rand line (a unit tap plus five weak
+    taps at random bins, synth.random_paths): delay shifts up to M/2 exceed the
+    halo, so runs are read one delay period over with the twist in the gain
+    (csrc/sscga_tm.cu wrap_run), and most taps shift Doppler (DSMEM runs)."""
+    from paper_2604_02266_b200.synth import random_paths
+    if fp32_kernel_name == "row":
+        monkeypatch.setenv("DDB_KERNEL", "row")
+    M, N, B = 512, 32, 4
+    s = pkg.SsCgaSolver(M, N, 10, precision="fp32")
+    pb = random_paths(B, M, N, 6, 99, s.cdtype)
+    rng = np.random.default_rng(5)
+    y = (rng.normal(size=(B, M * N)) + 1j * rng.normal(size=(B, M * N))) / np.sqrt(2)
+    yt = torch.as_tensor(y, device="cuda").to(s.cdtype).contiguous()
+    res = s.solve(yt, pb, np.full(B, 1e-2))
+    x = res.x.cpu().numpy()
+    off, k, l, g = (t.cpu().numpy() for t in (pb.offsets, pb.k, pb.l, pb.gain))
+    for f in range(B):
+        taps = [orc.Tap(int(a), int(b), complex(c)) for a, b, c in zip(k[off[f]:off[f + 1]], l[off[f]:off[f + 1]],
+                                                                       g[off[f]:off[f + 1]])]
+        xr, _ = orc.cga(orc.build_tables(taps, M, N), y[f], 10, 1e-2)
+        assert rel_l2(x[f], xr) < REL_L2_FP32, (f, rel_l2(x[f], xr))
