@@ -192,7 +192,7 @@ __device__ __forceinline__ void tap_elem(const SolveArgs& a, const TmThr& th, co
   const uint32_t colad = map_rank(smem_addr(buf + (size_t)lc * a.CS + a.H), (uint32_t)own);
   const int sg = HERM ? dl : -dl;  // coefficient phase exponent per row
   if (halo) {
-    constexpr int BS = R < 8 ? R : 8;  // rows per exact re-anchor
+    constexpr int BS = R;  // rows per exact re-anchor (16-step fp32 recurrence: ~1e-6 relative)
     const V step = twid_tm(sm, wrap1(sg, MN));
     int a0 = th.r0 + s;
     V hw = h0;
@@ -220,7 +220,8 @@ __device__ __forceinline__ void tap_elem(const SolveArgs& a, const TmThr& th, co
     }
 #pragma unroll
     for (int b = 0; b < R; b += BS) {
-      V c = cmul(hw, twid_tm(sm, wrap1(sg * (th.r0 + b) % MN, MN)));
+      // |sg (r0 + b)| < |d_l| M <= MN / 2: one conditional add reduces it mod MN
+      V c = cmul(hw, twid_tm(sm, wrap1(sg * (th.r0 + b), MN)));
 #pragma unroll
       for (int i = 0; i < BS; ++i) {
         Acc<float>::mac(acc[b + i], c, v[b + i]);
