@@ -56,3 +56,36 @@ def test_documented_stub_solves_reference_cases():
         np.testing.assert_allclose(tr.c_norm, d[p + "c_norm"], rtol=1e-9, atol=1e-12 * d[p + "c_norm"][0])
         assert tr.exact_converged == bool(d[p + "exact"])
         assert tr.mvm_count == int(d[p + "mvm_count"])
+
+
+def test_documented_frontend_stub_matches_reference_goldens():
+    """INTEGRATION.md's host-pointer front-end stub (Option B'), executed as
+    written, against the reference's own pilot DZT and detect_paths outputs
+    (tests/golden/frontend.npz, made by running ddlink)."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2604_02266_b200 as b200
+    text = (ROOT / "INTEGRATION.md").read_text()
+    m = re.search(r"```python\n# ddlink/_b200_frontend\.py\n(.*?)```", text, re.S)
+    assert m, "INTEGRATION.md lost its front-end stub"
+    code = m.group(1).replace("/path/to/paper_2604_02266_b200/libddb.so",
+                              str(ROOT / "paper_2604_02266_b200" / "libddb.so"))
+    pkg = types.ModuleType("ddlink_fe")
+    pkg.__path__ = []
+    sp = types.ModuleType("ddlink_fe.sparse")
+    sp.DominantPath = b200.DominantPath
+    mod = types.ModuleType("ddlink_fe._b200_frontend")
+    mod.__package__ = "ddlink_fe"
+    sys.modules.update({"ddlink_fe": pkg, "ddlink_fe.sparse": sp, "ddlink_fe._b200_frontend": mod})
+    exec(compile(code, "INTEGRATION.md:_b200_frontend.py", "exec"), mod.__dict__)
+    d = load_golden("frontend")
+    for tag in ("c1", "c3"):
+        M, N = (int(v) for v in d[tag + "_meta"][:2])
+        cfg = b200.GridConfig(M, N)
+        off = d[tag + "_path_off"]
+        for f in range(d[tag + "_pilot_rx"].shape[0]):
+            ypil = mod.dzt_gemm(d[tag + "_pilot_rx"][f], b200.build_zak_kernel(N), cfg)
+            np.testing.assert_allclose(ypil, d[tag + "_ypil"][f], atol=1e-12 * np.abs(d[tag + "_ypil"][f]).max())
+            taps = mod.detect_paths(d[tag + "_heff"][f], float(d[tag + "_theta"]), cfg)
+            assert [(t.k_p, t.l_p) for t in taps] == list(zip(d[tag + "_path_k"][off[f]:off[f + 1]].tolist(),
+                                                              d[tag + "_path_l"][off[f]:off[f + 1]].tolist()))
