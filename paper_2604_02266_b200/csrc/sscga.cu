@@ -440,8 +440,52 @@ __device__ __forceinline__ int epilogue(const SolveArgs& a, const Vec<T> (&xv)[X
   return errs;
 }
 
-template <typename T, int LC>
-__global__ void __launch_bounds__(sscga_max_threads(sizeof(T), LC), 1) sscga_kernel(const SolveArgs a) {
+// Plans compiled with their geometry as constants (SPEC > 0, as in sscga_tm.cu):
+// the fp64 drop-in default at the headline grid and at the harness's default
+// (32, 32) grid, and (128, 32).  Picked by exact match at launch.
+struct RowSpec {
+  int eb, LC, M, N, C, Lcta, S, RS, H, TL, TH, pcap, tcols, active;
+};
+constexpr RowSpec kRowSpecs[] = {
+    {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0},
+    {8, 8, 512, 32, 4, 8, 760, 9, 248, 128, 128, 64, 512, 512},   // 1: fp64 (512, 32)
+    {8, 4, 32, 32, 1, 32, 64, 33, 32, 32, 32, 64, 128, 256},      // 2: fp64 (32, 32), SimConfig's default
+    {8, 8, 128, 32, 1, 32, 209, 33, 81, 64, 64, 64, 512, 512},    // 3: fp64 (128, 32)
+};
+constexpr int kNumRowSpecs = sizeof(kRowSpecs) / sizeof(kRowSpecs[0]);
+inline int row_spec_index(const SolveArgs& a, int eb, int lc) {
+  if (getenv("DDB_NO_SPEC")) return 0;
+  for (int i = 1; i < kNumRowSpecs; ++i) {
+    const RowSpec& p = kRowSpecs[i];
+    if (eb == p.eb && lc == p.LC && a.M == p.M && a.N == p.N && a.C == p.C && a.Lcta == p.Lcta && a.S == p.S &&
+        a.RS == p.RS && a.H == p.H && a.TL == p.TL && a.TH == p.TH && a.pcap == p.pcap && a.tcols == p.tcols &&
+        a.active_threads == p.active)
+      return i;
+  }
+  return 0;
+}
+
+template <typename T, int LC, int SPEC = 0>
+__global__ void __launch_bounds__(sscga_max_threads(sizeof(T), LC), 1) sscga_kernel(const SolveArgs a_) {
+  SolveArgs a = a_;
+  if constexpr (SPEC > 0) {
+    constexpr RowSpec P = kRowSpecs[SPEC];
+    a.M = P.M;
+    a.N = P.N;
+    a.MN = P.M * P.N;
+    a.K0 = P.M / 2;
+    a.L0 = P.N / 2;
+    a.C = P.C;
+    a.Lcta = P.Lcta;
+    a.S = P.S;
+    a.RS = P.RS;
+    a.H = P.H;
+    a.TL = P.TL;
+    a.TH = P.TH;
+    a.pcap = P.pcap;
+    a.tcols = P.tcols;
+    a.active_threads = P.active;
+  }
   using V = Vec<T>;
   using A = Acc<T>;
   extern __shared__ __align__(16) unsigned char smem[];
@@ -790,9 +834,9 @@ __global__ void __launch_bounds__(sscga_max_threads(sizeof(T), LC), 1) sscga_ker
   if (warp == 0) tmem_dealloc(tbase, (uint32_t)a.tcols);
 }
 
-template <typename T, int LC>
-static cudaError_t launch_lc(SolveArgs a, const LaunchShape& s, cudaStream_t st) {
-  auto kern = sscga_kernel<T, LC>;
+template <typename T, int LC, int SPEC = 0>
+static cudaError_t launch_lc_spec(SolveArgs a, const LaunchShape& s, cudaStream_t st) {
+  auto kern = sscga_kernel<T, LC, SPEC>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, s.smem);
   if (e != cudaSuccess) return e;
   e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
@@ -825,6 +869,19 @@ static cudaError_t launch_lc(SolveArgs a, const LaunchShape& s, cudaStream_t st)
   // (compute-sanitizer runs: synccheck misreports cluster launches, profiles/r2_sanitizer.md)
   if (s.cluster == 1 && getenv("DDB_NO_CLUSTER_ATTR")) cfg.numAttrs = 0;
   return cudaLaunchKernelEx(&cfg, kern, a);
+}
+
+template <typename T, int LC>
+static cudaError_t launch_lc(SolveArgs a, const LaunchShape& s, cudaStream_t st) {
+  if constexpr (sizeof(T) == 8) {
+    switch (row_spec_index(a, (int)sizeof(T), LC)) {
+      case 1: if constexpr (LC == 8) return launch_lc_spec<T, LC, 1>(a, s, st); break;
+      case 2: if constexpr (LC == 4) return launch_lc_spec<T, LC, 2>(a, s, st); break;
+      case 3: if constexpr (LC == 8) return launch_lc_spec<T, LC, 3>(a, s, st); break;
+      default: break;
+    }
+  }
+  return launch_lc_spec<T, LC>(a, s, st);
 }
 
 template <typename T>
