@@ -238,9 +238,27 @@ __device__ __forceinline__ void block_pair_sum(Vec<T> v, Vec<T>* dst) {
   Vec<T>* tw = thi + a.TH;                                 \
   GTap<T>* taps = reinterpret_cast<GTap<T>*>(tw + a.N);
 
+// SPEC 1: the paper's real-time grid (16384, 32) with its geometry as
+// constants (index arithmetic by shifts, as in sscga_tm.cu's kSpecs); picked by
+// the launcher when the problem matches.
+constexpr int kGSpecM = 16384, kGSpecN = 32;
+#define G_SPEC_ARGS                                              \
+  GArgs<T> a = a_;                                               \
+  if constexpr (SPEC == 1) {                                     \
+    a.M = kGSpecM;                                               \
+    a.N = kGSpecN;                                               \
+    a.MN = kGSpecM * kGSpecN;                                    \
+    a.K0 = kGSpecM / 2;                                          \
+    a.L0 = kGSpecN / 2;                                          \
+    a.nblk = (kGSpecM * kGSpecN + kGBlock - 1) / kGBlock;        \
+    a.TL = 1024;                                                 \
+    a.TH = 512;                                                  \
+  }
+
 // b = H^H y -> c (equalize.py:52-57), x = 0, partial ||c||^2.
-template <typename T>
-__global__ void __launch_bounds__(kGThreads, 6) g_init(const GArgs<T> a) {
+template <typename T, int SPEC = 0>
+__global__ void __launch_bounds__(kGThreads, 6) g_init(const GArgs<T> a_) {
+  G_SPEC_ARGS
   using V = Vec<T>;
   G_SMEM_DECL
   const int f = blockIdx.y, blk = blockIdx.x;
@@ -262,8 +280,9 @@ __global__ void __launch_bounds__(kGThreads, 6) g_init(const GArgs<T> a) {
 }
 
 // u = H c + beta u_old, p = c + beta p_old (u-recurrence), partials (||u||^2, ||p||^2).
-template <typename T>
-__global__ void __launch_bounds__(kGThreads, 6) g_fwd(const GArgs<T> a, int it) {
+template <typename T, int SPEC = 0>
+__global__ void __launch_bounds__(kGThreads, 6) g_fwd(const GArgs<T> a_, int it) {
+  G_SPEC_ARGS
   using V = Vec<T>;
   G_SMEM_DECL
   const int f = blockIdx.y, blk = blockIdx.x;
@@ -291,8 +310,9 @@ __global__ void __launch_bounds__(kGThreads, 6) g_fwd(const GArgs<T> a, int it) 
 }
 
 // ap = H^H u + lam p; x += alpha p; c -= alpha ap; partial ||c||^2.
-template <typename T>
-__global__ void __launch_bounds__(kGThreads, 6) g_herm(const GArgs<T> a, int it) {
+template <typename T, int SPEC = 0>
+__global__ void __launch_bounds__(kGThreads, 6) g_herm(const GArgs<T> a_, int it) {
+  G_SPEC_ARGS
   using V = Vec<T>;
   G_SMEM_DECL
   const int f = blockIdx.y, blk = blockIdx.x;
@@ -455,9 +475,10 @@ __device__ __forceinline__ Vec<T> p_fold(const GArgs<T>& a, int f, int ph) {
   return t;
 }
 
-template <typename T, int BA>
-__global__ void __launch_bounds__(kGThreads) g_persist(const GArgs<T> a, uint8_t* labels, float* llr, const T* nvar,
+template <typename T, int BA, int SPEC = 0>
+__global__ void __launch_bounds__(kGThreads) g_persist(const GArgs<T> a_, uint8_t* labels, float* llr, const T* nvar,
                                                        const uint8_t* txl, int txpk, int* berr) {
+  G_SPEC_ARGS
   using V = Vec<T>;
   namespace cg = cooperative_groups;
   cg::grid_group grid = cg::this_grid();
@@ -699,12 +720,14 @@ cudaError_t launch_sscga_global(const SolveArgs& s, void* ws, cudaStream_t st) {
   a.snaps = reinterpret_cast<V*>(s.snaps);
   if (s.B == 0) return cudaSuccess;
   const size_t smem = (size_t)(a.TL + a.TH + a.N) * sizeof(V) + kGTaps * sizeof(GTap<T>);
+  const bool spec = a.M == kGSpecM && a.N == kGSpecN && a.TL == 1024 && a.TH == 512 && !getenv("DDB_NO_SPEC");
   cudaError_t e;
   if (s.B <= kPersistB && !getenv("DDB_NO_PERSIST")) {
     // one cooperative launch: grid = co-resident blocks, capped at the work
     const size_t psmem = (size_t)(a.TL + a.TH + a.N) * sizeof(V) + (size_t)s.B * kGTaps * sizeof(GTap<T>);
     const T* nvar = reinterpret_cast<const T*>(s.nvar);
-    void* kfn = s.bps == 2 ? (void*)g_persist<T, 1> : (s.bps == 6 ? (void*)g_persist<T, 3> : (void*)g_persist<T, 2>);
+    void* kfn = spec ? (s.bps == 2 ? (void*)g_persist<T, 1, 1> : (s.bps == 6 ? (void*)g_persist<T, 3, 1> : (void*)g_persist<T, 2, 1>))
+                     : (s.bps == 2 ? (void*)g_persist<T, 1> : (s.bps == 6 ? (void*)g_persist<T, 3> : (void*)g_persist<T, 2>));
     // attribute + occupancy query once per (kernel, shared memory, device): host time is latency here
     struct Occ { void* fn; size_t smem; int dev, sms, per_sm; };
     static thread_local Occ occ = {nullptr, 0, -1, 0, 0};
@@ -729,16 +752,19 @@ cudaError_t launch_sscga_global(const SolveArgs& s, void* ws, cudaStream_t st) {
       return cudaLaunchCooperativeKernel(kfn, dim3(blocks), dim3(kGThreads), args, psmem, st);
     }
   }
-  if ((e = cudaFuncSetAttribute(g_init<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem))) return e;
-  if ((e = cudaFuncSetAttribute(g_fwd<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem))) return e;
-  if ((e = cudaFuncSetAttribute(g_herm<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem))) return e;
+  auto ki = spec ? g_init<T, 1> : g_init<T>;
+  auto kf = spec ? g_fwd<T, 1> : g_fwd<T>;
+  auto kh = spec ? g_herm<T, 1> : g_herm<T>;
+  if ((e = cudaFuncSetAttribute(ki, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem))) return e;
+  if ((e = cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem))) return e;
+  if ((e = cudaFuncSetAttribute(kh, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem))) return e;
   const dim3 grid(a.nblk, s.B);
-  g_init<T><<<grid, kGThreads, smem, st>>>(a);
+  ki<<<grid, kGThreads, smem, st>>>(a);
   g_fold<T><<<s.B, kGThreads, 0, st>>>(a, 0, 0);
   for (int it = 0; it < s.iters; ++it) {
-    g_fwd<T><<<grid, kGThreads, smem, st>>>(a, it);
+    kf<<<grid, kGThreads, smem, st>>>(a, it);
     g_fold<T><<<s.B, kGThreads, 0, st>>>(a, 1, it);
-    g_herm<T><<<grid, kGThreads, smem, st>>>(a, it);
+    kh<<<grid, kGThreads, smem, st>>>(a, it);
     g_fold<T><<<s.B, kGThreads, 0, st>>>(a, 2, it);
   }
   g_finish<T><<<(s.B + 127) / 128, 128, 0, st>>>(a);
