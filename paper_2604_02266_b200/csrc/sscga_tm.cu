@@ -849,6 +849,7 @@ __global__ void __launch_bounds__(MAXT, 1) sscga_tm_kernel(const SolveArgs a_) {
 #pragma unroll
         for (int i = 0; i < E; ++i) z[i] = make_float2(0.f, 0.f);
         tm_st<E>(tX(c0), z);  // x = 0
+        tm_st<E>(tP(c0), z);  // p = 0: the first update is then p = c + 0 p like every other
       }
       // warm L2 with this cluster's next frame (y, TX labels) while this one solves
       if (fnext >= 0) {
@@ -915,21 +916,21 @@ __global__ void __launch_bounds__(MAXT, 1) sscga_tm_kernel(const SolveArgs a_) {
 #pragma unroll
         for (int c0 = 0; c0 < R; c0 += E) {
           uint32_t ru[2 * E], rc[2 * E], rp[2 * E];
+          // iteration 0 takes the same form with beta = 0: u still holds y and
+          // p was zeroed at setup, so u = Hc + 0 y and p = c + 0 p are exact
           tm_ld<E>(rb + 2 * c0, rc);
-          if (it > 0) {
-            tm_ld<E>(rb + 2 * (a.G + c0), ru);
-            tm_ld<E>(rb + 2 * (2 * a.G + c0), rp);
-            tmem_wait_ld_tie<2 * E>(ru);
-            tmem_wait_ld_tie<2 * E>(rp);
-          }
+          tm_ld<E>(rb + 2 * (a.G + c0), ru);
+          tm_ld<E>(rb + 2 * (2 * a.G + c0), rp);
+          tmem_wait_ld_tie<2 * E>(ru);
+          tmem_wait_ld_tie<2 * E>(rp);
           tmem_wait_ld_tie<2 * E>(rc);
           V w[E], pv[E];
 #pragma unroll
           for (int i = 0; i < E; ++i) {
             const V hc = unpack2(acc[c0 + i]);
             const V cr = tm_get_v<E>(rc, i);
-            w[i] = it == 0 ? hc : axpy(hc, beta, tm_get_v<E>(ru, i));
-            pv[i] = it == 0 ? cr : axpy(cr, beta, tm_get_v<E>(rp, i));
+            w[i] = axpy(hc, beta, tm_get_v<E>(ru, i));
+            pv[i] = axpy(cr, beta, tm_get_v<E>(rp, i));
             nacc(nu, w[i]);
             nacc(np, pv[i]);
           }
