@@ -550,6 +550,7 @@ __device__ __forceinline__ int epi_pass(const SolveArgs& a, const V* stg, int M,
 __device__ __forceinline__ bool frame_lean(const SolveArgs& a, int f) {
   const int P0 = __ldg(a.off + f), P = __ldg(a.off + f + 1) - P0;
   if (P <= 0) return true;
+  if (a.snaps) return false;  // per-iteration snapshots (cfg.profile) are written by the general kernel only
   if (P > 32 || P > a.pcap) return false;
   int dmin = INT_MAX, dmax = INT_MIN;
   bool dl0 = true;
@@ -988,7 +989,7 @@ __global__ void __launch_bounds__(MAXT, 1) sscga_tm_kernel(const SolveArgs a_) {
           tm_st<E>(rb + 2 * (3 * a.G + c0), xv);
           tm_st<E>(rb + 2 * c0, cv);
           put_col<E>(ccol, th.r0 + c0, M, lo_c, hi_c, twl, cv);
-          if (a.snaps) {
+          if (GEN && a.snaps) {  // profile runs: every frame goes to the general kernel (frame_lean)
             V* sp = reinterpret_cast<V*>(a.snaps) + ((size_t)f * a.iters + it) * a.MN + (qown - fo) + c0;
 #pragma unroll
             for (int i = 0; i < E; ++i) sp[i] = xv[i];
