@@ -307,7 +307,7 @@ __device__ __forceinline__ void mvm_local(const SolveArgs& a, const TmThr& th, c
                                           uint32_t tv, const V* vcol, U64 (&acc)[R]) {
 #pragma unroll
   for (int i = 0; i < R; ++i) acc[i] = 0ull;
-  if (fs.masks) {
+  if (!GEN || fs.masks) {  // lean frames always have their masks (P <= 32)
     const uint32_t* mk = fs.mk[th.jr / R] + (HERM ? 3 : 0);
     const uint32_t mt = mk[0], ms = mk[1];
     tmem_taps<R, HERM>(th.jr, sm, tv, mt, acc);
@@ -891,7 +891,7 @@ __global__ void __launch_bounds__(MAXT, 1) sscga_tm_kernel(const SolveArgs a_) {
       red_stage<float>(make_float2(nrm.x + nrm.y, 0.f), red + (2 + par1) * kPushSlots, warp, lane);
     }
     if constexpr (PROF) prof_mark(a.prof, psm, kArrive);
-    TM_WT(2, tm_arrive_red<PROF>(a.C, red + (2 + par1) * kPushSlots, nwarps, warp, lane, rank, !fs.remote, wt));  // c = b published
+    TM_WT(2, tm_arrive_red<PROF>(a.C, red + (2 + par1) * kPushSlots, nwarps, warp, lane, rank, !GEN || !fs.remote, wt));  // c = b published
     if constexpr (PROF) prof_mark(a.prof, psm, kMvmLocal);
     TM_WT(0, mvm_local<R, false, GEN>(a, th, sm, fs, tC(0) - 2 * th.jr, ccol, acc));
     if constexpr (PROF) prof_mark(a.prof, psm, kWait);
@@ -942,7 +942,7 @@ __global__ void __launch_bounds__(MAXT, 1) sscga_tm_kernel(const SolveArgs a_) {
         red_stage<float>(make_float2(nu.x + nu.y, np.x + np.y), red + par0 * kPushSlots, warp, lane);
       }
       if constexpr (PROF) prof_mark(a.prof, psm, kArrive);
-      TM_WT(2, tm_arrive_red<PROF>(a.C, red + par0 * kPushSlots, nwarps, warp, lane, rank, !fs.remote, wt));  // u published
+      TM_WT(2, tm_arrive_red<PROF>(a.C, red + par0 * kPushSlots, nwarps, warp, lane, rank, !GEN || !fs.remote, wt));  // u published
       // ap = H^H u + lam p;  x += alpha p;  c -= alpha ap      (equalize.py:60-70)
       if constexpr (PROF) prof_mark(a.prof, psm, kMvmLocal);
       TM_WT(1, mvm_local<R, true, GEN>(a, th, sm, fs, tU(0) - 2 * th.jr, ucol, acc));
@@ -998,7 +998,7 @@ __global__ void __launch_bounds__(MAXT, 1) sscga_tm_kernel(const SolveArgs a_) {
         red_stage<float>(make_float2(nc.x + nc.y, 0.f), red + (2 + par1) * kPushSlots, warp, lane);
       }
       if constexpr (PROF) prof_mark(a.prof, psm, kArrive);
-      TM_WT(2, tm_arrive_red<PROF>(a.C, red + (2 + par1) * kPushSlots, nwarps, warp, lane, rank, !fs.remote, wt));  // c published
+      TM_WT(2, tm_arrive_red<PROF>(a.C, red + (2 + par1) * kPushSlots, nwarps, warp, lane, rank, !GEN || !fs.remote, wt));  // c published
       if constexpr (PROF) prof_mark(a.prof, psm, kMvmLocal);
       if (it + 1 < a.iters) TM_WT(0, mvm_local<R, false, GEN>(a, th, sm, fs, tC(0) - 2 * th.jr, ccol, acc));  // next H c
       if constexpr (PROF) prof_mark(a.prof, psm, kWait);
