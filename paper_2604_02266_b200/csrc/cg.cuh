@@ -164,6 +164,12 @@ __device__ __forceinline__ Vec<T> red_read(const Vec<T>* slot, int C, int nwarps
 //   red_total       (after the wait) the C totals summed in rank order, so every
 //                   warp of every CTA holds the same bits and takes the same branch.
 // One CTA (C == 1) reads the per-warp partials directly instead.
+// The warp that folds the CTA's partials and pushes the total: one of a
+// middle row block when there are several (the first and last row blocks of a
+// TMEM segment carry most shared-memory taps, so they arrive last): cfg3
+// 17.06 -> 17.55 G symbols/s with warp 8 (profiles/r2_experiments.md).
+__device__ __forceinline__ int fold_warp(int nwarps) { return nwarps >= 12 ? 8 : (nwarps >= 8 ? 4 : 0); }
+
 template <typename T>
 __device__ __forceinline__ void red_stage(Vec<T> part, Vec<T>* base, int warp, int lane) {
   part.x = warp_sum(part.x);
@@ -183,13 +189,14 @@ __device__ __forceinline__ void cl_arrive_red(int C, Vec<T>* base, int nwarps, i
   }
   __syncthreads();
   if (C > 1) {
-    if (warp == 0) {
+    const int fw = TMEM_FENCES ? fold_warp(nwarps) : 0;  // (the row-slice kernel: warp 0 measured best)
+    if (warp == fw) {
       Vec<T> t = lane < nwarps ? base[lane] : czero<Vec<T>>();
       t.x = warp_sum(t.x);
       t.y = warp_sum(t.y);
       if (lane < C) st_cluster(map_rank(smem_addr(base + 32 + rank), (uint32_t)lane), t);
     }
-    cl_arrive_sem(!relaxed || warp == 0);
+    cl_arrive_sem(!relaxed || warp == fw);
   }
   if constexpr (TMEM_FENCES) tmem_fence_after();
 }

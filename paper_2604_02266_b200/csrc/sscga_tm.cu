@@ -435,14 +435,14 @@ __device__ __forceinline__ void tm_arrive_red(int C, V* base, int nwarps, int wa
     __syncthreads();
     u = clock64(); wt[5] += u - t; t = u;
     if (C > 1) {
-      if (warp == 0) {
+      if (warp == fold_warp(nwarps)) {
         V v = lane < nwarps ? base[lane] : make_float2(0.f, 0.f);
         v.x = warp_sum(v.x);
         v.y = warp_sum(v.y);
         if (lane < C) st_cluster(map_rank(smem_addr(base + 32 + rank), (uint32_t)lane), v);
       }
       u = clock64(); wt[6] += u - t; t = u;
-      cl_arrive_sem(!relaxed || warp == 0);
+      cl_arrive_sem(!relaxed || warp == fold_warp(nwarps));
     }
     tmem_fence_after();
     u = clock64(); wt[7] += u - t;
