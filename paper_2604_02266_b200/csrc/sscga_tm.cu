@@ -451,8 +451,21 @@ __device__ __forceinline__ void tm_arrive_red(int C, V* base, int nwarps, int wa
 
 // Epilogue for E equalized symbols of rows rr.. (contiguous in q): x_hat,
 // hard labels, max-log LLRs and the bit-error count vs TX labels.
+// The transmitted-label word of the 4 symbols at q0 (bps bits each when packed).
+template <int BA>
+__device__ __forceinline__ uint32_t tx_word(const SolveArgs& a, size_t q0) {
+  if (!a.txl || BA == 0) return 0u;
+  if (!a.txpk) return __ldg(reinterpret_cast<const uint32_t*>(a.txl + q0));
+  if constexpr (BA <= 2)
+    return BA == 2 ? (uint32_t)__ldg(reinterpret_cast<const uint16_t*>(a.txl + (q0 >> 1)))
+                   : (uint32_t)__ldg(a.txl + (q0 >> 2));
+  return 0u;
+}
+
+// txpre: the TX word, already loaded (epi_pass issues them before the x staging)
 template <int BA, int E>
-__device__ __forceinline__ int tm_epilogue(const SolveArgs& a, const V (&xv)[E], size_t q0, float scale) {
+__device__ __forceinline__ int tm_epilogue(const SolveArgs& a, const V (&xv)[E], size_t q0, float scale,
+                                           uint32_t txpre) {
   V* xo = reinterpret_cast<V*>(a.x) + q0;
 #pragma unroll
   for (int i = 0; i < E / 2; ++i)
@@ -464,13 +477,7 @@ __device__ __forceinline__ int tm_epilogue(const SolveArgs& a, const V (&xv)[E],
     // slicing (issued after the label / LLR stores it could not be hoisted
     // above them -- the pointers may alias as far as the compiler knows)
     static_assert(E == 4, "one TX word per call");
-    uint32_t txw = 0;
-    if (a.txl) {
-      if (!a.txpk) txw = __ldg(reinterpret_cast<const uint32_t*>(a.txl + q0));
-      else if constexpr (BA <= 2)
-        txw = BA == 2 ? (uint32_t)__ldg(reinterpret_cast<const uint16_t*>(a.txl + (q0 >> 1)))
-                      : (uint32_t)__ldg(a.txl + (q0 >> 2));
-    }
+    const uint32_t txw = txpre;
     uint8_t lab[E];
 #pragma unroll
     for (int i = 0; i < E; ++i) {
@@ -509,18 +516,33 @@ __device__ __forceinline__ int tm_epilogue(const SolveArgs& a, const V (&xv)[E],
 }
 
 // Coalesced epilogue pass over the CTA's staged x (column-major, stride M + 2).
-template <int BA>
-__device__ __forceinline__ int epi_pass(const SolveArgs& a, const V* stg, int M, size_t qb, float scale) {
+// The thread's TX words for its (at most R / 4) passes, loaded before the x
+// staging and its barrier so the L2 round trips overlap them.
+template <int BA, int NP>
+__device__ __forceinline__ void tx_preload(const SolveArgs& a, int M, size_t qb, uint32_t (&txp)[NP]) {
+  const int tot = a.Lcta * M;
+#pragma unroll
+  for (int k = 0; k < NP; ++k) {
+    const int e = 4 * ((int)threadIdx.x + k * (int)blockDim.x);
+    txp[k] = e < tot ? tx_word<BA>(a, qb + e) : 0u;
+  }
+}
+
+template <int BA, int NP>
+__device__ __forceinline__ int epi_pass(const SolveArgs& a, const V* stg, int M, size_t qb, float scale,
+                                        const uint32_t (&txp)[NP]) {
   const int tot = a.Lcta * M;
   int errs = 0;
-#pragma unroll 2
-  for (int e = 4 * (int)threadIdx.x; e < tot; e += 4 * (int)blockDim.x) {
+#pragma unroll
+  for (int k = 0; k < NP; ++k) {
+    const int e = 4 * ((int)threadIdx.x + k * (int)blockDim.x);
+    if (e >= tot) break;
     const int cl = e / M;
     const float4* sp = reinterpret_cast<const float4*>(stg + cl * (M + 2) + (e - cl * M));
     const float4 w0 = sp[0], w1 = sp[1];
     const V xv[4] = {make_float2(w0.x, w0.y), make_float2(w0.z, w0.w), make_float2(w1.x, w1.y),
                      make_float2(w1.z, w1.w)};
-    errs += tm_epilogue<BA, 4>(a, xv, qb + e, scale);
+    errs += tm_epilogue<BA, 4>(a, xv, qb + e, scale, txp[k]);
   }
   return errs;
 }
@@ -1027,6 +1049,15 @@ __global__ void __launch_bounds__(MAXT, 1) sscga_tm_kernel(const SolveArgs a_) {
       const float nv = a.nvar ? reinterpret_cast<const float*>(a.nvar)[f] : lam;
       scale = nv > 0.f ? 1.f / nv : 1.f;
     }
+    const size_t qb = fo + (size_t)rank * a.Lcta * M;
+    constexpr int NP = R / 4 > 0 ? R / 4 : 1;  // epilogue passes per thread: Lcta M / (4 threads) = R / 4
+    uint32_t txp[NP];
+    switch (a.bps) {
+      case 2: tx_preload<1, NP>(a, M, qb, txp); break;
+      case 4: tx_preload<2, NP>(a, M, qb, txp); break;
+      case 6: tx_preload<3, NP>(a, M, qb, txp); break;
+      default: for (int k = 0; k < NP; ++k) txp[k] = 0u; break;
+    }
     // x -> shared staging in q order (column-major, stride M + 2: conflict-free
     // 16-byte stores), then every thread takes 4 consecutive symbols at a time
     // so the x_hat / LLR / label stores and TX label loads are coalesced.  The
@@ -1047,14 +1078,11 @@ __global__ void __launch_bounds__(MAXT, 1) sscga_tm_kernel(const SolveArgs a_) {
     }
     __syncthreads();
     int errs = 0;
-    {
-      const size_t qb = fo + (size_t)rank * a.Lcta * M;
-      switch (a.bps) {
-        case 0: epi_pass<0>(a, sm.c, M, qb, scale); break;
-        case 2: errs = epi_pass<1>(a, sm.c, M, qb, scale); break;
-        case 4: errs = epi_pass<2>(a, sm.c, M, qb, scale); break;
-        default: errs = epi_pass<3>(a, sm.c, M, qb, scale); break;
-      }
+    switch (a.bps) {
+      case 0: epi_pass<0, NP>(a, sm.c, M, qb, scale, txp); break;
+      case 2: errs = epi_pass<1, NP>(a, sm.c, M, qb, scale, txp); break;
+      case 4: errs = epi_pass<2, NP>(a, sm.c, M, qb, scale, txp); break;
+      default: errs = epi_pass<3, NP>(a, sm.c, M, qb, scale, txp); break;
     }
     if (a.berr) {
       errs = warp_sum(errs);
