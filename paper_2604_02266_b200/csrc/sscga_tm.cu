@@ -442,7 +442,8 @@ __device__ __forceinline__ void tm_arrive_red(int C, V* base, int nwarps, int wa
         if (lane < C) st_cluster(map_rank(smem_addr(base + 32 + rank), (uint32_t)lane), v);
       }
       u = clock64(); wt[6] += u - t; t = u;
-      cl_arrive_sem(!relaxed || warp == fold_warp(nwarps));
+      (void)relaxed;
+      cl_arrive_sem(warp == fold_warp(nwarps));
     }
     tmem_fence_after();
     u = clock64(); wt[7] += u - t;

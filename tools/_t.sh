@@ -1,4 +1,5 @@
 cd "${GRAFT_REPO_ROOT:-/root/repo}"
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:sscga -s 6 -c 1 -o gpurun_out/r2y_full_cfg3 -f python bench.py --config cfg3 --steps 1 --warmup 3 --no-e2e --no-cpu --no-latency --no-frontend --no-dropin --no-geometry > /dev/null 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:sscga -s 7 -c 1 -o gpurun_out/r2y_full_cfg3det -f python bench.py --config cfg3det --steps 1 --warmup 3 --no-e2e --no-cpu --no-latency --no-frontend --no-dropin --no-geometry > /dev/null 2>&1
-ls gpurun_out/r2y*
+export DDB_LIB=paper_2604_02266_b200/libddb_sr.so
+for i in 1 2 3; do timeout 900 python -m pytest -q -x tests/test_gpu_parity.py tests/test_sweep_parity.py -k "random or batched or sweep or cfg4 or criterion or device_receiver or frontend or synth" 2>&1 | tail -1; done
+unset DDB_LIB
+CFGS="cfg3det cfg4 cfg3rand cfg3" TAG=sr bash tools/ab.sh sr
