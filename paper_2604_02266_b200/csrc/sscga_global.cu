@@ -241,18 +241,28 @@ __device__ __forceinline__ void block_pair_sum(Vec<T> v, Vec<T>* dst) {
 // SPEC 1: the paper's real-time grid (16384, 32) with its geometry as
 // constants (index arithmetic by shifts, as in sscga_tm.cu's kSpecs); picked by
 // the launcher when the problem matches.
-constexpr int kGSpecM = 16384, kGSpecN = 32;
+struct GSpec {
+  int M, N, TL, TH;
+};
+constexpr GSpec kGSpecs[] = {{0, 0, 0, 0}, {16384, 32, 1024, 512}, {1024, 64, 256, 256}};
+inline int g_spec_index(int M, int N, int TL, int TH) {
+  if (getenv("DDB_NO_SPEC")) return 0;
+  for (int i = 1; i < (int)(sizeof(kGSpecs) / sizeof(kGSpecs[0])); ++i)
+    if (M == kGSpecs[i].M && N == kGSpecs[i].N && TL == kGSpecs[i].TL && TH == kGSpecs[i].TH) return i;
+  return 0;
+}
 #define G_SPEC_ARGS                                              \
   GArgs<T> a = a_;                                               \
-  if constexpr (SPEC == 1) {                                     \
-    a.M = kGSpecM;                                               \
-    a.N = kGSpecN;                                               \
-    a.MN = kGSpecM * kGSpecN;                                    \
-    a.K0 = kGSpecM / 2;                                          \
-    a.L0 = kGSpecN / 2;                                          \
-    a.nblk = (kGSpecM * kGSpecN + kGBlock - 1) / kGBlock;        \
-    a.TL = 1024;                                                 \
-    a.TH = 512;                                                  \
+  if constexpr (SPEC > 0) {                                      \
+    constexpr GSpec P = kGSpecs[SPEC];                           \
+    a.M = P.M;                                                   \
+    a.N = P.N;                                                   \
+    a.MN = P.M * P.N;                                            \
+    a.K0 = P.M / 2;                                              \
+    a.L0 = P.N / 2;                                              \
+    a.nblk = (P.M * P.N + kGBlock - 1) / kGBlock;                \
+    a.TL = P.TL;                                                 \
+    a.TH = P.TH;                                                 \
   }
 
 // b = H^H y -> c (equalize.py:52-57), x = 0, partial ||c||^2.
@@ -720,14 +730,15 @@ cudaError_t launch_sscga_global(const SolveArgs& s, void* ws, cudaStream_t st) {
   a.snaps = reinterpret_cast<V*>(s.snaps);
   if (s.B == 0) return cudaSuccess;
   const size_t smem = (size_t)(a.TL + a.TH + a.N) * sizeof(V) + kGTaps * sizeof(GTap<T>);
-  const bool spec = a.M == kGSpecM && a.N == kGSpecN && a.TL == 1024 && a.TH == 512 && !getenv("DDB_NO_SPEC");
+  const int spec = g_spec_index(a.M, a.N, a.TL, a.TH);
   cudaError_t e;
   if (s.B <= kPersistB && !getenv("DDB_NO_PERSIST")) {
     // one cooperative launch: grid = co-resident blocks, capped at the work
     const size_t psmem = (size_t)(a.TL + a.TH + a.N) * sizeof(V) + (size_t)s.B * kGTaps * sizeof(GTap<T>);
     const T* nvar = reinterpret_cast<const T*>(s.nvar);
-    void* kfn = spec ? (s.bps == 2 ? (void*)g_persist<T, 1, 1> : (s.bps == 6 ? (void*)g_persist<T, 3, 1> : (void*)g_persist<T, 2, 1>))
-                     : (s.bps == 2 ? (void*)g_persist<T, 1> : (s.bps == 6 ? (void*)g_persist<T, 3> : (void*)g_persist<T, 2>));
+    void* kfn = spec == 1 ? (s.bps == 2 ? (void*)g_persist<T, 1, 1> : (s.bps == 6 ? (void*)g_persist<T, 3, 1> : (void*)g_persist<T, 2, 1>))
+              : spec == 2 ? (s.bps == 2 ? (void*)g_persist<T, 1, 2> : (s.bps == 6 ? (void*)g_persist<T, 3, 2> : (void*)g_persist<T, 2, 2>))
+                          : (s.bps == 2 ? (void*)g_persist<T, 1> : (s.bps == 6 ? (void*)g_persist<T, 3> : (void*)g_persist<T, 2>));
     // attribute + occupancy query once per (kernel, shared memory, device): host time is latency here
     struct Occ { void* fn; size_t smem; int dev, sms, per_sm; };
     static thread_local Occ occ = {nullptr, 0, -1, 0, 0};
@@ -752,9 +763,9 @@ cudaError_t launch_sscga_global(const SolveArgs& s, void* ws, cudaStream_t st) {
       return cudaLaunchCooperativeKernel(kfn, dim3(blocks), dim3(kGThreads), args, psmem, st);
     }
   }
-  auto ki = spec ? g_init<T, 1> : g_init<T>;
-  auto kf = spec ? g_fwd<T, 1> : g_fwd<T>;
-  auto kh = spec ? g_herm<T, 1> : g_herm<T>;
+  auto ki = spec == 1 ? g_init<T, 1> : spec == 2 ? g_init<T, 2> : g_init<T>;
+  auto kf = spec == 1 ? g_fwd<T, 1> : spec == 2 ? g_fwd<T, 2> : g_fwd<T>;
+  auto kh = spec == 1 ? g_herm<T, 1> : spec == 2 ? g_herm<T, 2> : g_herm<T>;
   if ((e = cudaFuncSetAttribute(ki, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem))) return e;
   if ((e = cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem))) return e;
   if ((e = cudaFuncSetAttribute(kh, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem))) return e;
