@@ -1300,3 +1300,61 @@ def test_random_geometry_bench_taps_vs_oracle(pkg, fp32_kernel_name, monkeypatch
                                                                        g[off[f]:off[f + 1]])]
         xr, _ = orc.cga(orc.build_tables(taps, M, N), y[f], 10, 1e-2)
         assert rel_l2(x[f], xr) < REL_L2_FP32, (f, rel_l2(x[f], xr))
+
+
+@pytest.mark.parametrize("split", ["1", "0"])
+@pytest.mark.parametrize("spec", ["default", "generic"])
+def test_lean_and_general_frames_in_one_batch(pkg, split, spec, monkeypatch):
+    """One cfg3 batch mixing lean frames (Doppler-preserving taps inside the
+    halo: the lean instantiation) with frames the general one takes (Doppler
+    taps, shifts beyond the halo, more than 32 taps, an empty channel): every
+    frame against the oracle, with the split on and off (DDB_TM_SPLIT) and with
+    the compile-time-geometry instantiation or the generic one (DDB_NO_SPEC)."""
+    monkeypatch.setenv("DDB_TM_SPLIT", split)
+    if spec == "generic":
+        monkeypatch.setenv("DDB_NO_SPEC", "1")
+    M, N = 512, 32
+    rng = np.random.default_rng(17)
+    frames = []
+    for f in range(12):
+        kind = f % 4
+        if kind == 0:    # lean: Veh-A-like delays, l = L0
+            P = 6
+            k = (M // 2 + rng.choice(40, P, replace=False)) % M
+            l = np.full(P, N // 2)
+        elif kind == 1:  # Doppler-leakage taps
+            P = 8
+            k = (M // 2 + rng.integers(0, 40, P)) % M
+            l = (N // 2 + rng.integers(-1, 2, P)) % N
+        elif kind == 2:  # anywhere (shifts beyond the halo)
+            P = 6
+            bins = rng.choice(M * N, P, replace=False)
+            k, l = bins // N, bins % N
+        else:            # many taps, or none
+            P = 40 if f == 3 else 0
+            bins = rng.choice(M * N, P, replace=False)
+            k, l = bins // N, bins % N
+        g = rng.uniform(0.05, 0.3, P) * np.exp(2j * np.pi * rng.random(P))
+        if P:
+            g[0] = 1.0
+        frames.append((np.asarray(k), np.asarray(l), g))
+    off = np.concatenate([[0], np.cumsum([len(fr[0]) for fr in frames])])
+    k = np.concatenate([fr[0] for fr in frames]).astype(np.int32)
+    l = np.concatenate([fr[1] for fr in frames]).astype(np.int32)
+    g = np.concatenate([fr[2] for fr in frames])
+    B = len(frames)
+    y = rng.normal(size=(B, M * N)) + 1j * rng.normal(size=(B, M * N))
+    s = pkg.SsCgaSolver(M, N, 10, precision="fp32")
+    paths = pkg.PathBatch.from_arrays(off, k, l, g, cdtype=s.cdtype)
+    yt = torch.as_tensor(y, device="cuda").to(s.cdtype).contiguous()
+    res = s.solve(yt, paths, np.full(B, 1e-2))
+    x = res.x.cpu().numpy()
+    status = res.status.cpu().numpy()
+    for f in range(B):
+        a, e = int(off[f]), int(off[f + 1])
+        if a == e:
+            assert status[f] & 1 and not np.any(x[f])
+            continue
+        taps = [orc.Tap(int(kk), int(ll), complex(gg)) for kk, ll, gg in zip(k[a:e], l[a:e], g[a:e])]
+        xr, _ = orc.cga(orc.build_tables(taps, M, N), yt[f].cpu().numpy().astype(np.complex128), 10, 1e-2)
+        assert rel_l2(x[f], xr) < REL_L2_FP32, (f, rel_l2(x[f], xr))
