@@ -17,6 +17,8 @@ REPO_DIR = PKG_DIR.parent
 CSRC = PKG_DIR / "csrc"
 LIB_PATH = PKG_DIR / "libddb.so"
 SOURCES = ("sscga.cu", "sscga_tm.cu", "sscga_global.cu", "aux.cu", "frontend.cu", "channel.cu", "dense.cu", "capi.cu")
+# sscga_tm.cu is compiled once per part (TM_PART, see the end of that file), in parallel
+PARTS = {"sscga_tm.cu": ("0", "1", "2", "3")}
 HEADERS = ("common.cuh", "cg.cuh", "demod.cuh", "internal.h")
 
 NVCC_FLAGS = [
@@ -60,12 +62,15 @@ def build(force: bool = False, verbose: bool = False, variant: str = "", defines
     objdir.mkdir(exist_ok=True)
     hdr_mtime = max(p.stat().st_mtime for p in [REPO_DIR / "include" / "ddb.h", *(CSRC / h for h in HEADERS)])
     objs, cmds = [], []
-    for src in SOURCES:
-        obj = objdir / (Path(src).stem + ".o")
+    units = [(src, None) for src in SOURCES if src not in PARTS]
+    units += [(src, part) for src in SOURCES if src in PARTS for part in PARTS[src]]
+    for src, part in units:
+        obj = objdir / (Path(src).stem + (f"_p{part}" if part is not None else "") + ".o")
         objs.append(str(obj))
         if not force and obj.exists() and obj.stat().st_mtime > max(hdr_mtime, (CSRC / src).stat().st_mtime):
             continue  # object up to date
-        cmd = [nvcc, *NVCC_FLAGS, *(f"-D{d}" for d in defines), "-c", str(CSRC / src), "-o", str(obj)]
+        extra = [f"-DTM_PART={part}"] if part is not None else []
+        cmd = [nvcc, *NVCC_FLAGS, *extra, *(f"-D{d}" for d in defines), "-c", str(CSRC / src), "-o", str(obj)]
         if verbose:
             cmd += ["-Xptxas", "-v"]
         cmds.append(cmd)

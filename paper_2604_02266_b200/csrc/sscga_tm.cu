@@ -1215,15 +1215,6 @@ cudaError_t launch_spec(SolveArgs a, const LaunchShape& s, cudaStream_t st) {
   return launch_one<R, MAXT, PROF, GEN>(a, s, st);
 }
 
-template <int R, int MAXT, bool PROF = false>
-cudaError_t launch_r(SolveArgs a, const LaunchShape& s, cudaStream_t st) {
-  if (a.split) {
-    cudaError_t e = launch_spec<R, MAXT, PROF, false>(a, s, st);
-    if (e != cudaSuccess) return e;
-  }
-  return launch_spec<R, MAXT, PROF, true>(a, s, st);
-}
-
 template <int R, int MAXT>
 cudaError_t occ_r(const LaunchShape& s, int* n) {
   auto kern = sscga_tm_kernel<R, MAXT, false, false>;
@@ -1242,32 +1233,63 @@ cudaError_t occ_r(const LaunchShape& s, int* n) {
 
 }  // namespace
 
+// ---- split compilation (build.py compiles this file once per TM_PART, in
+// parallel; without TM_PART one object carries everything): the R = 16 lean
+// and general instantiations, the small-R ones and the dispatcher.
+cudaError_t tm_launch16(bool gen, SolveArgs a, const LaunchShape& s, cudaStream_t st);
+cudaError_t tm_launch16_gen(SolveArgs a, const LaunchShape& s, cudaStream_t st);
+cudaError_t tm_launch_small(int R, bool gen, SolveArgs a, const LaunchShape& s, cudaStream_t st);
+cudaError_t tm_occ(int R, const LaunchShape& s, int* n);
+cudaError_t tm_occ16(const LaunchShape& s, int* n);
+
+#if !defined(TM_PART) || TM_PART == 1
+cudaError_t tm_launch16(bool gen, SolveArgs a, const LaunchShape& s, cudaStream_t st) {
+  if (gen) return tm_launch16_gen(a, s, st);
+  return a.prof ? launch_spec<16, 512, true, false>(a, s, st) : launch_spec<16, 512, false, false>(a, s, st);
+}
+cudaError_t tm_occ16(const LaunchShape& s, int* n) { return occ_r<16, 512>(s, n); }
+#endif
+#if !defined(TM_PART) || TM_PART == 2
+cudaError_t tm_launch16_gen(SolveArgs a, const LaunchShape& s, cudaStream_t st) {
+  return a.prof ? launch_spec<16, 512, true, true>(a, s, st) : launch_spec<16, 512, false, true>(a, s, st);
+}
+#endif
+#if !defined(TM_PART) || TM_PART == 3
+cudaError_t tm_launch_small(int R, bool gen, SolveArgs a, const LaunchShape& s, cudaStream_t st) {
+  if (a.prof) return cudaErrorNotSupported;  // the phase profile is an R = 16 measurement build
+  if (R == 8) return gen ? launch_spec<8, 512, false, true>(a, s, st) : launch_spec<8, 512, false, false>(a, s, st);
+  if (R == 4) return gen ? launch_spec<4, 512, false, true>(a, s, st) : launch_spec<4, 512, false, false>(a, s, st);
+  return cudaErrorInvalidValue;
+}
+cudaError_t tm_occ(int R, const LaunchShape& s, int* n) {
+  switch (R) {
+    case 4: return occ_r<4, 512>(s, n);
+    case 8: return occ_r<8, 512>(s, n);
+    default: return cudaErrorInvalidValue;
+  }
+}
+#endif
+
+#if !defined(TM_PART) || TM_PART == 0
 SmemLayout sscga_tm_layout(int M, int Lcta, int N, int CS, int TL, int TH, int pcap) {
   (void)M;
   return tm_layout_impl(Lcta, N, CS, TL, TH, pcap);
 }
 
+// Both instantiations on the stream: the lean frames, then the others.
 cudaError_t launch_sscga_tm(SolveArgs a, const LaunchShape& s, cudaStream_t st) {
   if (a.B == 0) return cudaSuccess;
-  if (a.prof) {  // clock64 phase profile (measurement launches only; R = 16 plans)
-    if (s.rows == 16) return launch_r<16, 512, true>(a, s, st);
-    return cudaErrorNotSupported;
+  if (s.rows != 4 && s.rows != 8 && s.rows != 16) return cudaErrorInvalidValue;
+  for (int gen = a.split ? 0 : 1; gen < 2; ++gen) {
+    const cudaError_t e = s.rows == 16 ? tm_launch16(gen != 0, a, s, st) : tm_launch_small(s.rows, gen != 0, a, s, st);
+    if (e != cudaSuccess) return e;
   }
-  switch (s.rows) {
-    case 4: return launch_r<4, 512>(a, s, st);
-    case 8: return launch_r<8, 512>(a, s, st);
-    case 16: return launch_r<16, 512>(a, s, st);
-    default: return cudaErrorInvalidValue;
-  }
+  return cudaSuccess;
 }
 
 cudaError_t sscga_tm_occupancy(const LaunchShape& s, int* n) {
-  switch (s.rows) {
-    case 4: return occ_r<4, 512>(s, n);
-    case 8: return occ_r<8, 512>(s, n);
-    case 16: return occ_r<16, 512>(s, n);
-    default: return cudaErrorInvalidValue;
-  }
+  return s.rows == 16 ? tm_occ16(s, n) : tm_occ(s.rows, s, n);
 }
+#endif
 
 }  // namespace ddb
