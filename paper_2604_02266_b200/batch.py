@@ -379,7 +379,9 @@ class HostPipeline:
 
     Frames are processed in chunks; chunk i+1's pinned H2D copy overlaps chunk
     i's solve and chunk i-1's D2H copy (three streams, events between them).
-    Returns hard-decision labels and per-frame bit errors on the host.
+    Returns hard-decision labels on the host, and per-frame bit errors when
+    the transmitted labels are given (tx_host; None: the equalizer alone, the
+    work the reference's build_ss_channel -> cga_equalize -> hard_demod does).
     """
 
     def __init__(self, solver: SsCgaSolver, chunk: int = 512, depth: int = 2):
@@ -402,14 +404,15 @@ class HostPipeline:
             ))
 
     def run(self, y_host: torch.Tensor, paths_host: tuple, lam_host: torch.Tensor,
-            tx_host: torch.Tensor, labels_host: torch.Tensor, errors_host: torch.Tensor) -> None:
+            tx_host: Optional[torch.Tensor], labels_host: torch.Tensor,
+            errors_host: Optional[torch.Tensor] = None) -> None:
         """All host tensors must be pinned.  paths_host = (offsets, k, l, gain) host tensors."""
         s = self.s
         B = y_host.shape[0]
         off, kk, ll, gg = paths_host
         dev = s.device
         for slot in self.slots:  # TX labels one byte per symbol, or packed (pack_labels)
-            if slot["tx"] is None or slot["tx"].shape[1] != tx_host.shape[1]:
+            if tx_host is not None and (slot["tx"] is None or slot["tx"].shape[1] != tx_host.shape[1]):
                 torch.cuda.synchronize(dev)
                 slot["tx"] = torch.empty(self.chunk, tx_host.shape[1], dtype=torch.uint8, device=dev)
         # taps are tiny: one copy for the whole batch, rebased per chunk on the device
@@ -425,20 +428,23 @@ class HostPipeline:
                 self.h2d.wait_event(slot["drained"])
                 slot["y"][:n].copy_(y_host[start:start + n], non_blocking=True)
                 slot["lam"][:n].copy_(lam_host[start:start + n], non_blocking=True)
-                slot["tx"][:n].copy_(tx_host[start:start + n], non_blocking=True)
+                if tx_host is not None:
+                    slot["tx"][:n].copy_(tx_host[start:start + n], non_blocking=True)
                 slot["loaded"].record(self.h2d)
             with torch.cuda.stream(self.comp):
                 self.comp.wait_event(slot["loaded"])
                 # offsets are absolute into the shared tap arrays: a slice is a valid CSR
                 paths = PathBatch(d_off[start:start + n + 1], d_k, d_l, d_g)
                 res = slot["res"]
-                view = SolveResult(x=res.x[:n], labels=res.labels[:n], bit_errors=res.bit_errors[:n])
-                s.solve(slot["y"][:n], paths, slot["lam"][:n], tx_labels=slot["tx"][:n], out=view,
-                        trace=False, stream=self.comp)
+                tx = slot["tx"][:n] if tx_host is not None else None
+                view = SolveResult(x=res.x[:n], labels=res.labels[:n],
+                                   bit_errors=res.bit_errors[:n] if tx is not None else None)
+                s.solve(slot["y"][:n], paths, slot["lam"][:n], tx_labels=tx, out=view, trace=False, stream=self.comp)
                 slot["solved"].record(self.comp)
             with torch.cuda.stream(self.d2h):
                 self.d2h.wait_event(slot["solved"])
                 labels_host[start:start + n].copy_(res.labels[:n], non_blocking=True)
-                errors_host[start:start + n].copy_(res.bit_errors[:n], non_blocking=True)
+                if tx_host is not None and errors_host is not None:
+                    errors_host[start:start + n].copy_(res.bit_errors[:n], non_blocking=True)
                 slot["drained"].record(self.d2h)
         self.d2h.synchronize()
