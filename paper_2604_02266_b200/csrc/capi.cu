@@ -62,6 +62,7 @@ int smem_optin() {
 // (cfg1 5.4 -> 12.9, cfg2 13.0 -> 15.8 G symbols/s, profiles/r2_residency.md).
 // Ties keep the larger CTA.  The halo then takes the rest of the CTA's share
 // (at least min(M, 64) rows: the Veh-A delay spread is <= 39 bins at M = 512).
+constexpr int kTmRegs128 = 96;  // sscga_tm.cu: __launch_bounds__(128, 5) for 128-thread plans
 bool make_plan_tm(int32_t M, int32_t N, ddb::LaunchShape* s) {
   const char* env_k = getenv("DDB_KERNEL");
   if (env_k && env_k[0] == 'r') return false;  // DDB_KERNEL=row: force the row-slice kernel
@@ -69,7 +70,9 @@ bool make_plan_tm(int32_t M, int32_t N, ddb::LaunchShape* s) {
   const int pcap = 64;
   int TL = 0, TH = 0;
   ddb::twiddle_split(M * N, &TL, &TH);
-  const int hmin = M < 64 ? M : 64;
+  // delay shifts |d_k| <= M / 2 (sparse.py:35-37): a halo of M / 2 rows covers
+  // every shift; 64 covers the Veh-A delay spread (<= 39 bins at M = 512)
+  const int hmin = M / 2 < 64 ? M / 2 : 64;
   const char* env_c = getenv("DDB_PLAN_C");
   const char* env_wq = getenv("DDB_PLAN_WQ");
   const char* env_cap = getenv("DDB_PLAN_SMEM_CAP");
@@ -95,7 +98,10 @@ bool make_plan_tm(int32_t M, int32_t N, ddb::LaunchShape* s) {
       const int threads = 128 * w;
       // frames per SM: TMEM columns, threads (<= 128 registers each), shared memory
       int n = 512 / tc;
-      if (65536 / (threads * 128) < n) n = 65536 / (threads * 128);
+      // registers per thread: 128 (the kernel's launch bounds), 96 for 128-thread
+      // CTAs (their instantiations are bounded for five CTAs per SM)
+      const int regs = threads == 128 ? kTmRegs128 : 128;
+      if (65536 / (threads * regs) < n) n = 65536 / (threads * regs);
       int share = 0, h = 0;
       for (; n >= 1; --n) {
         share = 233472 / n - 1024;  // 228 KiB per SM, 1 KiB reserved per CTA

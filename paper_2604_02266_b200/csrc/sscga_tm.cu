@@ -623,14 +623,15 @@ __device__ __forceinline__ int frame_list(const SolveArgs& a, int base, int* fli
 // (spec_index, launch_r); any other plan runs the generic instantiation.
 struct SpecPlan {
   int M, N, C, Lcta, G, WQ, CS, H, TL, TH, pcap, tcols;
+  int min_blocks;  // launch bounds: CTAs per SM the registers must allow (128-thread plans: 5)
 };
 constexpr SpecPlan kSpecs[] = {
-    {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0},                      // 0: generic
-    {512, 32, 2, 16, 64, 4, 874, 180, 128, 128, 64, 512},      // 1: cfg3   (R 16)
-    {64, 16, 1, 16, 8, 1, 194, 64, 32, 32, 64, 64},            // 2: cfg1   (R 8)
-    {256, 16, 1, 16, 32, 2, 422, 82, 64, 64, 64, 256},         // 3: cfg2   (R 16)
-    {1024, 64, 8, 8, 64, 4, 1730, 352, 256, 256, 64, 512},     // 4: cfg4   (R 16)
-    {128, 32, 1, 32, 32, 4, 386, 128, 64, 64, 64, 256},        // 5: (128, 32), the paper's grid (R 8)
+    {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 1},                   // 0: generic
+    {512, 32, 2, 16, 64, 4, 874, 180, 128, 128, 64, 512, 1},   // 1: cfg3   (R 16)
+    {64, 16, 1, 16, 8, 1, 150, 42, 32, 32, 64, 64, 5},         // 2: cfg1   (R 8, 128 threads: five CTAs per SM)
+    {256, 16, 1, 16, 32, 2, 422, 82, 64, 64, 64, 256, 1},      // 3: cfg2   (R 16)
+    {1024, 64, 8, 8, 64, 4, 1730, 352, 256, 256, 64, 512, 1},  // 4: cfg4   (R 16)
+    {128, 32, 1, 32, 32, 4, 386, 128, 64, 64, 64, 256, 1},     // 5: (128, 32), the paper's grid (R 8)
 };
 constexpr int kNumSpecs = sizeof(kSpecs) / sizeof(kSpecs[0]);
 inline int spec_index(const SolveArgs& a) {
@@ -645,7 +646,8 @@ inline int spec_index(const SolveArgs& a) {
 }
 
 template <int R, int MAXT, bool PROF, bool GEN, int SPEC = 0>
-__global__ void __launch_bounds__(MAXT, 1) sscga_tm_kernel(const SolveArgs a_) {
+__global__ void __launch_bounds__(kSpecs[SPEC].min_blocks > 1 ? 128 : MAXT, kSpecs[SPEC].min_blocks)
+    sscga_tm_kernel(const SolveArgs a_) {
   // a local copy whose plan fields are constants in the specialised instantiation
   SolveArgs a = a_;
   if constexpr (SPEC > 0) {
