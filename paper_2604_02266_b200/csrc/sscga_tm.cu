@@ -1217,9 +1217,41 @@ cudaError_t launch_spec(SolveArgs a, const LaunchShape& s, cudaStream_t st) {
   return launch_one<R, MAXT, PROF, GEN>(a, s, st);
 }
 
+// The compile-time-geometry instantiation a launch of this plan runs (spec_index
+// from the plan alone: M = CS - 2 H - 2, N = C Lcta), so the residency reported
+// with the plan is the launch's (cfg1's runs five CTAs per SM, the generic four).
+inline int spec_index_shape(const LaunchShape& s) {
+  SolveArgs a = {};
+  a.M = s.cs - 2 * s.halo - 2;
+  a.N = s.cluster * s.lcta;
+  a.C = s.cluster;
+  a.Lcta = s.lcta;
+  a.G = s.g;
+  a.WQ = s.wq;
+  a.CS = s.cs;
+  a.H = s.halo;
+  a.TL = s.tl;
+  a.TH = s.th;
+  a.pcap = s.pcap;
+  a.tcols = s.tcols;
+  return spec_index(a);
+}
+template <int R, int MAXT>
+const void* occ_kernel(const LaunchShape& s) {
+  switch (spec_index_shape(s)) {
+    case 1: if constexpr (R == 16) return (const void*)sscga_tm_kernel<R, MAXT, false, false, 1>; break;
+    case 2: if constexpr (R == 8) return (const void*)sscga_tm_kernel<R, MAXT, false, false, 2>; break;
+    case 3: if constexpr (R == 16) return (const void*)sscga_tm_kernel<R, MAXT, false, false, 3>; break;
+    case 4: if constexpr (R == 16) return (const void*)sscga_tm_kernel<R, MAXT, false, false, 4>; break;
+    case 5: if constexpr (R == 8) return (const void*)sscga_tm_kernel<R, MAXT, false, false, 5>; break;
+    default: break;
+  }
+  return (const void*)sscga_tm_kernel<R, MAXT, false, false>;
+}
+
 template <int R, int MAXT>
 cudaError_t occ_r(const LaunchShape& s, int* n) {
-  auto kern = sscga_tm_kernel<R, MAXT, false, false>;
+  const void* kern = occ_kernel<R, MAXT>(s);
   int dev = 0, optin = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);

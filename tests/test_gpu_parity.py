@@ -397,6 +397,15 @@ def _random_taps_case(pkg, M, N, P, precision):
             assert tr.c_norm[done + 1] < 1e-30 * tr.c_norm[0]
 
 
+def test_plan_residency_is_the_launched_instantiation(pkg):
+    """The plan's CTAs per SM come from the instantiation a solve of that plan
+    launches: cfg1 (64 x 16) runs its compile-time-geometry kernel at 96
+    registers, five CTAs per SM (the generic one would fit four); cfg3 one."""
+    from paper_2604_02266_b200 import _native as nat
+    assert nat.plan(64, 16, nat.DDB_F32).ctas_per_sm == 5
+    assert nat.plan(512, 32, nat.DDB_F32).ctas_per_sm == 1
+
+
 def test_empty_and_mixed_batch(pkg):
     s = solver_for(pkg, 64, 16, 10, "fp32", 2)
     rng = np.random.default_rng(1)
