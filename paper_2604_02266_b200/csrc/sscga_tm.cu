@@ -112,8 +112,11 @@ __device__ __forceinline__ PathEnt<float> tm_path(const SolveArgs& a, const TmSm
   PathEnt<float> e;
   e.dk = a.K0 - kp;
   e.dl = a.L0 - lp;
-  e.off = 0;
-  e.pad = 0;
+  // off / pad: the forward per-row coefficient step W^{-d_l} of a Doppler tap
+  // (tap_elem; the hermitian one is its conjugate), made once per frame
+  const V st = e.dl ? twid_tm(sm, wrap1(-e.dl, a.MN)) : make_float2(1.f, 0.f);
+  e.off = __float_as_int(st.x);
+  e.pad = __float_as_int(st.y);
   e.hf = quad(e.dl ? cmul(h, twid_tm(sm, wrap1(-e.dl * e.dk, a.MN))) : h);
   e.hh = quad(cconj(h));
   return e;
@@ -193,7 +196,7 @@ __device__ __forceinline__ void tap_elem(const SolveArgs& a, const TmThr& th, co
   const int sg = HERM ? dl : -dl;  // coefficient phase exponent per row
   if (halo) {
     constexpr int BS = R;  // rows per exact re-anchor (16-step fp32 recurrence: ~1e-6 relative)
-    const V step = twid_tm(sm, wrap1(sg, MN));
+    const V step = make_float2(__int_as_float(e.off), HERM ? -__int_as_float(e.pad) : __int_as_float(e.pad));
     int a0 = th.r0 + s;
     V hw = h0;
     if (fs.wrap) hw = cmul(h0, wrap_run<R>(a0, M, HERM ? fs.lo_u : fs.lo_c, HERM ? fs.hi_u : fs.hi_c, sm.tw[ls]));
