@@ -252,6 +252,12 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
   asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
                :: "r"(smem_addr(dst)), "l"(src), "r"(bytes), "r"(smem_addr(mb)) : "memory");
 }
+// Push `bytes` of this CTA's shared memory to a cluster address (another CTA's
+// shared memory) with the bulk-copy engine, completing on that CTA's mbarrier.
+__device__ __forceinline__ void bulk_s2c(uint32_t dst, const void* src, uint32_t bytes, uint32_t mb) {
+  asm volatile("cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+               :: "r"(dst), "r"(smem_addr(src)), "r"(bytes), "r"(mb) : "memory");
+}
 // Map a shared::cta address of this CTA to the same offset in CTA `rank`.
 __device__ __forceinline__ uint32_t map_rank(uint32_t saddr, uint32_t rank) {
   uint32_t r;

@@ -83,6 +83,7 @@ __host__ __device__ constexpr int row_stride(int lcta, int elem_bytes) {
 // Shared-memory layout of the fused kernel (byte offsets, 16-byte aligned).
 struct SmemLayout {
   size_t p, u, x, tlo, thi, tw, ptab, red, q, total;  // q: the TMEM kernel's frame list
+  size_t gh = 0, ghmb = 0;  // TMEM kernel, clusters: ghost columns of c and u and their mbarriers
 };
 SmemLayout sscga_layout(int M, int N, int C, int elem_bytes, int H, int TL, int TH, int pcap);
 void twiddle_split(int MN, int* TL, int* TH);

@@ -55,11 +55,15 @@ struct FrameSm {
   int lo_c, hi_c, lo_u, hi_u;  // extension rows written for c (gathered by H) and u (by H^H)
   int remote;                  // some warp gathers per element (DSMEM): publish c / u with release
   int wrap;                    // some shift exceeds the halo: runs beyond it wrap the delay period
-  int pad;
+  int ghost;                   // ghost columns pushed and read this frame (gh_push, tap_elem)
   uint32_t mk[8][6];           // [j][tmF, smF, gnF, tmH, smH, gnH]: TMEM run / shared run / per element
 };
 
 constexpr int kWarpTimers = 8;
+// Ghost columns (clusters of at least this many CTAs): their shared memory
+// comes out of the halo, which costs the two-CTA frames (cfg3det) more than the
+// ghosts win them; four or more CTAs per frame (cfg4) gain.
+constexpr int kGhostMinC = 4;
 
 __host__ __device__ inline size_t a16(size_t v) { return (v + 15) & ~size_t(15); }
 
@@ -78,6 +82,13 @@ __host__ __device__ inline SmemLayout tm_layout_impl(int Lcta, int N, int CS, in
   L.ptab = o; o = a16(o + (size_t)pcap * sizeof(PathEnt<float>));
   L.red = o; o = a16(o + 2 * 2 * kPushSlots * sizeof(V) + sizeof(ProfSm) + sizeof(FrameSm));
   L.q = o; o = a16(o + (128 + 16) * sizeof(int));       // frame list (kListChunk) of this CTA's class + warp counts
+  if (N / Lcta >= kGhostMinC) {
+    // clusters: ghost copies of the neighbouring CTAs' boundary columns of c and
+    // u ([c left, c right, u left, u right], extended like the own columns),
+    // pushed by their owners (gh_push), and one mbarrier per vector
+    L.gh = o; o = a16(o + (size_t)4 * CS * sizeof(V));
+    L.ghmb = o; o = a16(o + 16);
+  }
   L.total = o;
   return L;
 }
@@ -91,6 +102,7 @@ struct TmSm {
   const V* tw;
   PathEnt<float>* ptab;
   int tlb;
+  V* gh;  // ghost columns (clusters)
 };
 
 __device__ __forceinline__ V twid_tm(const TmSm& sm, int e) {
@@ -181,9 +193,13 @@ __device__ __forceinline__ V wrap_run(int& a0, int M, int lo, int hi, V tw_src) 
 // multiply per row from an exact table value every 8 rows; a run beyond the
 // written halo (wrap) is read one delay period over (wrap_run).  Without the
 // halo rows wrap the delay period individually (twist applied in registers).
-template <int R, bool HERM>
-__device__ __forceinline__ void tap_elem(const SolveArgs& a, const TmThr& th, const TmSm& sm, const FrameSm& fs,
-                                         bool halo, const V* buf, const PathEnt<float>& e, U64 (&acc)[R]) {
+// LDS: every lane reads this CTA's shared memory -- its own columns, or the
+// ghost copy of a neighbouring CTA's boundary column (frames with ghosts, taps
+// with |d_l| = 1) -- instead of DSMEM (≈ 5 B/clk/SM for these scattered
+// 16-byte reads, tools/ubench/dsmem_bw.cu).
+template <int R, bool HERM, bool LDS>
+__device__ __forceinline__ void tap_elem_impl(const SolveArgs& a, const TmThr& th, const TmSm& sm, const FrameSm& fs,
+                                              bool halo, const V* buf, const PathEnt<float>& e, U64 (&acc)[R]) {
   const int M = a.M, MN = a.MN;
   const int dl = e.dl;
   const int s = HERM ? -e.dk : e.dk;
@@ -192,7 +208,12 @@ __device__ __forceinline__ void tap_elem(const SolveArgs& a, const TmThr& th, co
   const int ls = wrap1(th.colg + (HERM ? -dl : dl), a.N);  // source Doppler column
   const int own = ls / a.Lcta;
   const int lc = ls - own * a.Lcta;
-  const uint32_t colad = map_rank(smem_addr(buf + (size_t)lc * a.CS + a.H), (uint32_t)own);
+  const V* colp = buf + (size_t)lc * a.CS + a.H;
+  if (LDS && own != th.colg / a.Lcta) {  // a neighbour's boundary column: its ghost copy
+    const int side = ls == wrap1(th.colg - th.col - 1, a.N) ? 0 : 1;
+    colp = sm.gh + (size_t)(2 * (HERM ? 1 : 0) + side) * a.CS + a.H;
+  }
+  const uint32_t colad = LDS ? 0u : map_rank(smem_addr(colp), (uint32_t)own);
   const int sg = HERM ? dl : -dl;  // coefficient phase exponent per row
   if (halo) {
     constexpr int BS = R;  // rows per exact re-anchor (16-step fp32 recurrence: ~1e-6 relative)
@@ -201,24 +222,26 @@ __device__ __forceinline__ void tap_elem(const SolveArgs& a, const TmThr& th, co
     V hw = h0;
     if (fs.wrap) hw = cmul(h0, wrap_run<R>(a0, M, HERM ? fs.lo_u : fs.lo_c, HERM ? fs.hi_u : fs.hi_c, sm.tw[ls]));
     const uint32_t run = colad + (uint32_t)(a0 * (int)sizeof(V));
+    const float4* lrun = reinterpret_cast<const float4*>(colp + a0 - (s & 1));
+    auto ld4 = [&](int m, uint32_t off) { return LDS ? lrun[m] : ld_cluster4(run + off); };
     V v[R];
     if ((s & 1) == 0) {
 #pragma unroll
       for (int m = 0; m < R / 2; ++m) {
-        const float4 w = ld_cluster4(run + 16u * m);
+        const float4 w = ld4(m, 16u * m);
         v[2 * m] = make_float2(w.x, w.y);
         v[2 * m + 1] = make_float2(w.z, w.w);
       }
     } else {
-      float4 w = ld_cluster4(run - 8u);
+      float4 w = ld4(0, 0u - 8u);
       v[0] = make_float2(w.z, w.w);
 #pragma unroll
       for (int m = 1; m < R / 2; ++m) {
-        w = ld_cluster4(run - 8u + 16u * m);
+        w = ld4(m, 16u * m - 8u);
         v[2 * m - 1] = make_float2(w.x, w.y);
         v[2 * m] = make_float2(w.z, w.w);
       }
-      w = ld_cluster4(run - 8u + 16u * (R / 2));
+      w = ld4(R / 2, 16u * (R / 2) - 8u);
       v[R - 1] = make_float2(w.x, w.y);
     }
 #pragma unroll
@@ -240,7 +263,7 @@ __device__ __forceinline__ void tap_elem(const SolveArgs& a, const TmThr& th, co
     int ar = k + s;
     const int nw = ar < 0 ? -1 : (ar >= M ? 1 : 0);
     ar -= nw * M;
-    V v = ld_cluster(static_cast<V*>(nullptr), colad + (uint32_t)(ar * (int)sizeof(V)));
+    V v = LDS ? colp[ar] : ld_cluster(static_cast<V*>(nullptr), colad + (uint32_t)(ar * (int)sizeof(V)));
     if (nw != 0) {
       V t = sm.tw[ls];
       if (nw < 0) t = cconj(t);
@@ -248,6 +271,16 @@ __device__ __forceinline__ void tap_elem(const SolveArgs& a, const TmThr& th, co
     }
     Acc<float>::mac(acc[i], coef, v);
   }
+}
+
+template <int R, bool HERM>
+__device__ __forceinline__ void tap_elem(const SolveArgs& a, const TmThr& th, const TmSm& sm, const FrameSm& fs,
+                                         bool halo, const V* buf, const PathEnt<float>& e, U64 (&acc)[R]) {
+  // (a.C is a constant in the compile-time-geometry instantiations: plans
+  // without ghosts carry no ghost code)
+  if (a.C >= kGhostMinC && halo && fs.ghost && (e.dl == 1 || e.dl == -1))
+    tap_elem_impl<R, HERM, true>(a, th, sm, fs, halo, buf, e, acc);
+  else tap_elem_impl<R, HERM, false>(a, th, sm, fs, halo, buf, e, acc);
 }
 
 // TMEM taps of a mask, software-pipelined in half runs (R / 2 values): the
@@ -345,8 +378,15 @@ __device__ __forceinline__ void mvm_local(const SolveArgs& a, const TmThr& th, c
 // Remote pass (after the cluster barrier's wait): per-element taps.
 template <int R, bool HERM>
 __device__ __forceinline__ void mvm_remote(const SolveArgs& a, const TmThr& th, const TmSm& sm, const FrameSm& fs,
-                                           const V* buf, U64 (&acc)[R]) {
+                                           const V* buf, void* ghmb, uint32_t& ghp, U64 (&acc)[R]) {
   const bool halo = fs.halo;
+  if (a.C >= kGhostMinC && fs.ghost) {  // this vector's ghost columns landed (gh_push of both neighbours)
+    constexpr int vec = HERM ? 1 : 0;
+    void* mb = static_cast<char*>(ghmb) + 8 * vec;
+    if (threadIdx.x == 0) mbar_expect_tx(mb, (uint32_t)(2 * a.CS * (int)sizeof(V)));
+    mbar_wait(mb, (ghp >> vec) & 1u);
+    ghp ^= 1u << vec;
+  }
   if (fs.masks) {
     for (uint32_t m = fs.mk[th.jr / R][HERM ? 5 : 2]; m; m &= m - 1)
       tap_elem<R, HERM>(a, th, sm, fs, halo, buf, sm.ptab[__ffs(m) - 1], acc);
@@ -565,6 +605,10 @@ __device__ __forceinline__ int epi_pass(const SolveArgs& a, const V* stg, int M,
     }                                                  \
   } while (0)
 
+#ifndef DDB_GHOST
+#define DDB_GHOST 1  // ghost columns for |d_l| = 1 taps (0: DSMEM for every Doppler tap, A/B builds)
+#endif
+
 // Frames are split between two instantiations of the kernel by tap geometry.
 // "Lean" frames -- 1..32 taps, all Doppler-preserving (l_p = L0), delay shifts
 // within the halo (every Veh-A frame with |nu| < dnu / 2, the headline's) --
@@ -633,7 +677,7 @@ constexpr SpecPlan kSpecs[] = {
     {512, 32, 2, 16, 64, 4, 874, 180, 128, 128, 64, 512, 1},   // 1: cfg3   (R 16)
     {64, 16, 1, 16, 8, 1, 150, 42, 32, 32, 64, 64, 5},         // 2: cfg1   (R 8, 128 threads: five CTAs per SM)
     {256, 16, 1, 16, 32, 2, 422, 82, 64, 64, 64, 256, 1},      // 3: cfg2   (R 16)
-    {1024, 64, 8, 8, 64, 4, 1730, 352, 256, 256, 64, 512, 1},  // 4: cfg4   (R 16)
+    {1024, 64, 8, 8, 64, 4, 1382, 178, 256, 256, 64, 512, 1},  // 4: cfg4   (R 16)
     {128, 32, 1, 32, 32, 4, 386, 128, 64, 64, 64, 256, 1},     // 5: (128, 32), the paper's grid (R 8)
 };
 constexpr int kNumSpecs = sizeof(kSpecs) / sizeof(kSpecs[0]);
@@ -687,6 +731,8 @@ __global__ void __launch_bounds__(kSpecs[SPEC].min_blocks > 1 ? 128 : MAXT, kSpe
   sm.tw = tw;
   sm.ptab = reinterpret_cast<PathEnt<float>*>(smem + L.ptab);
   sm.tlb = __ffs(a.TL) - 1;
+  sm.gh = reinterpret_cast<V*>(smem + L.gh);
+  void* const ghmb = smem + L.ghmb;
   V* red = reinterpret_cast<V*>(smem + L.red);
   ProfSm* const psm = reinterpret_cast<ProfSm*>(red + 2 * 2 * kPushSlots);
   FrameSm& fs = *reinterpret_cast<FrameSm*>(psm + 1);
@@ -743,6 +789,33 @@ __global__ void __launch_bounds__(kSpecs[SPEC].min_blocks > 1 ? 128 : MAXT, kSpe
   tmem_fence_after();
   const uint32_t tbase = *sm.tslot;
   th.tl = tbase + ((uint32_t)(32 * (warp & 3)) << 16);
+  // ghost-column mbarriers: initialised in every CTA of the cluster before any
+  // neighbour can push into them
+  uint32_t ghp = 0;  // their phase parities (bit 0: c, bit 1: u)
+  if constexpr (GEN) {
+    if (a.C >= kGhostMinC) {
+      if (tid == 0) {
+        mbar_init(ghmb, 1);
+        mbar_init(static_cast<char*>(ghmb) + 8, 1);
+      }
+      cl_sync<float>(a.C);
+    }
+  }
+  // Push this CTA's boundary columns of c (vec 0) or u (vec 1) into the
+  // neighbours' ghost slots (thread 0, after the CTA barrier that completed
+  // them; every writer fenced its generic stores for the async proxy first).
+  // The owner rewrites a column only after a cluster barrier the neighbour
+  // reaches after its wait for the push, so the copy's reads are never raced.
+  auto gh_push = [&](int vec) {
+    const V* src = vec ? sm.u : sm.c;
+    const uint32_t bytes = (uint32_t)(a.CS * (int)sizeof(V));
+    const uint32_t rr = (uint32_t)((rank + 1) % a.C), rl = (uint32_t)((rank + a.C - 1) % a.C);
+    const uint32_t mb = smem_addr(static_cast<char*>(ghmb) + 8 * vec);
+    // the last column -> the right neighbour's left ghost, the first -> the left neighbour's right ghost
+    bulk_s2c(map_rank(smem_addr(sm.gh + (size_t)(2 * vec) * a.CS), rr), src + (size_t)(a.Lcta - 1) * a.CS, bytes,
+             map_rank(mb, rr));
+    bulk_s2c(map_rank(smem_addr(sm.gh + (size_t)(2 * vec + 1) * a.CS), rl), src, bytes, map_rank(mb, rl));
+  };
   // TMEM regions of this lane: c | u (segment rows 0..G-1) | p | x (own runs)
   auto tC = [&](int c0) { return th.tl + (uint32_t)(2 * (th.jr + c0)); };
   auto tU = [&](int c0) { return th.tl + (uint32_t)(2 * (a.G + th.jr + c0)); };
@@ -810,14 +883,17 @@ __global__ void __launch_bounds__(kSpecs[SPEC].min_blocks > 1 ? 128 : MAXT, kSpe
     if (warp == 0) {  // tap table and shift extents, lanes over taps
       const V* gains = reinterpret_cast<const V*>(a.ph);
       int dmin = INT_MAX, dmax = INT_MIN;
+      bool d1 = false;  // a tap with |d_l| = 1 (ghost columns)
       for (int i = lane; i < P; i += 32) {
-        const int kp = __ldg(a.pk + P0 + i);
-        if (in_smem) sm.ptab[i] = tm_path(a, sm, kp, __ldg(a.pl + P0 + i), __ldg(gains + P0 + i));
+        const int kp = __ldg(a.pk + P0 + i), lp = __ldg(a.pl + P0 + i);
+        if (in_smem) sm.ptab[i] = tm_path(a, sm, kp, lp, __ldg(gains + P0 + i));
         dmin = min(dmin, a.K0 - kp);
         dmax = max(dmax, a.K0 - kp);
+        d1 |= lp == a.L0 + 1 || lp == a.L0 - 1;
       }
       dmin = __reduce_min_sync(0xffffffffu, dmin);
       dmax = __reduce_max_sync(0xffffffffu, dmax);
+      d1 = __any_sync(0xffffffffu, d1);
       if (lane == 0) {
         // halo rows written per side: what the shifts need, at most H; a run
         // beyond them is read one delay period over (wrap_run), which needs
@@ -835,6 +911,7 @@ __global__ void __launch_bounds__(kSpecs[SPEC].min_blocks > 1 ? 128 : MAXT, kSpe
         fs.lo_u = fs.hi_c;
         fs.hi_u = fs.lo_c;
         fs.remote = !fs.masks;  // without per-warp masks assume DSMEM taps
+        fs.ghost = DDB_GHOST && GEN && a.C >= kGhostMinC && halo && d1;
       }
     }
     __syncthreads();
@@ -893,13 +970,16 @@ __global__ void __launch_bounds__(kSpecs[SPEC].min_blocks > 1 ? 128 : MAXT, kSpe
 
     U64 acc[R];
     if constexpr (PROF) prof_mark(a.prof, psm, kArrive);
+    const bool ghost = GEN && a.C >= kGhostMinC && fs.ghost;  // (fs.ghost is written before the barrier above)
+    if (ghost) fence_proxy_async();
     tm_arrive(a.C);  // y and the tap classes published
+    if (ghost && tid == 0) gh_push(1);
     if constexpr (PROF) prof_mark(a.prof, psm, kMvmLocal);
     TM_WT(1, mvm_local<R, true, GEN>(a, th, sm, fs, tU(0) - 2 * th.jr, ucol, acc));  // b = H^H y (equalize.py:52)
     if constexpr (PROF) prof_mark(a.prof, psm, kWait);
     cl_wait(a.C);
     if constexpr (PROF) prof_mark(a.prof, psm, kMvmRemote);
-    if constexpr (GEN) mvm_remote<R, true>(a, th, sm, fs, sm.u, acc);
+    if constexpr (GEN) mvm_remote<R, true>(a, th, sm, fs, sm.u, ghmb, ghp, acc);
     if constexpr (PROF) prof_mark(a.prof, psm, kStep1);
     {
       V nrm = make_float2(0.f, 0.f);
@@ -919,7 +999,9 @@ __global__ void __launch_bounds__(kSpecs[SPEC].min_blocks > 1 ? 128 : MAXT, kSpe
       red_stage<float>(make_float2(nrm.x + nrm.y, 0.f), red + (2 + par1) * kPushSlots, warp, lane);
     }
     if constexpr (PROF) prof_mark(a.prof, psm, kArrive);
+    if (ghost) fence_proxy_async();
     TM_WT(2, tm_arrive_red<PROF>(a.C, red + (2 + par1) * kPushSlots, nwarps, warp, lane, rank, !GEN || !fs.remote, wt));  // c = b published
+    if (ghost && tid == 0 && a.iters > 0) gh_push(0);
     if constexpr (PROF) prof_mark(a.prof, psm, kMvmLocal);
     TM_WT(0, mvm_local<R, false, GEN>(a, th, sm, fs, tC(0) - 2 * th.jr, ccol, acc));
     if constexpr (PROF) prof_mark(a.prof, psm, kWait);
@@ -935,7 +1017,7 @@ __global__ void __launch_bounds__(kSpecs[SPEC].min_blocks > 1 ? 128 : MAXT, kSpe
     for (int it = 0; it < a.iters; ++it) {
       // u = H c + beta u_old, p = c + beta p_old      (= H p, p of equalize.py:60, 72)
       if constexpr (PROF) prof_mark(a.prof, psm, kMvmRemote);
-      if constexpr (GEN) mvm_remote<R, false>(a, th, sm, fs, sm.c, acc);
+      if constexpr (GEN) mvm_remote<R, false>(a, th, sm, fs, sm.c, ghmb, ghp, acc);
       if constexpr (PROF) prof_mark(a.prof, psm, kStep1);
       {
         V nu = make_float2(0.f, 0.f), np = make_float2(0.f, 0.f);
@@ -970,14 +1052,16 @@ __global__ void __launch_bounds__(kSpecs[SPEC].min_blocks > 1 ? 128 : MAXT, kSpe
         red_stage<float>(make_float2(nu.x + nu.y, np.x + np.y), red + par0 * kPushSlots, warp, lane);
       }
       if constexpr (PROF) prof_mark(a.prof, psm, kArrive);
+      if (ghost) fence_proxy_async();
       TM_WT(2, tm_arrive_red<PROF>(a.C, red + par0 * kPushSlots, nwarps, warp, lane, rank, !GEN || !fs.remote, wt));  // u published
+      if (ghost && tid == 0) gh_push(1);
       // ap = H^H u + lam p;  x += alpha p;  c -= alpha ap      (equalize.py:60-70)
       if constexpr (PROF) prof_mark(a.prof, psm, kMvmLocal);
       TM_WT(1, mvm_local<R, true, GEN>(a, th, sm, fs, tU(0) - 2 * th.jr, ucol, acc));
       if constexpr (PROF) prof_mark(a.prof, psm, kWait);
       TM_WT(3, cl_wait(a.C));
       if constexpr (PROF) prof_mark(a.prof, psm, kMvmRemote);
-      if constexpr (GEN) mvm_remote<R, true>(a, th, sm, fs, sm.u, acc);
+      if constexpr (GEN) mvm_remote<R, true>(a, th, sm, fs, sm.u, ghmb, ghp, acc);
       if constexpr (PROF) prof_mark(a.prof, psm, kRead);
       const V up = red_total<float>(a.C, red + par0 * kPushSlots, nwarps);
       par0 ^= 1;
@@ -1026,7 +1110,9 @@ __global__ void __launch_bounds__(kSpecs[SPEC].min_blocks > 1 ? 128 : MAXT, kSpe
         red_stage<float>(make_float2(nc.x + nc.y, 0.f), red + (2 + par1) * kPushSlots, warp, lane);
       }
       if constexpr (PROF) prof_mark(a.prof, psm, kArrive);
+      if (ghost) fence_proxy_async();
       TM_WT(2, tm_arrive_red<PROF>(a.C, red + (2 + par1) * kPushSlots, nwarps, warp, lane, rank, !GEN || !fs.remote, wt));  // c published
+      if (ghost && tid == 0 && it + 1 < a.iters) gh_push(0);
       if constexpr (PROF) prof_mark(a.prof, psm, kMvmLocal);
       if (it + 1 < a.iters) TM_WT(0, mvm_local<R, false, GEN>(a, th, sm, fs, tC(0) - 2 * th.jr, ccol, acc));  // next H c
       if constexpr (PROF) prof_mark(a.prof, psm, kWait);

@@ -397,6 +397,37 @@ def _random_taps_case(pkg, M, N, P, precision):
             assert tr.c_norm[done + 1] < 1e-30 * tr.c_norm[0]
 
 
+@pytest.mark.parametrize("M,N", [(1024, 64), (256, 64), (2048, 32)])
+def test_ghost_columns_across_frames(pkg, M, N):
+    """Clusters of four or more CTAs push their boundary columns into the
+    neighbours' ghost slots for |d_l| = 1 taps (bulk copies, one mbarrier phase
+    per vector and half iteration).  More frames than clusters, so each cluster
+    runs several frames in sequence (the phase parities carry over), with
+    Doppler shifts of 0, +-1 (ghosts) and +-3 (DSMEM) in the same frames."""
+    from paper_2604_02266_b200 import _native as nat
+    if nat.plan(M, N, nat.DDB_F32).cluster < 4:
+        pytest.skip("plan without ghost columns")
+    rng = np.random.default_rng(M + N)
+    s = solver_for(pkg, M, N, 10, "fp32")
+    B, P = 40, 6
+    off = np.arange(B + 1) * P
+    k = (M // 2 + rng.integers(0, min(40, M // 2), size=B * P)) % M
+    l = (N // 2 + rng.choice([-3, -1, 0, 1, 3], size=B * P)) % N
+    l[::P] = N // 2  # a dominant tap keeps H well conditioned
+    g = rng.uniform(0.05, 0.3, size=B * P) * np.exp(2j * np.pi * rng.random(B * P))
+    g[::P] = np.exp(2j * np.pi * rng.random(B))
+    y = rng.normal(size=(B, M * N)) + 1j * rng.normal(size=(B, M * N))
+    paths = pkg.PathBatch.from_arrays(off, k, l, g, cdtype=s.cdtype)
+    yt = torch.as_tensor(y, device="cuda").to(s.cdtype).contiguous()
+    res = s.solve(yt, paths, 1e-2)
+    x = res.x.cpu().numpy()
+    for f in (0, 19, 33, 39):
+        sl = slice(off[f], off[f + 1])
+        taps = [orc.Tap(int(a), int(b), complex(c)) for a, b, c in zip(k[sl], l[sl], g[sl])]
+        xr, _ = orc.cga(orc.build_tables(taps, M, N), yt[f].cpu().numpy().astype(np.complex128), 10, 1e-2)
+        assert rel_l2(x[f], xr) < REL_L2_FP32, (f, rel_l2(x[f], xr), s.plan())
+
+
 def test_plan_residency_is_the_launched_instantiation(pkg):
     """The plan's CTAs per SM come from the instantiation a solve of that plan
     launches: cfg1 (64 x 16) runs its compile-time-geometry kernel at 96
