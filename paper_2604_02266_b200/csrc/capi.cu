@@ -86,7 +86,14 @@ bool make_plan_tm(int32_t M, int32_t N, ddb::LaunchShape* s) {
     const int G = M / S;
     if (G > 64 || G % 2) continue;
     auto cs_of = [&](int h) { int cs = M + 2 * h + 2; return cs % 4 == 2 ? cs : cs + 2; };
-    auto smem_of = [&](int h) { return ddb::sscga_tm_layout(M, lcta, N, cs_of(h), TL, TH, pcap).total; };
+    // ghost columns (clusters of kGhostMinC+ CTAs): as deep as the shared memory allows
+    // with the minimum halo (DDB_NO_GHOST: none)
+    int gd = 0;
+    auto smem_of = [&](int h) { return ddb::sscga_tm_layout(M, lcta, N, cs_of(h), TL, TH, pcap, gd).total; };
+    if (C >= ddb::kGhostMinC && !getenv("DDB_NO_GHOST")) {
+      gd = lcta < ddb::kGhostMaxDepth ? lcta : ddb::kGhostMaxDepth;
+      while (gd > 0 && smem_of(hmin) > (size_t)cap) --gd;
+    }
     if (smem_of(hmin) > (size_t)cap) continue;
     int tc = 32;
     while (tc < 8 * G) tc *= 2;
@@ -128,6 +135,7 @@ bool make_plan_tm(int32_t M, int32_t N, ddb::LaunchShape* s) {
     s->threads = 128 * best_wq;
     s->halo = h;
     s->cs = cs_of(h);
+    s->gd = gd;
     s->tl = TL;
     s->th = TH;
     s->pcap = pcap;
@@ -324,6 +332,7 @@ static int32_t solve_impl(const ddb_sscga_problem* prob, const ddb_sscga_outputs
   a.G = s.g;
   a.WQ = s.wq;
   a.CS = s.cs;
+  a.gd = s.kind == 1 ? s.gd : 0;
   if (s.kind == 1) a.active_threads = s.threads;
   // TMEM kernel: frames' y streamed by cp.async.bulk (16-byte aligned y; DDB_NO_TMA=1 for A/B runs)
   a.stream_y = s.kind == 1 && (reinterpret_cast<uintptr_t>(prob->y) & 15) == 0 && !getenv("DDB_NO_TMA");

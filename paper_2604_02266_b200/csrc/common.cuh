@@ -246,6 +246,17 @@ __device__ __forceinline__ void mbar_wait(void* mb, uint32_t parity) {
       "WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
       " @!p bra WAIT_%=;\n}\n" :: "r"(smem_addr(mb)), "r"(parity) : "memory");
 }
+// the same with cluster-scope acquire (an mbarrier that other CTAs arrive on)
+__device__ __forceinline__ void mbar_wait_cluster(void* mb, uint32_t parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n"
+      "WAIT_%=:\n mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra WAIT_%=;\n}\n" :: "r"(smem_addr(mb)), "r"(parity) : "memory");
+}
+// arrive on another CTA's mbarrier (cluster address), releasing this CTA's prior accesses
+__device__ __forceinline__ void mbar_arrive_remote(uint32_t mb) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" :: "r"(mb) : "memory");
+}
 // generic-proxy accesses of shared memory before, async-proxy (bulk copy) after
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, void* mb) {

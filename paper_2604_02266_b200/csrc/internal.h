@@ -26,6 +26,7 @@ struct SolveArgs {
   int CS;             // column stride (complex elements) of the column-major extended slices
   int stream_y;       // 1: a frame's y arrives by cp.async.bulk into the u slice during the previous frame
   int split;          // 1: lean frames go to the lean instantiation, the rest to the general one; 0: general only
+  int gd;             // TMEM kernel: ghost depth (boundary columns per side pushed to the neighbours; 0: none)
   const int* off;
   const int* pk;
   const int* pl;
@@ -55,7 +56,12 @@ struct LaunchShape {
   int kind;        // 0: row-slice kernel (sscga.cu), 1: TMEM-operand kernel (sscga_tm.cu),
                    // 2: workspace-backed kernels (sscga_global.cu)
   int g, wq, rows, cs;  // kind 1: segment rows, warps per lane quarter, rows per thread, column stride
+  int gd = 0;           // kind 1: ghost depth (SolveArgs::gd)
 };
+// Ghost columns (TMEM kernel): clusters of at least this many CTAs, up to this
+// many columns per side.
+constexpr int kGhostMinC = 4;
+constexpr int kGhostMaxDepth = 4;
 
 // TMEM columns for the thread-private runs of x, p and the own-element copies
 // of c and u: (warps per lane quarter) x 4 runs x (32-bit words per run),
@@ -92,7 +98,7 @@ template <typename T>
 cudaError_t launch_sscga(SolveArgs a, const LaunchShape& s, cudaStream_t st);
 
 // TMEM-operand kernel (fp32): layout of its shared memory and launch.
-SmemLayout sscga_tm_layout(int M, int Lcta, int N, int CS, int TL, int TH, int pcap);
+SmemLayout sscga_tm_layout(int M, int Lcta, int N, int CS, int TL, int TH, int pcap, int gd);
 cudaError_t launch_sscga_tm(SolveArgs a, const LaunchShape& s, cudaStream_t st);
 cudaError_t sscga_tm_occupancy(const LaunchShape& s, int* ctas_per_sm);
 

@@ -60,14 +60,10 @@ struct FrameSm {
 };
 
 constexpr int kWarpTimers = 8;
-// Ghost columns (clusters of at least this many CTAs): their shared memory
-// comes out of the halo, which costs the two-CTA frames (cfg3det) more than the
-// ghosts win them; four or more CTAs per frame (cfg4) gain.
-constexpr int kGhostMinC = 4;
 
 __host__ __device__ inline size_t a16(size_t v) { return (v + 15) & ~size_t(15); }
 
-__host__ __device__ inline SmemLayout tm_layout_impl(int Lcta, int N, int CS, int TL, int TH, int pcap) {
+__host__ __device__ inline SmemLayout tm_layout_impl(int Lcta, int N, int CS, int TL, int TH, int pcap, int gd) {
   SmemLayout L;
   size_t o = 0;
   // extended c and u, column-major, each behind a 16-byte guard: odd-aligned
@@ -82,11 +78,14 @@ __host__ __device__ inline SmemLayout tm_layout_impl(int Lcta, int N, int CS, in
   L.ptab = o; o = a16(o + (size_t)pcap * sizeof(PathEnt<float>));
   L.red = o; o = a16(o + 2 * 2 * kPushSlots * sizeof(V) + sizeof(ProfSm) + sizeof(FrameSm));
   L.q = o; o = a16(o + (128 + 16) * sizeof(int));       // frame list (kListChunk) of this CTA's class + warp counts
-  if (N / Lcta >= kGhostMinC) {
-    // clusters: ghost copies of the neighbouring CTAs' boundary columns of c and
-    // u ([c left, c right, u left, u right], extended like the own columns),
-    // pushed by their owners (gh_push), and one mbarrier per vector
-    L.gh = o; o = a16(o + (size_t)4 * CS * sizeof(V));
+  if (gd > 0) {
+    // clusters: ghost copies of the gd boundary columns on either side (the
+    // left neighbour's last gd, then the right neighbour's first gd, extended
+    // like the own columns) of c or u, whichever the next MVM gathers, pushed
+    // by their owners (gh_push); a "full" mbarrier (bytes landed) and an
+    // "empty" one (both neighbours done reading this CTA's last push)
+    (void)N;
+    L.gh = o; o = a16(o + (size_t)2 * gd * CS * sizeof(V));
     L.ghmb = o; o = a16(o + 16);
   }
   L.total = o;
@@ -209,9 +208,10 @@ __device__ __forceinline__ void tap_elem_impl(const SolveArgs& a, const TmThr& t
   const int own = ls / a.Lcta;
   const int lc = ls - own * a.Lcta;
   const V* colp = buf + (size_t)lc * a.CS + a.H;
-  if (LDS && own != th.colg / a.Lcta) {  // a neighbour's boundary column: its ghost copy
-    const int side = ls == wrap1(th.colg - th.col - 1, a.N) ? 0 : 1;
-    colp = sm.gh + (size_t)(2 * (HERM ? 1 : 0) + side) * a.CS + a.H;
+  if (LDS) {  // a neighbour's boundary column: its ghost copy (|d_l| <= gd <= Lcta)
+    const int rel = th.col + (HERM ? -dl : dl);  // source column relative to this CTA's first
+    if (rel < 0) colp = sm.gh + (size_t)(a.gd + rel) * a.CS + a.H;
+    else if (rel >= a.Lcta) colp = sm.gh + (size_t)(a.gd + rel - a.Lcta) * a.CS + a.H;
   }
   const uint32_t colad = LDS ? 0u : map_rank(smem_addr(colp), (uint32_t)own);
   const int sg = HERM ? dl : -dl;  // coefficient phase exponent per row
@@ -276,9 +276,9 @@ __device__ __forceinline__ void tap_elem_impl(const SolveArgs& a, const TmThr& t
 template <int R, bool HERM>
 __device__ __forceinline__ void tap_elem(const SolveArgs& a, const TmThr& th, const TmSm& sm, const FrameSm& fs,
                                          bool halo, const V* buf, const PathEnt<float>& e, U64 (&acc)[R]) {
-  // (a.C is a constant in the compile-time-geometry instantiations: plans
+  // (a.gd is a constant in the compile-time-geometry instantiations: plans
   // without ghosts carry no ghost code)
-  if (a.C >= kGhostMinC && halo && fs.ghost && (e.dl == 1 || e.dl == -1))
+  if (a.gd > 0 && halo && fs.ghost && e.dl >= -a.gd && e.dl <= a.gd)
     tap_elem_impl<R, HERM, true>(a, th, sm, fs, halo, buf, e, acc);
   else tap_elem_impl<R, HERM, false>(a, th, sm, fs, halo, buf, e, acc);
 }
@@ -380,12 +380,11 @@ template <int R, bool HERM>
 __device__ __forceinline__ void mvm_remote(const SolveArgs& a, const TmThr& th, const TmSm& sm, const FrameSm& fs,
                                            const V* buf, void* ghmb, uint32_t& ghp, U64 (&acc)[R]) {
   const bool halo = fs.halo;
-  if (a.C >= kGhostMinC && fs.ghost) {  // this vector's ghost columns landed (gh_push of both neighbours)
-    constexpr int vec = HERM ? 1 : 0;
-    void* mb = static_cast<char*>(ghmb) + 8 * vec;
-    if (threadIdx.x == 0) mbar_expect_tx(mb, (uint32_t)(2 * a.CS * (int)sizeof(V)));
-    mbar_wait(mb, (ghp >> vec) & 1u);
-    ghp ^= 1u << vec;
+  if (a.gd > 0 && fs.ghost) {  // the ghost columns of this vector landed (gh_push of both neighbours)
+    if (threadIdx.x == 0) mbar_expect_tx(ghmb, (uint32_t)(2 * a.gd * a.CS * (int)sizeof(V)));
+    mbar_wait(ghmb, ghp & 1u);
+    ghp ^= 1u;
+    ghp |= 2u;  // to be released (gh_free) after the next CTA barrier
   }
   if (fs.masks) {
     for (uint32_t m = fs.mk[th.jr / R][HERM ? 5 : 2]; m; m &= m - 1)
@@ -669,16 +668,16 @@ __device__ __forceinline__ int frame_list(const SolveArgs& a, int base, int* fli
 // The host picks an entry only when the planner's plan matches it exactly
 // (spec_index, launch_r); any other plan runs the generic instantiation.
 struct SpecPlan {
-  int M, N, C, Lcta, G, WQ, CS, H, TL, TH, pcap, tcols;
+  int M, N, C, Lcta, G, WQ, CS, H, TL, TH, pcap, tcols, gd;
   int min_blocks;  // launch bounds: CTAs per SM the registers must allow (128-thread plans: 5)
 };
 constexpr SpecPlan kSpecs[] = {
-    {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 1},                   // 0: generic
-    {512, 32, 2, 16, 64, 4, 874, 180, 128, 128, 64, 512, 1},   // 1: cfg3   (R 16)
-    {64, 16, 1, 16, 8, 1, 150, 42, 32, 32, 64, 64, 5},         // 2: cfg1   (R 8, 128 threads: five CTAs per SM)
-    {256, 16, 1, 16, 32, 2, 422, 82, 64, 64, 64, 256, 1},      // 3: cfg2   (R 16)
-    {1024, 64, 8, 8, 64, 4, 1382, 178, 256, 256, 64, 512, 1},  // 4: cfg4   (R 16)
-    {128, 32, 1, 32, 32, 4, 386, 128, 64, 64, 64, 256, 1},     // 5: (128, 32), the paper's grid (R 8)
+    {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 1},                   // 0: generic
+    {512, 32, 2, 16, 64, 4, 874, 180, 128, 128, 64, 512, 0, 1},   // 1: cfg3   (R 16)
+    {64, 16, 1, 16, 8, 1, 150, 42, 32, 32, 64, 64, 0, 5},         // 2: cfg1   (R 8, 128 threads: five CTAs per SM)
+    {256, 16, 1, 16, 32, 2, 422, 82, 64, 64, 64, 256, 0, 1},      // 3: cfg2   (R 16)
+    {1024, 64, 8, 8, 64, 4, 1154, 64, 256, 256, 64, 512, 4, 1},  // 4: cfg4   (R 16, four ghost columns a side)
+    {128, 32, 1, 32, 32, 4, 386, 128, 64, 64, 64, 256, 0, 1},     // 5: (128, 32), the paper's grid (R 8)
 };
 constexpr int kNumSpecs = sizeof(kSpecs) / sizeof(kSpecs[0]);
 inline int spec_index(const SolveArgs& a) {
@@ -686,7 +685,7 @@ inline int spec_index(const SolveArgs& a) {
   for (int i = 1; i < kNumSpecs; ++i) {
     const SpecPlan& p = kSpecs[i];
     if (a.M == p.M && a.N == p.N && a.C == p.C && a.Lcta == p.Lcta && a.G == p.G && a.WQ == p.WQ && a.CS == p.CS &&
-        a.H == p.H && a.TL == p.TL && a.TH == p.TH && a.pcap == p.pcap && a.tcols == p.tcols)
+        a.H == p.H && a.TL == p.TL && a.TH == p.TH && a.pcap == p.pcap && a.tcols == p.tcols && a.gd == p.gd)
       return i;
   }
   return 0;
@@ -714,11 +713,12 @@ __global__ void __launch_bounds__(kSpecs[SPEC].min_blocks > 1 ? 128 : MAXT, kSpe
     a.TH = P.TH;
     a.pcap = P.pcap;
     a.tcols = P.tcols;
+    a.gd = P.gd;
   }
   constexpr int E = 4;  // elements per TMEM chunk of the elementwise steps
   extern __shared__ __align__(16) unsigned char smem[];
   const int M = a.M;
-  const SmemLayout L = tm_layout_impl(a.Lcta, a.N, a.CS, a.TL, a.TH, a.pcap);
+  const SmemLayout L = tm_layout_impl(a.Lcta, a.N, a.CS, a.TL, a.TH, a.pcap, a.gd);
   TmSm sm;
   sm.c = reinterpret_cast<V*>(smem + L.p);
   sm.u = reinterpret_cast<V*>(smem + L.u);
@@ -789,32 +789,48 @@ __global__ void __launch_bounds__(kSpecs[SPEC].min_blocks > 1 ? 128 : MAXT, kSpe
   tmem_fence_after();
   const uint32_t tbase = *sm.tslot;
   th.tl = tbase + ((uint32_t)(32 * (warp & 3)) << 16);
-  // ghost-column mbarriers: initialised in every CTA of the cluster before any
-  // neighbour can push into them
-  uint32_t ghp = 0;  // their phase parities (bit 0: c, bit 1: u)
+  // ghost-column mbarriers ("full" at +0: one arrival plus the bytes of both
+  // neighbours' pushes; "empty" at +8: both neighbours released this CTA's
+  // last push), initialised in every CTA before any neighbour can use them
+  uint32_t ghp = 0;  // bit 0: full-barrier parity; bit 1: a push read, to be released (gh_free)
+  uint32_t npush = 0;  // pushes this CTA made (thread 0): the empty-barrier phase to wait for
   if constexpr (GEN) {
-    if (a.C >= kGhostMinC) {
+    if (a.gd > 0) {
       if (tid == 0) {
         mbar_init(ghmb, 1);
-        mbar_init(static_cast<char*>(ghmb) + 8, 1);
+        mbar_init(static_cast<char*>(ghmb) + 8, 2);
       }
       cl_sync<float>(a.C);
     }
   }
-  // Push this CTA's boundary columns of c (vec 0) or u (vec 1) into the
-  // neighbours' ghost slots (thread 0, after the CTA barrier that completed
-  // them; every writer fenced its generic stores for the async proxy first).
-  // The owner rewrites a column only after a cluster barrier the neighbour
-  // reaches after its wait for the push, so the copy's reads are never raced.
+  const uint32_t rr = (uint32_t)((rank + 1) % a.C), rl = (uint32_t)((rank + a.C - 1) % a.C);
+  // Push this CTA's gd first and gd last columns of c (vec 0) or u (vec 1)
+  // into the neighbours' ghost slots (thread 0, after the CTA barrier that
+  // completed them; every writer fenced its generic stores for the async
+  // proxy first), once both neighbours released the previous push.  The owner
+  // rewrites a column only after a cluster barrier the neighbour reaches after
+  // its wait for the push, so the copy's reads are never raced.
   auto gh_push = [&](int vec) {
+    if (npush > 0) mbar_wait_cluster(static_cast<char*>(ghmb) + 8, (npush - 1) & 1u);
+    ++npush;
     const V* src = vec ? sm.u : sm.c;
-    const uint32_t bytes = (uint32_t)(a.CS * (int)sizeof(V));
-    const uint32_t rr = (uint32_t)((rank + 1) % a.C), rl = (uint32_t)((rank + a.C - 1) % a.C);
-    const uint32_t mb = smem_addr(static_cast<char*>(ghmb) + 8 * vec);
-    // the last column -> the right neighbour's left ghost, the first -> the left neighbour's right ghost
-    bulk_s2c(map_rank(smem_addr(sm.gh + (size_t)(2 * vec) * a.CS), rr), src + (size_t)(a.Lcta - 1) * a.CS, bytes,
-             map_rank(mb, rr));
-    bulk_s2c(map_rank(smem_addr(sm.gh + (size_t)(2 * vec + 1) * a.CS), rl), src, bytes, map_rank(mb, rl));
+    const uint32_t bytes = (uint32_t)(a.gd * a.CS * (int)sizeof(V));
+    const uint32_t mb = smem_addr(ghmb);
+    // the last gd columns -> the right neighbour's left ghosts, the first gd -> the left neighbour's right ghosts
+    bulk_s2c(map_rank(smem_addr(sm.gh), rr), src + (size_t)(a.Lcta - a.gd) * a.CS, bytes, map_rank(mb, rr));
+    bulk_s2c(map_rank(smem_addr(sm.gh + (size_t)a.gd * a.CS), rl), src, bytes, map_rank(mb, rl));
+  };
+  // After a CTA barrier that follows a read of the ghosts: release them to
+  // both neighbours (their next push may overwrite them).
+  auto gh_free = [&]() {
+    if (ghp & 2u) {
+      if (tid == 0) {
+        const uint32_t me = smem_addr(static_cast<char*>(ghmb) + 8);
+        mbar_arrive_remote(map_rank(me, rr));
+        mbar_arrive_remote(map_rank(me, rl));
+      }
+      ghp &= 1u;
+    }
   };
   // TMEM regions of this lane: c | u (segment rows 0..G-1) | p | x (own runs)
   auto tC = [&](int c0) { return th.tl + (uint32_t)(2 * (th.jr + c0)); };
@@ -883,13 +899,13 @@ __global__ void __launch_bounds__(kSpecs[SPEC].min_blocks > 1 ? 128 : MAXT, kSpe
     if (warp == 0) {  // tap table and shift extents, lanes over taps
       const V* gains = reinterpret_cast<const V*>(a.ph);
       int dmin = INT_MAX, dmax = INT_MIN;
-      bool d1 = false;  // a tap with |d_l| = 1 (ghost columns)
+      bool d1 = false;  // a tap with 1 <= |d_l| <= gd (ghost columns)
       for (int i = lane; i < P; i += 32) {
         const int kp = __ldg(a.pk + P0 + i), lp = __ldg(a.pl + P0 + i);
         if (in_smem) sm.ptab[i] = tm_path(a, sm, kp, lp, __ldg(gains + P0 + i));
         dmin = min(dmin, a.K0 - kp);
         dmax = max(dmax, a.K0 - kp);
-        d1 |= lp == a.L0 + 1 || lp == a.L0 - 1;
+        d1 |= lp != a.L0 && lp >= a.L0 - a.gd && lp <= a.L0 + a.gd;
       }
       dmin = __reduce_min_sync(0xffffffffu, dmin);
       dmax = __reduce_max_sync(0xffffffffu, dmax);
@@ -911,7 +927,7 @@ __global__ void __launch_bounds__(kSpecs[SPEC].min_blocks > 1 ? 128 : MAXT, kSpe
         fs.lo_u = fs.hi_c;
         fs.hi_u = fs.lo_c;
         fs.remote = !fs.masks;  // without per-warp masks assume DSMEM taps
-        fs.ghost = DDB_GHOST && GEN && a.C >= kGhostMinC && halo && d1;
+        fs.ghost = DDB_GHOST && GEN && a.gd > 0 && halo && d1;
       }
     }
     __syncthreads();
@@ -970,7 +986,7 @@ __global__ void __launch_bounds__(kSpecs[SPEC].min_blocks > 1 ? 128 : MAXT, kSpe
 
     U64 acc[R];
     if constexpr (PROF) prof_mark(a.prof, psm, kArrive);
-    const bool ghost = GEN && a.C >= kGhostMinC && fs.ghost;  // (fs.ghost is written before the barrier above)
+    const bool ghost = GEN && a.gd > 0 && fs.ghost;  // (fs.ghost is written before the barrier above)
     if (ghost) fence_proxy_async();
     tm_arrive(a.C);  // y and the tap classes published
     if (ghost && tid == 0) gh_push(1);
@@ -1001,6 +1017,7 @@ __global__ void __launch_bounds__(kSpecs[SPEC].min_blocks > 1 ? 128 : MAXT, kSpe
     if constexpr (PROF) prof_mark(a.prof, psm, kArrive);
     if (ghost) fence_proxy_async();
     TM_WT(2, tm_arrive_red<PROF>(a.C, red + (2 + par1) * kPushSlots, nwarps, warp, lane, rank, !GEN || !fs.remote, wt));  // c = b published
+    if (ghost) gh_free();
     if (ghost && tid == 0 && a.iters > 0) gh_push(0);
     if constexpr (PROF) prof_mark(a.prof, psm, kMvmLocal);
     TM_WT(0, mvm_local<R, false, GEN>(a, th, sm, fs, tC(0) - 2 * th.jr, ccol, acc));
@@ -1054,6 +1071,7 @@ __global__ void __launch_bounds__(kSpecs[SPEC].min_blocks > 1 ? 128 : MAXT, kSpe
       if constexpr (PROF) prof_mark(a.prof, psm, kArrive);
       if (ghost) fence_proxy_async();
       TM_WT(2, tm_arrive_red<PROF>(a.C, red + par0 * kPushSlots, nwarps, warp, lane, rank, !GEN || !fs.remote, wt));  // u published
+      if (ghost) gh_free();
       if (ghost && tid == 0) gh_push(1);
       // ap = H^H u + lam p;  x += alpha p;  c -= alpha ap      (equalize.py:60-70)
       if constexpr (PROF) prof_mark(a.prof, psm, kMvmLocal);
@@ -1071,6 +1089,7 @@ __global__ void __launch_bounds__(kSpecs[SPEC].min_blocks > 1 ? 128 : MAXT, kSpe
         exact = true;
         // peers may still be reading this CTA's u: one more full barrier
         tm_arrive(a.C);
+        if (ghost) gh_free();
         cl_wait(a.C);
         break;
       }
@@ -1112,6 +1131,7 @@ __global__ void __launch_bounds__(kSpecs[SPEC].min_blocks > 1 ? 128 : MAXT, kSpe
       if constexpr (PROF) prof_mark(a.prof, psm, kArrive);
       if (ghost) fence_proxy_async();
       TM_WT(2, tm_arrive_red<PROF>(a.C, red + (2 + par1) * kPushSlots, nwarps, warp, lane, rank, !GEN || !fs.remote, wt));  // c published
+      if (ghost) gh_free();
       if (ghost && tid == 0 && it + 1 < a.iters) gh_push(0);
       if constexpr (PROF) prof_mark(a.prof, psm, kMvmLocal);
       if (it + 1 < a.iters) TM_WT(0, mvm_local<R, false, GEN>(a, th, sm, fs, tC(0) - 2 * th.jr, ccol, acc));  // next H c
@@ -1394,9 +1414,9 @@ cudaError_t tm_occ(int R, const LaunchShape& s, int* n) {
 #endif
 
 #if !defined(TM_PART) || TM_PART == 0
-SmemLayout sscga_tm_layout(int M, int Lcta, int N, int CS, int TL, int TH, int pcap) {
+SmemLayout sscga_tm_layout(int M, int Lcta, int N, int CS, int TL, int TH, int pcap, int gd) {
   (void)M;
-  return tm_layout_impl(Lcta, N, CS, TL, TH, pcap);
+  return tm_layout_impl(Lcta, N, CS, TL, TH, pcap, gd);
 }
 
 // Both instantiations on the stream: the lean frames, then the others.
