@@ -83,7 +83,8 @@ __host__ __device__ inline SmemLayout tm_layout_impl(int Lcta, int N, int CS, in
     // left neighbour's last gd, then the right neighbour's first gd, extended
     // like the own columns) of c or u, whichever the next MVM gathers, pushed
     // by their owners (gh_push); a "full" mbarrier (bytes landed) and an
-    // "empty" one (both neighbours done reading this CTA's last push)
+    // "empty" one (every warp of both neighbours done reading this CTA's last
+    // push: each arrives remotely at the end of its remote pass)
     (void)N;
     L.gh = o; o = a16(o + (size_t)2 * gd * CS * sizeof(V));
     L.ghmb = o; o = a16(o + 16);
@@ -384,7 +385,6 @@ __device__ __forceinline__ void mvm_remote(const SolveArgs& a, const TmThr& th, 
     if (threadIdx.x == 0) mbar_expect_tx(ghmb, (uint32_t)(2 * a.gd * a.CS * (int)sizeof(V)));
     mbar_wait(ghmb, ghp & 1u);
     ghp ^= 1u;
-    ghp |= 2u;  // to be released (gh_free) after the next CTA barrier
   }
   if (fs.masks) {
     for (uint32_t m = fs.mk[th.jr / R][HERM ? 5 : 2]; m; m &= m - 1)
@@ -393,6 +393,15 @@ __device__ __forceinline__ void mvm_remote(const SolveArgs& a, const TmThr& th, 
     for (int p = 0; p < fs.P; ++p) {
       const PathEnt<float> e = tm_get(a, sm, fs, p);
       if (tap_class<R, HERM>(a, th.jr, halo, e) == 2) tap_elem<R, HERM>(a, th, sm, fs, halo, buf, e, acc);
+    }
+  }
+  if (a.gd > 0 && fs.ghost) {  // this warp is done with the ghosts: release them to both neighbours
+    __syncwarp();
+    if ((threadIdx.x & 31) == 0) {
+      const int rank = th.colg / a.Lcta;
+      const uint32_t me = smem_addr(static_cast<char*>(ghmb) + 8);
+      mbar_arrive_remote(map_rank(me, (uint32_t)((rank + 1) % a.C)));
+      mbar_arrive_remote(map_rank(me, (uint32_t)((rank + a.C - 1) % a.C)));
     }
   }
 }
@@ -792,13 +801,13 @@ __global__ void __launch_bounds__(kSpecs[SPEC].min_blocks > 1 ? 128 : MAXT, kSpe
   // ghost-column mbarriers ("full" at +0: one arrival plus the bytes of both
   // neighbours' pushes; "empty" at +8: both neighbours released this CTA's
   // last push), initialised in every CTA before any neighbour can use them
-  uint32_t ghp = 0;  // bit 0: full-barrier parity; bit 1: a push read, to be released (gh_free)
+  uint32_t ghp = 0;  // full-barrier parity
   uint32_t npush = 0;  // pushes this CTA made (thread 0): the empty-barrier phase to wait for
   if constexpr (GEN) {
     if (a.gd > 0) {
       if (tid == 0) {
         mbar_init(ghmb, 1);
-        mbar_init(static_cast<char*>(ghmb) + 8, 2);
+        mbar_init(static_cast<char*>(ghmb) + 8, 2 * nwarps);  // every warp of both neighbours
       }
       cl_sync<float>(a.C);
     }
@@ -819,18 +828,6 @@ __global__ void __launch_bounds__(kSpecs[SPEC].min_blocks > 1 ? 128 : MAXT, kSpe
     // the last gd columns -> the right neighbour's left ghosts, the first gd -> the left neighbour's right ghosts
     bulk_s2c(map_rank(smem_addr(sm.gh), rr), src + (size_t)(a.Lcta - a.gd) * a.CS, bytes, map_rank(mb, rr));
     bulk_s2c(map_rank(smem_addr(sm.gh + (size_t)a.gd * a.CS), rl), src, bytes, map_rank(mb, rl));
-  };
-  // After a CTA barrier that follows a read of the ghosts: release them to
-  // both neighbours (their next push may overwrite them).
-  auto gh_free = [&]() {
-    if (ghp & 2u) {
-      if (tid == 0) {
-        const uint32_t me = smem_addr(static_cast<char*>(ghmb) + 8);
-        mbar_arrive_remote(map_rank(me, rr));
-        mbar_arrive_remote(map_rank(me, rl));
-      }
-      ghp &= 1u;
-    }
   };
   // TMEM regions of this lane: c | u (segment rows 0..G-1) | p | x (own runs)
   auto tC = [&](int c0) { return th.tl + (uint32_t)(2 * (th.jr + c0)); };
@@ -1017,7 +1014,6 @@ __global__ void __launch_bounds__(kSpecs[SPEC].min_blocks > 1 ? 128 : MAXT, kSpe
     if constexpr (PROF) prof_mark(a.prof, psm, kArrive);
     if (ghost) fence_proxy_async();
     TM_WT(2, tm_arrive_red<PROF>(a.C, red + (2 + par1) * kPushSlots, nwarps, warp, lane, rank, !GEN || !fs.remote, wt));  // c = b published
-    if (ghost) gh_free();
     if (ghost && tid == 0 && a.iters > 0) gh_push(0);
     if constexpr (PROF) prof_mark(a.prof, psm, kMvmLocal);
     TM_WT(0, mvm_local<R, false, GEN>(a, th, sm, fs, tC(0) - 2 * th.jr, ccol, acc));
@@ -1071,8 +1067,7 @@ __global__ void __launch_bounds__(kSpecs[SPEC].min_blocks > 1 ? 128 : MAXT, kSpe
       if constexpr (PROF) prof_mark(a.prof, psm, kArrive);
       if (ghost) fence_proxy_async();
       TM_WT(2, tm_arrive_red<PROF>(a.C, red + par0 * kPushSlots, nwarps, warp, lane, rank, !GEN || !fs.remote, wt));  // u published
-      if (ghost) gh_free();
-      if (ghost && tid == 0) gh_push(1);
+        if (ghost && tid == 0) gh_push(1);
       // ap = H^H u + lam p;  x += alpha p;  c -= alpha ap      (equalize.py:60-70)
       if constexpr (PROF) prof_mark(a.prof, psm, kMvmLocal);
       TM_WT(1, mvm_local<R, true, GEN>(a, th, sm, fs, tU(0) - 2 * th.jr, ucol, acc));
@@ -1089,8 +1084,7 @@ __global__ void __launch_bounds__(kSpecs[SPEC].min_blocks > 1 ? 128 : MAXT, kSpe
         exact = true;
         // peers may still be reading this CTA's u: one more full barrier
         tm_arrive(a.C);
-        if (ghost) gh_free();
-        cl_wait(a.C);
+            cl_wait(a.C);
         break;
       }
       const float alpha = cn / denom;
@@ -1131,8 +1125,7 @@ __global__ void __launch_bounds__(kSpecs[SPEC].min_blocks > 1 ? 128 : MAXT, kSpe
       if constexpr (PROF) prof_mark(a.prof, psm, kArrive);
       if (ghost) fence_proxy_async();
       TM_WT(2, tm_arrive_red<PROF>(a.C, red + (2 + par1) * kPushSlots, nwarps, warp, lane, rank, !GEN || !fs.remote, wt));  // c published
-      if (ghost) gh_free();
-      if (ghost && tid == 0 && it + 1 < a.iters) gh_push(0);
+        if (ghost && tid == 0 && it + 1 < a.iters) gh_push(0);
       if constexpr (PROF) prof_mark(a.prof, psm, kMvmLocal);
       if (it + 1 < a.iters) TM_WT(0, mvm_local<R, false, GEN>(a, th, sm, fs, tC(0) - 2 * th.jr, ccol, acc));  // next H c
       if constexpr (PROF) prof_mark(a.prof, psm, kWait);
