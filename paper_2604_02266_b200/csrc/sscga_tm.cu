@@ -55,7 +55,7 @@ struct FrameSm {
   int lo_c, hi_c, lo_u, hi_u;  // extension rows written for c (gathered by H) and u (by H^H)
   int remote;                  // some warp gathers per element (DSMEM): publish c / u with release
   int wrap;                    // some shift exceeds the halo: runs beyond it wrap the delay period
-  int ghost;                   // ghost columns pushed and read this frame (gh_push, tap_elem)
+  int ghost;                   // ghost columns pushed per side this frame (0: none; the frame's largest |d_l| <= gd)
   uint32_t mk[8][6];           // [j][tmF, smF, gnF, tmH, smH, gnH]: TMEM run / shared run / per element
 };
 
@@ -382,7 +382,7 @@ __device__ __forceinline__ void mvm_remote(const SolveArgs& a, const TmThr& th, 
                                            const V* buf, void* ghmb, uint32_t& ghp, U64 (&acc)[R]) {
   const bool halo = fs.halo;
   if (a.gd > 0 && fs.ghost) {  // the ghost columns of this vector landed (gh_push of both neighbours)
-    if (threadIdx.x == 0) mbar_expect_tx(ghmb, (uint32_t)(2 * a.gd * a.CS * (int)sizeof(V)));
+    if (threadIdx.x == 0) mbar_expect_tx(ghmb, (uint32_t)(2 * fs.ghost * a.CS * (int)sizeof(V)));
     mbar_wait(ghmb, ghp & 1u);
     ghp ^= 1u;
   }
@@ -823,10 +823,13 @@ __global__ void __launch_bounds__(kSpecs[SPEC].min_blocks > 1 ? 128 : MAXT, kSpe
     if (npush > 0) mbar_wait_cluster(static_cast<char*>(ghmb) + 8, (npush - 1) & 1u);
     ++npush;
     const V* src = vec ? sm.u : sm.c;
-    const uint32_t bytes = (uint32_t)(a.gd * a.CS * (int)sizeof(V));
+    // only the gx columns a side this frame's taps reach (gx = max |d_l| <= gd)
+    const int gx = fs.ghost;
+    const uint32_t bytes = (uint32_t)(gx * a.CS * (int)sizeof(V));
     const uint32_t mb = smem_addr(ghmb);
-    // the last gd columns -> the right neighbour's left ghosts, the first gd -> the left neighbour's right ghosts
-    bulk_s2c(map_rank(smem_addr(sm.gh), rr), src + (size_t)(a.Lcta - a.gd) * a.CS, bytes, map_rank(mb, rr));
+    // the last gx columns -> the right neighbour's innermost left ghost slots, the first gx -> its left neighbour's right ones
+    bulk_s2c(map_rank(smem_addr(sm.gh + (size_t)(a.gd - gx) * a.CS), rr), src + (size_t)(a.Lcta - gx) * a.CS, bytes,
+             map_rank(mb, rr));
     bulk_s2c(map_rank(smem_addr(sm.gh + (size_t)a.gd * a.CS), rl), src, bytes, map_rank(mb, rl));
   };
   // TMEM regions of this lane: c | u (segment rows 0..G-1) | p | x (own runs)
@@ -896,17 +899,18 @@ __global__ void __launch_bounds__(kSpecs[SPEC].min_blocks > 1 ? 128 : MAXT, kSpe
     if (warp == 0) {  // tap table and shift extents, lanes over taps
       const V* gains = reinterpret_cast<const V*>(a.ph);
       int dmin = INT_MAX, dmax = INT_MIN;
-      bool d1 = false;  // a tap with 1 <= |d_l| <= gd (ghost columns)
+      int d1 = 0;  // the largest |d_l| <= gd of a tap (ghost columns per side)
       for (int i = lane; i < P; i += 32) {
         const int kp = __ldg(a.pk + P0 + i), lp = __ldg(a.pl + P0 + i);
         if (in_smem) sm.ptab[i] = tm_path(a, sm, kp, lp, __ldg(gains + P0 + i));
         dmin = min(dmin, a.K0 - kp);
         dmax = max(dmax, a.K0 - kp);
-        d1 |= lp != a.L0 && lp >= a.L0 - a.gd && lp <= a.L0 + a.gd;
+        const int adl = abs(lp - a.L0);
+        if (adl <= a.gd) d1 = max(d1, adl);
       }
       dmin = __reduce_min_sync(0xffffffffu, dmin);
       dmax = __reduce_max_sync(0xffffffffu, dmax);
-      d1 = __any_sync(0xffffffffu, d1);
+      d1 = __reduce_max_sync(0xffffffffu, d1);
       if (lane == 0) {
         // halo rows written per side: what the shifts need, at most H; a run
         // beyond them is read one delay period over (wrap_run), which needs
@@ -924,7 +928,7 @@ __global__ void __launch_bounds__(kSpecs[SPEC].min_blocks > 1 ? 128 : MAXT, kSpe
         fs.lo_u = fs.hi_c;
         fs.hi_u = fs.lo_c;
         fs.remote = !fs.masks;  // without per-warp masks assume DSMEM taps
-        fs.ghost = DDB_GHOST && GEN && a.gd > 0 && halo && d1;
+        fs.ghost = DDB_GHOST && GEN && a.gd > 0 && halo ? d1 : 0;
       }
     }
     __syncthreads();
