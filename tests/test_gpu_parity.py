@@ -428,6 +428,40 @@ def test_ghost_columns_across_frames(pkg, M, N):
         assert rel_l2(x[f], xr) < REL_L2_FP32, (f, rel_l2(x[f], xr), s.plan())
 
 
+def test_ghost_push_width_varies_per_frame(pkg):
+    """A ghost push carries only the gx = max |d_l| (<= gd) boundary columns a
+    side that the frame's taps reach, so consecutive frames of one cluster push
+    different widths into the same ghost slots (gx = 0, 1, 2, 3, 4 in turn,
+    plus a |d_l| = 6 tap beyond the ghosts read by DSMEM).  Every checked frame
+    must still match the oracle."""
+    from paper_2604_02266_b200 import _native as nat
+    M, N = 1024, 64
+    if nat.plan(M, N, nat.DDB_F32).cluster < 4:
+        pytest.skip("plan without ghost columns")
+    rng = np.random.default_rng(2024)
+    s = solver_for(pkg, M, N, 10, "fp32")
+    shift_sets = [[0], [1, -1], [2, 0, -2], [3, -1], [4, -4, 1], [6, 1], [-2], [4]]
+    B, P = 96, 5  # more frames than the plan's clusters: several per cluster
+    off = np.arange(B + 1) * P
+    k = (M // 2 + rng.integers(0, 40, size=B * P)) % M
+    l = np.empty(B * P, np.int64)
+    for f in range(B):
+        ss = shift_sets[f % len(shift_sets)]
+        l[f * P:(f + 1) * P] = (N // 2 + np.array([0] + [ss[i % len(ss)] for i in range(P - 1)])) % N
+    g = rng.uniform(0.05, 0.3, size=B * P) * np.exp(2j * np.pi * rng.random(B * P))
+    g[::P] = np.exp(2j * np.pi * rng.random(B))
+    y = rng.normal(size=(B, M * N)) + 1j * rng.normal(size=(B, M * N))
+    paths = pkg.PathBatch.from_arrays(off, k, l, g, cdtype=s.cdtype)
+    yt = torch.as_tensor(y, device="cuda").to(s.cdtype).contiguous()
+    res = s.solve(yt, paths, 1e-2)
+    x = res.x.cpu().numpy()
+    for f in (1, 2, 3, 4, 5, 22, 50, 95):
+        sl = slice(off[f], off[f + 1])
+        taps = [orc.Tap(int(a), int(b), complex(c)) for a, b, c in zip(k[sl], l[sl], g[sl])]
+        xr, _ = orc.cga(orc.build_tables(taps, M, N), yt[f].cpu().numpy().astype(np.complex128), 10, 1e-2)
+        assert rel_l2(x[f], xr) < REL_L2_FP32, (f, rel_l2(x[f], xr), s.plan())
+
+
 def test_plan_residency_is_the_launched_instantiation(pkg):
     """The plan's CTAs per SM come from the instantiation a solve of that plan
     launches: cfg1 (64 x 16) runs its compile-time-geometry kernel at 96
