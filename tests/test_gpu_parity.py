@@ -462,6 +462,36 @@ def test_ghost_push_width_varies_per_frame(pkg):
         assert rel_l2(x[f], xr) < REL_L2_FP32, (f, rel_l2(x[f], xr), s.plan())
 
 
+def test_doppler_tap_mix_two_cta_plan(pkg):
+    """The two-CTA plan (512 x 32) on frames with 0-5 Doppler taps (|d_l| up
+    to 5: boundary lanes read the peer CTA by DSMEM) and delays inside and
+    beyond the halo (wrapped runs), lean and general frames mixed in one batch,
+    several frames per cluster, against the oracle."""
+    M, N = 512, 32
+    rng = np.random.default_rng(77)
+    s = solver_for(pkg, M, N, 10, "fp32")
+    B, P = 200, 6
+    off = np.arange(B + 1) * P
+    k = (M // 2 + rng.integers(0, 40, size=B * P)) % M
+    k[P * 7 + 1::P * 9] = (M // 2 + 200) % M  # some frames with a shift beyond the halo (wrapped runs)
+    l = np.full(B * P, N // 2)
+    for f in range(B):
+        nd = f % 6  # Doppler taps in this frame
+        l[f * P + 1:f * P + 1 + nd] = (N // 2 + rng.choice([-5, -2, -1, 1, 2, 5], size=nd)) % N
+    g = rng.uniform(0.05, 0.3, size=B * P) * np.exp(2j * np.pi * rng.random(B * P))
+    g[::P] = np.exp(2j * np.pi * rng.random(B))
+    y = rng.normal(size=(B, M * N)) + 1j * rng.normal(size=(B, M * N))
+    paths = pkg.PathBatch.from_arrays(off, k, l, g, cdtype=s.cdtype)
+    yt = torch.as_tensor(y, device="cuda").to(s.cdtype).contiguous()
+    res = s.solve(yt, paths, 1e-2)
+    x = res.x.cpu().numpy()
+    for f in (0, 1, 2, 3, 4, 5, 16, 97, 151, 199):
+        sl = slice(off[f], off[f + 1])
+        taps = [orc.Tap(int(a), int(b), complex(c)) for a, b, c in zip(k[sl], l[sl], g[sl])]
+        xr, _ = orc.cga(orc.build_tables(taps, M, N), yt[f].cpu().numpy().astype(np.complex128), 10, 1e-2)
+        assert rel_l2(x[f], xr) < REL_L2_FP32, (f, rel_l2(x[f], xr), s.plan())
+
+
 def test_plan_residency_is_the_launched_instantiation(pkg):
     """The plan's CTAs per SM come from the instantiation a solve of that plan
     launches: cfg1 (64 x 16) runs its compile-time-geometry kernel at 96
