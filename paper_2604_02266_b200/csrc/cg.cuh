@@ -183,14 +183,14 @@ __device__ __forceinline__ void cl_arrive_sem(bool release) {
 }
 template <typename T, bool TMEM_FENCES>
 __device__ __forceinline__ void cl_arrive_red(int C, Vec<T>* base, int nwarps, int warp, int lane, int rank,
-                                              bool relaxed) {
+                                              bool relaxed, int fold = -1) {
   if constexpr (TMEM_FENCES) {
     tmem_wait_st();
     tmem_fence_before();
   }
   __syncthreads();
   if (C > 1) {
-    const int fw = TMEM_FENCES ? fold_warp(nwarps) : 0;  // (the row-slice kernel: warp 0 measured best)
+    const int fw = fold >= 0 ? fold : TMEM_FENCES ? fold_warp(nwarps) : 0;  // (the row-slice kernel: warp 0 measured best)
     if (warp == fw) {
       Vec<T> t = lane < nwarps ? base[lane] : czero<Vec<T>>();
       t.x = warp_sum(t.x);

@@ -473,11 +473,20 @@ __device__ __forceinline__ void tm_arrive(int C, bool relaxed = false) {
 // Timed variant (measurement builds): wt[4] TMEM store wait + fence, wt[5] CTA
 // barrier, wt[6] fold + push, wt[7] cluster arrive.  BAR.SYNC defers blocking,
 // so the CTA-barrier wait mostly lands in wt[6].
-template <bool PROF>
+// The warp that folds the CTA partials (and then starts its next MVM late):
+// one of a middle row block (fold_warp); in the lean kernel the lightest row
+// block of the MVM that follows -- the first before a hermitian MVM, the last
+// before a forward one (per-warp MVM times, profiles/r2_final_phase.json):
+// cfg3 +0.4 %; the general kernel keeps the middle one (cfg4 -3.6 % otherwise).
+__device__ __forceinline__ int tm_fold(int nwarps, bool before_herm, bool lean) {
+  if (lean && nwarps == 16) return before_herm ? 0 : 12;
+  return fold_warp(nwarps);
+}
+template <bool PROF, bool LEAN = false>
 __device__ __forceinline__ void tm_arrive_red(int C, V* base, int nwarps, int warp, int lane, int rank,
-                                              bool relaxed, long long* wt) {
+                                              bool relaxed, long long* wt, bool before_herm = false) {
   if constexpr (!PROF) {
-    cl_arrive_red<float, true>(C, base, nwarps, warp, lane, rank, relaxed);
+    cl_arrive_red<float, true>(C, base, nwarps, warp, lane, rank, relaxed, tm_fold(nwarps, before_herm, LEAN));
   } else {
     long long t = clock64(), u;
     tmem_wait_st();
@@ -486,7 +495,7 @@ __device__ __forceinline__ void tm_arrive_red(int C, V* base, int nwarps, int wa
     __syncthreads();
     u = clock64(); wt[5] += u - t; t = u;
     if (C > 1) {
-      if (warp == fold_warp(nwarps)) {
+      if (warp == tm_fold(nwarps, before_herm, LEAN)) {
         V v = lane < nwarps ? base[lane] : make_float2(0.f, 0.f);
         v.x = warp_sum(v.x);
         v.y = warp_sum(v.y);
@@ -494,7 +503,7 @@ __device__ __forceinline__ void tm_arrive_red(int C, V* base, int nwarps, int wa
       }
       u = clock64(); wt[6] += u - t; t = u;
       (void)relaxed;
-      cl_arrive_sem(warp == fold_warp(nwarps));
+      cl_arrive_sem(warp == tm_fold(nwarps, before_herm, LEAN));
     }
     tmem_fence_after();
     u = clock64(); wt[7] += u - t;
@@ -1017,7 +1026,7 @@ __global__ void __launch_bounds__(kSpecs[SPEC].min_blocks > 1 ? 128 : MAXT, kSpe
     }
     if constexpr (PROF) prof_mark(a.prof, psm, kArrive);
     if (ghost) fence_proxy_async();
-    TM_WT(2, tm_arrive_red<PROF>(a.C, red + (2 + par1) * kPushSlots, nwarps, warp, lane, rank, !GEN || !fs.remote, wt));  // c = b published
+    TM_WT(2, tm_arrive_red<PROF, !GEN>(a.C, red + (2 + par1) * kPushSlots, nwarps, warp, lane, rank, !GEN || !fs.remote, wt));  // c = b published
     if (ghost && tid == 0 && a.iters > 0) gh_push(0);
     if constexpr (PROF) prof_mark(a.prof, psm, kMvmLocal);
     TM_WT(0, mvm_local<R, false, GEN>(a, th, sm, fs, tC(0) - 2 * th.jr, ccol, acc));
@@ -1070,7 +1079,8 @@ __global__ void __launch_bounds__(kSpecs[SPEC].min_blocks > 1 ? 128 : MAXT, kSpe
       }
       if constexpr (PROF) prof_mark(a.prof, psm, kArrive);
       if (ghost) fence_proxy_async();
-      TM_WT(2, tm_arrive_red<PROF>(a.C, red + par0 * kPushSlots, nwarps, warp, lane, rank, !GEN || !fs.remote, wt));  // u published
+      TM_WT(2, tm_arrive_red<PROF, !GEN>(a.C, red + par0 * kPushSlots, nwarps, warp, lane, rank, !GEN || !fs.remote, wt,
+                                   true));  // u published
         if (ghost && tid == 0) gh_push(1);
       // ap = H^H u + lam p;  x += alpha p;  c -= alpha ap      (equalize.py:60-70)
       if constexpr (PROF) prof_mark(a.prof, psm, kMvmLocal);
@@ -1128,7 +1138,7 @@ __global__ void __launch_bounds__(kSpecs[SPEC].min_blocks > 1 ? 128 : MAXT, kSpe
       }
       if constexpr (PROF) prof_mark(a.prof, psm, kArrive);
       if (ghost) fence_proxy_async();
-      TM_WT(2, tm_arrive_red<PROF>(a.C, red + (2 + par1) * kPushSlots, nwarps, warp, lane, rank, !GEN || !fs.remote, wt));  // c published
+      TM_WT(2, tm_arrive_red<PROF, !GEN>(a.C, red + (2 + par1) * kPushSlots, nwarps, warp, lane, rank, !GEN || !fs.remote, wt));  // c published
         if (ghost && tid == 0 && it + 1 < a.iters) gh_push(0);
       if constexpr (PROF) prof_mark(a.prof, psm, kMvmLocal);
       if (it + 1 < a.iters) TM_WT(0, mvm_local<R, false, GEN>(a, th, sm, fs, tC(0) - 2 * th.jr, ccol, acc));  // next H c
