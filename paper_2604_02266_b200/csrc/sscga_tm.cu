@@ -786,8 +786,8 @@ __global__ void __launch_bounds__(kSpecs[SPEC].min_blocks > 1 ? 128 : MAXT, kSpe
     mbar_expect_tx(ymb, (uint32_t)(a.Lcta * M * (int)sizeof(V)));
     for (int c = 0; c < a.Lcta; ++c) bulk_g2s(sm.u + (size_t)c * a.CS + a.H, src + (size_t)c * M, M * sizeof(V), ymb);
   };
-  // the same from the lanes of the last warp, one column each: the copy of the
-  // next frame after the CG loop (the one on the frame's critical path)
+  // the same from the lanes of the last warp, one column each: the lean kernel's
+  // copy of the next frame after the CG loop
   auto issue_y_warp = [&](int fy) {  // every lane of one warp
     const V* src = yg + (size_t)fy * a.MN + (size_t)rank * a.Lcta * M;
     fence_proxy_async();
@@ -1163,7 +1163,11 @@ __global__ void __launch_bounds__(kSpecs[SPEC].min_blocks > 1 ? 128 : MAXT, kSpe
       if (lead && a.cnorm) reinterpret_cast<float*>(a.cnorm)[(size_t)f * stride + done] = cn;
     }
     // every gather of this frame's u (here and in the peers) is behind the last barrier
-    if (a.stream_y && fnext >= 0 && warp == nwarps - 1) issue_y_warp(fnext);
+    if constexpr (!GEN) {  // (the general kernel keeps thread 0: cfg4 -2.4 % with the warp)
+      if (a.stream_y && fnext >= 0 && warp == nwarps - 1) issue_y_warp(fnext);
+    } else if (a.stream_y && tid == 0 && fnext >= 0) {
+      issue_y(fnext);
+    }
     if (lead) {
       float* cnorm = reinterpret_cast<float*>(a.cnorm);
       if (cnorm) for (int i = done + 1; i < stride; ++i) cnorm[(size_t)f * stride + i] = 0.f;
